@@ -1,0 +1,496 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 RaPP prediction path (BASELINE.json metric, config 2 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload stream|lattice]
+
+Default workload (N=1 headline, BASELINE.json configs[1]): the 4-model sweep — tables
+b=[1,2,4,8,16,32] x s=1..100 x q=1..100 for resnet50/vgg19/bert-base/mobilenet
+(pkg/scripts/gen_tables.py:26-29 surface), 10^8 random (batch, sm%, quota%) queries per
+model (1% exactly on grid nodes).  One step = interp3_many over all 4 x 10^8 queries.
+  value : predictions/s with inputs resident in HBM (CUDA events, max over ranks)
+  e2e   : same metric through the reference-shaped host API (kernels.interp3_many) with
+          pinned host buffers: H2D of the step's queries + kernel + D2H of latencies.
+Inputs (9.6 GB/GPU) are far larger than the 126 MB L2, so no flush is needed between
+steps.  `--workload lattice` times config 5 instead: 3,125 functions x (32 x 100 x 100)
+lattice = 1.0e9 most_efficient_config predictions per step, functions sharded over
+ranks with an NCCL all-gather of the per-function (b, s, q) decisions.
+
+Rank 0 prints ONE JSON line.  --impl reference times the reference's own compiled CPU
+kernel (oracle/_ref: hs/_kernels/_grid_cy.c built from /root/reference) on all host
+cores with a process pool (its nogil loop re-acquires the GIL, so threads do not scale;
+SURVEY.md finding 0.6), on a bounded sample of the same workload per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "RaPP config predictions/sec and scaling decisions/tick latency at 1/2/4/8 B200"
+UNIT = "predictions/s"
+QUERIES_PER_MODEL = 100_000_000
+
+# gen_tables.py:19-23 reference params; the other three are invented
+MODELS = {
+    "resnet50": (8.0, 1.5, 0.35, 0.65),
+    "vgg19": (14.0, 4.0, 0.30, 0.70),
+    "bert-base": (22.0, 5.0, 0.25, 0.75),
+    "mobilenet": (3.0, 0.5, 0.50, 0.50),
+}
+BATCHES = [1, 2, 4, 8, 16, 32]
+
+
+def surface(fixed, per_item, sm_floor, sm_weight, b, s, q):
+    """pkg/scripts/gen_tables.py:26-29, evaluated left to right in float64 (vectorised)."""
+    b = np.asarray(b, dtype=np.float64)[:, None, None]
+    s = np.asarray(s, dtype=np.float64)[None, :, None]
+    q = np.asarray(q, dtype=np.float64)[None, None, :]
+    compute = fixed + per_item * b
+    sm_penalty = sm_floor + sm_weight * (100.0 / s)
+    return np.ascontiguousarray(compute * sm_penalty * (100.0 / q))
+
+
+def config2_arrays():
+    """[(name, b_axis, s_axis, q_axis, values)] for the 4-model sweep."""
+    s = list(range(1, 101))
+    q = list(range(1, 101))
+    out = []
+    for name, p in MODELS.items():
+        out.append((name, np.array(BATCHES, float), np.array(s, float), np.array(q, float),
+                    surface(*p, BATCHES, s, q)))
+    return out
+
+
+def make_config5_tables(n, seed=0, device=None):
+    """Config 5 tables: b=[1..32 pow2] x s=1..100 x q=10..100/10 per function, random
+    gen_tables parameters (fixed~U(4,20), per_item~U(0.5,4),
+    sm_floor~U(0.2,0.4)).  The lattice a search walks is B x table.sms x quota steps
+    (hs/perf.py:123-125), so the sm axis is 1..100 to give the 32x100x100 lattice."""
+    from paper_2505_01968_b200 import PerfTable
+    rng = random.Random(seed)
+    s = list(range(1, 101))
+    q = list(range(10, 101, 10))
+    tables = []
+    for i in range(n):
+        fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
+        tables.append(PerfTable(f"fn-{i:05d}", BATCHES, s, q,
+                                surface(fixed, per, floor, 1.0 - floor, BATCHES, s, q),
+                                device=device))
+    return tables
+
+
+def max_lattice_rps(table):
+    """Max throughput of the (monotone) table's lattice: the (b_max, s_max, q=100) node."""
+    lat = float(table.latency_ms[-1, -1, -1])
+    return table.batches[-1] / (lat / 1000.0)
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ----------------------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------------------
+
+
+def dist_init(gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------------------
+# our arm: stream workload (config 2)
+# ----------------------------------------------------------------------------------------
+
+
+def gen_queries(b, s, q, n, seed, device):
+    """Uniform over the axis ranges, 1% of rows exactly on grid nodes (device RNG)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    c = torch.empty((n, 3), dtype=torch.float64, device=device)
+    for col, axis in enumerate((b, s, q)):
+        lo, hi = float(axis[0]), float(axis[-1])
+        c[:, col].uniform_(lo, hi, generator=g)
+    m = n // 100
+    ax = [torch.from_numpy(a).to(device) for a in (b, s, q)]
+    for col in range(3):
+        idx = torch.randint(0, len(ax[col]), (m,), generator=g, device=device)
+        c[:m, col] = ax[col][idx]
+    return c
+
+
+def run_stream(args, rank, world, local):
+    import torch
+    from paper_2505_01968_b200 import PerfTable, _lib, kernels
+    dev = torch.device("cuda", local)
+    n = args.queries
+    tables, coords, outs = [], [], []
+    for mi, (name, b, s, q, v) in enumerate(config2_arrays()):
+        t = PerfTable(name, BATCHES, list(range(1, 101)), list(range(1, 101)), v, device=local)
+        t.device_table()
+        tables.append(t)
+        coords.append(gen_queries(b, s, q, n, 1000 * rank + mi, dev))
+        outs.append(torch.empty(n, dtype=torch.float64, device=dev))
+    stream = torch.cuda.current_stream(dev)
+    preds_per_step = len(tables) * n
+
+    def step(evs=None):
+        for k, t in enumerate(tables):
+            if evs is not None:
+                evs[k][0].record(stream)
+            t.predict_latency_many(coords[k], outs[k], stream=stream.cuda_stream)
+            if evs is not None:
+                evs[k][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    launches0 = _lib.launch_count()
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in tables] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(kev[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    barrier(world)
+    ms = max_over_ranks(start.elapsed_time(end), world)
+    kernel_ms = [a.elapsed_time(b) for row in kev for (a, b) in row]
+    avg_launch_ms = float(np.mean(kernel_ms))
+    value = world * preds_per_step * args.steps / (ms / 1000.0)
+
+    # e2e: the reference-shaped host API with pinned host buffers, copies inside the timing
+    e2e = None
+    if not args.no_e2e:
+        hc = [c.cpu().pin_memory() for c in coords]
+        ho = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in tables]
+        arrays = config2_arrays()
+
+        def e2e_step():
+            for k, (_, b, s, q, v) in enumerate(arrays):
+                kernels.interp3_many(b, s, q, v, hc[k].numpy(), ho[k].numpy())
+
+        e2e_step()
+        ok = all(np.array_equal(ho[k].numpy().view(np.int64),
+                                outs[k].cpu().numpy().view(np.int64)) for k in range(len(ho)))
+        if not ok:
+            raise RuntimeError("e2e host path disagrees with the device path")
+        barrier(world)
+        e2e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        e2e = {"value": world * preds_per_step * e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": preds_per_step * 24, "d2h_bytes_per_step": preds_per_step * 8,
+               "steps": e2e_steps, "api": "paper_2505_01968_b200.kernels.interp3_many "
+               "(C ABI rapp_interp3_many, pinned host buffers)"}
+
+    peak, peak_kind = load_peak()
+    alg_bytes = 32.0 * n  # 24 B coords read + 8 B latency written per prediction
+    achieved = alg_bytes / (avg_launch_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": load_traffic(n),
+                "kernel": "k_interp_stream<false>", "peak_source": peak_kind,
+                "alg_bytes_per_prediction": 32}
+    cfg = {"workload": "config2: 4-model sweep (resnet50, vgg19, bert-base, mobilenet), tables "
+           "6x100x100 (b=1..32 pow2, sm 1..100%, quota 1..100%), 1e8 random queries/model/GPU",
+           "queries_per_step_per_gpu": preds_per_step, "l2": "inputs 9.6 GB/GPU >> 126 MB L2 "
+           "(no flush needed)", "parallelism": f"replicas x{world} (queries sharded, no "
+           "collective on the data path)"}
+    return {"value": value, "ms": ms, "roofline": roofline, "e2e": e2e, "config": cfg,
+            "launches": launches, "clocks": clk.summary(), "dtype": "f64",
+            "scaling": "weak", "avg_launch_ms": avg_launch_ms}
+
+
+def load_traffic(n):
+    """DRAM bytes per launch for the stream kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            per_pred = float(json.load(fh)["k_interp_stream"]["dram_bytes_per_prediction"])
+        return round(per_pred * n)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------
+# our arm: lattice workload (config 5)
+# ----------------------------------------------------------------------------------------
+
+
+def run_lattice(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2505_01968_b200 import PerfTableSet, _lib
+    dev = torch.device("cuda", local)
+    nfn = args.functions
+    tables = make_config5_tables(nfn, seed=0, device=local)
+    allowed = list(range(1, 33))
+    tset = PerfTableSet([(t, allowed) for t in tables], quota_step=1)
+    f0, f1 = rank * nfn // world, (rank + 1) * nfn // world
+    targets = torch.tensor([0.5 * max_lattice_rps(t) for t in tables], dtype=torch.float64,
+                           device=dev)
+    per = (nfn + world - 1) // world
+    local_out = torch.full((per, 3), -1, dtype=torch.int32, device=dev)
+    gathered = torch.empty((per * world, 3), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        tset.search_dev(targets, local_out, fn_begin=f0, fn_end=f1, stream=stream.cuda_stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, local_out)
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    launches0 = _lib.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    barrier(world)
+    ms = max_over_ranks(start.elapsed_time(end), world)
+    points = tset.points
+    value = points * args.steps / (ms / 1000.0)
+    cfg = {"workload": f"config5: {nfn} functions x 32 batches x 100 sm x 100 quota lattice "
+           "(most_efficient_config, target 0.5 x max rps), tables 6x100x10",
+           "points_per_step": points, "parallelism": f"functions sharded x{world}, NCCL "
+           "all-gather of decisions"}
+    return {"value": value, "ms": ms, "roofline": None, "e2e": None, "config": cfg,
+            "launches": launches, "clocks": clk.summary(), "dtype": "f64",
+            "scaling": "strong"}
+
+
+# ----------------------------------------------------------------------------------------
+# CPU baseline / reference arm: the reference's own compiled kernel on all host cores
+# ----------------------------------------------------------------------------------------
+
+_W = {}
+
+
+def _worker_init(rows, seed):
+    from oracle.binding import load_oracle, load_reference_kernel
+    ref = load_reference_kernel()
+    if ref is not None:
+        fn, kind = ref.interp3_many, "reference"
+    else:
+        from oracle.binding import or_interp3_many
+
+        def fn(b, s, q, v, c, out):
+            out[:] = or_interp3_many(b, s, q, v, c)
+        load_oracle()
+        kind = "port"
+    arrays = config2_arrays()
+    rng = np.random.default_rng(seed + os.getpid())
+    work = []
+    for _, b, s, q, v in arrays:
+        c = np.column_stack([rng.uniform(b[0], b[-1], rows), rng.uniform(s[0], s[-1], rows),
+                             rng.uniform(q[0], q[-1], rows)])
+        work.append((b, s, q, v, np.ascontiguousarray(c), np.empty(rows)))
+    _W.update(fn=fn, kind=kind, work=work)
+
+
+def _worker_run(_):
+    for b, s, q, v, c, out in _W["work"]:
+        _W["fn"](b, s, q, v, c, out)
+    return _W["kind"]
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference(steps, warmup, rows_per_model=250_000, procs=None):
+    """Times the reference kernel over a process pool; returns (predictions/s, info)."""
+    import multiprocessing as mp
+    procs = procs or host_cores()
+    ctx = mp.get_context("spawn")  # the parent holds a CUDA context: never fork it
+    with ctx.Pool(procs, initializer=_worker_init, initargs=(rows_per_model, 12345)) as pool:
+        kinds = pool.map(_worker_run, range(procs))
+        for _ in range(max(0, warmup - 1)):
+            pool.map(_worker_run, range(procs))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pool.map(_worker_run, range(procs))
+        dt = time.perf_counter() - t0
+    preds = steps * procs * len(MODELS) * rows_per_model
+    kind = kinds[0]
+    sample = (f"{len(MODELS)} config-2 tables x {rows_per_model} random queries per process "
+              f"per step, {procs} processes, {steps} steps ({preds} predictions, {dt:.2f} s)")
+    return preds / dt, {"kind": kind, "cores": procs, "sample": sample}
+
+
+# ----------------------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["stream", "lattice"], default="stream")
+    ap.add_argument("--queries", type=int, default=QUERIES_PER_MODEL)
+    ap.add_argument("--functions", type=int, default=3125)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        value, info = cpu_reference(args.steps, args.warmup)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+                "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "config2 4-model sweep (bounded CPU sample per step)",
+                           "parallelism": f"{info['cores']} host processes"},
+                "cpu_baseline": {"value": value, "unit": UNIT, **info},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    rank, world, local = dist_init(args.gpus)
+    res = (run_stream if args.workload == "stream" else run_lattice)(args, rank, world, local)
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and args.workload == "stream":
+        v, info = cpu_reference(steps=3, warmup=1)
+        cpu = {"value": v, "unit": UNIT, **info}
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
+            "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None,
+            "dtype": res["dtype"], "data": "synthetic", "config": res["config"],
+            "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
+            "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours"}
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

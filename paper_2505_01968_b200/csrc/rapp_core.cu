@@ -1,0 +1,492 @@
+// Contexts, the device table pool, the stream-interpolation kernel (K2) and the
+// reference-shaped stateless entry points (locate / interp3 / interp3_many).
+//
+// Reference: hs/_kernels/_grid_cy.pyx (paths relative to /root/reference/pkg/src/hybridscale).
+#include <cstdarg>
+#include <cstring>
+#include <memory>
+
+#include "rapp_device.cuh"
+#include "rapp_internal.h"
+
+namespace rapp {
+
+static thread_local char t_err[1024] = "";
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof t_err, fmt, ap);
+  va_end(ap);
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: stream interpolation, interp3_many semantics (_grid_cy.pyx:67-74).
+// coords (n,3) row-major -> out[n]; optional rps[n] = b / (lat / 1000.0).
+// SMEM=true: the whole table segment is bulk-copied to shared memory first.
+// Each thread handles kIlp rows per grid-stride step so the coordinate loads of several
+// rows are in flight together.
+// ---------------------------------------------------------------------------------------
+constexpr int kThreads = 256;
+constexpr int kIlp = 4;
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads)
+    k_interp_stream(const TableDesc td, const double* __restrict__ pool,
+                    const double* __restrict__ coords, int64_t n, double* __restrict__ out,
+                    double* __restrict__ rps) {
+  extern __shared__ __align__(16) double s_tab[];
+  __shared__ uint64_t bar;
+  const double* seg = pool + td.off;
+  if (SMEM) {
+    bulk_load_table(s_tab, seg, uint32_t(td.seg_doubles) * 8u, &bar);
+    seg = s_tab;
+  }
+  const double* __restrict__ ba = seg + td.ob;
+  const double* __restrict__ sa = seg + td.os;
+  const double* __restrict__ qa = seg + td.oq;
+  const double* __restrict__ v = seg + td.ov;
+  const int64_t stride = int64_t(gridDim.x) * kThreads * kIlp;
+  for (int64_t base = int64_t(blockIdx.x) * kThreads * kIlp + threadIdx.x; base < n;
+       base += stride) {
+    double cb[kIlp], cs[kIlp], cq[kIlp];
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const int64_t i = base + int64_t(k) * kThreads;
+      if (i < n) {
+        cb[k] = __ldcs(coords + 3 * i);
+        cs[k] = __ldcs(coords + 3 * i + 1);
+        cq[k] = __ldcs(coords + 3 * i + 2);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const int64_t i = base + int64_t(k) * kThreads;
+      if (i < n) {
+        const double lat = interp3(ba, td.nb, sa, td.ns, qa, td.nq, v, cb[k], cs[k], cq[k]);
+        __stcs(out + i, lat);
+        if (rps != nullptr) __stcs(rps + i, throughput(cb[k], lat));
+      }
+    }
+  }
+}
+
+// Scalar entry points run as one-thread kernels: slow per call but they keep every
+// prediction on the device path (there is no CPU fallback in the product).
+__global__ void k_locate1(const double* axis, int n, double x, int64_t* out_i, double* out_t) {
+  int lo, hi;
+  double t;
+  locate(axis, n, x, lo, hi, t);
+  out_i[0] = lo;
+  out_i[1] = hi;
+  out_t[0] = t;
+}
+
+constexpr int64_t kSmemTableLimit = 96 * 1024;  // bytes; leaves room for 2 CTAs per SM
+
+int launch_interp(rapp_ctx* ctx, int32_t table_id, const double* d_coords, int64_t n,
+                  double* d_out, double* d_rps, cudaStream_t st) {
+  if (table_id < 0 || table_id >= (int32_t)ctx->tables.size()) {
+    set_error("unknown table id %d", table_id);
+    return RAPP_E_ARG;
+  }
+  if (n <= 0) return RAPP_OK;
+  const TableDesc td = ctx->tables[table_id];
+  const int64_t seg_bytes = int64_t(td.seg_doubles) * 8;
+  const int64_t per_block = int64_t(kThreads) * kIlp;
+  int64_t blocks = (n + per_block - 1) / per_block;
+  if (seg_bytes <= kSmemTableLimit) {
+    const int64_t cap = int64_t(ctx->sm_count) * 8;
+    if (blocks > cap) blocks = cap;
+    if (!ctx->interp_attr_set) {
+      RAPP_CUDA(cudaFuncSetAttribute(k_interp_stream<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemTableLimit));
+      ctx->interp_attr_set = true;
+    }
+    k_interp_stream<true><<<(unsigned)blocks, kThreads, (size_t)seg_bytes, st>>>(
+        td, ctx->d_pool, d_coords, n, d_out, d_rps);
+  } else {
+    const int64_t cap = int64_t(ctx->sm_count) * 16;
+    if (blocks > cap) blocks = cap;
+    k_interp_stream<false><<<(unsigned)blocks, kThreads, 0, st>>>(td, ctx->d_pool, d_coords,
+                                                                   n, d_out, d_rps);
+  }
+  RAPP_LAUNCHED();
+  return RAPP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Table pool
+// ---------------------------------------------------------------------------------------
+static bool strictly_ascending(const double* a, int64_t n) {
+  for (int64_t i = 1; i < n; ++i)
+    if (!(a[i - 1] < a[i])) return false;
+  return true;
+}
+
+int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b,
+              const double* s, const double* q, const double* v, bool scratch, int32_t* id) {
+  if (nb < 1 || ns < 1 || nq < 1) {
+    set_error("empty table");  // hs/perf.py:86-87 "empty table"
+    return RAPP_E_TABLE;
+  }
+  if (nb > (1 << 20) || ns > (1 << 20) || nq > (1 << 20) || nb * ns * nq > (int64_t(1) << 31)) {
+    set_error("table too large (%lld x %lld x %lld)", (long long)nb, (long long)ns,
+              (long long)nq);
+    return RAPP_E_ARG;
+  }
+  TableDesc td{};
+  td.nb = (int32_t)nb;
+  td.ns = (int32_t)ns;
+  td.nq = (int32_t)nq;
+  td.ob = 0;
+  td.os = td.ob + pad2(nb);
+  td.oq = td.os + pad2(ns);
+  td.ov = td.oq + pad2(nq);
+  td.seg_doubles = td.ov + pad2(nb * ns * nq);
+  td.sm_keyable = 1;
+  for (int64_t i = 0; i < ns; ++i)
+    if (!(s[i] >= 0.0 && s[i] < 16777216.0 && s[i] == (double)(int64_t)s[i])) td.sm_keyable = 0;
+  std::vector<double> seg((size_t)td.seg_doubles, 0.0);
+  memcpy(seg.data() + td.ob, b, sizeof(double) * nb);
+  memcpy(seg.data() + td.os, s, sizeof(double) * ns);
+  memcpy(seg.data() + td.oq, q, sizeof(double) * nq);
+  memcpy(seg.data() + td.ov, v, sizeof(double) * nb * ns * nq);
+
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  int32_t slot;
+  if (scratch && ctx->scratch_table >= 0 && ctx->scratch_cap >= td.seg_doubles) {
+    slot = ctx->scratch_table;  // reuse the scratch segment in place
+    td.off = ctx->tables[slot].off;
+  } else {
+    const int64_t need = ctx->pool_used + td.seg_doubles;
+    if (need > ctx->pool_cap) {
+      int64_t cap = ctx->pool_cap ? ctx->pool_cap : (1 << 16);
+      while (cap < need) cap *= 2;
+      double* np = nullptr;
+      RAPP_CUDA(cudaMalloc(&np, (size_t)cap * 8));
+      if (ctx->pool_used) {
+        RAPP_CUDA(cudaDeviceSynchronize());  // no kernel may still read the old pool
+        RAPP_CUDA(cudaMemcpy(np, ctx->d_pool, (size_t)ctx->pool_used * 8,
+                             cudaMemcpyDeviceToDevice));
+      }
+      if (ctx->d_pool) RAPP_CUDA(cudaFree(ctx->d_pool));
+      ctx->d_pool = np;
+      ctx->pool_cap = cap;
+    }
+    td.off = ctx->pool_used;
+    ctx->pool_used += td.seg_doubles;
+    slot = (int32_t)ctx->tables.size();
+    ctx->tables.push_back(td);
+    if (scratch) {
+      ctx->scratch_table = slot;
+      ctx->scratch_cap = td.seg_doubles;
+    }
+  }
+  ctx->tables[slot] = td;
+  RAPP_CUDA(cudaMemcpy(ctx->d_pool + td.off, seg.data(), seg.size() * 8,
+                       cudaMemcpyHostToDevice));
+  if ((int64_t)ctx->tables.size() > ctx->desc_cap) {
+    int64_t cap = ctx->desc_cap ? ctx->desc_cap * 2 : 256;
+    while (cap < (int64_t)ctx->tables.size()) cap *= 2;
+    if (ctx->d_desc) {
+      RAPP_CUDA(cudaDeviceSynchronize());
+      RAPP_CUDA(cudaFree(ctx->d_desc));
+    }
+    RAPP_CUDA(cudaMalloc(&ctx->d_desc, (size_t)cap * sizeof(TableDesc)));
+    ctx->desc_cap = cap;
+    RAPP_CUDA(cudaMemcpy(ctx->d_desc, ctx->tables.data(),
+                         ctx->tables.size() * sizeof(TableDesc), cudaMemcpyHostToDevice));
+  } else {
+    RAPP_CUDA(cudaMemcpy(ctx->d_desc + slot, &td, sizeof(TableDesc), cudaMemcpyHostToDevice));
+  }
+  *id = slot;
+  return RAPP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Host pipeline: chunked copy-in / kernel / copy-out over kDepth streams.
+// ---------------------------------------------------------------------------------------
+int ensure_pipe(rapp_ctx* ctx, int64_t rows) {
+  HostPipe& p = ctx->pipe;
+  if (p.rows >= rows) return RAPP_OK;
+  for (int k = 0; k < HostPipe::kDepth; ++k) {
+    if (!p.stream[k]) {
+      RAPP_CUDA(cudaStreamCreateWithFlags(&p.stream[k], cudaStreamNonBlocking));
+      RAPP_CUDA(cudaEventCreateWithFlags(&p.done[k], cudaEventDisableTiming));
+    }
+    if (p.h_in[k]) RAPP_CUDA(cudaFreeHost(p.h_in[k]));
+    if (p.h_out[k]) RAPP_CUDA(cudaFreeHost(p.h_out[k]));
+    if (p.d_in[k]) RAPP_CUDA(cudaFree(p.d_in[k]));
+    if (p.d_out[k]) RAPP_CUDA(cudaFree(p.d_out[k]));
+    RAPP_CUDA(cudaMallocHost(&p.h_in[k], (size_t)rows * 24));
+    RAPP_CUDA(cudaMallocHost(&p.h_out[k], (size_t)rows * 8));
+    RAPP_CUDA(cudaMalloc(&p.d_in[k], (size_t)rows * 24));
+    RAPP_CUDA(cudaMalloc(&p.d_out[k], (size_t)rows * 8));
+  }
+  p.rows = rows;
+  return RAPP_OK;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static int interp_host(rapp_ctx* ctx, int32_t table_id, const double* coords, int64_t n,
+                       double* out) {
+  if (n <= 0) return RAPP_OK;
+  constexpr int64_t kChunk = int64_t(1) << 21;  // rows per stage (48 MiB in, 16 MiB out)
+  const int64_t chunk = n < kChunk ? n : kChunk;
+  int rc = ensure_pipe(ctx, chunk);
+  if (rc) return rc;
+  HostPipe& p = ctx->pipe;
+  const bool pin_in = is_pinned(coords), pin_out = is_pinned(out);
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  // pending host copy-out for pageable `out`: (chunk index) per stage
+  int64_t pending[HostPipe::kDepth];
+  for (int k = 0; k < HostPipe::kDepth; ++k) pending[k] = -1;
+  auto drain = [&](int k) -> int {
+    if (pending[k] < 0) return RAPP_OK;
+    RAPP_CUDA(cudaEventSynchronize(p.done[k]));
+    if (!pin_out) {
+      const int64_t c = pending[k];
+      const int64_t r0 = c * chunk, rn = (n - r0) < chunk ? (n - r0) : chunk;
+      memcpy(out + r0, p.h_out[k], (size_t)rn * 8);
+    }
+    pending[k] = -1;
+    return RAPP_OK;
+  };
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int k = int(c % HostPipe::kDepth);
+    if ((rc = drain(k))) return rc;
+    const int64_t r0 = c * chunk, rn = (n - r0) < chunk ? (n - r0) : chunk;
+    cudaStream_t st = p.stream[k];
+    const double* src = coords + 3 * r0;
+    if (!pin_in) {
+      memcpy(p.h_in[k], src, (size_t)rn * 24);
+      src = p.h_in[k];
+    }
+    RAPP_CUDA(cudaMemcpyAsync(p.d_in[k], src, (size_t)rn * 24, cudaMemcpyHostToDevice, st));
+    if ((rc = launch_interp(ctx, table_id, p.d_in[k], rn, p.d_out[k], nullptr, st))) return rc;
+    double* dst = pin_out ? out + r0 : p.h_out[k];
+    RAPP_CUDA(cudaMemcpyAsync(dst, p.d_out[k], (size_t)rn * 8, cudaMemcpyDeviceToHost, st));
+    RAPP_CUDA(cudaEventRecord(p.done[k], st));
+    pending[k] = c;
+  }
+  for (int k = 0; k < HostPipe::kDepth; ++k)
+    if ((rc = drain(k))) return rc;
+  return RAPP_OK;
+}
+
+static std::mutex g_default_mu;
+static rapp_ctx* g_default[64] = {};
+
+int default_ctx(rapp_ctx** out) {
+  int dev = 0;
+  RAPP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_default_mu);
+  if (dev < 0 || dev >= 64) {
+    set_error("device %d out of range", dev);
+    return RAPP_E_ARG;
+  }
+  if (!g_default[dev]) {
+    rapp_ctx* c = nullptr;
+    int rc = rapp_ctx_create(dev, &c);
+    if (rc) return rc;
+    g_default[dev] = c;
+  }
+  *out = g_default[dev];
+  return RAPP_OK;
+}
+
+}  // namespace rapp
+
+using namespace rapp;
+
+extern "C" {
+
+const char* rapp_last_error(void) { return t_err; }
+
+const char* rapp_version(void) { return "rapp_b200 0.1 (sm_100a, fp64 no-FMA)"; }
+
+int64_t rapp_launch_count(void) { return g_launches.load(); }
+
+int rapp_ctx_create(int device, rapp_ctx** out) {
+  if (!out) {
+    set_error("null output pointer");
+    return RAPP_E_ARG;
+  }
+  int ndev = 0;
+  RAPP_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("device %d not present (%d visible)", device, ndev);
+    return RAPP_E_ARG;
+  }
+  RAPP_CUDA(cudaSetDevice(device));
+  std::unique_ptr<rapp_ctx> c(new rapp_ctx());
+  c->device = device;
+  RAPP_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  RAPP_CUDA(cudaMalloc(&c->d_small, 64 * sizeof(double)));
+  *out = c.release();
+  return RAPP_OK;
+}
+
+int rapp_ctx_destroy(rapp_ctx* ctx) {
+  if (!ctx) return RAPP_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  HostPipe& p = ctx->pipe;
+  for (int k = 0; k < HostPipe::kDepth; ++k) {
+    if (p.stream[k]) cudaStreamDestroy(p.stream[k]);
+    if (p.done[k]) cudaEventDestroy(p.done[k]);
+    if (p.h_in[k]) cudaFreeHost(p.h_in[k]);
+    if (p.h_out[k]) cudaFreeHost(p.h_out[k]);
+    if (p.d_in[k]) cudaFree(p.d_in[k]);
+    if (p.d_out[k]) cudaFree(p.d_out[k]);
+  }
+  if (ctx->d_pool) cudaFree(ctx->d_pool);
+  if (ctx->d_desc) cudaFree(ctx->d_desc);
+  if (ctx->d_small) cudaFree(ctx->d_small);
+  {
+    std::lock_guard<std::mutex> lk(g_default_mu);
+    for (auto& d : g_default)
+      if (d == ctx) d = nullptr;
+  }
+  delete ctx;
+  return RAPP_OK;
+}
+
+int rapp_ctx_info(rapp_ctx* ctx, int* device, int* sm_count) {
+  if (!ctx) {
+    set_error("null context");
+    return RAPP_E_ARG;
+  }
+  if (device) *device = ctx->device;
+  if (sm_count) *sm_count = ctx->sm_count;
+  return RAPP_OK;
+}
+
+int rapp_table_create(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b_axis,
+                      const double* s_axis, const double* q_axis, const double* values,
+                      int32_t* table_id) {
+  if (!ctx || !table_id) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  if (nb >= 1 && ns >= 1 && nq >= 1 &&
+      (!strictly_ascending(b_axis, nb) || !strictly_ascending(s_axis, ns) ||
+       !strictly_ascending(q_axis, nq))) {
+    set_error("table axes must be strictly ascending");
+    return RAPP_E_TABLE;
+  }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return table_put(ctx, nb, ns, nq, b_axis, s_axis, q_axis, values, false, table_id);
+}
+
+int rapp_table_count(rapp_ctx* ctx, int32_t* count) {
+  if (!ctx || !count) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  *count = (int32_t)ctx->tables.size();
+  return RAPP_OK;
+}
+
+int rapp_interp3_many_dev(rapp_ctx* ctx, int32_t table_id, const double* d_coords, int64_t n,
+                          double* d_out, double* d_rps, void* stream) {
+  if (!ctx) {
+    set_error("null context");
+    return RAPP_E_ARG;
+  }
+  if (n < 0) {
+    set_error("negative row count");
+    return RAPP_E_ARG;
+  }
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  return launch_interp(ctx, table_id, d_coords, n, d_out, d_rps, (cudaStream_t)stream);
+}
+
+int rapp_interp3_many_host(rapp_ctx* ctx, int32_t table_id, const double* coords, int64_t n,
+                           double* out) {
+  if (!ctx) {
+    set_error("null context");
+    return RAPP_E_ARG;
+  }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  return interp_host(ctx, table_id, coords, n, out);
+}
+
+int rapp_locate(const double* axis, int64_t n, double x, int64_t* lo, int64_t* hi, double* t) {
+  if (n < 1) {
+    // the reference indexes axis[0] and raises IndexError on an empty axis
+    set_error("locate on an empty axis");
+    return RAPP_E_ARG;
+  }
+  rapp_ctx* ctx = nullptr;
+  int rc = default_ctx(&ctx);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  double* d_axis = nullptr;
+  RAPP_CUDA(cudaMalloc(&d_axis, (size_t)n * 8));
+  RAPP_CUDA(cudaMemcpy(d_axis, axis, (size_t)n * 8, cudaMemcpyHostToDevice));
+  int64_t* d_i = reinterpret_cast<int64_t*>(ctx->d_small);
+  k_locate1<<<1, 1>>>(d_axis, (int)n, x, d_i, ctx->d_small + 2);
+  g_launches.fetch_add(1);
+  int64_t hv[2];
+  double tv;
+  cudaError_t e1 = cudaMemcpy(hv, d_i, sizeof hv, cudaMemcpyDeviceToHost);
+  cudaError_t e2 = cudaMemcpy(&tv, ctx->d_small + 2, sizeof tv, cudaMemcpyDeviceToHost);
+  cudaFree(d_axis);
+  RAPP_CUDA(e1);
+  RAPP_CUDA(e2);
+  *lo = hv[0];
+  *hi = hv[1];
+  *t = tv;
+  return RAPP_OK;
+}
+
+static int stateless_table(rapp_ctx* ctx, const double* b_axis, int64_t nb, const double* s_axis,
+                           int64_t ns, const double* q_axis, int64_t nq, const double* values,
+                           int32_t* id) {
+  // The reference kernel accepts any ascending axes without validation; so does this
+  // entry point (no strictness check), matching _grid_cy.pyx's raw-buffer contract.
+  return table_put(ctx, nb, ns, nq, b_axis, s_axis, q_axis, values, true, id);
+}
+
+int rapp_interp3(const double* b_axis, int64_t nb, const double* s_axis, int64_t ns,
+                 const double* q_axis, int64_t nq, const double* values, double b, double s,
+                 double q, double* out) {
+  rapp_ctx* ctx = nullptr;
+  int rc = default_ctx(&ctx);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  int32_t id;
+  if ((rc = stateless_table(ctx, b_axis, nb, s_axis, ns, q_axis, nq, values, &id))) return rc;
+  double h[3] = {b, s, q};
+  RAPP_CUDA(cudaMemcpy(ctx->d_small, h, sizeof h, cudaMemcpyHostToDevice));
+  if ((rc = launch_interp(ctx, id, ctx->d_small, 1, ctx->d_small + 4, nullptr, 0))) return rc;
+  RAPP_CUDA(cudaMemcpy(out, ctx->d_small + 4, sizeof(double), cudaMemcpyDeviceToHost));
+  return RAPP_OK;
+}
+
+int rapp_interp3_many(const double* b_axis, int64_t nb, const double* s_axis, int64_t ns,
+                      const double* q_axis, int64_t nq, const double* values,
+                      const double* coords, int64_t n, double* out) {
+  rapp_ctx* ctx = nullptr;
+  int rc = default_ctx(&ctx);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  int32_t id;
+  if ((rc = stateless_table(ctx, b_axis, nb, s_axis, ns, q_axis, nq, values, &id))) return rc;
+  return interp_host(ctx, id, coords, n, out);
+}
+
+}  // extern "C"

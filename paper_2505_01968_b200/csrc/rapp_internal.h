@@ -1,0 +1,97 @@
+// Host-side internals shared by the library's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rapp_b200.h"
+
+namespace rapp {
+
+// Thread-local error message behind rapp_last_error().
+void set_error(const char* fmt, ...);
+extern std::atomic<int64_t> g_launches;
+
+#define RAPP_CUDA(expr)                                                                   \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      ::rapp::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__,     \
+                        __LINE__, cudaGetErrorString(_e));                                \
+      return RAPP_E_CUDA;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+#define RAPP_LAUNCHED()                                                                   \
+  do {                                                                                    \
+    ::rapp::g_launches.fetch_add(1, std::memory_order_relaxed);                           \
+    cudaError_t _e = cudaGetLastError();                                                  \
+    if (_e != cudaSuccess) {                                                              \
+      ::rapp::set_error("kernel launch failed at %s:%d: %s", __FILE__, __LINE__,          \
+                        cudaGetErrorString(_e));                                          \
+      return RAPP_E_CUDA;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+// One immutable table inside the context's device pool.  Offsets are in doubles and
+// even (16-byte aligned) so a table segment can be moved with one bulk copy:
+//   [b_axis | pad][s_axis | pad][q_axis | pad][values | pad]
+struct TableDesc {
+  int32_t nb, ns, nq;
+  int32_t seg_doubles;  // length of the whole segment (even)
+  int64_t off;          // segment start in the pool
+  int32_t ob, os, oq, ov;  // axis/value offsets relative to the segment start
+  int32_t sm_keyable;       // sm axis integral in [0, 2^24): usable in packed search keys
+};
+
+inline int32_t pad2(int64_t n) { return int32_t((n + 1) & ~int64_t(1)); }
+
+// Host pipeline resources for host-pointer entry points.
+struct HostPipe {
+  static constexpr int kDepth = 3;
+  cudaStream_t stream[kDepth] = {};
+  cudaEvent_t done[kDepth] = {};
+  double* h_in[kDepth] = {};
+  double* h_out[kDepth] = {};
+  double* d_in[kDepth] = {};
+  double* d_out[kDepth] = {};
+  int64_t rows = 0;  // capacity per stage (rows of 3 doubles in, 1 double out)
+};
+
+}  // namespace rapp
+
+struct rapp_ctx {
+  int device = 0;
+  int sm_count = 0;
+  std::mutex mu;
+  std::vector<rapp::TableDesc> tables;  // host mirror of d_desc
+  double* d_pool = nullptr;
+  int64_t pool_cap = 0, pool_used = 0;  // doubles
+  rapp::TableDesc* d_desc = nullptr;
+  int64_t desc_cap = 0;
+  // scratch table for the stateless reference-shaped entry points
+  int32_t scratch_table = -1;
+  int32_t scratch_cap = 0;  // reserved doubles of the scratch segment
+  bool interp_attr_set = false;
+  rapp::HostPipe pipe;
+  double* d_small = nullptr;  // 64 doubles of scratch for scalar calls
+};
+
+namespace rapp {
+// Appends a table to the pool (or overwrites the scratch slot when scratch == true).
+int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b,
+              const double* s, const double* q, const double* v, bool scratch,
+              int32_t* id);
+// The per-device default context used by the stateless entry points.
+int default_ctx(rapp_ctx** out);
+int ensure_pipe(rapp_ctx* ctx, int64_t rows);
+// Launches the stream-interpolation kernel for one table.
+int launch_interp(rapp_ctx* ctx, int32_t table_id, const double* d_coords, int64_t n,
+                  double* d_out, double* d_rps, cudaStream_t st);
+}  // namespace rapp

@@ -1,0 +1,144 @@
+"""K2 stream interpolation on the B200 vs the reference's golden vectors and the oracle
+(0-ulp).  Mirrors pkg/tests/test_kernels.py and the interpolation half of test_perf.py."""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+from oracle.binding import or_interp3_many, or_locate, or_throughput
+
+from .conftest import fromhex, golden_table_arrays, same_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kern():
+    from paper_2505_01968_b200 import kernels
+    return kernels
+
+
+def test_golden_vectors_bit_exact(kern, interp_golden):
+    for rec in interp_golden["tables"]:
+        b, s, q, v = golden_table_arrays(rec["table"])
+        coords = fromhex(rec["coords"]).reshape(-1, 3)
+        out = np.empty(len(coords))
+        kern.interp3_many(b, s, q, v, coords, out)
+        assert same_bits(out, fromhex(rec["latency"])), rec["table"]["function_id"]
+
+
+def test_locate_golden(kern, interp_golden):
+    for rec in interp_golden["locate"]:
+        lo, hi, t = kern.locate(fromhex(rec["axis"]), float.fromhex(rec["x"]))
+        want = float.fromhex(rec["t"])
+        assert (lo, hi) == (rec["lo"], rec["hi"])
+        assert (math.isnan(t) and math.isnan(want)) or t == want
+
+
+def _grid():
+    # pkg/tests/test_kernels.py:12-19
+    b = np.array([1.0, 2.0, 4.0, 8.0])
+    s = np.array([25.0, 50.0, 75.0, 100.0])
+    q = np.array([10.0, 40.0, 70.0, 100.0])
+    rng = random.Random(7)
+    v = np.array([[[10.0 + 5 * bi + 2 * (3 - si) + (3 - qi) + rng.random()
+                    for qi in range(4)] for si in range(4)] for bi in range(4)])
+    return b, s, q, np.ascontiguousarray(v)
+
+
+def test_exact_at_every_node(kern):
+    b, s, q, v = _grid()
+    for bi, bv in enumerate(b):
+        for si, sv in enumerate(s):
+            for qi, qv in enumerate(q):
+                assert kern.interp3(b, s, q, v, bv, sv, qv) == v[bi, si, qi]
+
+
+def test_quota_midpoint_and_clamps(kern):
+    assert kern.interp3(np.array([1.0]), np.array([50.0]), np.array([20.0, 40.0]),
+                        np.array([[[20.0, 30.0]]]), 1.0, 50.0, 30.0) == 25.0
+    b, s, q, v = _grid()
+    assert kern.interp3(b, s, q, v, 1.0, 5.0, 50.0) == kern.interp3(b, s, q, v, 1.0, 25.0, 50.0)
+    assert kern.interp3(b, s, q, v, 1.0, 50.0, 300.0) == kern.interp3(b, s, q, v, 1.0, 50.0, 100.0)
+
+
+@pytest.mark.parametrize("shape", [(4, 4, 10), (6, 10, 10), (6, 100, 100), (1, 1, 1),
+                                   (1, 3, 2), (32, 91, 100)])
+def test_random_coords_match_oracle(kern, shape):
+    nb, ns, nq = shape
+    rng = np.random.default_rng(sum(shape))
+    b = np.cumsum(rng.uniform(0.5, 3, nb))
+    s = np.cumsum(rng.uniform(0.5, 3, ns))
+    q = np.cumsum(rng.uniform(0.5, 3, nq))
+    v = np.ascontiguousarray(rng.uniform(1, 1000, shape))
+    n = 200_003
+    c = np.column_stack([rng.uniform(b[0] - 1, b[-1] + 1, n), rng.uniform(s[0] - 1, s[-1] + 1, n),
+                         rng.uniform(q[0] - 1, q[-1] + 1, n)])
+    c[::5, 0] = rng.choice(b, len(c[::5]))
+    c[1::5, 1] = rng.choice(s, len(c[1::5]))
+    c[2::5, 2] = rng.choice(q, len(c[2::5]))
+    c[3] = [np.nan, s[0], q[0]]
+    out = np.empty(n)
+    kern.interp3_many(b, s, q, v, c, out)
+    assert same_bits(out, or_interp3_many(b, s, q, v, c))
+
+
+def test_empty_and_pinned_multi_chunk(kern):
+    import torch
+    b, s, q, v = _grid()
+    out = np.empty(0)
+    kern.interp3_many(b, s, q, v, np.empty((0, 3)), out)
+    n = (1 << 21) * 2 + 12345  # three pipeline chunks
+    rng = np.random.default_rng(3)
+    c = np.column_stack([rng.uniform(0, 9, n), rng.uniform(20, 105, n), rng.uniform(5, 105, n)])
+    want = or_interp3_many(b, s, q, v, c)
+    got = np.empty(n)
+    kern.interp3_many(b, s, q, v, c, got)  # pageable path
+    assert same_bits(got, want)
+    pc = torch.from_numpy(c).pin_memory()
+    po = torch.empty(n, dtype=torch.float64).pin_memory()
+    kern.interp3_many(b, s, q, v, pc.numpy(), po.numpy())  # pinned DMA path
+    assert same_bits(po.numpy(), want)
+
+
+def test_perftable_device_api_latency_and_rps():
+    import torch
+    from paper_2505_01968_b200 import PerfTable
+    rng = np.random.default_rng(11)
+    lat = np.sort(rng.uniform(1, 50, (6, 10, 10)), axis=0)[:, ::-1, ::-1].copy()
+    lat = np.maximum.accumulate(lat, axis=0)
+    lat = np.minimum.accumulate(lat, axis=1)
+    lat = np.minimum.accumulate(lat, axis=2)
+    t = PerfTable("f", [1, 2, 4, 8, 16, 32], list(range(10, 101, 10)), list(range(10, 101, 10)),
+                  np.ascontiguousarray(lat))
+    n = 100_000
+    c = np.column_stack([rng.integers(1, 33, n).astype(float), rng.integers(1, 101, n).astype(float),
+                         rng.integers(1, 101, n).astype(float)])
+    dc = torch.from_numpy(c).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    rps = torch.empty_like(out)
+    t.predict_latency_many(dc, out, rps)
+    want = or_interp3_many(t._b_axis, t._s_axis, t._q_axis, t.latency_ms, c)
+    assert same_bits(out.cpu().numpy(), want)
+    want_rps = np.array([or_throughput(bb, ll) for bb, ll in zip(c[:2000, 0], want[:2000])])
+    assert same_bits(rps.cpu().numpy()[:2000], want_rps)
+    # scalar API + error convention (hs/perf.py:88-91)
+    assert t.predict_latency(8, 50, 50) == want_at(t, 8, 50, 50)
+    assert t.throughput(8, 100, 100) == or_throughput(8, t.latency_ms[3, 9, 9])
+    with pytest.raises(ValueError, match="batch"):
+        t.predict_latency(33, 50, 50)
+
+
+def want_at(t, b, s, q):
+    return or_interp3_many(t._b_axis, t._s_axis, t._q_axis, t.latency_ms,
+                           np.array([[b, s, q]], dtype=float))[0]
+
+
+def test_throughput_definition():
+    from paper_2505_01968_b200 import PerfTable
+    t = PerfTable("fn", [8], [100], [100], np.full((1, 1, 1), 20.0))
+    assert t.throughput(8, 100, 100) == 400.0
+    t1 = PerfTable("fn", [1], [100], [100], np.full((1, 1, 1), 1000.0))
+    assert t1.throughput(1, 100, 100) == 1.0
