@@ -93,6 +93,7 @@ int launch_interp(rapp_ctx* ctx, int32_t table_id, const double* d_coords, int64
   }
   if (n <= 0) return RAPP_OK;
   const TableDesc td = ctx->tables[table_id];
+  if (td.fast && !ctx->force_literal) return launch_interp_fast(ctx, td, d_coords, n, d_out, d_rps, st);
   const int64_t seg_bytes = int64_t(td.seg_doubles) * 8;
   const int64_t per_block = int64_t(kThreads) * kIlp;
   int64_t blocks = (n + per_block - 1) / per_block;
@@ -155,13 +156,31 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
   memcpy(seg.data() + td.oq, q, sizeof(double) * nq);
   memcpy(seg.data() + td.ov, v, sizeof(double) * nb * ns * nq);
 
+  // fast-path extras (bucket tables, pow2 reciprocals, cell layout) for validated axes
+  std::vector<double> ext;
+  td.fast = strictly_ascending(b, nb) && strictly_ascending(s, ns) && strictly_ascending(q, nq);
+  if (td.fast) {
+    FastLayout L{};
+    if (build_fast_extras(nb, ns, nq, b, s, q, v, ext, L) != RAPP_OK) {
+      td.fast = 0;
+      ext.clear();
+    } else {
+      td.x_small = L.small_doubles;
+      td.x_total = L.total_doubles;
+      td.x_inv_b = L.o_inv_b;
+      td.x_inv_s = L.o_inv_s;
+      td.x_inv_q = L.o_inv_q;
+    }
+  }
+  const int64_t total = td.seg_doubles + (int64_t)ext.size();
+
   RAPP_CUDA(cudaSetDevice(ctx->device));
   int32_t slot;
-  if (scratch && ctx->scratch_table >= 0 && ctx->scratch_cap >= td.seg_doubles) {
+  if (scratch && ctx->scratch_table >= 0 && ctx->scratch_cap >= total) {
     slot = ctx->scratch_table;  // reuse the scratch segment in place
     td.off = ctx->tables[slot].off;
   } else {
-    const int64_t need = ctx->pool_used + td.seg_doubles;
+    const int64_t need = ctx->pool_used + total;
     if (need > ctx->pool_cap) {
       int64_t cap = ctx->pool_cap ? ctx->pool_cap : (1 << 16);
       while (cap < need) cap *= 2;
@@ -177,17 +196,21 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
       ctx->pool_cap = cap;
     }
     td.off = ctx->pool_used;
-    ctx->pool_used += td.seg_doubles;
+    ctx->pool_used += total;
     slot = (int32_t)ctx->tables.size();
     ctx->tables.push_back(td);
     if (scratch) {
       ctx->scratch_table = slot;
-      ctx->scratch_cap = td.seg_doubles;
+      ctx->scratch_cap = (int32_t)total;
     }
   }
+  td.xoff = td.off + td.seg_doubles;
   ctx->tables[slot] = td;
   RAPP_CUDA(cudaMemcpy(ctx->d_pool + td.off, seg.data(), seg.size() * 8,
                        cudaMemcpyHostToDevice));
+  if (!ext.empty())
+    RAPP_CUDA(cudaMemcpy(ctx->d_pool + td.xoff, ext.data(), ext.size() * 8,
+                         cudaMemcpyHostToDevice));
   if ((int64_t)ctx->tables.size() > ctx->desc_cap) {
     int64_t cap = ctx->desc_cap ? ctx->desc_cap * 2 : 256;
     while (cap < (int64_t)ctx->tables.size()) cap *= 2;
@@ -332,6 +355,8 @@ int rapp_ctx_create(int device, rapp_ctx** out) {
   RAPP_CUDA(cudaSetDevice(device));
   std::unique_ptr<rapp_ctx> c(new rapp_ctx());
   c->device = device;
+  const char* lit = getenv("RAPP_FORCE_LITERAL");
+  c->force_literal = lit && lit[0] == '1';
   RAPP_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   RAPP_CUDA(cudaMalloc(&c->d_small, 64 * sizeof(double)));
   *out = c.release();

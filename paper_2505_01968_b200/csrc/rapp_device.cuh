@@ -130,4 +130,44 @@ __device__ __forceinline__ void bulk_load_table(double* s_dst, const double* g_s
   }
 }
 
+// Two regions in one transaction (e.g. axes + bucket tables).  Either size may be 0;
+// sizes and addresses must be multiples of 16 bytes.
+__device__ __forceinline__ void bulk_load_2(void* d1, const void* s1, uint32_t n1, void* d2,
+                                            const void* s2, uint32_t n2, uint64_t* bar) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar),
+                 "r"(n1 + n2)
+                 : "memory");
+    constexpr uint32_t kChunk = 65536;
+    const void* srcs[2] = {s1, s2};
+    void* dsts[2] = {d1, d2};
+    const uint32_t ns[2] = {n1, n2};
+    for (int r = 0; r < 2; ++r)
+      for (uint32_t off = 0; off < ns[r]; off += kChunk) {
+        const uint32_t n = ns[r] - off < kChunk ? ns[r] - off : kChunk;
+        const uint32_t sdst = (uint32_t)__cvta_generic_to_shared((char*)dsts[r] + off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+            "%2, [%3];" ::"r"(sdst),
+            "l"((const char*)srcs[r] + off), "r"(n), "r"(sbar)
+            : "memory");
+      }
+  }
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(sbar)
+        : "memory");
+  }
+}
+
 }  // namespace rapp

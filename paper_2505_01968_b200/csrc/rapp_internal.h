@@ -48,6 +48,11 @@ struct TableDesc {
   int64_t off;          // segment start in the pool
   int32_t ob, os, oq, ov;  // axis/value offsets relative to the segment start
   int32_t sm_keyable;       // sm axis integral in [0, 2^24): usable in packed search keys
+  // fast-path extras (rapp_stream.cu), present when fast != 0 (strictly ascending axes)
+  int32_t fast;
+  int32_t x_small, x_total;             // doubles: small part (-> smem), whole extras
+  int32_t x_inv_b, x_inv_s, x_inv_q;    // reciprocal-table offsets inside the extras
+  int64_t xoff;                         // extras start in the pool
 };
 
 inline int32_t pad2(int64_t n) { return int32_t((n + 1) & ~int64_t(1)); }
@@ -79,6 +84,8 @@ struct rapp_ctx {
   int32_t scratch_table = -1;
   int32_t scratch_cap = 0;  // reserved doubles of the scratch segment
   bool interp_attr_set = false;
+  bool fast_attr_set = false;
+  bool force_literal = false;  // RAPP_FORCE_LITERAL=1: always use the literal K2 kernel
   rapp::HostPipe pipe;
   double* d_small = nullptr;  // 64 doubles of scratch for scalar calls
 };
@@ -91,6 +98,16 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
 // The per-device default context used by the stateless entry points.
 int default_ctx(rapp_ctx** out);
 int ensure_pipe(rapp_ctx* ctx, int64_t rows);
+// fast-path extras layout (doubles): [params 3 x 4][lut_b|lut_s|lut_q int32 x 256 each]
+//                                    [inv_b|inv_s|inv_q (pad2(n-1) each)][cells]
+struct FastLayout {
+  int32_t o_par, o_lut, o_inv_b, o_inv_s, o_inv_q, o_cells, small_doubles, total_doubles;
+};
+int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const double* s,
+                      const double* q, const double* v, std::vector<double>& ext,
+                      FastLayout& L);
+int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coords, int64_t n,
+                       double* d_out, double* d_rps, cudaStream_t st);
 // Launches the stream-interpolation kernel for one table.
 int launch_interp(rapp_ctx* ctx, int32_t table_id, const double* d_coords, int64_t n,
                   double* d_out, double* d_rps, cudaStream_t st);

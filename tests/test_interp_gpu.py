@@ -142,3 +142,41 @@ def test_throughput_definition():
     assert t.throughput(8, 100, 100) == 400.0
     t1 = PerfTable("fn", [1], [100], [100], np.full((1, 1, 1), 1000.0))
     assert t1.throughput(1, 100, 100) == 1.0
+
+
+def test_non_strict_axes_use_literal_search(kern):
+    """Duplicate axis values (accepted by the reference's raw kernel) follow the literal
+    binary search, so even its tie behaviour matches (_grid_cy.pyx:20-26)."""
+    b = np.array([1.0, 2.0, 2.0, 2.0, 3.0])
+    s = np.array([10.0, 10.0, 20.0])
+    q = np.array([5.0, 7.0, 7.0, 9.0])
+    rng = np.random.default_rng(1)
+    v = np.ascontiguousarray(rng.uniform(1, 9, (5, 3, 4)))
+    c = np.column_stack([rng.choice([0.5, 1, 1.5, 2, 2.5, 3, 4], 5000),
+                         rng.choice([5, 10, 15, 20, 25], 5000),
+                         rng.choice([4, 5, 6, 7, 8, 9, 10], 5000)]).astype(float)
+    out = np.empty(len(c))
+    kern.interp3_many(b, s, q, v, c, out)
+    assert same_bits(out, or_interp3_many(b, s, q, v, c))
+
+
+def test_literal_kernel_also_bit_exact(interp_golden, tmp_path):
+    """RAPP_FORCE_LITERAL=1 routes every table through the literal-search kernel; it must
+    reproduce the same golden vectors as the fast path."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "from tests.conftest import load_golden, golden_table_arrays, fromhex, same_bits\n"
+        "from paper_2505_01968_b200 import kernels\n"
+        "g = load_golden('interp.json')\n"
+        "for rec in g['tables']:\n"
+        "    b, s, q, v = golden_table_arrays(rec['table'])\n"
+        "    c = fromhex(rec['coords']).reshape(-1, 3); out = np.empty(len(c))\n"
+        "    kernels.interp3_many(b, s, q, v, c, out)\n"
+        "    assert same_bits(out, fromhex(rec['latency']))\n"
+        "print('literal ok')\n") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RAPP_FORCE_LITERAL="1")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert res.returncode == 0 and "literal ok" in res.stdout, res.stderr[-2000:]
