@@ -146,7 +146,9 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
   td.os = td.ob + pad2(nb);
   td.oq = td.os + pad2(ns);
   td.ov = td.oq + pad2(nq);
-  td.seg_doubles = td.ov + pad2(nb * ns * nq);
+  // segments start on 64-byte boundaries so the fast path's 64-byte cells never straddle
+  // a 128-byte line (pool base is 256-byte aligned; every segment length is a multiple of 8)
+  td.seg_doubles = (td.ov + pad2(nb * ns * nq) + 7) & ~7;
   td.sm_keyable = 1;
   for (int64_t i = 0; i < ns; ++i)
     if (!(s[i] >= 0.0 && s[i] < 16777216.0 && s[i] == (double)(int64_t)s[i])) td.sm_keyable = 0;
@@ -167,9 +169,9 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
     } else {
       td.x_small = L.small_doubles;
       td.x_total = L.total_doubles;
-      td.x_inv_b = L.o_inv_b;
-      td.x_inv_s = L.o_inv_s;
-      td.x_inv_q = L.o_inv_q;
+      td.x_iv_b = L.o_iv_b;
+      td.x_iv_s = L.o_iv_s;
+      td.x_iv_q = L.o_iv_q;
     }
   }
   const int64_t total = td.seg_doubles + (int64_t)ext.size();

@@ -51,7 +51,7 @@ struct TableDesc {
   // fast-path extras (rapp_stream.cu), present when fast != 0 (strictly ascending axes)
   int32_t fast;
   int32_t x_small, x_total;             // doubles: small part (-> smem), whole extras
-  int32_t x_inv_b, x_inv_s, x_inv_q;    // reciprocal-table offsets inside the extras
+  int32_t x_iv_b, x_iv_s, x_iv_q;       // interval-table offsets inside the extras
   int64_t xoff;                         // extras start in the pool
 };
 
@@ -98,10 +98,10 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
 // The per-device default context used by the stateless entry points.
 int default_ctx(rapp_ctx** out);
 int ensure_pipe(rapp_ctx* ctx, int64_t rows);
-// fast-path extras layout (doubles): [params 3 x 4][lut_b|lut_s|lut_q int32 x 256 each]
-//                                    [inv_b|inv_s|inv_q (pad2(n-1) each)][cells]
+// fast-path extras layout (doubles, see rapp_stream.cu):
+//   [params 3 x 8][lut_b|lut_s|lut_q int32 x kLut each][iv_b|iv_s|iv_q (2n each)][pad][cells]
 struct FastLayout {
-  int32_t o_par, o_lut, o_inv_b, o_inv_s, o_inv_q, o_cells, small_doubles, total_doubles;
+  int32_t o_par, o_lut, o_iv_b, o_iv_s, o_iv_q, o_cells, small_doubles, total_doubles;
 };
 int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const double* s,
                       const double* q, const double* v, std::vector<double>& ext,

@@ -1,18 +1,24 @@
 // K2 fast path: stream interpolation for validated tables (strictly ascending axes).
 //
 // Same results, bit for bit, as the literal kernel (rapp_core.cu) and the reference
-// (hs/_kernels/_grid_cy.pyx:9-51); three data-layout changes make it cheaper:
-//  1. locate() without a binary search: a per-axis bucket table (LUT, in shared memory)
-//     gives a starting index that is then corrected by exact comparisons, so the bracket
-//     is the unique lo with a[lo] <= x < a[lo+1] — the binary search's answer for a
-//     strictly ascending axis — in 1-3 shared-memory reads instead of log2(n) dependent
-//     global loads.
-//  2. t = (x - a[lo]) / (a[hi] - a[lo]): when the interval width is a power of two the
-//     quotient is computed as an exact multiply by its (exactly representable) reciprocal.
-//     RN(n * 2^-e) == RN(n / 2^e), so this is still the IEEE-correct quotient.  Other
-//     widths use the IEEE division.
-//  3. "cell" layout: the 8 corners of every grid cell are stored contiguously (64 B), so a
-//     query is 4 x 16-byte loads from 2 sectors instead of 8 scattered 8-byte loads.
+// (hs/_kernels/_grid_cy.pyx:9-51).  What changes is how the work is laid out:
+//
+//  1. locate() without a binary search.  For a strictly ascending axis the binary search
+//     returns the unique lo with a[lo] <= x < a[lo+1]; any method that finds that index
+//     exactly is equivalent.  Two per-axis modes, chosen at upload:
+//       UNIFORM  a[k] == a0 + k*h exactly with h a power of two (e.g. sm% / quota% 1..100):
+//                k = floor((x - a0) / h) corrected by one exact comparison — no memory.
+//       LUT      a bucket table in shared memory gives the interval; buckets that lie
+//                (with a one-bucket margin) inside a single interval are flagged exact,
+//                the rest are corrected by exact comparisons.
+//  2. t = (x - a[lo]) / (a[hi] - a[lo]): for a power-of-two width the quotient is an exact
+//     multiply by the (exactly representable) reciprocal: RN(n * 2^-e) == RN(n / 2^e).
+//     Other widths use the IEEE division.
+//  3. "Cell" layout: the 8 corners of each grid cell are stored contiguously (64 B,
+//     64-byte aligned).  Two lanes cooperate on one query: each loads one batch row of the
+//     cell (4 doubles) with a single 256-bit load and does that row's two quota lerps and
+//     its sm lerp; one shuffle exchanges the row values for the batch lerp.  A warp thus
+//     touches 16 lines per load instruction instead of 32 x 4.
 //     Clamped / node-hit brackets (lo == hi) select the same corner twice, exactly as the
 //     reference reads v[lo] twice.
 #include <cmath>
@@ -24,17 +30,18 @@
 
 namespace rapp {
 
-constexpr int kLut = 256;  // buckets per axis
-
+constexpr int kLut = 512;  // buckets per axis (LUT mode)
+constexpr uint32_t kExact = 0x80000000u;
+enum : int { kModeLut = 0, kModeUniform = 1 };
 
 static FastLayout fast_layout(int64_t nb, int64_t ns, int64_t nq) {
   FastLayout L{};
   L.o_par = 0;
-  L.o_lut = 12;
-  L.o_inv_b = L.o_lut + 3 * kLut / 2;
-  L.o_inv_s = L.o_inv_b + pad2(nb > 1 ? nb - 1 : 1);
-  L.o_inv_q = L.o_inv_s + pad2(ns > 1 ? ns - 1 : 1);
-  L.o_cells = L.o_inv_q + pad2(nq > 1 ? nq - 1 : 1);
+  L.o_lut = 24;
+  L.o_iv_b = L.o_lut + 3 * kLut / 2;
+  L.o_iv_s = L.o_iv_b + int32_t(2 * nb);
+  L.o_iv_q = L.o_iv_s + int32_t(2 * ns);
+  L.o_cells = (L.o_iv_q + int32_t(2 * nq) + 7) & ~7;  // 64-byte aligned cells
   L.small_doubles = L.o_cells;
   const int64_t cb = nb > 1 ? nb - 1 : 1, cs = ns > 1 ? ns - 1 : 1, cq = nq > 1 ? nq - 1 : 1;
   L.total_doubles = int32_t(L.o_cells + cb * cs * cq * 8);
@@ -53,6 +60,7 @@ static bool pow2_recip(double d, double* r) {
 }
 
 // Builds the fast-path extras for a strictly ascending table.
+// params per axis (8 doubles): a0, a_last, lut_scale, mode, h, 1/h, n, 0
 int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const double* s,
                       const double* q, const double* v, std::vector<double>& ext,
                       FastLayout& L) {
@@ -60,30 +68,57 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
   if ((int64_t)L.total_doubles > (int64_t(1) << 30)) return RAPP_E_ARG;
   ext.assign((size_t)L.total_doubles, 0.0);
   const double* axes[3] = {b, s, q};
-  const int64_t ns_[3] = {nb, ns, nq};
-  const int32_t o_inv[3] = {L.o_inv_b, L.o_inv_s, L.o_inv_q};
-  int32_t* lut = reinterpret_cast<int32_t*>(ext.data() + L.o_lut);
+  const int64_t lens[3] = {nb, ns, nq};
+  const int32_t o_iv[3] = {L.o_iv_b, L.o_iv_s, L.o_iv_q};
+  uint32_t* lut = reinterpret_cast<uint32_t*>(ext.data() + L.o_lut);
   for (int a = 0; a < 3; ++a) {
     const double* ax = axes[a];
-    const int64_t n = ns_[a];
+    const int64_t n = lens[a];
     const double a0 = ax[0], al = ax[n - 1];
-    double invw = 0.0;
-    if (n > 1 && std::isfinite(al - a0) && (al - a0) > 0.0) invw = double(kLut) / (al - a0);
-    ext[L.o_par + 4 * a + 0] = a0;
-    ext[L.o_par + 4 * a + 1] = al;
-    ext[L.o_par + 4 * a + 2] = invw;
-    ext[L.o_par + 4 * a + 3] = 0.0;
-    for (int k = 0; k < kLut; ++k) {
-      // largest i <= n-2 with a[i] <= bucket start; the kernel corrects any rounding
-      const double xk = a0 + (al - a0) * (double(k) / kLut);
-      int64_t i = 0;
-      while (i + 1 <= n - 2 && ax[i + 1] <= xk) ++i;
-      lut[a * kLut + k] = (int32_t)i;
+    double* par = ext.data() + L.o_par + 8 * a;
+    double scale = 0.0;
+    if (n > 1 && std::isfinite(al - a0) && (al - a0) > 0.0) scale = double(kLut) / (al - a0);
+    par[0] = a0;
+    par[1] = al;
+    par[2] = scale;
+    par[6] = double(n);
+    // UNIFORM: power-of-two step, every node exactly a0 + k*h and every width exactly h
+    double h = n > 1 ? ax[1] - ax[0] : 0.0, invh = 0.0;
+    bool uniform = n > 1 && pow2_recip(h, &invh);
+    for (int64_t k = 0; uniform && k < n; ++k) {
+      if (ax[k] != a0 + double(k) * h) uniform = false;
+      if (k + 1 < n && ax[k + 1] - ax[k] != h) uniform = false;
     }
-    for (int64_t i = 0; i + 1 < n; ++i) {
+    par[3] = uniform ? kModeUniform : kModeLut;
+    par[4] = uniform ? h : 0.0;
+    par[5] = uniform ? invh : 0.0;
+    // bucket k covers lut-space [k, k+1); its start in x-space:
+    auto xs = [&](int64_t k) -> double {
+      if (k <= 0) return a0;
+      if (k >= kLut) return al;
+      return a0 + (al - a0) * (double(k) / kLut);
+    };
+    auto interval_of = [&](double x) -> int64_t {  // largest i <= n-2 with a[i] <= x
+      int64_t i = 0;
+      while (i + 1 <= n - 2 && ax[i + 1] <= x) ++i;
+      return i;
+    };
+    for (int64_t k = 0; k < kLut; ++k) {
+      const int64_t i = interval_of(xs(k));
+      // exact if buckets k-1..k+1 (the computed bucket is off by at most one) lie in
+      // [a[i], a[i+1]) with room to spare
+      bool exact = n >= 2 && ax[i] < xs(k - 1) && xs(k + 2) < ax[i + 1];
+      if (k == 0) exact = n >= 2 && xs(k + 2) < ax[i + 1];  // x > a0 == a[0] is known
+      if (k == kLut - 1) exact = n >= 2 && ax[i] < xs(k - 1) && i == n - 2;  // x < a_last
+      lut[a * kLut + k] = uint32_t(i) | (exact ? kExact : 0u);
+    }
+    // intervals: iv[i] = (a[i], exact reciprocal of a[i+1]-a[i] or 0); iv[n-1] = (a_last, 0)
+    double* iv = ext.data() + o_iv[a];
+    for (int64_t i = 0; i < n; ++i) {
       double r = 0.0;
-      if (!pow2_recip(ax[i + 1] - ax[i], &r)) r = 0.0;
-      ext[o_inv[a] + i] = r;
+      if (i + 1 < n && !pow2_recip(ax[i + 1] - ax[i], &r)) r = 0.0;
+      iv[2 * i] = ax[i];
+      iv[2 * i + 1] = r;
     }
   }
   const int64_t cb = nb > 1 ? nb - 1 : 1, cs = ns > 1 ? ns - 1 : 1, cq = nq > 1 ? nq - 1 : 1;
@@ -92,7 +127,7 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
     for (int64_t j = 0; j < cs; ++j)
       for (int64_t k = 0; k < cq; ++k) {
         double* c = cells + ((i * cs + j) * cq + k) * 8;
-        for (int d = 0; d < 8; ++d) {
+        for (int d = 0; d < 8; ++d) {  // corner d = (db << 2) | (ds << 1) | dq
           const int64_t ii = std::min(i + ((d >> 2) & 1), nb - 1);
           const int64_t jj = std::min(j + ((d >> 1) & 1), ns - 1);
           const int64_t kk = std::min(k + (d & 1), nq - 1);
@@ -103,15 +138,30 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
 }
 
 struct FastAxis {
-  const double* a;
-  const int32_t* lut;
-  const double* inv;
-  int n;
-  double a0, al, invw;
+  const uint32_t* lut;
+  const double2* iv;
+  int n, mode;
+  double a0, al, scale, h, invh;
 };
 
-// Bracket of x as (cell index c, corner selectors s0/s1 for lo/hi, t).  Identical
-// (lo, hi, t) to rapp::locate() for a strictly ascending axis: lo = c + s0, hi = c + s1.
+__device__ __forceinline__ FastAxis load_axis(const double* ext, int a, const uint32_t* lut,
+                                              const double* iv) {
+  const double* p = ext + 8 * a;
+  FastAxis ax;
+  ax.lut = lut + a * kLut;
+  ax.iv = reinterpret_cast<const double2*>(iv);
+  ax.a0 = p[0];
+  ax.al = p[1];
+  ax.scale = p[2];
+  ax.mode = int(p[3]);
+  ax.h = p[4];
+  ax.invh = p[5];
+  ax.n = int(p[6]);
+  return ax;
+}
+
+// Bracket of x as (cell c, corner selectors s0/s1, t): identical (lo, hi, t) to
+// rapp::locate() for a strictly ascending axis, with lo = c + s0 and hi = c + s1.
 __device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c, int& s0,
                                             int& s1, double& t) {
   const int last = ax.n - 1;
@@ -122,106 +172,149 @@ __device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c
     t = 0.0;
     return;
   }
-  if (x != x) {  // NaN: the reference's search ends at (0, min(1, last))
+  if (x != x) {  // NaN: the reference's search ends at (0, min(1, last)), t = NaN
     c = 0;
     s0 = 0;
     s1 = last > 0 ? 1 : 0;
-    t = __ddiv_rn(__dsub_rn(x, ax.a0), __dsub_rn(ax.a[s1], ax.a0));
+    t = __ddiv_rn(__dsub_rn(x, ax.a0), __dsub_rn(ax.iv[s1].x, ax.a0));
     return;
   }
-  // here a0 < x < a_last, so n >= 2 and the answer lies in [0, n-2]
-  int k = int(__dmul_rn(__dsub_rn(x, ax.a0), ax.invw));
+  // a0 < x < a_last here, so n >= 2 and lo lies in [0, n-2]
+  double lo;
+  int i;
+  if (ax.mode == kModeUniform) {
+    i = int(__dmul_rn(__dsub_rn(x, ax.a0), ax.invh));
+    i = i < last - 1 ? i : last - 1;
+    i = i > 0 ? i : 0;
+    lo = __dadd_rn(ax.a0, __dmul_rn(double(i), ax.h));
+    if (lo > x) {
+      --i;
+      lo = __dadd_rn(ax.a0, __dmul_rn(double(i), ax.h));
+    } else if (i < last - 1) {
+      const double nx = __dadd_rn(ax.a0, __dmul_rn(double(i + 1), ax.h));
+      if (nx <= x) {
+        ++i;
+        lo = nx;
+      }
+    }
+    c = i;
+    s0 = 0;
+    if (lo == x) { s1 = 0; t = 0.0; return; }
+    s1 = 1;
+    t = __dmul_rn(__dsub_rn(x, lo), ax.invh);
+    return;
+  }
+  int k = int(__dmul_rn(__dsub_rn(x, ax.a0), ax.scale));
   k = k < kLut - 1 ? k : kLut - 1;
   k = k > 0 ? k : 0;
-  int i = ax.lut[k];
-  while (i < last - 1 && ax.a[i + 1] <= x) ++i;
-  while (i > 0 && ax.a[i] > x) --i;
-  const double lo = ax.a[i];
+  const uint32_t e = ax.lut[k];
+  i = int(e & ~kExact);
+  if (!(e & kExact)) {
+    while (i < last - 1 && ax.iv[i + 1].x <= x) ++i;
+    while (i > 0 && ax.iv[i].x > x) --i;
+  }
+  const double2 w = ax.iv[i];
+  lo = w.x;
   c = i;
   s0 = 0;
   if (lo == x) { s1 = 0; t = 0.0; return; }
   s1 = 1;
   const double num = __dsub_rn(x, lo);
-  const double r = ax.inv[i];
-  t = r != 0.0 ? __dmul_rn(num, r) : __ddiv_rn(num, __dsub_rn(ax.a[i + 1], lo));
+  t = w.y != 0.0 ? __dmul_rn(num, w.y) : __ddiv_rn(num, __dsub_rn(ax.iv[i + 1].x, lo));
 }
 
-__device__ __forceinline__ double2 pick2(int sel, double2 a, double2 b) { return sel ? b : a; }
-__device__ __forceinline__ double pickq(int sel, double2 w) { return sel ? w.y : w.x; }
+__device__ __forceinline__ void load_row(const double* p, bool smem, double& v0, double& v1,
+                                         double& v2, double& v3) {
+  if (smem) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    const double2 b = reinterpret_cast<const double2*>(p)[1];
+    v0 = a.x; v1 = a.y; v2 = b.x; v3 = b.y;
+  } else {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
+        : "l"(p));
+  }
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
 
 constexpr int kFastThreads = 256;
-constexpr int kFastIlp = 2;
+constexpr int kFastIlp = 2;  // rows per lane per warp-step
 
 template <bool CELLS_SMEM>
-__global__ void __launch_bounds__(kFastThreads)
+__global__ void __launch_bounds__(kFastThreads, 3)
     k_interp_fast(const TableDesc td, const double* __restrict__ pool,
                   const double* __restrict__ coords, int64_t n, double* __restrict__ out,
                   double* __restrict__ rps) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   __shared__ uint64_t bar;
-  const int axes_doubles = td.ov;  // [b | s | q] with padding
-  double* s_axes = sm;
-  double* s_ext = sm + axes_doubles;
   const double* ext_g = pool + td.xoff;
   const uint32_t small_bytes = uint32_t(td.x_small) * 8u;
   const uint32_t cell_bytes = CELLS_SMEM ? uint32_t(td.x_total - td.x_small) * 8u : 0u;
-  bulk_load_2(s_axes, pool + td.off, uint32_t(axes_doubles) * 8u, s_ext, ext_g,
-              small_bytes + cell_bytes, &bar);
-  const double* cells = CELLS_SMEM ? s_ext + td.x_small : ext_g + td.x_small;
-  const int32_t* lut = reinterpret_cast<const int32_t*>(s_ext + 12);
-  FastAxis ab{s_axes + td.ob, lut, s_ext + td.x_inv_b, td.nb, s_ext[0], s_ext[1], s_ext[2]};
-  FastAxis as{s_axes + td.os, lut + kLut, s_ext + td.x_inv_s, td.ns, s_ext[4], s_ext[5],
-              s_ext[6]};
-  FastAxis aq{s_axes + td.oq, lut + 2 * kLut, s_ext + td.x_inv_q, td.nq, s_ext[8], s_ext[9],
-              s_ext[10]};
+  bulk_load_2(sm, ext_g, small_bytes + cell_bytes, nullptr, nullptr, 0u, &bar);
+  const double* cells = CELLS_SMEM ? sm + td.x_small : ext_g + td.x_small;
+  const uint32_t* lut = reinterpret_cast<const uint32_t*>(sm + 24);
+  const FastAxis ab = load_axis(sm, 0, lut, sm + td.x_iv_b);
+  const FastAxis as = load_axis(sm, 1, lut, sm + td.x_iv_s);
+  const FastAxis aq = load_axis(sm, 2, lut, sm + td.x_iv_q);
   const int CS = td.ns > 1 ? td.ns - 1 : 1, CQ = td.nq > 1 ? td.nq - 1 : 1;
 
-  const int64_t stride = int64_t(gridDim.x) * kFastThreads * kFastIlp;
-  for (int64_t base = int64_t(blockIdx.x) * kFastThreads * kFastIlp + threadIdx.x; base < n;
-       base += stride) {
-    double cb[kFastIlp], cs[kFastIlp], cq[kFastIlp];
+  const int lane = threadIdx.x & 31;
+  const int half = lane & 1;  // which batch row of a cell this lane evaluates
+  const int64_t warps = int64_t(gridDim.x) * (kFastThreads / 32);
+  const int64_t per_warp = 32 * kFastIlp;
+  for (int64_t wb = (int64_t(blockIdx.x) * (kFastThreads / 32) + (threadIdx.x >> 5)) * per_warp;
+       wb < n; wb += warps * per_warp) {  // warp-uniform loop: every lane shuffles
+    double x[kFastIlp][3];
 #pragma unroll
     for (int k = 0; k < kFastIlp; ++k) {
-      const int64_t i = base + int64_t(k) * kFastThreads;
+      const int64_t i = wb + k * 32 + lane;
       if (i < n) {
-        cb[k] = __ldcs(coords + 3 * i);
-        cs[k] = __ldcs(coords + 3 * i + 1);
-        cq[k] = __ldcs(coords + 3 * i + 2);
+        x[k][0] = __ldcs(coords + 3 * i);
+        x[k][1] = __ldcs(coords + 3 * i + 1);
+        x[k][2] = __ldcs(coords + 3 * i + 2);
+      } else {
+        x[k][0] = x[k][1] = x[k][2] = ab.a0;  // harmless in-range filler
       }
     }
 #pragma unroll
     for (int k = 0; k < kFastIlp; ++k) {
-      const int64_t i = base + int64_t(k) * kFastThreads;
-      if (i >= n) continue;
+      const int64_t i = wb + k * 32 + lane;
       int ib, bs0, bs1, js, ss0, ss1, kq, qs0, qs1;
       double tb, ts, tq;
-      locate_fast(ab, cb[k], ib, bs0, bs1, tb);
-      locate_fast(as, cs[k], js, ss0, ss1, ts);
-      locate_fast(aq, cq[k], kq, qs0, qs1, tq);
-      const double2* cp =
-          reinterpret_cast<const double2*>(cells + ((int64_t(ib) * CS + js) * CQ + kq) * 8);
-      double2 w[4];
-      if (CELLS_SMEM) {
+      locate_fast(ab, x[k][0], ib, bs0, bs1, tb);
+      locate_fast(as, x[k][1], js, ss0, ss1, ts);
+      locate_fast(aq, x[k][2], kq, qs0, qs1, tq);
+      const int cell = (ib * CS + js) * CQ + kq;
+      const int sel = bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) | (qs0 << 4) | (qs1 << 5);
+      double lat = 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = cp[u];
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = __ldg(cp + u);
+      for (int r = 0; r < 2; ++r) {  // round r: pair (2p, 2p+1) evaluates lane 2p+r's query
+        const int src = (lane & ~1) | r;
+        const int c_cell = __shfl_sync(0xffffffffu, cell, src);
+        const int c_sel = __shfl_sync(0xffffffffu, sel, src);
+        const double c_tq = shfl_d(tq, src), c_ts = shfl_d(ts, src), c_tb = shfl_d(tb, src);
+        const int db = half ? (c_sel >> 1) & 1 : c_sel & 1;
+        double v0, v1, v2, v3;  // (ds,dq) = (0,0) (0,1) (1,0) (1,1) of batch row db
+        load_row(cells + int64_t(c_cell) * 8 + db * 4, CELLS_SMEM, v0, v1, v2, v3);
+        const int s0 = (c_sel >> 2) & 1, s1 = (c_sel >> 3) & 1;
+        const int q0 = (c_sel >> 4) & 1, q1 = (c_sel >> 5) & 1;
+        const double r0a = s0 ? v2 : v0, r0b = s0 ? v3 : v1;  // ds = s0 row: (dq=0, dq=1)
+        const double r1a = s1 ? v2 : v0, r1b = s1 ? v3 : v1;  // ds = s1 row
+        const double cj0 = lerp_rn(q0 ? r0b : r0a, q1 ? r0b : r0a, c_tq);  // c_{db,j0}
+        const double cj1 = lerp_rn(q0 ? r1b : r1a, q1 ? r1b : r1a, c_tq);  // c_{db,j1}
+        const double cdb = lerp_rn(cj0, cj1, c_ts);                          // c0 or c1
+        const double other = shfl_d(cdb, lane ^ 1);
+        const double c0 = half ? other : cdb, c1 = half ? cdb : other;
+        const double l = lerp_rn(c0, c1, c_tb);
+        if (half == r) lat = l;
       }
-      // w[db*2 + ds] = (corner dq=0, corner dq=1)
-      const double2 b0 = pick2(ss0, w[0], w[1]), b0h = pick2(ss1, w[0], w[1]);
-      const double2 b1 = pick2(ss0, w[2], w[3]), b1h = pick2(ss1, w[2], w[3]);
-      const double2 w00 = pick2(bs0, b0, b1), w01 = pick2(bs0, b0h, b1h);
-      const double2 w10 = pick2(bs1, b0, b1), w11 = pick2(bs1, b0h, b1h);
-      const double c00 = lerp_rn(pickq(qs0, w00), pickq(qs1, w00), tq);
-      const double c01 = lerp_rn(pickq(qs0, w01), pickq(qs1, w01), tq);
-      const double c10 = lerp_rn(pickq(qs0, w10), pickq(qs1, w10), tq);
-      const double c11 = lerp_rn(pickq(qs0, w11), pickq(qs1, w11), tq);
-      const double c0 = lerp_rn(c00, c01, ts);
-      const double c1 = lerp_rn(c10, c11, ts);
-      const double lat = lerp_rn(c0, c1, tb);
-      __stcs(out + i, lat);
-      if (rps != nullptr) __stcs(rps + i, throughput(cb[k], lat));
+      if (i < n) {
+        __stcs(out + i, lat);
+        if (rps != nullptr) __stcs(rps + i, throughput(x[k][0], lat));
+      }
     }
   }
 }
@@ -231,20 +324,22 @@ constexpr int64_t kFastCellsSmem = 96 * 1024;
 int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coords, int64_t n,
                        double* d_out, double* d_rps, cudaStream_t st) {
   const int64_t cell_bytes = int64_t(td.x_total - td.x_small) * 8;
-  const int64_t small_bytes = (int64_t(td.ov) + td.x_small) * 8;
+  const int64_t small_bytes = int64_t(td.x_small) * 8;
   const bool cells_smem = cell_bytes + small_bytes <= kFastCellsSmem;
   const size_t smem = (size_t)(small_bytes + (cells_smem ? cell_bytes : 0));
+  if (smem > 200 * 1024) {
+    set_error("fast-path shared-memory footprint %zu too large", smem);
+    return RAPP_E_ARG;
+  }
   const int64_t per_block = int64_t(kFastThreads) * kFastIlp;
   int64_t blocks = (n + per_block - 1) / per_block;
-  const int64_t cap = int64_t(ctx->sm_count) * (cells_smem ? 2 : 8);
+  const int64_t cap = int64_t(ctx->sm_count) * (cells_smem ? 2 : 3);
   if (blocks > cap) blocks = cap;
   if (!ctx->fast_attr_set) {
     RAPP_CUDA(cudaFuncSetAttribute(k_interp_fast<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kFastCellsSmem));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     RAPP_CUDA(cudaFuncSetAttribute(k_interp_fast<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kFastCellsSmem));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     ctx->fast_attr_set = true;
   }
   if (cells_smem)

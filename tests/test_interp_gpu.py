@@ -180,3 +180,35 @@ def test_literal_kernel_also_bit_exact(interp_golden, tmp_path):
     env = dict(os.environ, RAPP_FORCE_LITERAL="1")
     res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert res.returncode == 0 and "literal ok" in res.stdout, res.stderr[-2000:]
+
+
+AXIS_KINDS = {
+    "unit": lambda n: np.arange(1.0, n + 1.0),                 # uniform, pow2 step
+    "half": lambda n: 0.5 * np.arange(n) - 3.0,                # uniform, step 0.5
+    "tens": lambda n: 10.0 * np.arange(1, n + 1),              # uniform step 10 (not pow2)
+    "pow2": lambda n: 2.0 ** np.arange(n),                     # geometric (1,2,4,...)
+    "tenth": lambda n: 0.1 + np.arange(n),                     # step 1 but inexact nodes
+    "irregular": lambda n: np.cumsum(np.random.default_rng(n).uniform(1e-3, 7, n)),
+    "tiny": lambda n: 1e-300 * np.arange(1, n + 1),
+}
+
+
+@pytest.mark.parametrize("kind", sorted(AXIS_KINDS))
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 100])
+def test_axis_layouts_bit_exact(kern, kind, n):
+    """Every locate mode of the fast path (uniform arithmetic, exact buckets, corrected
+    buckets, pow2 reciprocal vs division) against the oracle, incl. nodes and midpoints."""
+    ax = AXIS_KINDS[kind](n).astype(np.float64)
+    rng = np.random.default_rng(n * 31 + len(kind))
+    b = np.array([1.0, 2.0, 4.0])
+    v = np.ascontiguousarray(rng.uniform(1, 100, (3, n, n)))
+    m = 60_000
+    lo, hi = ax[0], ax[-1]
+    span = (hi - lo) if hi > lo else 1.0
+    xs = np.concatenate([rng.uniform(lo - 0.1 * span, hi + 0.1 * span, m - 3 * n), ax,
+                         (ax[:-1] + ax[1:]) / 2 if n > 1 else ax, np.nextafter(ax, np.inf)])
+    xs = xs[:m]
+    c = np.column_stack([rng.uniform(0, 5, len(xs)), rng.permutation(xs), xs])
+    out = np.empty(len(c))
+    kern.interp3_many(b, ax, ax, v, c, out)
+    assert same_bits(out, or_interp3_many(b, ax, ax, v, c))
