@@ -241,32 +241,158 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 }
 
 constexpr int kFastThreads = 256;
-constexpr int kFastIlp = 2;  // rows per lane per warp-step
+constexpr int kFastIlp = 2;     // rows per lane per warp-step
+constexpr int kTile = 1024;     // rows per TMA tile (24 KiB of coordinates)
+constexpr int kInterior = 0x2A; // selector bits of an interior query on every axis
 
+// Interpolates kFastIlp rows per lane (row index base + k*32 + lane, coordinates in x).
+// Lane pairs cooperate: in round r the pair (2p, 2p+1) evaluates lane 2p+r's query, each
+// lane loading one batch row of the cell with one 256-bit load.
+template <bool CELLS_SMEM>
+__device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& as,
+                                            const FastAxis& aq, const double* cells, int CS,
+                                            int CQ, double (&x)[kFastIlp][3], int64_t base,
+                                            int64_t n, double* __restrict__ out,
+                                            double* __restrict__ rps) {
+  const int lane = threadIdx.x & 31;
+  const int half = lane & 1;
+#pragma unroll
+  for (int k = 0; k < kFastIlp; ++k) {
+    const int64_t i = base + k * 32 + lane;
+    int ib, bs0, bs1, js, ss0, ss1, kq, qs0, qs1;
+    double tb, ts, tq;
+    locate_fast(ab, x[k][0], ib, bs0, bs1, tb);
+    locate_fast(as, x[k][1], js, ss0, ss1, ts);
+    locate_fast(aq, x[k][2], kq, qs0, qs1, tq);
+    const int cell = (ib * CS + js) * CQ + kq;
+    const int sel = bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) | (qs0 << 4) | (qs1 << 5);
+    double lat = 0.0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int src = (lane & ~1) | r;
+      const int c_cell = __shfl_sync(0xffffffffu, cell, src);
+      const int c_sel = __shfl_sync(0xffffffffu, sel, src);
+      const double c_tq = shfl_d(tq, src), c_ts = shfl_d(ts, src), c_tb = shfl_d(tb, src);
+      double cdb;
+      if (c_sel == kInterior) {  // lo/hi = cell/cell+1 on all axes: no corner selection
+        double v0, v1, v2, v3;
+        load_row(cells + int64_t(c_cell) * 8 + half * 4, CELLS_SMEM, v0, v1, v2, v3);
+        cdb = lerp_rn(lerp_rn(v0, v1, c_tq), lerp_rn(v2, v3, c_tq), c_ts);
+      } else {
+        const int db = half ? (c_sel >> 1) & 1 : c_sel & 1;
+        double v0, v1, v2, v3;  // (ds,dq) = (0,0) (0,1) (1,0) (1,1) of batch row db
+        load_row(cells + int64_t(c_cell) * 8 + db * 4, CELLS_SMEM, v0, v1, v2, v3);
+        const int s0 = (c_sel >> 2) & 1, s1 = (c_sel >> 3) & 1;
+        const int q0 = (c_sel >> 4) & 1, q1 = (c_sel >> 5) & 1;
+        const double r0a = s0 ? v2 : v0, r0b = s0 ? v3 : v1;
+        const double r1a = s1 ? v2 : v0, r1b = s1 ? v3 : v1;
+        const double cj0 = lerp_rn(q0 ? r0b : r0a, q1 ? r0b : r0a, c_tq);
+        const double cj1 = lerp_rn(q0 ? r1b : r1a, q1 ? r1b : r1a, c_tq);
+        cdb = lerp_rn(cj0, cj1, c_ts);
+      }
+      const double other = shfl_d(cdb, lane ^ 1);
+      const double c0 = half ? other : cdb, c1 = half ? cdb : other;
+      const double l = lerp_rn(c0, c1, c_tb);
+      if (half == r) lat = l;
+    }
+    if (i < n) {
+      __stcs(out + i, lat);
+      if (rps != nullptr) __stcs(rps + i, throughput(x[k][0], lat));
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(sbar), "r"(parity)
+        : "memory");
+  }
+}
+
+// One elected thread: bulk-copy `bytes` from global to shared, completing on `bar`.
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"(sbar)
+      : "memory");
+}
+
+// Persistent CTAs stream full kTile-row tiles of coordinates through a double-buffered
+// TMA pipeline (tile j+1 is in flight while tile j is interpolated); rows past the last
+// full tile (or everything, when coords is not 16-byte aligned) use direct loads.
 template <bool CELLS_SMEM>
 __global__ void __launch_bounds__(kFastThreads, 3)
     k_interp_fast(const TableDesc td, const double* __restrict__ pool,
-                  const double* __restrict__ coords, int64_t n, double* __restrict__ out,
-                  double* __restrict__ rps) {
+                  const double* __restrict__ coords, int64_t n, int64_t n_tiles,
+                  double* __restrict__ out, double* __restrict__ rps) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar_ext;
+  __shared__ uint64_t bar[2];
   const double* ext_g = pool + td.xoff;
-  const uint32_t small_bytes = uint32_t(td.x_small) * 8u;
-  const uint32_t cell_bytes = CELLS_SMEM ? uint32_t(td.x_total - td.x_small) * 8u : 0u;
-  bulk_load_2(sm, ext_g, small_bytes + cell_bytes, nullptr, nullptr, 0u, &bar);
+  const int ext_doubles = CELLS_SMEM ? td.x_total : td.x_small;
+  double* buf0 = sm + ((ext_doubles + 15) & ~15);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+  }
+  bulk_load_2(sm, ext_g, uint32_t(ext_doubles) * 8u, nullptr, nullptr, 0u, &bar_ext);
   const double* cells = CELLS_SMEM ? sm + td.x_small : ext_g + td.x_small;
   const uint32_t* lut = reinterpret_cast<const uint32_t*>(sm + 24);
   const FastAxis ab = load_axis(sm, 0, lut, sm + td.x_iv_b);
   const FastAxis as = load_axis(sm, 1, lut, sm + td.x_iv_s);
   const FastAxis aq = load_axis(sm, 2, lut, sm + td.x_iv_q);
   const int CS = td.ns > 1 ? td.ns - 1 : 1, CQ = td.nq > 1 ? td.nq - 1 : 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kFastThreads / 32;
+  constexpr int kRowsPerWarp = kTile / kWarps;
 
-  const int lane = threadIdx.x & 31;
-  const int half = lane & 1;  // which batch row of a cell this lane evaluates
-  const int64_t warps = int64_t(gridDim.x) * (kFastThreads / 32);
+  // ---- TMA pipeline over full tiles ----
+  int64_t t = blockIdx.x;
+  if (threadIdx.x == 0 && t < n_tiles)
+    tma_load(buf0, coords + 3 * t * kTile, kTile * 24u, &bar[0]);
+  for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
+    const int s = j & 1;
+    const int64_t tn = t + gridDim.x;
+    if (threadIdx.x == 0 && tn < n_tiles)  // buffer s^1 was released by the last barrier
+      tma_load(buf0 + (s ^ 1) * 3 * kTile, coords + 3 * tn * kTile, kTile * 24u, &bar[s ^ 1]);
+    mbar_wait(&bar[s], (j >> 1) & 1);
+    const double* tile = buf0 + s * 3 * kTile;
+    for (int r0 = warp * kRowsPerWarp; r0 < (warp + 1) * kRowsPerWarp; r0 += 32 * kFastIlp) {
+      double x[kFastIlp][3];
+#pragma unroll
+      for (int k = 0; k < kFastIlp; ++k) {
+        const double* row = tile + 3 * (r0 + k * 32 + lane);
+        x[k][0] = row[0];
+        x[k][1] = row[1];
+        x[k][2] = row[2];
+      }
+      interp_rows<CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, t * kTile + r0, n, out, rps);
+    }
+    __syncthreads();  // every warp is done with buffer s before it is refilled
+  }
+
+  // ---- remainder rows: direct loads, warp-uniform grid-stride ----
+  const int64_t rem0 = n_tiles * kTile;
   const int64_t per_warp = 32 * kFastIlp;
-  for (int64_t wb = (int64_t(blockIdx.x) * (kFastThreads / 32) + (threadIdx.x >> 5)) * per_warp;
-       wb < n; wb += warps * per_warp) {  // warp-uniform loop: every lane shuffles
+  const int64_t warps_total = int64_t(gridDim.x) * kWarps;
+  for (int64_t wb = rem0 + (int64_t(blockIdx.x) * kWarps + warp) * per_warp; wb < n;
+       wb += warps_total * per_warp) {
     double x[kFastIlp][3];
 #pragma unroll
     for (int k = 0; k < kFastIlp; ++k) {
@@ -279,43 +405,7 @@ __global__ void __launch_bounds__(kFastThreads, 3)
         x[k][0] = x[k][1] = x[k][2] = ab.a0;  // harmless in-range filler
       }
     }
-#pragma unroll
-    for (int k = 0; k < kFastIlp; ++k) {
-      const int64_t i = wb + k * 32 + lane;
-      int ib, bs0, bs1, js, ss0, ss1, kq, qs0, qs1;
-      double tb, ts, tq;
-      locate_fast(ab, x[k][0], ib, bs0, bs1, tb);
-      locate_fast(as, x[k][1], js, ss0, ss1, ts);
-      locate_fast(aq, x[k][2], kq, qs0, qs1, tq);
-      const int cell = (ib * CS + js) * CQ + kq;
-      const int sel = bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) | (qs0 << 4) | (qs1 << 5);
-      double lat = 0.0;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {  // round r: pair (2p, 2p+1) evaluates lane 2p+r's query
-        const int src = (lane & ~1) | r;
-        const int c_cell = __shfl_sync(0xffffffffu, cell, src);
-        const int c_sel = __shfl_sync(0xffffffffu, sel, src);
-        const double c_tq = shfl_d(tq, src), c_ts = shfl_d(ts, src), c_tb = shfl_d(tb, src);
-        const int db = half ? (c_sel >> 1) & 1 : c_sel & 1;
-        double v0, v1, v2, v3;  // (ds,dq) = (0,0) (0,1) (1,0) (1,1) of batch row db
-        load_row(cells + int64_t(c_cell) * 8 + db * 4, CELLS_SMEM, v0, v1, v2, v3);
-        const int s0 = (c_sel >> 2) & 1, s1 = (c_sel >> 3) & 1;
-        const int q0 = (c_sel >> 4) & 1, q1 = (c_sel >> 5) & 1;
-        const double r0a = s0 ? v2 : v0, r0b = s0 ? v3 : v1;  // ds = s0 row: (dq=0, dq=1)
-        const double r1a = s1 ? v2 : v0, r1b = s1 ? v3 : v1;  // ds = s1 row
-        const double cj0 = lerp_rn(q0 ? r0b : r0a, q1 ? r0b : r0a, c_tq);  // c_{db,j0}
-        const double cj1 = lerp_rn(q0 ? r1b : r1a, q1 ? r1b : r1a, c_tq);  // c_{db,j1}
-        const double cdb = lerp_rn(cj0, cj1, c_ts);                          // c0 or c1
-        const double other = shfl_d(cdb, lane ^ 1);
-        const double c0 = half ? other : cdb, c1 = half ? cdb : other;
-        const double l = lerp_rn(c0, c1, c_tb);
-        if (half == r) lat = l;
-      }
-      if (i < n) {
-        __stcs(out + i, lat);
-        if (rps != nullptr) __stcs(rps + i, throughput(x[k][0], lat));
-      }
-    }
+    interp_rows<CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, wb, n, out, rps);
   }
 }
 
@@ -326,28 +416,32 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   const int64_t cell_bytes = int64_t(td.x_total - td.x_small) * 8;
   const int64_t small_bytes = int64_t(td.x_small) * 8;
   const bool cells_smem = cell_bytes + small_bytes <= kFastCellsSmem;
-  const size_t smem = (size_t)(small_bytes + (cells_smem ? cell_bytes : 0));
-  if (smem > 200 * 1024) {
+  const int64_t ext_bytes = cells_smem ? small_bytes + cell_bytes : small_bytes;
+  const size_t smem = (size_t)(((ext_bytes + 127) & ~int64_t(127)) + 2 * 3 * kTile * 8);
+  if (smem > 220 * 1024) {
     set_error("fast-path shared-memory footprint %zu too large", smem);
     return RAPP_E_ARG;
   }
-  const int64_t per_block = int64_t(kFastThreads) * kFastIlp;
-  int64_t blocks = (n + per_block - 1) / per_block;
-  const int64_t cap = int64_t(ctx->sm_count) * (cells_smem ? 2 : 3);
+  const bool aligned = (reinterpret_cast<uintptr_t>(d_coords) & 15) == 0;
+  const int64_t n_tiles = aligned ? n / kTile : 0;
+  int64_t blocks = n_tiles > 0 ? n_tiles : (n + 32 * kFastIlp * 8 - 1) / (32 * kFastIlp * 8);
+  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(3, (220 * 1024) / (int64_t)smem));
+  const int64_t cap = int64_t(ctx->sm_count) * per_sm;
   if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
   if (!ctx->fast_attr_set) {
     RAPP_CUDA(cudaFuncSetAttribute(k_interp_fast<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     RAPP_CUDA(cudaFuncSetAttribute(k_interp_fast<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     ctx->fast_attr_set = true;
   }
   if (cells_smem)
-    k_interp_fast<true><<<(unsigned)blocks, kFastThreads, smem, st>>>(td, ctx->d_pool, d_coords,
-                                                                      n, d_out, d_rps);
+    k_interp_fast<true><<<(unsigned)blocks, kFastThreads, smem, st>>>(
+        td, ctx->d_pool, d_coords, n, n_tiles, d_out, d_rps);
   else
-    k_interp_fast<false><<<(unsigned)blocks, kFastThreads, smem, st>>>(td, ctx->d_pool,
-                                                                       d_coords, n, d_out, d_rps);
+    k_interp_fast<false><<<(unsigned)blocks, kFastThreads, smem, st>>>(
+        td, ctx->d_pool, d_coords, n, n_tiles, d_out, d_rps);
   RAPP_LAUNCHED();
   return RAPP_OK;
 }
