@@ -172,6 +172,7 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
       td.x_iv_b = L.o_iv_b;
       td.x_iv_s = L.o_iv_s;
       td.x_iv_q = L.o_iv_q;
+      td.modes = L.modes;
     }
   }
   const int64_t total = td.seg_doubles + (int64_t)ext.size();

@@ -52,6 +52,7 @@ struct TableDesc {
   int32_t fast;
   int32_t x_small, x_total;             // doubles: small part (-> smem), whole extras
   int32_t x_iv_b, x_iv_s, x_iv_q;       // interval-table offsets inside the extras
+  int32_t modes;                        // FastLayout::modes
   int64_t xoff;                         // extras start in the pool
 };
 
@@ -102,6 +103,7 @@ int ensure_pipe(rapp_ctx* ctx, int64_t rows);
 //   [params 3 x 8][lut_b|lut_s|lut_q int32 x kLut each][iv_b|iv_s|iv_q (2n each)][pad][cells]
 struct FastLayout {
   int32_t o_par, o_lut, o_iv_b, o_iv_s, o_iv_q, o_cells, small_doubles, total_doubles;
+  int32_t modes;  // bit a: axis a (0=b, 1=s, 2=q) is an exact power-of-two-step grid
 };
 int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const double* s,
                       const double* q, const double* v, std::vector<double>& ext,

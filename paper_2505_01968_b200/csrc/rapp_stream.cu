@@ -59,11 +59,43 @@ static bool pow2_recip(double d, double* r) {
   return true;
 }
 
+// True when a[k] == a0 + k*h holds exactly in the reals for every k (checked in scaled
+// int64 arithmetic).  Then every fma(k, h, a0) is exact and equals a[k], every interval
+// width a[k+1] - a[k] is exactly h, and x strictly between a0 + i*h and a0 + (i+1)*h
+// can be read off the exact quotient RN(x - a0) / h (see locate_uniform).
+static bool exact_uniform_grid(const double* a, int64_t n, double h) {
+  auto scale_of = [](double v) -> int {  // smallest e >= 0 with v * 2^e integral
+    if (v == 0.0) return 0;
+    for (int e = 0; e <= 1100; ++e) {
+      const double w = std::ldexp(v, e);
+      if (std::isinf(w)) return -1;
+      if (w == std::floor(w)) return e;
+    }
+    return -1;
+  };
+  int e = std::max(scale_of(a[0]), scale_of(h));
+  if (scale_of(a[0]) < 0 || scale_of(h) < 0) return false;
+  const double A0 = std::ldexp(a[0], e), H = std::ldexp(h, e);
+  const double lim = 4.0e18;  // stay well inside int64
+  if (std::fabs(A0) > lim || std::fabs(H) * double(n) > lim || std::fabs(A0) + std::fabs(H) * double(n) > lim)
+    return false;
+  const int64_t ia0 = (int64_t)A0, ih = (int64_t)H;
+  for (int64_t k = 0; k < n; ++k) {
+    const double w = std::ldexp(a[k], e);
+    if (w != std::floor(w) || std::fabs(w) > lim) return false;
+    if ((int64_t)w != ia0 + k * ih) return false;
+  }
+  return true;
+}
+
 // Builds the fast-path extras for a strictly ascending table.
 // params per axis (8 doubles): a0, a_last, lut_scale, mode, h, 1/h, n, 0
 int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const double* s,
                       const double* q, const double* v, std::vector<double>& ext,
                       FastLayout& L) {
+  // the kernel packs (cell index << 6 | selectors) into one int32
+  if ((nb > 1 ? nb - 1 : 1) * (ns > 1 ? ns - 1 : 1) * (nq > 1 ? nq - 1 : 1) >= (int64_t(1) << 25))
+    return RAPP_E_ARG;
   L = fast_layout(nb, ns, nq);
   if ((int64_t)L.total_doubles > (int64_t(1) << 30)) return RAPP_E_ARG;
   ext.assign((size_t)L.total_doubles, 0.0);
@@ -82,14 +114,11 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
     par[1] = al;
     par[2] = scale;
     par[6] = double(n);
-    // UNIFORM: power-of-two step, every node exactly a0 + k*h and every width exactly h
+    // UNIFORM: power-of-two step h and every node EXACTLY a0 + k*h as a real number
     double h = n > 1 ? ax[1] - ax[0] : 0.0, invh = 0.0;
-    bool uniform = n > 1 && pow2_recip(h, &invh);
-    for (int64_t k = 0; uniform && k < n; ++k) {
-      if (ax[k] != a0 + double(k) * h) uniform = false;
-      if (k + 1 < n && ax[k + 1] - ax[k] != h) uniform = false;
-    }
+    const bool uniform = n > 1 && pow2_recip(h, &invh) && exact_uniform_grid(ax, n, h);
     par[3] = uniform ? kModeUniform : kModeLut;
+    if (uniform) L.modes |= 1 << a;
     par[4] = uniform ? h : 0.0;
     par[5] = uniform ? invh : 0.0;
     // bucket k covers lut-space [k, k+1); its start in x-space:
@@ -136,11 +165,10 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
       }
   return RAPP_OK;
 }
-
 struct FastAxis {
   const uint32_t* lut;
   const double2* iv;
-  int n, mode;
+  int n;
   double a0, al, scale, h, invh;
 };
 
@@ -153,74 +181,88 @@ __device__ __forceinline__ FastAxis load_axis(const double* ext, int a, const ui
   ax.a0 = p[0];
   ax.al = p[1];
   ax.scale = p[2];
-  ax.mode = int(p[3]);
   ax.h = p[4];
   ax.invh = p[5];
   ax.n = int(p[6]);
   return ax;
 }
 
-// Bracket of x as (cell c, corner selectors s0/s1, t): identical (lo, hi, t) to
-// rapp::locate() for a strictly ascending axis, with lo = c + s0 and hi = c + s1.
-__device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c, int& s0,
-                                            int& s1, double& t) {
+// Rare cases of every mode: clamps, NaN.  Returns true if it produced the bracket.
+__device__ __forceinline__ bool locate_edges(const FastAxis& ax, double x, int& c, int& s0,
+                                             int& s1, double& t) {
   const int last = ax.n - 1;
-  if (x <= ax.a0) { c = 0; s0 = 0; s1 = 0; t = 0.0; return; }
+  if (x <= ax.a0) { c = 0; s0 = 0; s1 = 0; t = 0.0; return true; }
   if (x >= ax.al) {
     c = last > 0 ? last - 1 : 0;
     s0 = s1 = last - c;
     t = 0.0;
-    return;
+    return true;
   }
   if (x != x) {  // NaN: the reference's search ends at (0, min(1, last)), t = NaN
     c = 0;
     s0 = 0;
     s1 = last > 0 ? 1 : 0;
     t = __ddiv_rn(__dsub_rn(x, ax.a0), __dsub_rn(ax.iv[s1].x, ax.a0));
+    return true;
+  }
+  return false;
+}
+
+// Bracket of x as (cell c, corner selectors s0/s1, t): identical (lo, hi, t) to
+// rapp::locate() for a strictly ascending axis, with lo = c + s0 and hi = c + s1.
+template <int MODE>
+__device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c, int& s0,
+                                            int& s1, double& t) {
+  if (!(x > ax.a0 && x < ax.al)) {  // clamps and NaN (all fail the test)
+    locate_edges(ax, x, c, s0, s1, t);
     return;
   }
-  // a0 < x < a_last here, so n >= 2 and lo lies in [0, n-2]
-  double lo;
-  int i;
-  if (ax.mode == kModeUniform) {
-    i = int(__dmul_rn(__dsub_rn(x, ax.a0), ax.invh));
+  const int last = ax.n - 1;  // a0 < x < a_last: n >= 2, lo in [0, n-2]
+  if (MODE == kModeUniform) {
+    // d = RN(x - a0) > 0 and u = d / h exactly.  If u is not an integer, i = trunc(u)
+    // satisfies i*h < d < (i+1)*h, and since every a0 + k*h is exact and RN monotone,
+    // a[i] < x < a[i+1]: the bracket is (i, i+1) and x is not a node.  Otherwise (u
+    // integral: x within rounding of a node) fall back to exact comparisons.
+    const double u = __dmul_rn(__dsub_rn(x, ax.a0), ax.invh);
+    int i = int(u);
     i = i < last - 1 ? i : last - 1;
-    i = i > 0 ? i : 0;
-    lo = __dadd_rn(ax.a0, __dmul_rn(double(i), ax.h));
-    if (lo > x) {
-      --i;
-      lo = __dadd_rn(ax.a0, __dmul_rn(double(i), ax.h));
-    } else if (i < last - 1) {
-      const double nx = __dadd_rn(ax.a0, __dmul_rn(double(i + 1), ax.h));
-      if (nx <= x) {
-        ++i;
-        lo = nx;
+    double lo = fma(double(i), ax.h, ax.a0);  // exact: == a[i]
+    if (double(i) == u) {
+      if (lo > x) {
+        --i;
+        lo = fma(double(i), ax.h, ax.a0);
+      } else if (i < last - 1) {
+        const double nx = fma(double(i + 1), ax.h, ax.a0);
+        if (nx <= x) {
+          ++i;
+          lo = nx;
+        }
       }
+      c = i;
+      s0 = 0;
+      if (lo == x) { s1 = 0; t = 0.0; return; }
     }
     c = i;
     s0 = 0;
-    if (lo == x) { s1 = 0; t = 0.0; return; }
     s1 = 1;
-    t = __dmul_rn(__dsub_rn(x, lo), ax.invh);
+    t = __dmul_rn(__dsub_rn(x, lo), ax.invh);  // == RN((x - a[i]) / (a[i+1] - a[i]))
     return;
   }
   int k = int(__dmul_rn(__dsub_rn(x, ax.a0), ax.scale));
   k = k < kLut - 1 ? k : kLut - 1;
-  k = k > 0 ? k : 0;
   const uint32_t e = ax.lut[k];
-  i = int(e & ~kExact);
+  int i = int(e & ~kExact);
   if (!(e & kExact)) {
     while (i < last - 1 && ax.iv[i + 1].x <= x) ++i;
     while (i > 0 && ax.iv[i].x > x) --i;
   }
   const double2 w = ax.iv[i];
-  lo = w.x;
   c = i;
   s0 = 0;
-  if (lo == x) { s1 = 0; t = 0.0; return; }
+  if (w.x == x) { s1 = 0; t = 0.0; return; }
   s1 = 1;
-  const double num = __dsub_rn(x, lo);
-  t = w.y != 0.0 ? __dmul_rn(num, w.y) : __ddiv_rn(num, __dsub_rn(ax.iv[i + 1].x, lo));
+  const double num = __dsub_rn(x, w.x);
+  t = w.y != 0.0 ? __dmul_rn(num, w.y) : __ddiv_rn(num, __dsub_rn(ax.iv[i + 1].x, w.x));
 }
 
 __device__ __forceinline__ void load_row(const double* p, bool smem, double& v0, double& v1,
@@ -242,13 +284,13 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 
 constexpr int kFastThreads = 256;
 constexpr int kFastIlp = 2;     // rows per lane per warp-step
-constexpr int kTile = 1024;     // rows per TMA tile (24 KiB of coordinates)
+constexpr int kTile = 512;      // rows per TMA tile (12 KiB of coordinates)
 constexpr int kInterior = 0x2A; // selector bits of an interior query on every axis
 
 // Interpolates kFastIlp rows per lane (row index base + k*32 + lane, coordinates in x).
 // Lane pairs cooperate: in round r the pair (2p, 2p+1) evaluates lane 2p+r's query, each
 // lane loading one batch row of the cell with one 256-bit load.
-template <bool CELLS_SMEM>
+template <int MB, int MS, int MQ, bool CELLS_SMEM>
 __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& as,
                                             const FastAxis& aq, const double* cells, int CS,
                                             int CQ, double (&x)[kFastIlp][3], int64_t base,
@@ -261,27 +303,29 @@ __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& 
     const int64_t i = base + k * 32 + lane;
     int ib, bs0, bs1, js, ss0, ss1, kq, qs0, qs1;
     double tb, ts, tq;
-    locate_fast(ab, x[k][0], ib, bs0, bs1, tb);
-    locate_fast(as, x[k][1], js, ss0, ss1, ts);
-    locate_fast(aq, x[k][2], kq, qs0, qs1, tq);
-    const int cell = (ib * CS + js) * CQ + kq;
-    const int sel = bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) | (qs0 << 4) | (qs1 << 5);
+    locate_fast<MB>(ab, x[k][0], ib, bs0, bs1, tb);
+    locate_fast<MS>(as, x[k][1], js, ss0, ss1, ts);
+    locate_fast<MQ>(aq, x[k][2], kq, qs0, qs1, tq);
+    // cell index (< 2^26 by the table-size limit) and the 6 selector bits in one word
+    const int cs = (((ib * CS + js) * CQ + kq) << 6) | bs0 | (bs1 << 1) | (ss0 << 2) |
+                   (ss1 << 3) | (qs0 << 4) | (qs1 << 5);
     double lat = 0.0;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int src = (lane & ~1) | r;
-      const int c_cell = __shfl_sync(0xffffffffu, cell, src);
-      const int c_sel = __shfl_sync(0xffffffffu, sel, src);
+      const int c_cs = __shfl_sync(0xffffffffu, cs, src);
       const double c_tq = shfl_d(tq, src), c_ts = shfl_d(ts, src), c_tb = shfl_d(tb, src);
+      const int c_sel = c_cs & 63;
+      const double* cell = cells + int64_t(c_cs >> 6) * 8;
       double cdb;
       if (c_sel == kInterior) {  // lo/hi = cell/cell+1 on all axes: no corner selection
         double v0, v1, v2, v3;
-        load_row(cells + int64_t(c_cell) * 8 + half * 4, CELLS_SMEM, v0, v1, v2, v3);
+        load_row(cell + half * 4, CELLS_SMEM, v0, v1, v2, v3);
         cdb = lerp_rn(lerp_rn(v0, v1, c_tq), lerp_rn(v2, v3, c_tq), c_ts);
       } else {
         const int db = half ? (c_sel >> 1) & 1 : c_sel & 1;
         double v0, v1, v2, v3;  // (ds,dq) = (0,0) (0,1) (1,0) (1,1) of batch row db
-        load_row(cells + int64_t(c_cell) * 8 + db * 4, CELLS_SMEM, v0, v1, v2, v3);
+        load_row(cell + db * 4, CELLS_SMEM, v0, v1, v2, v3);
         const int s0 = (c_sel >> 2) & 1, s1 = (c_sel >> 3) & 1;
         const int q0 = (c_sel >> 4) & 1, q1 = (c_sel >> 5) & 1;
         const double r0a = s0 ? v2 : v0, r0b = s0 ? v3 : v1;
@@ -335,8 +379,8 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 // Persistent CTAs stream full kTile-row tiles of coordinates through a double-buffered
 // TMA pipeline (tile j+1 is in flight while tile j is interpolated); rows past the last
 // full tile (or everything, when coords is not 16-byte aligned) use direct loads.
-template <bool CELLS_SMEM>
-__global__ void __launch_bounds__(kFastThreads, 3)
+template <int MB, int MS, int MQ, bool CELLS_SMEM>
+__global__ void __launch_bounds__(kFastThreads, 4)
     k_interp_fast(const TableDesc td, const double* __restrict__ pool,
                   const double* __restrict__ coords, int64_t n, int64_t n_tiles,
                   double* __restrict__ out, double* __restrict__ rps) {
@@ -346,7 +390,6 @@ __global__ void __launch_bounds__(kFastThreads, 3)
   const double* ext_g = pool + td.xoff;
   const int ext_doubles = CELLS_SMEM ? td.x_total : td.x_small;
   double* buf0 = sm + ((ext_doubles + 15) & ~15);
-
   if (threadIdx.x == 0) {
     mbar_init(&bar[0]);
     mbar_init(&bar[1]);
@@ -373,6 +416,7 @@ __global__ void __launch_bounds__(kFastThreads, 3)
       tma_load(buf0 + (s ^ 1) * 3 * kTile, coords + 3 * tn * kTile, kTile * 24u, &bar[s ^ 1]);
     mbar_wait(&bar[s], (j >> 1) & 1);
     const double* tile = buf0 + s * 3 * kTile;
+#pragma unroll 1
     for (int r0 = warp * kRowsPerWarp; r0 < (warp + 1) * kRowsPerWarp; r0 += 32 * kFastIlp) {
       double x[kFastIlp][3];
 #pragma unroll
@@ -382,7 +426,8 @@ __global__ void __launch_bounds__(kFastThreads, 3)
         x[k][1] = row[1];
         x[k][2] = row[2];
       }
-      interp_rows<CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, t * kTile + r0, n, out, rps);
+      interp_rows<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, t * kTile + r0, n,
+                                          out, rps);
     }
     __syncthreads();  // every warp is done with buffer s before it is refilled
   }
@@ -402,14 +447,31 @@ __global__ void __launch_bounds__(kFastThreads, 3)
         x[k][1] = __ldcs(coords + 3 * i + 1);
         x[k][2] = __ldcs(coords + 3 * i + 2);
       } else {
-        x[k][0] = x[k][1] = x[k][2] = ab.a0;  // harmless in-range filler
+        x[k][0] = ab.a0;  // harmless in-range filler
+        x[k][1] = as.a0;
+        x[k][2] = aq.a0;
       }
     }
-    interp_rows<CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, wb, n, out, rps);
+    interp_rows<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, wb, n, out, rps);
   }
 }
 
 constexpr int64_t kFastCellsSmem = 96 * 1024;
+
+template <int MB, int MS, int MQ>
+static void launch_modes(bool cells_smem, unsigned blocks, size_t smem, cudaStream_t st,
+                         const TableDesc& td, const double* pool, const double* coords,
+                         int64_t n, int64_t n_tiles, double* out, double* rps) {
+  if (cells_smem) {
+    auto k = k_interp_fast<MB, MS, MQ, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    k<<<blocks, kFastThreads, smem, st>>>(td, pool, coords, n, n_tiles, out, rps);
+  } else {
+    auto k = k_interp_fast<MB, MS, MQ, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    k<<<blocks, kFastThreads, smem, st>>>(td, pool, coords, n, n_tiles, out, rps);
+  }
+}
 
 int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coords, int64_t n,
                        double* d_out, double* d_rps, cudaStream_t st) {
@@ -425,23 +487,23 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   const bool aligned = (reinterpret_cast<uintptr_t>(d_coords) & 15) == 0;
   const int64_t n_tiles = aligned ? n / kTile : 0;
   int64_t blocks = n_tiles > 0 ? n_tiles : (n + 32 * kFastIlp * 8 - 1) / (32 * kFastIlp * 8);
-  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(3, (220 * 1024) / (int64_t)smem));
+  const int64_t per_sm =
+      std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / (int64_t)(smem + 1024)));
   const int64_t cap = int64_t(ctx->sm_count) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  if (!ctx->fast_attr_set) {
-    RAPP_CUDA(cudaFuncSetAttribute(k_interp_fast<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    RAPP_CUDA(cudaFuncSetAttribute(k_interp_fast<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    ctx->fast_attr_set = true;
+  const unsigned nb = (unsigned)blocks;
+  const double* pool = ctx->d_pool;
+  switch (td.modes & 7) {  // bit 0: batch axis uniform, bit 1: sm, bit 2: quota
+    case 0: launch_modes<0, 0, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    case 1: launch_modes<1, 0, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    case 2: launch_modes<0, 1, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    case 3: launch_modes<1, 1, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    case 4: launch_modes<0, 0, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    case 5: launch_modes<1, 0, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    case 6: launch_modes<0, 1, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+    default: launch_modes<1, 1, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
   }
-  if (cells_smem)
-    k_interp_fast<true><<<(unsigned)blocks, kFastThreads, smem, st>>>(
-        td, ctx->d_pool, d_coords, n, n_tiles, d_out, d_rps);
-  else
-    k_interp_fast<false><<<(unsigned)blocks, kFastThreads, smem, st>>>(
-        td, ctx->d_pool, d_coords, n, n_tiles, d_out, d_rps);
   RAPP_LAUNCHED();
   return RAPP_OK;
 }
