@@ -41,20 +41,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple[str, ...] = ()) -> str:
+    """Builds the library; `out`/`defines` make tuning variants (e.g. RAPP_STREAM_ILP=1)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *sources(), "-lcudart"]
+    tmp = target + ".tmp"
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", tmp, *sources(),
+           "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building librapp_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                out=outs[0] if outs else None, defines=defs))

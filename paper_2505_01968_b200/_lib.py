@@ -13,7 +13,8 @@ import threading
 from .errors import (DeviceError, FilterDegenerateError, InvariantViolation, PlacementError,
                      TableFormatError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librapp_b200.so")
+LIB_PATH = os.environ.get(
+    "RAPP_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "librapp_b200.so"))
 
 RAPP_OK = 0
 RAPP_E_VALUE = 1

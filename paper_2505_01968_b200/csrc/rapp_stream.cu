@@ -283,62 +283,81 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 }
 
 constexpr int kFastThreads = 256;
-constexpr int kFastIlp = 2;     // rows per lane per warp-step
+#ifndef RAPP_STREAM_ILP
+#define RAPP_STREAM_ILP 1
+#endif
+#ifndef RAPP_STREAM_MINB
+#define RAPP_STREAM_MINB 4
+#endif
+constexpr int kFastIlp = RAPP_STREAM_ILP;  // rows per lane per warp-step
 constexpr int kTile = 512;      // rows per TMA tile (12 KiB of coordinates)
 constexpr int kInterior = 0x2A; // selector bits of an interior query on every axis
 
-// Interpolates kFastIlp rows per lane (row index base + k*32 + lane, coordinates in x).
+// Interpolates ILP rows per lane (row index base + k*32 + lane, coordinates in x).
 // Lane pairs cooperate: in round r the pair (2p, 2p+1) evaluates lane 2p+r's query, each
-// lane loading one batch row of the cell with one 256-bit load.
-template <int MB, int MS, int MQ, bool CELLS_SMEM>
+// lane loading one batch row of the cell with one 256-bit load.  All 2*ILP loads of a
+// lane are issued before any of them is consumed, so their L2 latencies overlap.
+template <int ILP, int MB, int MS, int MQ, bool CELLS_SMEM>
 __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& as,
                                             const FastAxis& aq, const double* cells, int CS,
-                                            int CQ, double (&x)[kFastIlp][3], int64_t base,
+                                            int CQ, double (&x)[ILP][3], int64_t base,
                                             int64_t n, double* __restrict__ out,
                                             double* __restrict__ rps) {
   const int lane = threadIdx.x & 31;
   const int half = lane & 1;
+  int cs[ILP];
+  double tb[ILP], ts[ILP], tq[ILP];
 #pragma unroll
-  for (int k = 0; k < kFastIlp; ++k) {
-    const int64_t i = base + k * 32 + lane;
+  for (int k = 0; k < ILP; ++k) {
     int ib, bs0, bs1, js, ss0, ss1, kq, qs0, qs1;
-    double tb, ts, tq;
-    locate_fast<MB>(ab, x[k][0], ib, bs0, bs1, tb);
-    locate_fast<MS>(as, x[k][1], js, ss0, ss1, ts);
-    locate_fast<MQ>(aq, x[k][2], kq, qs0, qs1, tq);
-    // cell index (< 2^26 by the table-size limit) and the 6 selector bits in one word
-    const int cs = (((ib * CS + js) * CQ + kq) << 6) | bs0 | (bs1 << 1) | (ss0 << 2) |
-                   (ss1 << 3) | (qs0 << 4) | (qs1 << 5);
+    locate_fast<MB>(ab, x[k][0], ib, bs0, bs1, tb[k]);
+    locate_fast<MS>(as, x[k][1], js, ss0, ss1, ts[k]);
+    locate_fast<MQ>(aq, x[k][2], kq, qs0, qs1, tq[k]);
+    // cell index (< 2^25, checked at upload) and the 6 selector bits in one word
+    cs[k] = (((ib * CS + js) * CQ + kq) << 6) | bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) |
+            (qs0 << 4) | (qs1 << 5);
+  }
+  // phase 1: fetch the pair's query descriptors and issue every cell-row load
+  int sel[ILP][2];
+  double v[ILP][2][4];
+#pragma unroll
+  for (int k = 0; k < ILP; ++k)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int c_cs = __shfl_sync(0xffffffffu, cs[k], (lane & ~1) | r);
+      sel[k][r] = c_cs & 63;
+      const int db = half ? (c_cs >> 1) & 1 : c_cs & 1;  // batch row of this lane
+      load_row(cells + int64_t(c_cs >> 6) * 8 + db * 4, CELLS_SMEM, v[k][r][0], v[k][r][1],
+               v[k][r][2], v[k][r][3]);
+    }
+  // phase 2: lerps
+#pragma unroll
+  for (int k = 0; k < ILP; ++k) {
     double lat = 0.0;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int src = (lane & ~1) | r;
-      const int c_cs = __shfl_sync(0xffffffffu, cs, src);
-      const double c_tq = shfl_d(tq, src), c_ts = shfl_d(ts, src), c_tb = shfl_d(tb, src);
-      const int c_sel = c_cs & 63;
-      const double* cell = cells + int64_t(c_cs >> 6) * 8;
-      double cdb;
-      if (c_sel == kInterior) {  // lo/hi = cell/cell+1 on all axes: no corner selection
-        double v0, v1, v2, v3;
-        load_row(cell + half * 4, CELLS_SMEM, v0, v1, v2, v3);
-        cdb = lerp_rn(lerp_rn(v0, v1, c_tq), lerp_rn(v2, v3, c_tq), c_ts);
-      } else {
-        const int db = half ? (c_sel >> 1) & 1 : c_sel & 1;
-        double v0, v1, v2, v3;  // (ds,dq) = (0,0) (0,1) (1,0) (1,1) of batch row db
-        load_row(cell + db * 4, CELLS_SMEM, v0, v1, v2, v3);
+      const double c_tq = shfl_d(tq[k], src), c_ts = shfl_d(ts[k], src);
+      const double c_tb = shfl_d(tb[k], src);
+      const int c_sel = sel[k][r];
+      double a0 = v[k][r][0], a1 = v[k][r][1], b0 = v[k][r][2], b1 = v[k][r][3];
+      if (c_sel != kInterior) {  // clamp / node hit somewhere: pick the corners it reads
         const int s0 = (c_sel >> 2) & 1, s1 = (c_sel >> 3) & 1;
         const int q0 = (c_sel >> 4) & 1, q1 = (c_sel >> 5) & 1;
-        const double r0a = s0 ? v2 : v0, r0b = s0 ? v3 : v1;
-        const double r1a = s1 ? v2 : v0, r1b = s1 ? v3 : v1;
-        const double cj0 = lerp_rn(q0 ? r0b : r0a, q1 ? r0b : r0a, c_tq);
-        const double cj1 = lerp_rn(q0 ? r1b : r1a, q1 ? r1b : r1a, c_tq);
-        cdb = lerp_rn(cj0, cj1, c_ts);
+        const double r0a = s0 ? b0 : a0, r0b = s0 ? b1 : a1;  // ds = s0 row (dq = 0, 1)
+        const double r1a = s1 ? b0 : a0, r1b = s1 ? b1 : a1;  // ds = s1 row
+        a0 = q0 ? r0b : r0a;
+        a1 = q1 ? r0b : r0a;
+        b0 = q0 ? r1b : r1a;
+        b1 = q1 ? r1b : r1a;
       }
+      const double cdb = lerp_rn(lerp_rn(a0, a1, c_tq), lerp_rn(b0, b1, c_tq), c_ts);
       const double other = shfl_d(cdb, lane ^ 1);
       const double c0 = half ? other : cdb, c1 = half ? cdb : other;
       const double l = lerp_rn(c0, c1, c_tb);
       if (half == r) lat = l;
     }
+    const int64_t i = base + k * 32 + lane;
     if (i < n) {
       __stcs(out + i, lat);
       if (rps != nullptr) __stcs(rps + i, throughput(x[k][0], lat));
@@ -380,7 +399,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 // TMA pipeline (tile j+1 is in flight while tile j is interpolated); rows past the last
 // full tile (or everything, when coords is not 16-byte aligned) use direct loads.
 template <int MB, int MS, int MQ, bool CELLS_SMEM>
-__global__ void __launch_bounds__(kFastThreads, 4)
+__global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     k_interp_fast(const TableDesc td, const double* __restrict__ pool,
                   const double* __restrict__ coords, int64_t n, int64_t n_tiles,
                   double* __restrict__ out, double* __restrict__ rps) {
@@ -426,7 +445,7 @@ __global__ void __launch_bounds__(kFastThreads, 4)
         x[k][1] = row[1];
         x[k][2] = row[2];
       }
-      interp_rows<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, t * kTile + r0, n,
+      interp_rows<kFastIlp, MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, t * kTile + r0, n,
                                           out, rps);
     }
     __syncthreads();  // every warp is done with buffer s before it is refilled
@@ -452,7 +471,7 @@ __global__ void __launch_bounds__(kFastThreads, 4)
         x[k][2] = aq.a0;
       }
     }
-    interp_rows<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, wb, n, out, rps);
+    interp_rows<kFastIlp, MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, wb, n, out, rps);
   }
 }
 
@@ -488,7 +507,7 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   const int64_t n_tiles = aligned ? n / kTile : 0;
   int64_t blocks = n_tiles > 0 ? n_tiles : (n + 32 * kFastIlp * 8 - 1) / (32 * kFastIlp * 8);
   const int64_t per_sm =
-      std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / (int64_t)(smem + 1024)));
+      std::max<int64_t>(1, std::min<int64_t>(RAPP_STREAM_MINB, (220 * 1024) / (int64_t)(smem + 1024)));
   const int64_t cap = int64_t(ctx->sm_count) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
