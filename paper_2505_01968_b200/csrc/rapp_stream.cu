@@ -294,9 +294,9 @@ constexpr int kTile = 512;      // rows per TMA tile (12 KiB of coordinates)
 constexpr int kInterior = 0x2A; // selector bits of an interior query on every axis
 
 // Interpolates ILP rows per lane (row index base + k*32 + lane, coordinates in x).
-// Lane pairs cooperate: in round r the pair (2p, 2p+1) evaluates lane 2p+r's query, each
-// lane loading one batch row of the cell with one 256-bit load.  All 2*ILP loads of a
-// lane are issued before any of them is consumed, so their L2 latencies overlap.
+// Lane pairs cooperate on their two queries, each lane loading one batch row of each cell
+// with one 256-bit load (see below).  All 2*ILP loads of a lane are issued before any of
+// them is consumed, so their L2 latencies overlap.
 template <int ILP, int MB, int MS, int MQ, bool CELLS_SMEM>
 __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& as,
                                             const FastAxis& aq, const double* cells, int CS,
@@ -317,33 +317,31 @@ __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& 
     cs[k] = (((ib * CS + js) * CQ + kq) << 6) | bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) |
             (qs0 << 4) | (qs1 << 5);
   }
-  // phase 1: fetch the pair's query descriptors and issue every cell-row load
-  int sel[ILP][2];
-  double v[ILP][2][4];
-#pragma unroll
-  for (int k = 0; k < ILP; ++k)
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int c_cs = __shfl_sync(0xffffffffu, cs[k], (lane & ~1) | r);
-      sel[k][r] = c_cs & 63;
-      const int db = half ? (c_cs >> 1) & 1 : c_cs & 1;  // batch row of this lane
-      load_row(cells + int64_t(c_cs >> 6) * 8 + db * 4, CELLS_SMEM, v[k][r][0], v[k][r][1],
-               v[k][r][2], v[k][r][3]);
-    }
-  // phase 2: lerps
+  // Lane h of a pair evaluates batch row h (i0 for h=0, i1 for h=1) of BOTH queries of
+  // the pair: its own (o) and its partner's (p).  One exchange then gives each lane the
+  // other row of its own query for the batch lerp.
+  int csp[ILP];
+  double tqp[ILP], tsp[ILP], vo[ILP][4], vp[ILP][4];
 #pragma unroll
   for (int k = 0; k < ILP; ++k) {
-    double lat = 0.0;
+    csp[k] = __shfl_xor_sync(0xffffffffu, cs[k], 1);
+    tqp[k] = __shfl_xor_sync(0xffffffffu, tq[k], 1);
+    tsp[k] = __shfl_xor_sync(0xffffffffu, ts[k], 1);
+    const int dbo = half ? (cs[k] >> 1) & 1 : cs[k] & 1;  // which corner row is "row h"
+    const int dbp = half ? (csp[k] >> 1) & 1 : csp[k] & 1;
+    load_row(cells + int64_t(cs[k] >> 6) * 8 + dbo * 4, CELLS_SMEM, vo[k][0], vo[k][1],
+             vo[k][2], vo[k][3]);
+    load_row(cells + int64_t(csp[k] >> 6) * 8 + dbp * 4, CELLS_SMEM, vp[k][0], vp[k][1],
+             vp[k][2], vp[k][3]);
+  }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int src = (lane & ~1) | r;
-      const double c_tq = shfl_d(tq[k], src), c_ts = shfl_d(ts[k], src);
-      const double c_tb = shfl_d(tb[k], src);
-      const int c_sel = sel[k][r];
-      double a0 = v[k][r][0], a1 = v[k][r][1], b0 = v[k][r][2], b1 = v[k][r][3];
-      if (c_sel != kInterior) {  // clamp / node hit somewhere: pick the corners it reads
-        const int s0 = (c_sel >> 2) & 1, s1 = (c_sel >> 3) & 1;
-        const int q0 = (c_sel >> 4) & 1, q1 = (c_sel >> 5) & 1;
+  for (int k = 0; k < ILP; ++k) {
+    // row value c_h = lerp(lerp(v[j0,k0], v[j0,k1], tq), lerp(v[j1,k0], v[j1,k1], tq), ts)
+    auto row = [&](int sel, double (&v)[4], double t_q, double t_s) -> double {
+      double a0 = v[0], a1 = v[1], b0 = v[2], b1 = v[3];
+      if ((sel & 63) != kInterior) {  // clamp / node hit: pick the corners the reference reads
+        const int s0 = (sel >> 2) & 1, s1 = (sel >> 3) & 1;
+        const int q0 = (sel >> 4) & 1, q1 = (sel >> 5) & 1;
         const double r0a = s0 ? b0 : a0, r0b = s0 ? b1 : a1;  // ds = s0 row (dq = 0, 1)
         const double r1a = s1 ? b0 : a0, r1b = s1 ? b1 : a1;  // ds = s1 row
         a0 = q0 ? r0b : r0a;
@@ -351,12 +349,12 @@ __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& 
         b0 = q0 ? r1b : r1a;
         b1 = q1 ? r1b : r1a;
       }
-      const double cdb = lerp_rn(lerp_rn(a0, a1, c_tq), lerp_rn(b0, b1, c_tq), c_ts);
-      const double other = shfl_d(cdb, lane ^ 1);
-      const double c0 = half ? other : cdb, c1 = half ? cdb : other;
-      const double l = lerp_rn(c0, c1, c_tb);
-      if (half == r) lat = l;
-    }
+      return lerp_rn(lerp_rn(a0, a1, t_q), lerp_rn(b0, b1, t_q), t_s);
+    };
+    const double co = row(cs[k], vo[k], tq[k], ts[k]);    // row h of my query
+    const double cp = row(csp[k], vp[k], tqp[k], tsp[k]);  // row h of my partner's query
+    const double other = __shfl_xor_sync(0xffffffffu, cp, 1);  // row 1-h of my query
+    const double lat = half ? lerp_rn(other, co, tb[k]) : lerp_rn(co, other, tb[k]);
     const int64_t i = base + k * 32 + lane;
     if (i < n) {
       __stcs(out + i, lat);
