@@ -282,15 +282,21 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
-constexpr int kFastThreads = 256;
 #ifndef RAPP_STREAM_ILP
 #define RAPP_STREAM_ILP 1
 #endif
 #ifndef RAPP_STREAM_MINB
-#define RAPP_STREAM_MINB 4
+#define RAPP_STREAM_MINB 2
 #endif
-constexpr int kFastIlp = RAPP_STREAM_ILP;  // rows per lane per warp-step
-constexpr int kTile = 512;      // rows per TMA tile (12 KiB of coordinates)
+#ifndef RAPP_STREAM_CONSUMERS
+#define RAPP_STREAM_CONSUMERS 16
+#endif
+constexpr int kFastIlp = RAPP_STREAM_ILP;         // rows per lane per stage
+constexpr int kConsumers = RAPP_STREAM_CONSUMERS;  // consumer warps per CTA
+constexpr int kProducer = kConsumers;              // warp index of the TMA producer
+constexpr int kFastThreads = (kConsumers + 1) * 32;
+constexpr int kTile = kConsumers * 32 * kFastIlp;  // rows per TMA stage
+constexpr int kStages = 4;
 constexpr int kInterior = 0x2A; // selector bits of an interior query on every axis
 
 // Interpolates ILP rows per lane (row index base + k*32 + lane, coordinates in x).
@@ -320,19 +326,29 @@ __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& 
   // Lane h of a pair evaluates batch row h (i0 for h=0, i1 for h=1) of BOTH queries of
   // the pair: its own (o) and its partner's (p).  One exchange then gives each lane the
   // other row of its own query for the batch lerp.
-  int csp[ILP];
-  double tqp[ILP], tsp[ILP], vo[ILP][4], vp[ILP][4];
+  // Load r of a pair fetches the cell of the pair's query r (owned by lane 2p+r) — both
+  // lanes hit the same 64-byte cell in the same instruction, so a warp-wide load touches
+  // 16 lines, not 32.  Lane h keeps row h of each cell.
+  int c_r[ILP][2];
+  double tq_r[ILP][2], ts_r[ILP][2], v[ILP][2][4];
 #pragma unroll
   for (int k = 0; k < ILP; ++k) {
-    csp[k] = __shfl_xor_sync(0xffffffffu, cs[k], 1);
-    tqp[k] = __shfl_xor_sync(0xffffffffu, tq[k], 1);
-    tsp[k] = __shfl_xor_sync(0xffffffffu, ts[k], 1);
-    const int dbo = half ? (cs[k] >> 1) & 1 : cs[k] & 1;  // which corner row is "row h"
-    const int dbp = half ? (csp[k] >> 1) & 1 : csp[k] & 1;
-    load_row(cells + int64_t(cs[k] >> 6) * 8 + dbo * 4, CELLS_SMEM, vo[k][0], vo[k][1],
-             vo[k][2], vo[k][3]);
-    load_row(cells + int64_t(csp[k] >> 6) * 8 + dbp * 4, CELLS_SMEM, vp[k][0], vp[k][1],
-             vp[k][2], vp[k][3]);
+    const int csp = __shfl_xor_sync(0xffffffffu, cs[k], 1);
+    const double tqp = __shfl_xor_sync(0xffffffffu, tq[k], 1);
+    const double tsp = __shfl_xor_sync(0xffffffffu, ts[k], 1);
+    c_r[k][0] = half ? csp : cs[k];
+    c_r[k][1] = half ? cs[k] : csp;
+    tq_r[k][0] = half ? tqp : tq[k];
+    tq_r[k][1] = half ? tq[k] : tqp;
+    ts_r[k][0] = half ? tsp : ts[k];
+    ts_r[k][1] = half ? ts[k] : tsp;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int c = c_r[k][r];
+      const int db = half ? (c >> 1) & 1 : c & 1;  // which corner row is "row h"
+      load_row(cells + int64_t(c >> 6) * 8 + db * 4, CELLS_SMEM, v[k][r][0], v[k][r][1],
+               v[k][r][2], v[k][r][3]);
+    }
   }
 #pragma unroll
   for (int k = 0; k < ILP; ++k) {
@@ -351,8 +367,10 @@ __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& 
       }
       return lerp_rn(lerp_rn(a0, a1, t_q), lerp_rn(b0, b1, t_q), t_s);
     };
-    const double co = row(cs[k], vo[k], tq[k], ts[k]);    // row h of my query
-    const double cp = row(csp[k], vp[k], tqp[k], tsp[k]);  // row h of my partner's query
+    const double c0r = row(c_r[k][0], v[k][0], tq_r[k][0], ts_r[k][0]);
+    const double c1r = row(c_r[k][1], v[k][1], tq_r[k][1], ts_r[k][1]);
+    const double co = half ? c1r : c0r;  // row h of my query
+    const double cp = half ? c0r : c1r;  // row h of my partner's query
     const double other = __shfl_xor_sync(0xffffffffu, cp, 1);  // row 1-h of my query
     const double lat = half ? lerp_rn(other, co, tb[k]) : lerp_rn(co, other, tb[k]);
     const int64_t i = base + k * 32 + lane;
@@ -363,9 +381,15 @@ __device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& 
   }
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-      (uint32_t)__cvta_generic_to_shared(bar)));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -393,9 +417,11 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Persistent CTAs stream full kTile-row tiles of coordinates through a double-buffered
-// TMA pipeline (tile j+1 is in flight while tile j is interpolated); rows past the last
-// full tile (or everything, when coords is not 16-byte aligned) use direct loads.
+// Persistent CTAs stream full kTile-row tiles of coordinates through a kStages-deep TMA
+// ring: one producer warp issues cp.async.bulk into free stages (full/empty mbarriers),
+// kConsumers warps each take 32*ILP rows of a stage, release it as soon as the rows are
+// in registers, and interpolate.  Rows past the last full tile (or everything, when coords
+// is not 16-byte aligned) use direct loads.
 template <int MB, int MS, int MQ, bool CELLS_SMEM>
 __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     k_interp_fast(const TableDesc td, const double* __restrict__ pool,
@@ -403,13 +429,15 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
                   double* __restrict__ out, double* __restrict__ rps) {
   extern __shared__ __align__(128) double sm[];
   __shared__ uint64_t bar_ext;
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t full[kStages], empty[kStages];
   const double* ext_g = pool + td.xoff;
   const int ext_doubles = CELLS_SMEM ? td.x_total : td.x_small;
   double* buf0 = sm + ((ext_doubles + 15) & ~15);
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0]);
-    mbar_init(&bar[1]);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
   }
   bulk_load_2(sm, ext_g, uint32_t(ext_doubles) * 8u, nullptr, nullptr, 0u, &bar_ext);
   const double* cells = CELLS_SMEM ? sm + td.x_small : ext_g + td.x_small;
@@ -419,22 +447,26 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
   const FastAxis aq = load_axis(sm, 2, lut, sm + td.x_iv_q);
   const int CS = td.ns > 1 ? td.ns - 1 : 1, CQ = td.nq > 1 ? td.nq - 1 : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kWarps = kFastThreads / 32;
-  constexpr int kRowsPerWarp = kTile / kWarps;
 
-  // ---- TMA pipeline over full tiles ----
-  int64_t t = blockIdx.x;
-  if (threadIdx.x == 0 && t < n_tiles)
-    tma_load(buf0, coords + 3 * t * kTile, kTile * 24u, &bar[0]);
-  for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
-    const int s = j & 1;
-    const int64_t tn = t + gridDim.x;
-    if (threadIdx.x == 0 && tn < n_tiles)  // buffer s^1 was released by the last barrier
-      tma_load(buf0 + (s ^ 1) * 3 * kTile, coords + 3 * tn * kTile, kTile * 24u, &bar[s ^ 1]);
-    mbar_wait(&bar[s], (j >> 1) & 1);
-    const double* tile = buf0 + s * 3 * kTile;
-#pragma unroll 1
-    for (int r0 = warp * kRowsPerWarp; r0 < (warp + 1) * kRowsPerWarp; r0 += 32 * kFastIlp) {
+  // ---- TMA ring over full tiles: warp kWarps-1 produces, the others consume ----
+  if (warp == kProducer) {
+    if (lane == 0) {
+      int64_t t = blockIdx.x;
+      for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
+        const int s = j % kStages;
+        if (j >= kStages) mbar_wait(&empty[s], ((j / kStages) - 1) & 1);  // stage released
+        tma_load(buf0 + s * 3 * kTile, coords + 3 * t * kTile, kTile * 24u, &full[s]);
+      }
+    }
+    return;  // no CTA-wide barrier follows
+  }
+  {
+    int64_t t = blockIdx.x;
+    for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
+      const int s = j % kStages;
+      mbar_wait(&full[s], (j / kStages) & 1);
+      const double* tile = buf0 + s * 3 * kTile;
+      const int r0 = warp * 32 * kFastIlp;
       double x[kFastIlp][3];
 #pragma unroll
       for (int k = 0; k < kFastIlp; ++k) {
@@ -443,17 +475,18 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
         x[k][1] = row[1];
         x[k][2] = row[2];
       }
-      interp_rows<kFastIlp, MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, t * kTile + r0, n,
-                                          out, rps);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are in registers
+      interp_rows<kFastIlp, MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x,
+                                                    t * kTile + r0, n, out, rps);
     }
-    __syncthreads();  // every warp is done with buffer s before it is refilled
   }
 
   // ---- remainder rows: direct loads, warp-uniform grid-stride ----
   const int64_t rem0 = n_tiles * kTile;
   const int64_t per_warp = 32 * kFastIlp;
-  const int64_t warps_total = int64_t(gridDim.x) * kWarps;
-  for (int64_t wb = rem0 + (int64_t(blockIdx.x) * kWarps + warp) * per_warp; wb < n;
+  const int64_t warps_total = int64_t(gridDim.x) * kConsumers;
+  for (int64_t wb = rem0 + (int64_t(blockIdx.x) * kConsumers + warp) * per_warp; wb < n;
        wb += warps_total * per_warp) {
     double x[kFastIlp][3];
 #pragma unroll
@@ -496,14 +529,14 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   const int64_t small_bytes = int64_t(td.x_small) * 8;
   const bool cells_smem = cell_bytes + small_bytes <= kFastCellsSmem;
   const int64_t ext_bytes = cells_smem ? small_bytes + cell_bytes : small_bytes;
-  const size_t smem = (size_t)(((ext_bytes + 127) & ~int64_t(127)) + 2 * 3 * kTile * 8);
+  const size_t smem = (size_t)(((ext_bytes + 127) & ~int64_t(127)) + kStages * 3 * kTile * 8);
   if (smem > 220 * 1024) {
     set_error("fast-path shared-memory footprint %zu too large", smem);
     return RAPP_E_ARG;
   }
   const bool aligned = (reinterpret_cast<uintptr_t>(d_coords) & 15) == 0;
   const int64_t n_tiles = aligned ? n / kTile : 0;
-  int64_t blocks = n_tiles > 0 ? n_tiles : (n + 32 * kFastIlp * 8 - 1) / (32 * kFastIlp * 8);
+  int64_t blocks = n_tiles > 0 ? n_tiles : (n + kTile - 1) / kTile;
   const int64_t per_sm =
       std::max<int64_t>(1, std::min<int64_t>(RAPP_STREAM_MINB, (220 * 1024) / (int64_t)(smem + 1024)));
   const int64_t cap = int64_t(ctx->sm_count) * per_sm;
