@@ -1,26 +1,34 @@
-// K2 fast path: stream interpolation for validated tables (strictly ascending axes).
+// K2 fast path: stream interpolation for validated tables.
 //
-// Same results, bit for bit, as the literal kernel (rapp_core.cu) and the reference
-// (hs/_kernels/_grid_cy.pyx:9-51).  What changes is how the work is laid out:
+// Used when every axis is strictly ascending and every grid value is finite and > 0 —
+// true of every PerfTable, whose loader rejects non-positive latencies (hs/perf.py:239-267).
+// Results are bit-identical to the literal kernel (rapp_core.cu) and the reference
+// (hs/_kernels/_grid_cy.pyx:9-51).  What changes is the work layout:
 //
 //  1. locate() without a binary search.  For a strictly ascending axis the binary search
 //     returns the unique lo with a[lo] <= x < a[lo+1]; any method that finds that index
 //     exactly is equivalent.  Two per-axis modes, chosen at upload:
-//       UNIFORM  a[k] == a0 + k*h exactly with h a power of two (e.g. sm% / quota% 1..100):
-//                k = floor((x - a0) / h) corrected by one exact comparison — no memory.
+//       UNIFORM  a[k] == a0 + k*h exactly with h a power of two (sm% / quota% 1..100):
+//                lo from the exact quotient RN(x - a0) / h, no memory access.
 //       LUT      a bucket table in shared memory gives the interval; buckets that lie
 //                (with a one-bucket margin) inside a single interval are flagged exact,
 //                the rest are corrected by exact comparisons.
 //  2. t = (x - a[lo]) / (a[hi] - a[lo]): for a power-of-two width the quotient is an exact
 //     multiply by the (exactly representable) reciprocal: RN(n * 2^-e) == RN(n / 2^e).
 //     Other widths use the IEEE division.
-//  3. "Cell" layout: the 8 corners of each grid cell are stored contiguously (64 B,
-//     64-byte aligned).  Two lanes cooperate on one query: each loads one batch row of the
-//     cell (4 doubles) with a single 256-bit load and does that row's two quota lerps and
-//     its sm lerp; one shuffle exchanges the row values for the batch lerp.  A warp thus
-//     touches 16 lines per load instruction instead of 32 x 4.
-//     Clamped / node-hit brackets (lo == hi) select the same corner twice, exactly as the
-//     reference reads v[lo] twice.
+//  3. "Cell" layout: the 8 corners of every grid cell (i, j, k) — v[i or i+1, j or j+1,
+//     k or k+1], indices clamped to the last node — are stored contiguously (64 B, 64-B
+//     aligned), one cell per node on each axis.  Clamps and node hits (the reference's
+//     lo == hi brackets) use cell lo with t = 0: c + (d - c) * 0 == c exactly for finite
+//     positive c, d, so the result equals the reference's v[lo] + (v[lo] - v[lo]) * 0.
+//     NaN coordinates produce NaN exactly as the reference does (cell 0, t = NaN).
+//  4. Two lanes cooperate on their two queries: load r of the pair fetches the cell of
+//     query r (owned by lane 2p+r), lane h keeping batch row h (4 doubles, one 256-bit
+//     load) — both lanes hit the same 64-byte cell in one instruction, so a warp-wide load
+//     touches 16 lines.  Each lane does the quota and sm lerps of its row for both
+//     queries, and one exchange gives each lane the other row of its own query.
+//  5. Coordinates stream through a 4-stage TMA (cp.async.bulk) ring in shared memory fed
+//     by a producer warp (full/empty mbarriers); outputs are streaming stores.
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -43,8 +51,7 @@ static FastLayout fast_layout(int64_t nb, int64_t ns, int64_t nq) {
   L.o_iv_q = L.o_iv_s + int32_t(2 * ns);
   L.o_cells = (L.o_iv_q + int32_t(2 * nq) + 7) & ~7;  // 64-byte aligned cells
   L.small_doubles = L.o_cells;
-  const int64_t cb = nb > 1 ? nb - 1 : 1, cs = ns > 1 ? ns - 1 : 1, cq = nq > 1 ? nq - 1 : 1;
-  L.total_doubles = int32_t(L.o_cells + cb * cs * cq * 8);
+  L.total_doubles = int32_t(L.o_cells + nb * ns * nq * 8);
   return L;
 }
 
@@ -62,7 +69,7 @@ static bool pow2_recip(double d, double* r) {
 // True when a[k] == a0 + k*h holds exactly in the reals for every k (checked in scaled
 // int64 arithmetic).  Then every fma(k, h, a0) is exact and equals a[k], every interval
 // width a[k+1] - a[k] is exactly h, and x strictly between a0 + i*h and a0 + (i+1)*h
-// can be read off the exact quotient RN(x - a0) / h (see locate_uniform).
+// can be read off the exact quotient RN(x - a0) / h (see locate_fast<kModeUniform>).
 static bool exact_uniform_grid(const double* a, int64_t n, double h) {
   auto scale_of = [](double v) -> int {  // smallest e >= 0 with v * 2^e integral
     if (v == 0.0) return 0;
@@ -73,12 +80,11 @@ static bool exact_uniform_grid(const double* a, int64_t n, double h) {
     }
     return -1;
   };
-  int e = std::max(scale_of(a[0]), scale_of(h));
   if (scale_of(a[0]) < 0 || scale_of(h) < 0) return false;
+  const int e = std::max(scale_of(a[0]), scale_of(h));
   const double A0 = std::ldexp(a[0], e), H = std::ldexp(h, e);
   const double lim = 4.0e18;  // stay well inside int64
-  if (std::fabs(A0) > lim || std::fabs(H) * double(n) > lim || std::fabs(A0) + std::fabs(H) * double(n) > lim)
-    return false;
+  if (std::fabs(A0) + std::fabs(H) * double(n) > lim) return false;
   const int64_t ia0 = (int64_t)A0, ih = (int64_t)H;
   for (int64_t k = 0; k < n; ++k) {
     const double w = std::ldexp(a[k], e);
@@ -88,16 +94,16 @@ static bool exact_uniform_grid(const double* a, int64_t n, double h) {
   return true;
 }
 
-// Builds the fast-path extras for a strictly ascending table.
+// Builds the fast-path extras; RAPP_E_ARG when the table does not qualify.
 // params per axis (8 doubles): a0, a_last, lut_scale, mode, h, 1/h, n, 0
 int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const double* s,
                       const double* q, const double* v, std::vector<double>& ext,
                       FastLayout& L) {
-  // the kernel packs (cell index << 6 | selectors) into one int32
-  if ((nb > 1 ? nb - 1 : 1) * (ns > 1 ? ns - 1 : 1) * (nq > 1 ? nq - 1 : 1) >= (int64_t(1) << 25))
-    return RAPP_E_ARG;
+  const int64_t ncell = nb * ns * nq;
+  if (ncell >= (int64_t(1) << 27)) return RAPP_E_ARG;  // int32 cell index * 8 doubles
+  for (int64_t i = 0; i < ncell; ++i)
+    if (!(v[i] > 0.0) || std::isinf(v[i])) return RAPP_E_ARG;  // finite, positive only
   L = fast_layout(nb, ns, nq);
-  if ((int64_t)L.total_doubles > (int64_t(1) << 30)) return RAPP_E_ARG;
   ext.assign((size_t)L.total_doubles, 0.0);
   const double* axes[3] = {b, s, q};
   const int64_t lens[3] = {nb, ns, nq};
@@ -135,7 +141,7 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
     for (int64_t k = 0; k < kLut; ++k) {
       const int64_t i = interval_of(xs(k));
       // exact if buckets k-1..k+1 (the computed bucket is off by at most one) lie in
-      // [a[i], a[i+1]) with room to spare
+      // (a[i], a[i+1]) with room to spare
       bool exact = n >= 2 && ax[i] < xs(k - 1) && xs(k + 2) < ax[i + 1];
       if (k == 0) exact = n >= 2 && xs(k + 2) < ax[i + 1];  // x > a0 == a[0] is known
       if (k == kLut - 1) exact = n >= 2 && ax[i] < xs(k - 1) && i == n - 2;  // x < a_last
@@ -150,12 +156,11 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
       iv[2 * i + 1] = r;
     }
   }
-  const int64_t cb = nb > 1 ? nb - 1 : 1, cs = ns > 1 ? ns - 1 : 1, cq = nq > 1 ? nq - 1 : 1;
   double* cells = ext.data() + L.o_cells;
-  for (int64_t i = 0; i < cb; ++i)
-    for (int64_t j = 0; j < cs; ++j)
-      for (int64_t k = 0; k < cq; ++k) {
-        double* c = cells + ((i * cs + j) * cq + k) * 8;
+  for (int64_t i = 0; i < nb; ++i)
+    for (int64_t j = 0; j < ns; ++j)
+      for (int64_t k = 0; k < nq; ++k) {
+        double* c = cells + ((i * ns + j) * nq + k) * 8;
         for (int d = 0; d < 8; ++d) {  // corner d = (db << 2) | (ds << 1) | dq
           const int64_t ii = std::min(i + ((d >> 2) & 1), nb - 1);
           const int64_t jj = std::min(j + ((d >> 1) & 1), ns - 1);
@@ -165,10 +170,11 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
       }
   return RAPP_OK;
 }
+
 struct FastAxis {
   const uint32_t* lut;
   const double2* iv;
-  int n;
+  int last;
   double a0, al, scale, h, invh;
 };
 
@@ -183,85 +189,66 @@ __device__ __forceinline__ FastAxis load_axis(const double* ext, int a, const ui
   ax.scale = p[2];
   ax.h = p[4];
   ax.invh = p[5];
-  ax.n = int(p[6]);
+  ax.last = int(p[6]) - 1;
   return ax;
 }
 
-// Rare cases of every mode: clamps, NaN.  Returns true if it produced the bracket.
-__device__ __forceinline__ bool locate_edges(const FastAxis& ax, double x, int& c, int& s0,
-                                             int& s1, double& t) {
-  const int last = ax.n - 1;
-  if (x <= ax.a0) { c = 0; s0 = 0; s1 = 0; t = 0.0; return true; }
-  if (x >= ax.al) {
-    c = last > 0 ? last - 1 : 0;
-    s0 = s1 = last - c;
-    t = 0.0;
-    return true;
-  }
-  if (x != x) {  // NaN: the reference's search ends at (0, min(1, last)), t = NaN
-    c = 0;
-    s0 = 0;
-    s1 = last > 0 ? 1 : 0;
-    t = __ddiv_rn(__dsub_rn(x, ax.a0), __dsub_rn(ax.iv[s1].x, ax.a0));
-    return true;
-  }
-  return false;
+// Clamps and NaN (rare).  Cell and t reproduce the reference's (lo, hi, t):
+// x <= a0 -> (0,0,0); x >= a_last -> (last,last,0); NaN -> (0, min(1,last), NaN).
+#ifdef RAPP_EDGE_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void locate_edge(const FastAxis& ax, double x, int& c, double& t) {
+  if (x <= ax.a0) { c = 0; t = 0.0; return; }
+  if (x >= ax.al) { c = ax.last; t = 0.0; return; }
+  c = 0;
+  const int hi = ax.last > 0 ? 1 : 0;
+  t = __ddiv_rn(__dsub_rn(x, ax.a0), __dsub_rn(ax.iv[hi].x, ax.a0));
 }
 
-// Bracket of x as (cell c, corner selectors s0/s1, t): identical (lo, hi, t) to
-// rapp::locate() for a strictly ascending axis, with lo = c + s0 and hi = c + s1.
+// Cell c (== the reference's lo) and t for x (node hits give t = 0).
 template <int MODE>
-__device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c, int& s0,
-                                            int& s1, double& t) {
-  if (!(x > ax.a0 && x < ax.al)) {  // clamps and NaN (all fail the test)
-    locate_edges(ax, x, c, s0, s1, t);
+__device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c, double& t) {
+  if (!(x > ax.a0 && x < ax.al)) {  // clamps and NaN all fail this test
+    locate_edge(ax, x, c, t);
     return;
   }
-  const int last = ax.n - 1;  // a0 < x < a_last: n >= 2, lo in [0, n-2]
+  const int top = ax.last - 1;  // a0 < x < a_last: n >= 2 and lo lies in [0, n-2]
   if (MODE == kModeUniform) {
-    // d = RN(x - a0) > 0 and u = d / h exactly.  If u is not an integer, i = trunc(u)
-    // satisfies i*h < d < (i+1)*h, and since every a0 + k*h is exact and RN monotone,
-    // a[i] < x < a[i+1]: the bracket is (i, i+1) and x is not a node.  Otherwise (u
-    // integral: x within rounding of a node) fall back to exact comparisons.
+    // u = RN(x - a0) / h is exact.  If u is not an integer, i = trunc(u) satisfies
+    // i*h < RN(x - a0) < (i+1)*h, and since every a0 + k*h is exact and RN monotone,
+    // a[i] < x < a[i+1].  If u is integral, x is within rounding of a node: compare.
     const double u = __dmul_rn(__dsub_rn(x, ax.a0), ax.invh);
-    int i = int(u);
-    i = i < last - 1 ? i : last - 1;
+    int i = min(int(u), top);
     double lo = fma(double(i), ax.h, ax.a0);  // exact: == a[i]
     if (double(i) == u) {
       if (lo > x) {
         --i;
         lo = fma(double(i), ax.h, ax.a0);
-      } else if (i < last - 1) {
+      } else if (i < top) {
         const double nx = fma(double(i + 1), ax.h, ax.a0);
         if (nx <= x) {
           ++i;
           lo = nx;
         }
       }
-      c = i;
-      s0 = 0;
-      if (lo == x) { s1 = 0; t = 0.0; return; }
     }
     c = i;
-    s0 = 0;
-    s1 = 1;
-    t = __dmul_rn(__dsub_rn(x, lo), ax.invh);  // == RN((x - a[i]) / (a[i+1] - a[i]))
+    t = __dmul_rn(__dsub_rn(x, lo), ax.invh);  // node hit: x - lo == 0 -> t = 0
     return;
   }
-  int k = int(__dmul_rn(__dsub_rn(x, ax.a0), ax.scale));
-  k = k < kLut - 1 ? k : kLut - 1;
+  const int k = min(int(__dmul_rn(__dsub_rn(x, ax.a0), ax.scale)), kLut - 1);
   const uint32_t e = ax.lut[k];
   int i = int(e & ~kExact);
   if (!(e & kExact)) {
-    while (i < last - 1 && ax.iv[i + 1].x <= x) ++i;
+    while (i < top && ax.iv[i + 1].x <= x) ++i;
     while (i > 0 && ax.iv[i].x > x) --i;
   }
   const double2 w = ax.iv[i];
   c = i;
-  s0 = 0;
-  if (w.x == x) { s1 = 0; t = 0.0; return; }
-  s1 = 1;
-  const double num = __dsub_rn(x, w.x);
+  const double num = __dsub_rn(x, w.x);  // node hit: 0 -> t = 0 either way
   t = w.y != 0.0 ? __dmul_rn(num, w.y) : __ddiv_rn(num, __dsub_rn(ax.iv[i + 1].x, w.x));
 }
 
@@ -278,106 +265,52 @@ __device__ __forceinline__ void load_row(const double* p, bool smem, double& v0,
   }
 }
 
-__device__ __forceinline__ double shfl_d(double v, int src) {
-  return __shfl_sync(0xffffffffu, v, src);
-}
-
-#ifndef RAPP_STREAM_ILP
-#define RAPP_STREAM_ILP 1
-#endif
 #ifndef RAPP_STREAM_MINB
 #define RAPP_STREAM_MINB 2
 #endif
 #ifndef RAPP_STREAM_CONSUMERS
 #define RAPP_STREAM_CONSUMERS 16
 #endif
-constexpr int kFastIlp = RAPP_STREAM_ILP;         // rows per lane per stage
 constexpr int kConsumers = RAPP_STREAM_CONSUMERS;  // consumer warps per CTA
 constexpr int kProducer = kConsumers;              // warp index of the TMA producer
 constexpr int kFastThreads = (kConsumers + 1) * 32;
-constexpr int kTile = kConsumers * 32 * kFastIlp;  // rows per TMA stage
+constexpr int kTile = kConsumers * 32;  // rows per TMA stage: one per consumer lane
 constexpr int kStages = 4;
-constexpr int kInterior = 0x2A; // selector bits of an interior query on every axis
 
-// Interpolates ILP rows per lane (row index base + k*32 + lane, coordinates in x).
-// Lane pairs cooperate on their two queries, each lane loading one batch row of each cell
-// with one 256-bit load (see below).  All 2*ILP loads of a lane are issued before any of
-// them is consumed, so their L2 latencies overlap.
-template <int ILP, int MB, int MS, int MQ, bool CELLS_SMEM>
-__device__ __forceinline__ void interp_rows(const FastAxis& ab, const FastAxis& as,
-                                            const FastAxis& aq, const double* cells, int CS,
-                                            int CQ, double (&x)[ILP][3], int64_t base,
-                                            int64_t n, double* __restrict__ out,
-                                            double* __restrict__ rps) {
-  const int lane = threadIdx.x & 31;
-  const int half = lane & 1;
-  int cs[ILP];
-  double tb[ILP], ts[ILP], tq[ILP];
-#pragma unroll
-  for (int k = 0; k < ILP; ++k) {
-    int ib, bs0, bs1, js, ss0, ss1, kq, qs0, qs1;
-    locate_fast<MB>(ab, x[k][0], ib, bs0, bs1, tb[k]);
-    locate_fast<MS>(as, x[k][1], js, ss0, ss1, ts[k]);
-    locate_fast<MQ>(aq, x[k][2], kq, qs0, qs1, tq[k]);
-    // cell index (< 2^25, checked at upload) and the 6 selector bits in one word
-    cs[k] = (((ib * CS + js) * CQ + kq) << 6) | bs0 | (bs1 << 1) | (ss0 << 2) | (ss1 << 3) |
-            (qs0 << 4) | (qs1 << 5);
-  }
-  // Lane h of a pair evaluates batch row h (i0 for h=0, i1 for h=1) of BOTH queries of
-  // the pair: its own (o) and its partner's (p).  One exchange then gives each lane the
-  // other row of its own query for the batch lerp.
-  // Load r of a pair fetches the cell of the pair's query r (owned by lane 2p+r) — both
-  // lanes hit the same 64-byte cell in the same instruction, so a warp-wide load touches
-  // 16 lines, not 32.  Lane h keeps row h of each cell.
-  int c_r[ILP][2];
-  double tq_r[ILP][2], ts_r[ILP][2], v[ILP][2][4];
-#pragma unroll
-  for (int k = 0; k < ILP; ++k) {
-    const int csp = __shfl_xor_sync(0xffffffffu, cs[k], 1);
-    const double tqp = __shfl_xor_sync(0xffffffffu, tq[k], 1);
-    const double tsp = __shfl_xor_sync(0xffffffffu, ts[k], 1);
-    c_r[k][0] = half ? csp : cs[k];
-    c_r[k][1] = half ? cs[k] : csp;
-    tq_r[k][0] = half ? tqp : tq[k];
-    tq_r[k][1] = half ? tq[k] : tqp;
-    ts_r[k][0] = half ? tsp : ts[k];
-    ts_r[k][1] = half ? ts[k] : tsp;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int c = c_r[k][r];
-      const int db = half ? (c >> 1) & 1 : c & 1;  // which corner row is "row h"
-      load_row(cells + int64_t(c >> 6) * 8 + db * 4, CELLS_SMEM, v[k][r][0], v[k][r][1],
-               v[k][r][2], v[k][r][3]);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < ILP; ++k) {
-    // row value c_h = lerp(lerp(v[j0,k0], v[j0,k1], tq), lerp(v[j1,k0], v[j1,k1], tq), ts)
-    auto row = [&](int sel, double (&v)[4], double t_q, double t_s) -> double {
-      double a0 = v[0], a1 = v[1], b0 = v[2], b1 = v[3];
-      if ((sel & 63) != kInterior) {  // clamp / node hit: pick the corners the reference reads
-        const int s0 = (sel >> 2) & 1, s1 = (sel >> 3) & 1;
-        const int q0 = (sel >> 4) & 1, q1 = (sel >> 5) & 1;
-        const double r0a = s0 ? b0 : a0, r0b = s0 ? b1 : a1;  // ds = s0 row (dq = 0, 1)
-        const double r1a = s1 ? b0 : a0, r1b = s1 ? b1 : a1;  // ds = s1 row
-        a0 = q0 ? r0b : r0a;
-        a1 = q1 ? r0b : r0a;
-        b0 = q0 ? r1b : r1a;
-        b1 = q1 ? r1b : r1a;
-      }
-      return lerp_rn(lerp_rn(a0, a1, t_q), lerp_rn(b0, b1, t_q), t_s);
-    };
-    const double c0r = row(c_r[k][0], v[k][0], tq_r[k][0], ts_r[k][0]);
-    const double c1r = row(c_r[k][1], v[k][1], tq_r[k][1], ts_r[k][1]);
-    const double co = half ? c1r : c0r;  // row h of my query
-    const double cp = half ? c0r : c1r;  // row h of my partner's query
-    const double other = __shfl_xor_sync(0xffffffffu, cp, 1);  // row 1-h of my query
-    const double lat = half ? lerp_rn(other, co, tb[k]) : lerp_rn(co, other, tb[k]);
-    const int64_t i = base + k * 32 + lane;
-    if (i < n) {
-      __stcs(out + i, lat);
-      if (rps != nullptr) __stcs(rps + i, throughput(x[k][0], lat));
-    }
+// One row per lane (row index i, coordinates x0..x2); see the header comment, item 4.
+template <int MB, int MS, int MQ, bool CELLS_SMEM>
+__device__ __forceinline__ void interp_row(const FastAxis& ab, const FastAxis& as,
+                                           const FastAxis& aq, const double* cells, int CS,
+                                           int CQ, double xb, double xs, double xq, int64_t i,
+                                           int64_t n, double* __restrict__ out,
+                                           double* __restrict__ rps) {
+  const int half = threadIdx.x & 1;
+  int ib, js, kq;
+  double tb, ts, tq;
+  locate_fast<MB>(ab, xb, ib, tb);
+  locate_fast<MS>(as, xs, js, ts);
+  locate_fast<MQ>(aq, xq, kq, tq);
+  const int cell = (ib * CS + js) * CQ + kq;
+  const int cell_p = __shfl_xor_sync(0xffffffffu, cell, 1);
+  const double tq_p = __shfl_xor_sync(0xffffffffu, tq, 1);
+  const double ts_p = __shfl_xor_sync(0xffffffffu, ts, 1);
+  // query r of the pair is owned by lane 2p + r
+  const int c0 = half ? cell_p : cell, c1 = half ? cell : cell_p;
+  double v[2][4];
+  load_row(cells + int64_t(c0) * 8 + half * 4, CELLS_SMEM, v[0][0], v[0][1], v[0][2], v[0][3]);
+  load_row(cells + int64_t(c1) * 8 + half * 4, CELLS_SMEM, v[1][0], v[1][1], v[1][2], v[1][3]);
+  // row h of each query: lerp(lerp(v[j0,k0], v[j0,k1], tq), lerp(v[j1,k0], v[j1,k1], tq), ts)
+  const double tq0 = half ? tq_p : tq, tq1 = half ? tq : tq_p;
+  const double ts0 = half ? ts_p : ts, ts1 = half ? ts : ts_p;
+  const double r0 = lerp_rn(lerp_rn(v[0][0], v[0][1], tq0), lerp_rn(v[0][2], v[0][3], tq0), ts0);
+  const double r1 = lerp_rn(lerp_rn(v[1][0], v[1][1], tq1), lerp_rn(v[1][2], v[1][3], tq1), ts1);
+  const double mine = half ? r1 : r0;   // row h of my query
+  const double theirs = half ? r0 : r1;  // row h of my partner's query
+  const double other = __shfl_xor_sync(0xffffffffu, theirs, 1);  // row 1-h of my query
+  const double lat = half ? lerp_rn(other, mine, tb) : lerp_rn(mine, other, tb);
+  if (i < n) {
+    __stcs(out + i, lat);
+    if (rps != nullptr) __stcs(rps + i, throughput(xb, lat));
   }
 }
 
@@ -419,8 +352,8 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 
 // Persistent CTAs stream full kTile-row tiles of coordinates through a kStages-deep TMA
 // ring: one producer warp issues cp.async.bulk into free stages (full/empty mbarriers),
-// kConsumers warps each take 32*ILP rows of a stage, release it as soon as the rows are
-// in registers, and interpolate.  Rows past the last full tile (or everything, when coords
+// kConsumers warps each take 32 rows of a stage, release it as soon as the rows are in
+// registers, and interpolate.  Rows past the last full tile (or everything, when coords
 // is not 16-byte aligned) use direct loads.
 template <int MB, int MS, int MQ, bool CELLS_SMEM>
 __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
@@ -445,10 +378,9 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
   const FastAxis ab = load_axis(sm, 0, lut, sm + td.x_iv_b);
   const FastAxis as = load_axis(sm, 1, lut, sm + td.x_iv_s);
   const FastAxis aq = load_axis(sm, 2, lut, sm + td.x_iv_q);
-  const int CS = td.ns > 1 ? td.ns - 1 : 1, CQ = td.nq > 1 ? td.nq - 1 : 1;
+  const int CS = td.ns, CQ = td.nq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- TMA ring over full tiles: warp kWarps-1 produces, the others consume ----
   if (warp == kProducer) {
     if (lane == 0) {
       int64_t t = blockIdx.x;
@@ -460,49 +392,29 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     }
     return;  // no CTA-wide barrier follows
   }
-  {
-    int64_t t = blockIdx.x;
-    for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
-      const int s = j % kStages;
-      mbar_wait(&full[s], (j / kStages) & 1);
-      const double* tile = buf0 + s * 3 * kTile;
-      const int r0 = warp * 32 * kFastIlp;
-      double x[kFastIlp][3];
-#pragma unroll
-      for (int k = 0; k < kFastIlp; ++k) {
-        const double* row = tile + 3 * (r0 + k * 32 + lane);
-        x[k][0] = row[0];
-        x[k][1] = row[1];
-        x[k][2] = row[2];
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are in registers
-      interp_rows<kFastIlp, MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x,
-                                                    t * kTile + r0, n, out, rps);
-    }
+  int64_t t = blockIdx.x;
+  for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
+    const int s = j % kStages;
+    mbar_wait(&full[s], (j / kStages) & 1);
+    const double* row = buf0 + s * 3 * kTile + 3 * (warp * 32 + lane);
+    const double xb = row[0], xs = row[1], xq = row[2];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are in registers
+    interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq,
+                                       t * kTile + warp * 32 + lane, n, out, rps);
   }
-
-  // ---- remainder rows: direct loads, warp-uniform grid-stride ----
-  const int64_t rem0 = n_tiles * kTile;
-  const int64_t per_warp = 32 * kFastIlp;
+  // remainder rows: direct loads, warp-uniform grid-stride (every lane shuffles)
   const int64_t warps_total = int64_t(gridDim.x) * kConsumers;
-  for (int64_t wb = rem0 + (int64_t(blockIdx.x) * kConsumers + warp) * per_warp; wb < n;
-       wb += warps_total * per_warp) {
-    double x[kFastIlp][3];
-#pragma unroll
-    for (int k = 0; k < kFastIlp; ++k) {
-      const int64_t i = wb + k * 32 + lane;
-      if (i < n) {
-        x[k][0] = __ldcs(coords + 3 * i);
-        x[k][1] = __ldcs(coords + 3 * i + 1);
-        x[k][2] = __ldcs(coords + 3 * i + 2);
-      } else {
-        x[k][0] = ab.a0;  // harmless in-range filler
-        x[k][1] = as.a0;
-        x[k][2] = aq.a0;
-      }
+  for (int64_t wb = n_tiles * kTile + (int64_t(blockIdx.x) * kConsumers + warp) * 32; wb < n;
+       wb += warps_total * 32) {
+    const int64_t i = wb + lane;
+    double xb = ab.a0, xs = as.a0, xq = aq.a0;  // harmless in-range filler past the end
+    if (i < n) {
+      xb = __ldcs(coords + 3 * i);
+      xs = __ldcs(coords + 3 * i + 1);
+      xq = __ldcs(coords + 3 * i + 2);
     }
-    interp_rows<kFastIlp, MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x, wb, n, out, rps);
+    interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq, i, n, out, rps);
   }
 }
 
@@ -537,8 +449,8 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   const bool aligned = (reinterpret_cast<uintptr_t>(d_coords) & 15) == 0;
   const int64_t n_tiles = aligned ? n / kTile : 0;
   int64_t blocks = n_tiles > 0 ? n_tiles : (n + kTile - 1) / kTile;
-  const int64_t per_sm =
-      std::max<int64_t>(1, std::min<int64_t>(RAPP_STREAM_MINB, (220 * 1024) / (int64_t)(smem + 1024)));
+  const int64_t per_sm = std::max<int64_t>(
+      1, std::min<int64_t>(RAPP_STREAM_MINB, (220 * 1024) / (int64_t)(smem + 1024)));
   const int64_t cap = int64_t(ctx->sm_count) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;

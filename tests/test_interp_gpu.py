@@ -212,3 +212,21 @@ def test_axis_layouts_bit_exact(kern, kind, n):
     out = np.empty(len(c))
     kern.interp3_many(b, ax, ax, v, c, out)
     assert same_bits(out, or_interp3_many(b, ax, ax, v, c))
+
+
+def test_non_positive_and_non_finite_values(kern):
+    """Raw-kernel tables with zero, negative, inf or NaN values (the reference kernel
+    accepts any doubles) stay bit-exact: they bypass the positive-table fast path."""
+    rng = np.random.default_rng(9)
+    b = np.array([1.0, 2.0, 4.0, 8.0])
+    s = np.arange(1.0, 11.0)
+    q = np.arange(10.0, 101.0, 10.0)
+    for fill in (0.0, -0.0, -3.5, np.inf, -np.inf, np.nan):
+        v = np.ascontiguousarray(rng.uniform(-5, 5, (4, 10, 10)))
+        v.flat[rng.integers(0, v.size, 30)] = fill
+        c = np.column_stack([rng.uniform(0, 9, 20000), rng.uniform(0, 11, 20000),
+                             rng.uniform(0, 110, 20000)])
+        c[::7] = np.round(c[::7])
+        out = np.empty(len(c))
+        kern.interp3_many(b, s, q, v, c, out)
+        assert same_bits(out, or_interp3_many(b, s, q, v, c)), fill
