@@ -195,12 +195,7 @@ __device__ __forceinline__ FastAxis load_axis(const double* ext, int a, const ui
 
 // Clamps and NaN (rare).  Cell and t reproduce the reference's (lo, hi, t):
 // x <= a0 -> (0,0,0); x >= a_last -> (last,last,0); NaN -> (0, min(1,last), NaN).
-#ifdef RAPP_EDGE_INLINE
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
-void locate_edge(const FastAxis& ax, double x, int& c, double& t) {
+__device__ __forceinline__ void locate_edge(const FastAxis& ax, double x, int& c, double& t) {
   if (x <= ax.a0) { c = 0; t = 0.0; return; }
   if (x >= ax.al) { c = ax.last; t = 0.0; return; }
   c = 0;
