@@ -40,7 +40,18 @@ namespace rapp {
 
 constexpr int kLut = 512;  // buckets per axis (LUT mode)
 constexpr uint32_t kExact = 0x80000000u;
-enum : int { kModeLut = 0, kModeUniform = 1 };
+enum : int { kModeLut = 0, kModeUniform = 1, kModeGeom2 = 2 };
+
+// GEOM2: a[k] == a0 * 2^k with a0 a normal power of two (batch axes 1, 2, 4, ..., 32).
+// For a0 < x < a_last the bracket is read off x's binary exponent exactly.
+static bool exact_geom2_grid(const double* a, int64_t n) {
+  if (n < 2 || !(a[0] > 0.0) || !std::isnormal(a[0])) return false;
+  int e;
+  if (std::frexp(a[0], &e) != 0.5) return false;
+  for (int64_t k = 0; k < n; ++k)
+    if (a[k] != std::ldexp(a[0], (int)k) || std::isinf(a[k])) return false;
+  return std::isnormal(1.0 / a[n - 1]);  // every reciprocal 2^-e stays exactly representable
+}
 
 static FastLayout fast_layout(int64_t nb, int64_t ns, int64_t nq) {
   FastLayout L{};
@@ -123,10 +134,17 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
     // UNIFORM: power-of-two step h and every node EXACTLY a0 + k*h as a real number
     double h = n > 1 ? ax[1] - ax[0] : 0.0, invh = 0.0;
     const bool uniform = n > 1 && pow2_recip(h, &invh) && exact_uniform_grid(ax, n, h);
-    par[3] = uniform ? kModeUniform : kModeLut;
+    const bool geom2 = !uniform && a == 0 && exact_geom2_grid(ax, n);  // batch axis only
+    par[3] = uniform ? kModeUniform : geom2 ? kModeGeom2 : kModeLut;
     if (uniform) L.modes |= 1 << a;
+    if (geom2) L.modes |= 8;
     par[4] = uniform ? h : 0.0;
     par[5] = uniform ? invh : 0.0;
+    if (geom2) {
+      int e0;
+      std::frexp(a0, &e0);
+      par[4] = double(e0 - 1);  // binary exponent of a0
+    }
     // bucket k covers lut-space [k, k+1); its start in x-space:
     auto xs = [&](int64_t k) -> double {
       if (k <= 0) return a0;
@@ -211,6 +229,16 @@ __device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c
     return;
   }
   const int top = ax.last - 1;  // a0 < x < a_last: n >= 2 and lo lies in [0, n-2]
+  if (MODE == kModeGeom2) {
+    // x is normal and a0*2^i <= x < a0*2^(i+1)  <=>  exponent(x) == exponent(a0) + i.
+    // lo = 2^ex exactly; width a[i+1] - a[i] = 2^ex, so t = RN((x - lo) * 2^-ex) exactly.
+    const int ex = ((__double2hiint(x) >> 20) & 0x7FF) - 1023;
+    c = ex - int(ax.h);
+    const double lo = __hiloint2double((ex + 1023) << 20, 0);
+    const double inv = __hiloint2double((1023 - ex) << 20, 0);
+    t = __dmul_rn(__dsub_rn(x, lo), inv);
+    return;
+  }
   if (MODE == kModeUniform) {
     // u = RN(x - a0) / h is exact.  If u is not an integer, i = trunc(u) satisfies
     // i*h < RN(x - a0) < (i+1)*h, and since every a0 + k*h is exact and RN monotone,
@@ -451,16 +479,25 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   if (blocks < 1) blocks = 1;
   const unsigned nb = (unsigned)blocks;
   const double* pool = ctx->d_pool;
-  switch (td.modes & 7) {  // bit 0: batch axis uniform, bit 1: sm, bit 2: quota
-    case 0: launch_modes<0, 0, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    case 1: launch_modes<1, 0, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    case 2: launch_modes<0, 1, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    case 3: launch_modes<1, 1, 0>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    case 4: launch_modes<0, 0, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    case 5: launch_modes<1, 0, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    case 6: launch_modes<0, 1, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
-    default: launch_modes<1, 1, 1>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps); break;
+#define RAPP_LM(B, S, Q) \
+  launch_modes<B, S, Q>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps)
+  // bit 0: batch axis uniform, bit 1: sm uniform, bit 2: quota uniform, bit 3: batch geom2
+  switch (td.modes & 15) {
+    case 0: RAPP_LM(0, 0, 0); break;
+    case 1: RAPP_LM(1, 0, 0); break;
+    case 2: RAPP_LM(0, 1, 0); break;
+    case 3: RAPP_LM(1, 1, 0); break;
+    case 4: RAPP_LM(0, 0, 1); break;
+    case 5: RAPP_LM(1, 0, 1); break;
+    case 6: RAPP_LM(0, 1, 1); break;
+    case 7: RAPP_LM(1, 1, 1); break;
+    case 8: RAPP_LM(2, 0, 0); break;
+    case 10: RAPP_LM(2, 1, 0); break;
+    case 12: RAPP_LM(2, 0, 1); break;
+    case 14: RAPP_LM(2, 1, 1); break;
+    default: RAPP_LM(0, 0, 0); break;  // not produced by build_fast_extras
   }
+#undef RAPP_LM
   RAPP_LAUNCHED();
   return RAPP_OK;
 }

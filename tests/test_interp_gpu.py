@@ -230,3 +230,22 @@ def test_non_positive_and_non_finite_values(kern):
         out = np.empty(len(c))
         kern.interp3_many(b, s, q, v, c, out)
         assert same_bits(out, or_interp3_many(b, s, q, v, c)), fill
+
+
+@pytest.mark.parametrize("b_axis", [[1, 2, 4, 8, 16, 32], [0.5, 1, 2], [2, 4, 8, 16], [1, 2],
+                                    [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024],
+                                    [1, 2, 4, 9], [0.25, 0.5, 1.0, 2.0, 4.0]])
+def test_batch_axis_modes_bit_exact(kern, b_axis):
+    """Geometric power-of-two batch axes (exponent-bit locate) and near-misses (LUT)."""
+    b = np.asarray(b_axis, dtype=np.float64)
+    s = np.arange(1.0, 101.0)
+    q = np.arange(1.0, 101.0)
+    rng = np.random.default_rng(len(b_axis))
+    v = np.ascontiguousarray(rng.uniform(1, 100, (len(b), 100, 100)))
+    m = 100_000
+    xb = np.concatenate([rng.uniform(b[0] / 4, b[-1] * 2, m - 3 * len(b)), b,
+                         np.nextafter(b, 0), np.nextafter(b, np.inf)])
+    c = np.column_stack([xb, rng.uniform(0, 101, m), rng.uniform(0, 101, m)])
+    out = np.empty(m)
+    kern.interp3_many(b, s, q, v, c, out)
+    assert same_bits(out, or_interp3_many(b, s, q, v, c))
