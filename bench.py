@@ -110,27 +110,36 @@ def load_peak():
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.6)  # let the sampler start before the timed region
         except Exception:
             self.proc = None
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *exc):
         self.lines = []
         if self.proc is not None:
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
@@ -140,18 +149,27 @@ class ClockSampler:
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
+        import datetime
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in getattr(self, "lines", []):
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
             try:
-                sms.append(float(parts[0]))
-                mx = float(parts[1])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            # keep samples inside the timed region (with 50 ms slack either side)
+            if ts is not None and self.t0 is not None and self.t1 is not None and \
+                    not (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = float(parts[2])
             except ValueError:
                 continue
-            for name, val in zip(names, parts[2:6]):
+            for name, val in zip(names, parts[3:7]):
                 if val.lower() == "active":
                     reasons.add(name)
         if not sms:
@@ -251,11 +269,13 @@ def run_stream(args, rank, world, local):
             for _ in tables] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.mark_start()
         start.record(stream)
         for i in range(args.steps):
             step(kev[i])
         end.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
     launches = _lib.launch_count() - launches0
     barrier(world)
     ms = max_over_ranks(start.elapsed_time(end), world)
@@ -296,7 +316,7 @@ def run_stream(args, rank, world, local):
     achieved = alg_bytes / (avg_launch_ms / 1000.0) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": load_traffic(n),
-                "kernel": "k_interp_stream<false>", "peak_source": peak_kind,
+                "kernel": "k_interp_fast (rapp_stream.cu)", "peak_source": peak_kind,
                 "alg_bytes_per_prediction": 32}
     cfg = {"workload": "config2: 4-model sweep (resnet50, vgg19, bert-base, mobilenet), tables "
            "6x100x100 (b=1..32 pow2, sm 1..100%, quota 1..100%), 1e8 random queries/model/GPU",
@@ -352,11 +372,13 @@ def run_lattice(args, rank, world, local):
     launches0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.mark_start()
         start.record(stream)
         for _ in range(args.steps):
             step()
         end.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
     launches = _lib.launch_count() - launches0
     barrier(world)
     ms = max_over_ranks(start.elapsed_time(end), world)
@@ -413,7 +435,7 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def cpu_reference(steps, warmup, rows_per_model=250_000, procs=None):
+def cpu_reference(steps, warmup, rows_per_model=1_000_000, procs=None):
     """Times the reference kernel over a process pool; returns (predictions/s, info)."""
     import multiprocessing as mp
     procs = procs or host_cores()
@@ -439,8 +461,8 @@ def cpu_reference(steps, warmup, rows_per_model=250_000, procs=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["stream", "lattice"], default="stream")
     ap.add_argument("--queries", type=int, default=QUERIES_PER_MODEL)
@@ -456,7 +478,8 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        value, info = cpu_reference(args.steps, args.warmup)
+        # each step is a bounded sample (~0.5 s of work per host core) of the workload
+        value, info = cpu_reference(args.steps, args.warmup, rows_per_model=250_000)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "impl": "reference",
                 "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
