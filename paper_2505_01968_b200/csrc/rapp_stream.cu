@@ -421,6 +421,9 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     mbar_wait(&full[s], (j / kStages) & 1);
     const double* row = buf0 + s * 3 * kTile + 3 * (warp * 32 + lane);
     const double xb = row[0], xs = row[1], xq = row[2];
+    // The next TMA write into this stage is an async-proxy access; order our generic-proxy
+    // reads before it (WAR across proxies), then release the stage.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are in registers
     interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq,

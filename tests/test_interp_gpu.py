@@ -249,3 +249,17 @@ def test_batch_axis_modes_bit_exact(kern, b_axis):
     out = np.empty(m)
     kern.interp3_many(b, s, q, v, c, out)
     assert same_bits(out, or_interp3_many(b, s, q, v, c))
+
+
+def test_config2_stream_large_vs_oracle():
+    """Long streams exercise every stage reuse of the TMA ring (a cross-proxy race there
+    would show up as rare wrong rows): 12M queries on two config-2 tables, 0 ulp."""
+    import torch
+    import bench
+    from paper_2505_01968_b200 import PerfTable
+    dev = torch.device("cuda", 0)
+    for mi, (name, b, s, q, v) in list(enumerate(bench.config2_arrays()))[::2]:
+        t = PerfTable(name, bench.BATCHES, list(range(1, 101)), list(range(1, 101)), v)
+        c = bench.gen_queries(b, s, q, 6_000_000, 77 + mi, dev)
+        got = t.predict_latency_many(c).cpu().numpy()
+        assert same_bits(got, or_interp3_many(b, s, q, v, c.cpu().numpy())), name
