@@ -142,7 +142,200 @@ def gen_mec(hs):
     dump("mec.json", {"tables": [table_dict(t) for t in tables], "cases": cases})
 
 
-GENERATORS = {"interp": gen_interp, "mec": gen_mec}
+# -- scaler decisions (Autoscaler.scale) ------------------------------------------------
+
+
+def cluster_dict(cluster) -> dict:
+    return {
+        "clock_ms": hx(cluster.clock_ms),
+        "gpus": [{"id": g.gpu_id, "partitions": [
+            {"sm": p.sm_percent, "residents": list(p.resident_pods), "alloc": p.quota_allocated}
+            for p in g.partitions]} for g in cluster.gpus.values()],
+        "pods": [{"id": p.pod_id, "fid": p.function_id, "b": p.batch, "s": p.sm_percent,
+                  "q": p.quota_percent, "gpu": p.gpu_id, "state": p.state.value}
+                 for p in cluster.pods.values()],
+    }
+
+
+def action_list(actions) -> list:
+    return [[a.function_id, a.kind.value, a.batch, a.sm_percent, a.quota_percent, a.pod_id,
+             a.gpu_id] for a in actions]
+
+
+def fn_dict(f) -> dict:
+    return {"id": f.function_id, "table": f.perf_table_ref or f.function_id,
+            "min_rps": None if f.min_rps is None else hx(f.min_rps),
+            "allowed": list(f.allowed_batches),
+            "initial": [f.initial.batch, f.initial.sm_percent, f.initial.quota_percent,
+                        f.initial.replicas]}
+
+
+def gen_scale(hs):
+    """Single-function decisions: the six hand-traced scenarios (test_acceptance.py C2),
+    the extra branch cases of test_autoscaler.py and its three randomized loops."""
+    import copy
+    from hybridscale import Autoscaler, ScalerConfig, build_cluster
+    from tests.conftest import make_conformance_table, make_function, place_running_pod
+    from tests.test_acceptance import _conformance_scenarios
+    from tests.test_autoscaler import _random_cluster
+
+    cfg = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=20, cooldown_ms=30000, r_min=1.0)
+    table = make_conformance_table()
+    fn = make_function("conf-fn")
+    cases = []
+
+    def record(name, cluster, rate, last_down=None, config=cfg):
+        sc = Autoscaler(config, {"conf-fn": table})
+        if last_down is not None:
+            sc._last_scale_down["conf-fn"] = last_down
+        before = cluster_dict(cluster)
+        acts = sc.scale(fn, copy.deepcopy(cluster), rate)
+        cases.append({"name": name, "cluster": before, "rate": hx(rate),
+                      "last_down": None if last_down is None else hx(last_down),
+                      "cfg": [hx(config.alpha), hx(config.beta), config.delta_iq,
+                              hx(config.cooldown_ms), hx(config.r_min)],
+                      "actions": action_list(acts),
+                      "stamp": None if "conf-fn" not in sc._last_scale_down else
+                      hx(sc._last_scale_down["conf-fn"])})
+
+    for name, build, rate, _ in _conformance_scenarios():
+        record(name, build(), rate)
+    c = build_cluster(2, functions=[make_function("conf-fn")])
+    place_running_pod(c, "p0", "conf-fn", 8, 50, 100, "gpu-000")
+    place_running_pod(c, "other", "other-fn", 1, 50, 100, "gpu-000")
+    record("fresh-gpu fallback", c, 1000.0)
+    c = build_cluster(3, functions=[make_function("conf-fn")])
+    place_running_pod(c, "pa", "conf-fn", 8, 25, 20, "gpu-000")
+    place_running_pod(c, "pb", "conf-fn", 8, 50, 20, "gpu-000")
+    record("vertical before horizontal", c, 500.0)
+    c = build_cluster(3, functions=[make_function("conf-fn")])
+    place_running_pod(c, "p0", "conf-fn", 8, 50, 100, "gpu-000")
+    c.clock_ms = 60_000.0
+    record("cooldown blocks", c, 50.0, last_down=50_000.0)
+    c.clock_ms = 80_001.0
+    record("cooldown expired", c, 50.0, last_down=50_000.0)
+    for seed, lo, hi, kind in ((99, 0, 600, "legal"), (7, None, None, "cover"),
+                               (31, 1.01, 20, "last-pod")):
+        rng = random.Random(seed)
+        for trial in range(300 if kind != "last-pod" else 200):
+            cluster = _random_cluster(rng)
+            if kind == "cover":
+                pods = cluster.pods_of("conf-fn")
+                cap = sum(table.throughput(8, p.sm_percent, p.quota_percent) for p in pods)
+                rate = rng.uniform(cap, cap * 3 + 50)
+            else:
+                rate = rng.uniform(lo, hi)
+            for step in (20, 7):
+                conf = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=step, cooldown_ms=30000,
+                                    r_min=1.0)
+                record(f"{kind}-{trial}-d{step}", cluster, rate, config=conf)
+    dump("scale.json", {"table": table_dict(table), "function": fn_dict(fn), "cases": cases})
+
+
+# -- whole scaler ticks (SimulationEngine._handle_scaler) --------------------------------
+
+
+def make_tick_world(hs, nfn, ngpu, seed, ns=10, nq=10, allowed_all=False):
+    """Functions with random gen_tables-style surfaces and a cluster."""
+    from hybridscale import FunctionSpec, PerfTable, PodConfig, build_cluster
+    rng = random.Random(seed)
+    bs = [1, 2, 4, 8, 16, 32]
+    ss = list(range(100 // ns, 101, 100 // ns))
+    qs = list(range(100 // nq, 101, 100 // nq))
+    tables, fns, params = {}, [], []
+    for i in range(nfn):
+        fid = f"fn-{i:04d}"
+        fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
+        params.append([hx(fixed), hx(per), hx(floor)])
+        lat = np.array([[[(fixed + per * b) * (floor + (1.0 - floor) * (100.0 / s)) * (100.0 / q)
+                          for q in qs] for s in ss] for b in bs])
+        tables[fid] = PerfTable(fid, bs, ss, qs, lat)
+        allowed = list(range(1, 33)) if allowed_all else rng.choice([[8], [1, 2, 4, 8], [4, 8, 16]])
+        fns.append(FunctionSpec(function_id=fid, baseline_latency_ms=20.0, perf_table_ref=fid,
+                                min_rps=rng.choice([None, 1.0, 5.0]), allowed_batches=allowed,
+                                initial=PodConfig(8, rng.choice([20, 25, 30]), 20, 1)))
+    cluster = build_cluster(ngpu, functions=fns)
+    return fns, tables, cluster, {"batches": bs, "sms": ss, "quotas": qs, "params": params}
+
+
+def gen_tick(hs):
+    """Multi-tick runs of the reference's per-tick loop.  Arrivals and the set of idle pods
+    are drawn per tick; the engine's own bootstrap places the initial pods."""
+    from hybridscale import ScalerConfig, SimConfig, WorkloadTrace
+    from hybridscale.sim import SimulationEngine
+    runs = []
+    specs = [  # (nfn, ngpu, seed, ticks, delta, alpha, beta)
+        (12, 6, 1, 8, 10, 0.9, 0.5), (40, 16, 2, 8, 10, 0.65, 0.45),
+        (100, 64, 3, 8, 10, 0.9, 0.5), (60, 20, 4, 8, 20, 0.8, 0.3),
+        (30, 40, 5, 8, 1, 0.9, 0.5),
+    ]
+    if os.environ.get("GOLDEN_BIG"):
+        specs.append((1000, 400, 0, 1, 10, 0.9, 0.5))
+    for nfn, ngpu, seed, nticks, delta, alpha, beta in specs:
+        fns, tables, cluster, tparams = make_tick_world(hs, nfn, ngpu, seed)
+        cfg = ScalerConfig(alpha=alpha, beta=beta, delta_iq=delta, cooldown_ms=3000.0, r_min=1.0)
+        simcfg = SimConfig(scaler_interval_ms=1000.0, cold_start_ms=1500.0)
+        trace = WorkloadTrace(entries=[], horizon_ms=1.0) if hasattr(hs, "WorkloadTrace") else None
+        kal = {"A": 1.0, "Q": 25.0, "H": 1.0, "D": 4.0, "P0": 1.0}
+        eng = SimulationEngine(trace, fns, tables, cluster, cfg, simcfg, "hybrid", kal)
+        eng._bootstrap()
+        recorded = []
+        orig = eng.policy.decide
+
+        def spy(function, cl, rate, _orig=orig):
+            acts = _orig(function, cl, rate)
+            recorded.extend(acts)
+            return acts
+        eng.policy.decide = spy
+        rng = random.Random(seed * 7919)
+        run = {"nfn": nfn, "ngpu": ngpu, "seed": seed, "delta": delta, "alpha": hx(alpha),
+               "beta": hx(beta), "cooldown_ms": hx(3000.0), "r_min": hx(1.0),
+               "interval_ms": hx(1000.0), "cold_start_ms": hx(1500.0),
+               "kalman": {k: hx(v) for k, v in kal.items()},
+               "functions": [fn_dict(f) for f in fns],
+               "tables": tparams,
+               "initial": cluster_dict(eng.cluster), "ticks": []}
+        caps = {f.function_id: tables[f.function_id].throughput(8, f.initial.sm_percent, 20)
+                for f in fns}
+        counter0 = eng._pod_counter
+        run["pod_counter0"] = counter0
+        for k in range(nticks):
+            now = 1000.0 * (k + 1)
+            # load swings (up, up, collapse, ...) so pods are added and then drained
+            swing = (2.5, 3.5, 0.15, 0.05, 2.0, 0.3, 4.0, 0.02)[k % 8]
+            arrivals = {f.function_id: int(rng.uniform(0.2, 1.5) * swing * caps[f.function_id])
+                        for f in fns}
+            busy = {pid for pid in eng._runtimes if rng.random() < 0.3}
+            for pid, rt in eng._runtimes.items():
+                rt.in_service = [] if pid in busy else None
+                rt.queue.clear()
+            for fid, a in arrivals.items():
+                eng._tick_arrivals[fid] = a
+            # ready events at or before `now` precede the scaler tick (hs/sim.py:40-44)
+            for pid, rt in list(eng._runtimes.items()):
+                if rt.pod.state.value == "cold_starting" and rt.pod.ready_at_ms <= now:
+                    eng._handle_ready(now, pid)
+            idle = sorted(pid for pid in eng._runtimes if pid not in busy)
+            recorded.clear()
+            before = cluster_dict(eng.cluster)
+            n_before = eng._pod_counter
+            eng._handle_scaler(now)
+            tl = eng._timeline[-nfn:]
+            run["ticks"].append({
+                "now": hx(now), "arrivals": [arrivals[f.function_id] for f in fns],
+                "idle": idle,
+                "actions": action_list(recorded),
+                "new_pods": [f"pod-{i:06d}" for i in range(n_before, eng._pod_counter)],
+                "observed": [hx(p.observed_rps) for p in tl],
+                "predicted": [hx(p.predicted_rps) for p in tl]})
+            for rt in eng._runtimes.values():
+                rt.in_service = None
+        run["final"] = cluster_dict(eng.cluster)
+        runs.append(run)
+    dump("tick.json", {"runs": runs})
+
+
+GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick}
 
 
 def main(argv):
