@@ -92,6 +92,44 @@ def make_config5_tables(n, seed=0, device=None):
     return tables
 
 
+def make_config4_world(nfn=1000, ngpu=400, seed=0, full_grid=False, device=None):
+    """Config 4: nfn functions with random gen_tables surfaces (6x10x10:
+    b=1..32 pow2, s,q=10..100 step 10; full_grid: 32x91x100 and delta 1), one pod each at
+    (b=8, s=20, q=20) placed round-robin over ngpu GPUs.  Returns (functions, tables,
+    cluster, caps) with caps[f] = throughput of the initial pod."""
+    from paper_2505_01968_b200 import PerfTable, allocator
+    from paper_2505_01968_b200.core import (ClusterState, FunctionSpec, GpuDevice, PodConfig,
+                                            PodInstance, PodState)
+    rng = random.Random(seed)
+    if full_grid:
+        bs, ss, qs = list(range(1, 33)), list(range(10, 101)), list(range(1, 101))
+    else:
+        bs, ss, qs = BATCHES, list(range(10, 101, 10)), list(range(10, 101, 10))
+    fns, tables, caps = [], {}, {}
+    for i in range(nfn):
+        fid = f"fn-{i:04d}"
+        fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
+        lat = surface(fixed, per, floor, 1.0 - floor, bs, ss, qs)
+        tables[fid] = PerfTable(fid, bs, ss, qs, lat, device=device)
+        fns.append(FunctionSpec(function_id=fid, baseline_latency_ms=20.0, perf_table_ref=fid,
+                                allowed_batches=list(BATCHES), initial=PodConfig(8, 20, 20)))
+        node = lat[bs.index(8), ss.index(20), qs.index(20)]
+        caps[fid] = 8 / (node / 1000.0)
+    cluster = ClusterState(gpus={f"gpu-{g:03d}": GpuDevice(f"gpu-{g:03d}") for g in range(ngpu)},
+                           functions={f.function_id: f for f in fns})
+    for i, f in enumerate(fns):
+        pod = PodInstance(f"pod-{i:06d}", f.function_id, 8, 20, 20, "",
+                          state=PodState.RUNNING)
+        allocator.place_pod(cluster, pod, f"gpu-{i % ngpu:03d}")
+    return fns, tables, cluster, caps
+
+
+def config4_arrivals(fns, caps, rng, interval_s, lo=0.0, hi=3.0):
+    """Per-tick request counts giving observed rates ~ U(lo, hi) x initial capability."""
+    return {f.function_id: int(rng.uniform(lo, hi) * caps[f.function_id] * interval_s)
+            for f in fns}
+
+
 def max_lattice_rps(table):
     """Max throughput of the (monotone) table's lattice: the (b_max, s_max, q=100) node."""
     lat = float(table.latency_ms[-1, -1, -1])

@@ -117,6 +117,93 @@ int rapp_mec_plan_run_dev(rapp_mec_plan *plan, const double *d_targets, int64_t 
                           int64_t fn_end, int32_t *d_out_bsq, uint64_t *d_out_key,
                           void *stream);
 
+/* ---- batched scaler tick (hs/sim.py:470-491 driving hs/autoscaler.py:73-234) ---------
+ * A device-resident scaler world: functions (in sorted-id order), their tables, the
+ * cluster (GPUs in sorted-id order with their partition lists in insertion order, pods),
+ * per-function Kalman state and scale-down stamps.  rapp_tick_run evaluates one scaler
+ * tick for every function — Kalman update, Autoscaler.scale, and the apply step — with
+ * the reference's sequential-commit semantics: function k decides against the cluster as
+ * left by functions 0..k-1 of the same tick. */
+
+typedef struct {
+    double alpha, beta;        /* ScalerConfig (hs/autoscaler.py:28-43) */
+    double cooldown_ms, r_min;
+    int32_t delta_iq;
+    int32_t _pad;
+    double interval_s;         /* scaler_interval_ms / 1000.0, computed by the caller */
+    double cold_start_ms;      /* SimConfig.cold_start_ms (new pods become RUNNING then) */
+    double kal_A, kal_Q, kal_H, kal_D, kal_P0;  /* Kalman defaults (hs/kalman.py:15-19) */
+} rapp_scaler_config;
+
+typedef struct {
+    int32_t table_id;          /* rapp_table_create id of perf_table_ref or function_id */
+    int32_t _pad;
+    double min_rps;            /* NaN: None (the scaler-wide r_min applies) */
+    int64_t lattice_off;       /* its most_efficient_config batch lattice (after the   */
+    int64_t lattice_len;       /*   _batch_lattice rule) inside `batch_lattice`        */
+    int32_t kal_init;          /* 1: R/P below hold state; 0: first tick initialises  */
+    int32_t _pad2;
+    double kal_R, kal_P;
+    double last_down_ms;       /* -inf when the function never scaled down */
+} rapp_fn_desc;
+
+typedef struct {
+    int32_t fn;                /* function index, or -1 for pods of unmanaged functions */
+    int32_t batch, sm, quota;
+    int32_t gpu;               /* GPU rank (position in sorted GPU ids) */
+    int32_t part;              /* position of its partition in the GPU's list */
+    int32_t state;             /* 0 COLD_STARTING, 1 RUNNING, 2 DRAINING */
+    int32_t _pad;
+    double ready_at_ms;
+    char id[32];               /* pod id, NUL-padded (string order decides ties) */
+} rapp_pod_desc;
+
+typedef struct {
+    int32_t fn;                /* function index */
+    int32_t kind;              /* 0 VERTICAL_UP 1 VERTICAL_DOWN 2 HORIZONTAL_UP 3 HORIZONTAL_DOWN */
+    int32_t batch, sm, quota;
+    int32_t pod;               /* pod index (new pods: the index created by the apply) */
+    int32_t gpu;               /* GPU rank */
+    int32_t released;          /* HORIZONTAL_DOWN: 1 if the idle pod was released */
+} rapp_action;
+
+typedef struct rapp_tick rapp_tick;
+
+/* part_off has n_gpus+1 entries; partitions are (sm, quota_allocated) pairs in list order.
+ * pod_counter is the next `pod-%06d` counter value for pods the ticks create. */
+int rapp_tick_create(rapp_ctx *ctx, const rapp_scaler_config *cfg, int64_t n_fns,
+                     const rapp_fn_desc *fns, const int64_t *batch_lattice, int64_t n_gpus,
+                     const int64_t *part_off, const int32_t *part_sm,
+                     const int32_t *part_alloc, int64_t n_pods, const rapp_pod_desc *pods,
+                     int64_t pod_counter, rapp_tick **out);
+int rapp_tick_destroy(rapp_tick *t);
+
+/* One tick at time now_ms.  arrivals[n_fns] are the tick's request counts; idle[i] (for
+ * every pod index < rapp_tick_pod_count) marks pods with no queued or in-service work, so
+ * that a HORIZONTAL_DOWN releases them at once.  If predicted != NULL the Kalman step is
+ * skipped and predicted[f] is used as the rate (Autoscaler.scale semantics).  Outputs:
+ * actions (capacity max_actions), n_actions, observed/predicted rates per function (either
+ * may be NULL).  The device world is updated in place. */
+int rapp_tick_run(rapp_tick *t, double now_ms, const int64_t *arrivals, const uint8_t *idle,
+                  const double *predicted_in, rapp_action *actions, int64_t max_actions,
+                  int64_t *n_actions, double *observed_out, double *predicted_out);
+
+/* Same with device buffers and no host synchronisation (for timing / graphs). */
+int rapp_tick_run_dev(rapp_tick *t, double now_ms, const int64_t *d_arrivals,
+                      const uint8_t *d_idle, void *stream);
+/* Device views of the last tick's outputs (valid until the next run). */
+int rapp_tick_outputs_dev(rapp_tick *t, const rapp_action **d_actions, const int32_t **d_count,
+                          const double **d_observed, const double **d_predicted);
+
+int rapp_tick_pod_count(rapp_tick *t, int64_t *n_pods);
+/* Host copy of the world (after any number of ticks): pods (alive flag via state -1 for
+ * released pods), per-function Kalman / stamp state, partitions per GPU, pod counter. */
+int rapp_tick_read_pods(rapp_tick *t, rapp_pod_desc *pods, int64_t cap, int64_t *n);
+int rapp_tick_read_fns(rapp_tick *t, rapp_fn_desc *fns);
+int rapp_tick_read_parts(rapp_tick *t, int64_t *part_off, int32_t *part_sm,
+                         int32_t *part_alloc, int32_t *part_npods, int64_t cap);
+int rapp_tick_counter(rapp_tick *t, int64_t *pod_counter);
+
 /* ---- kernel-launch accounting (evidence for bench.py's gpu_launches) ----------------- */
 int64_t rapp_launch_count(void);
 

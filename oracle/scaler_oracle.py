@@ -160,10 +160,28 @@ def scale(cfg, fn, table: OTable, cluster, R, last_down, pod_factory, part_facto
     return [], None
 
 
+class _Scratch:
+    """Independent copy of the parts of a cluster a scale-up stages on (gpus with their
+    partition lists, pods) — what copy.deepcopy(cluster) gives hs/autoscaler.py:111,
+    without copying the unrelated function specs."""
+
+    def __init__(self, cluster):
+        self.gpus = {}
+        for gid, g in cluster.gpus.items():
+            ng = copy.copy(g)
+            ng.partitions = []
+            for p in g.partitions:
+                np_ = copy.copy(p)
+                np_.resident_pods = list(p.resident_pods)
+                ng.partitions.append(np_)
+            self.gpus[gid] = ng
+        self.pods = {pid: copy.copy(p) for pid, p in cluster.pods.items()}
+
+
 def _up(cfg, fn, table, cluster, pods, gap, pod_factory, part_factory):
     d = cfg["delta"]
     fid = fn.function_id
-    scratch = copy.deepcopy(cluster)
+    scratch = _Scratch(cluster)
     out = []
     for pod in pods:
         if gap <= 0:
@@ -182,11 +200,10 @@ def _up(cfg, fn, table, cluster, pods, gap, pod_factory, part_factory):
             gap -= gain
     bref = pods[0].batch
     if gap > 0:
-        used = sorted({p.gpu_id for p in scratch.pods.values()})
-        def occ(g):
-            return sum(p.sm_percent * p.quota_percent for p in scratch.pods.values()
-                       if p.gpu_id == g) / 10000.0
-        gid = min(used, key=lambda g: (occ(g), g))
+        totals = {}
+        for p in scratch.pods.values():  # hgo: sum(sm * quota) / 10000.0 per GPU
+            totals[p.gpu_id] = totals.get(p.gpu_id, 0) + p.sm_percent * p.quota_percent
+        gid = min(sorted(totals), key=lambda g: (totals[g] / 10000.0, g))
         sm, qmax = best_slot(scratch.gpus[gid])
         if sm > 0 and qmax > 0:
             if table.thr(bref, sm, qmax) > gap:

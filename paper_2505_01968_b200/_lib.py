@@ -63,6 +63,21 @@ SIGNATURES = [
     ("rapp_mec_plan_points", ctypes.c_int, [c_vp, c_i64p]),
     ("rapp_mec_plan_run_dev", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp,
                                              c_vp, c_vp]),
+    ("rapp_tick_create", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_i64p,
+                                        ctypes.c_int64, c_i64p, c_i32p, c_i32p, ctypes.c_int64,
+                                        c_vp, ctypes.c_int64, ctypes.POINTER(c_vp)]),
+    ("rapp_tick_destroy", ctypes.c_int, [c_vp]),
+    ("rapp_tick_run", ctypes.c_int, [c_vp, ctypes.c_double, c_i64p, c_vp, c_vp, c_vp,
+                                     ctypes.c_int64, c_i64p, c_vp, c_vp]),
+    ("rapp_tick_run_dev", ctypes.c_int, [c_vp, ctypes.c_double, c_vp, c_vp, c_vp]),
+    ("rapp_tick_outputs_dev", ctypes.c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                             ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    ("rapp_tick_pod_count", ctypes.c_int, [c_vp, c_i64p]),
+    ("rapp_tick_read_pods", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_i64p]),
+    ("rapp_tick_read_fns", ctypes.c_int, [c_vp, c_vp]),
+    ("rapp_tick_read_parts", ctypes.c_int, [c_vp, c_i64p, c_i32p, c_i32p, c_i32p,
+                                            ctypes.c_int64]),
+    ("rapp_tick_counter", ctypes.c_int, [c_vp, c_i64p]),
     ("rapp_launch_count", ctypes.c_int64, []),
 ]
 

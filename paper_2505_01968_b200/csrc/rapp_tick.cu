@@ -1,0 +1,1379 @@
+// Batched scaler tick: every function's Kalman update + Autoscaler.scale + apply, in one
+// sequence of launches, with the reference's sequential-commit semantics.
+//
+// Reference (paths relative to /root/reference/pkg/src/hybridscale):
+//   tick driver        sim.py:470-491   (sorted functions; decide; apply; next function)
+//   apply              sim.py:493-525   (change_quota / place new COLD_STARTING pod /
+//                                        DRAINING + immediate release when idle)
+//   decision           autoscaler.py:73-234
+//   allocator          allocator.py:17-139
+//   Kalman             kalman.py:45-62
+//
+// Decomposition (exact):
+//  phase A (k_tick_phase_a, one warp per function, all functions in parallel) computes
+//    everything a function's decision reads from its OWN state only: the Kalman step, the
+//    non-draining pods sorted by (-sm, pod_id), capability (CPython 3.12 sum(): Neumaier
+//    compensated), the up / down / no-op classification, the whole scale-down walk (it
+//    never reads shared state), and for scale-up the throughput of every pod at every
+//    quota step.  No other function can change these inputs within a tick.
+//  phase A2 (k_tick_grid) tabulates throughput(batch_ref, sm, q) for sm, q in 1..100 of
+//    every scale-up function: the used-GPU branch reads only this table once the GPU and
+//    its best slot are known.
+//  phase B (k_tick_commit, one warp) walks the functions in order and performs the parts
+//    that read shared state — partition headroom for the vertical walk, the lowest
+//    (occupancy, gpu id) used GPU, its best slot, the covering quota, the first free GPU
+//    and the fresh-GPU configuration search (prefix-max index, see below) — applying each
+//    action to the device cluster before the next function decides.
+//
+// Every floating-point expression is evaluated in the reference's order with individually
+// rounded operations (interp3 / throughput from rapp_device.cuh; explicit _rn intrinsics).
+#include <array>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <algorithm>
+#include <vector>
+
+#include "rapp_device.cuh"
+#include "rapp_internal.h"
+
+namespace rapp {
+
+constexpr int kMaxPods = 32;   // pods per managed function
+constexpr int kPartCap = 100;  // partitions per GPU (each >= 1 SM%, sum <= 100)
+constexpr int kRow = 101;      // quota steps per pod row
+constexpr int kCold = 0, kRunning = 1, kDraining = 2, kDead = -1;
+constexpr int kNone = 0, kUp = 1, kDown = 2;
+enum : int { kVUp = 0, kVDown = 1, kHUp = 2, kHDown = 3 };
+
+struct PodId {
+  uint64_t w[4];  // id bytes, big-endian packed: integer order == byte-string order
+};
+
+__host__ __device__ inline bool id_less(const PodId& a, const PodId& b) {
+  for (int i = 0; i < 4; ++i)
+    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  return false;
+}
+
+struct DownAct {
+  int32_t kind, pod, quota, _pad;
+};
+
+// partition entry: sm (8 bits) | alloc (8 bits) | npods (16 bits) | uid (32 bits)
+__host__ __device__ inline uint64_t part_pack(int sm, int alloc, int npods, uint32_t uid) {
+  return uint64_t(uint32_t(sm) & 0xFF) | (uint64_t(uint32_t(alloc) & 0xFF) << 8) |
+         (uint64_t(uint32_t(npods) & 0xFFFF) << 16) | (uint64_t(uid) << 32);
+}
+__host__ __device__ inline int part_sm(uint64_t e) { return int(e & 0xFF); }
+__host__ __device__ inline int part_alloc(uint64_t e) { return int((e >> 8) & 0xFF); }
+__host__ __device__ inline int part_npods(uint64_t e) { return int((e >> 16) & 0xFFFF); }
+__host__ __device__ inline uint32_t part_uid(uint64_t e) { return uint32_t(e >> 32); }
+
+struct World {
+  // config
+  double alpha, beta, cooldown, r_min, interval_s, cold_start, kA, kQ, kH, kD, kP0;
+  int delta, F, G, pod_cap;
+  // tables
+  const TableDesc* tds;
+  const double* pool;
+  // functions
+  const int32_t* fn_table;
+  const double* fn_min_rps;
+  const int64_t* fn_lat_off;     // most_efficient_config lattice offsets (prefix-max index)
+  const int64_t* fn_lat_len;     // lattice points of f = nB_f * nS * nQ
+  const int32_t* fn_nb;          // |B_f|
+  const int64_t* fn_boff;        // batch list offset
+  const double* blist;           // batch lattices (sorted unique, as doubles)
+  const int32_t* fn_pairs_off;   // (s,q) pairs in key order, per lattice shape
+  const int32_t* fn_npairs;
+  const int32_t* pairs;          // packed s_index << 16 | q
+  const double* pmax;            // prefix max of rps along the key-sorted lattice
+  int32_t* k_init;
+  double* k_R;
+  double* k_P;
+  double* last_down;
+  int32_t* fn_npods;
+  int32_t* fn_pods;              // [F][kMaxPods]
+  // gpus
+  int32_t* g_npods;
+  int32_t* g_hgo;                // sum of sm*quota over resident pods (any state)
+  int32_t* g_nparts;
+  int32_t* g_freesm;
+  uint32_t* g_nextuid;
+  uint64_t* g_parts;             // [G][kPartCap] in list order
+  // pods
+  int32_t* n_pods;               // device counter (pods ever created, incl. released)
+  int32_t* p_fn;
+  int32_t* p_b;
+  int32_t* p_s;
+  int32_t* p_q;
+  int32_t* p_gpu;
+  uint32_t* p_puid;
+  int32_t* p_state;
+  double* p_ready;
+  PodId* p_id;
+  const uint8_t* p_idle;         // per tick input
+  int64_t* counter;              // next pod-%06d counter
+  // phase A / A2 outputs
+  double* obs;
+  double* pred;
+  int32_t* cls;
+  double* gap0;
+  int32_t* nsorted;              // non-draining pods of f, sorted by (-sm, id)
+  int32_t* sorted;               // [F][kMaxPods]
+  int32_t* row_kd;               // [F][kMaxPods] index of q0 inside the row
+  double* rows;                  // [F][kMaxPods][kRow] throughput at q0 + k*delta
+  int32_t* bref;                 // batch of sorted[0]
+  double* tgrid;                 // [F][100][100] throughput(bref, sm, q)
+  int32_t* ndown;
+  DownAct* down;                 // [F][kMaxPods]
+  int32_t* stamp;                // 1: record last_down = now
+  // outputs
+  rapp_action* actions;
+  int32_t* n_actions;
+  int32_t* err;                  // first error code (RAPP_E_*)
+  int32_t* err_fn;
+};
+
+__device__ __forceinline__ double thr_at(const World& w, int f, double b, double s, double q) {
+  const TableDesc td = w.tds[w.fn_table[f]];
+  const double* seg = w.pool + td.off;
+  const double lat = interp3(seg + td.ob, td.nb, seg + td.os, td.ns, seg + td.oq, td.nq,
+                             seg + td.ov, b, s, q);
+  return throughput(b, lat);  // b / (lat / 1000.0), hs/perf.py:95-98
+}
+
+__device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
+  const TableDesc td = w.tds[w.fn_table[f]];
+  const double* ba = w.pool + td.off + td.ob;
+  const double x = double(b);
+  return !(x < ba[0] || x > ba[td.nb - 1]);  // hs/perf.py:88-91
+}
+
+__device__ void set_err(const World& w, int code, int f) {
+  if (atomicCAS(w.err, 0, code) == 0) *w.err_fn = f;
+}
+
+// ---------------------------------------------------------------------------------------
+// prologue: cold starts that ended at or before `now` (ready events precede the scaler
+// event at equal timestamps, sim.py:40-44), output reset
+// ---------------------------------------------------------------------------------------
+__global__ void k_tick_prologue(World w, double now) {
+  const int n = *w.n_pods;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    if (w.p_state[p] == kCold && w.p_ready[p] <= now) w.p_state[p] = kRunning;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *w.n_actions = 0;
+    *w.err = 0;
+    *w.err_fn = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// phase A: one warp per function
+// ---------------------------------------------------------------------------------------
+__global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ arrivals,
+                               const double* __restrict__ pred_in) {
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= w.F) return;
+  __shared__ int s_sorted[8][kMaxPods];
+  __shared__ int s_run[8][kMaxPods];
+  int* srt = s_sorted[(threadIdx.x >> 5) & 7];
+  int* run = s_run[(threadIdx.x >> 5) & 7];
+
+  // Kalman (kalman.py:45-62; first tick initialises R = observed, P = P0, sim.py:476-479)
+  double R = 0.0;
+  if (lane == 0) {
+    const double obs = __ddiv_rn(double(arrivals[f]), w.interval_s);
+    if (pred_in != nullptr) {
+      R = pred_in[f];
+    } else {
+      double kR = w.k_init[f] ? w.k_R[f] : obs;
+      double kP = w.k_init[f] ? w.k_P[f] : w.kP0;
+      const double r_pred = __dmul_rn(w.kA, kR);
+      const double p_pred = __dadd_rn(__dmul_rn(__dmul_rn(w.kA, kP), w.kA), w.kQ);
+      const double denom = __dadd_rn(__dmul_rn(__dmul_rn(w.kH, p_pred), w.kH), w.kD);
+      if (denom == 0.0) set_err(w, RAPP_E_DEGENERATE, f);
+      const double gain = __ddiv_rn(__dmul_rn(p_pred, w.kH), denom);
+      const double r_new =
+          __dadd_rn(r_pred, __dmul_rn(gain, __dsub_rn(obs, __dmul_rn(w.kH, r_pred))));
+      const double p_new = __dmul_rn(__dsub_rn(1.0, __dmul_rn(gain, w.kH)), p_pred);
+      w.k_R[f] = r_new;
+      w.k_P[f] = p_new;
+      w.k_init[f] = 1;
+      R = r_new > 0.0 ? r_new : 0.0;  // max(0.0, r_new)
+    }
+    w.obs[f] = obs;
+    w.pred[f] = R;
+  }
+  R = __shfl_sync(0xffffffffu, R, 0);
+
+  // non-draining pods sorted by (-sm, pod_id) (autoscaler.py:81-85)
+  int m = 0;
+  if (lane == 0) {
+    const int n = w.fn_npods[f];
+    for (int i = 0; i < n; ++i) {
+      const int p = w.fn_pods[f * kMaxPods + i];
+      if (w.p_state[p] == kDraining) continue;
+      int j = m++;
+      while (j > 0) {
+        const int o = srt[j - 1];
+        const bool before = w.p_s[p] > w.p_s[o] || (w.p_s[p] == w.p_s[o] && id_less(w.p_id[p], w.p_id[o]));
+        if (!before) break;
+        srt[j] = o;
+        --j;
+      }
+      srt[j] = p;
+    }
+    w.nsorted[f] = m;
+    for (int j = 0; j < m; ++j) w.sorted[f * kMaxPods + j] = srt[j];
+  }
+  __syncwarp();
+  m = __shfl_sync(0xffffffffu, m, 0);
+  if (m == 0) {
+    if (lane == 0) w.cls[f] = kNone;
+    return;
+  }
+
+  // throughput at the current quota of every pod (row entry k = 0)
+  const int d = w.delta;
+  double* rows = w.rows + int64_t(f) * kMaxPods * kRow;
+  for (int j = lane; j < m; j += 32) {
+    const int p = srt[j];
+    const int q0 = w.p_q[p];
+    const int kd = (q0 - 1) / d;
+    w.row_kd[f * kMaxPods + j] = kd;
+    if (!batch_ok(w, f, w.p_b[p])) set_err(w, RAPP_E_VALUE, f);
+    rows[j * kRow + kd] = thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0));
+  }
+  __syncwarp();
+
+  int cls = kNone;
+  double cap = 0.0;
+  if (lane == 0) {
+    // capability = sum(...) in sorted order: CPython 3.12 float sum (Neumaier), started
+    // from the first element (int 0 + x == x)
+    double s = rows[0 * kRow + w.row_kd[f * kMaxPods + 0]], c = 0.0;
+    for (int j = 1; j < m; ++j) {
+      const double x = rows[j * kRow + w.row_kd[f * kMaxPods + j]];
+      const double t = __dadd_rn(s, x);
+      if (fabs(s) >= fabs(x))
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
+      else
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+      s = t;
+    }
+    if (c != 0.0 && isfinite(c)) s = __dadd_rn(s, c);
+    cap = s;
+    const double up_thr = __dmul_rn(cap, w.alpha);
+    if (R > up_thr) {
+      cls = kUp;
+      w.gap0[f] = __dsub_rn(R, up_thr);
+      w.bref[f] = w.p_b[srt[0]];
+    } else {
+      const double mr = w.fn_min_rps[f];
+      const double r_min = mr != mr ? w.r_min : mr;
+      if (R < __dmul_rn(cap, w.beta) && R > r_min &&
+          __dsub_rn(now, w.last_down[f]) >= w.cooldown)
+        cls = kDown;
+    }
+  }
+  cls = __shfl_sync(0xffffffffu, cls, 0);
+
+  if (cls == kUp) {
+    // rows k = 1..ku of RUNNING pods (the vertical walk skips the others)
+    for (int j = 0; j < m; ++j) {
+      const int p = srt[j];
+      if (w.p_state[p] != kRunning) continue;
+      const int q0 = w.p_q[p];
+      const int kd = (q0 - 1) / d, ku = (100 - q0) / d;
+      for (int k = 1 + lane; k <= ku; k += 32)
+        rows[j * kRow + kd + k] =
+            thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 + k * d));
+    }
+    if (lane == 0) w.cls[f] = kUp;
+    return;
+  }
+  if (cls != kDown) {
+    if (lane == 0) w.cls[f] = kNone;
+    return;
+  }
+
+  // ---- scale-down (autoscaler.py:188-234): RUNNING pods by (sm, pod_id) ascending ----
+  int nr = 0;
+  if (lane == 0) {
+    for (int j = 0; j < m; ++j) {
+      const int p = srt[j];
+      if (w.p_state[p] != kRunning) continue;
+      int i = nr++;
+      while (i > 0) {
+        const int o = run[i - 1];
+        const bool before = w.p_s[p] < w.p_s[o] || (w.p_s[p] == w.p_s[o] && id_less(w.p_id[p], w.p_id[o]));
+        if (!before) break;
+        run[i] = o;
+        --i;
+      }
+      run[i] = p;
+    }
+  }
+  __syncwarp();
+  nr = __shfl_sync(0xffffffffu, nr, 0);
+  // rows k = -kd..-1 for those pods; reuse the sorted-order row slots by pod lookup
+  for (int i = 0; i < nr; ++i) {
+    const int p = run[i];
+    int j = 0;
+    while (srt[j] != p) ++j;
+    const int q0 = w.p_q[p];
+    const int kd = (q0 - 1) / d;
+    for (int k = 1 + lane; k <= kd; k += 32)
+      rows[j * kRow + kd - k] =
+          thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 - k * d));
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double excess = __dsub_rn(cap, R);
+    int alive = nr, na = 0;
+    DownAct* out = w.down + f * kMaxPods;
+    for (int i = 0; i < nr; ++i) {
+      if (excess <= 0.0) break;
+      const int p = run[i];
+      int j = 0;
+      while (srt[j] != p) ++j;
+      const double* row = rows + j * kRow;
+      const int q0 = w.p_q[p];
+      const int kd = (q0 - 1) / d;
+      const double cur = row[kd];
+      int q = q0;
+      double shed = 0.0;
+      while (q > 0 && __dsub_rn(excess, shed) > 0.0) {
+        q = q - d > 0 ? q - d : 0;
+        shed = q == 0 ? cur : __dsub_rn(cur, row[kd - (q0 - q) / d]);
+      }
+      if (q == 0) {
+        if (alive <= 1) {
+          const int floor_q = q0 - d * ((q0 - 1) / d);
+          if (floor_q < q0) {
+            shed = __dsub_rn(cur, row[kd - (q0 - floor_q) / d]);
+            out[na++] = DownAct{kVDown, p, floor_q, 0};
+            excess = __dsub_rn(excess, shed);
+          }
+          continue;
+        }
+        --alive;
+        out[na++] = DownAct{kHDown, p, 0, 0};
+        excess = __dsub_rn(excess, cur);
+      } else if (q < q0) {
+        out[na++] = DownAct{kVDown, p, q, 0};
+        excess = __dsub_rn(excess, shed);
+      }
+    }
+    w.ndown[f] = na;
+    w.stamp[f] = na > 0;
+    w.cls[f] = kDown;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// phase A2: throughput(batch_ref, sm, q) for sm, q in 1..100 of every scale-up function
+// ---------------------------------------------------------------------------------------
+__global__ void k_tick_grid(World w) {
+  const int f = blockIdx.x / 100, sm = blockIdx.x % 100 + 1;
+  if (w.cls[f] != kUp) return;
+  const int b = w.bref[f];
+  if (!batch_ok(w, f, b)) return;  // phase B raises if the value is ever needed
+  for (int q = threadIdx.x + 1; q <= 100; q += blockDim.x)
+    w.tgrid[(int64_t(f) * 100 + (sm - 1)) * 100 + (q - 1)] =
+        thr_at(w, f, double(b), double(sm), double(q));
+}
+
+// ---------------------------------------------------------------------------------------
+// phase B: sequential commit (one warp)
+// ---------------------------------------------------------------------------------------
+struct Commit {
+  const World& w;
+  int lane;
+
+  __device__ uint64_t* parts(int g) const { return w.g_parts + int64_t(g) * kPartCap; }
+
+  // position of the partition with this uid on GPU g (partition_of, core.py:148-158)
+  __device__ int find_part(int g, uint32_t uid) const {
+    const uint64_t* P = parts(g);
+    const int n = w.g_nparts[g];
+    int pos = 1 << 30;
+    for (int i = lane; i < n; i += 32)
+      if (part_uid(P[i]) == uid) pos = min(pos, i);
+    for (int o = 16; o > 0; o >>= 1) pos = min(pos, __shfl_xor_sync(0xffffffffu, pos, o));
+    return pos;
+  }
+
+  __device__ void set_entry(int g, int pos, uint64_t e) const {
+    __syncwarp();
+    if (lane == 0) parts(g)[pos] = e;
+    __syncwarp();
+  }
+
+  // change_quota (allocator.py:111-125) + occupancy bookkeeping
+  __device__ void change_quota(int p, int new_q) const {
+    const int g = w.p_gpu[p];
+    const int pos = find_part(g, w.p_puid[p]);
+    const uint64_t e = parts(g)[pos];
+    const int delta = new_q - w.p_q[p];
+    set_entry(g, pos, part_pack(part_sm(e), part_alloc(e) + delta, part_npods(e), part_uid(e)));
+    if (lane == 0) {
+      w.g_hgo[g] += w.p_s[p] * delta;
+      w.p_q[p] = new_q;
+    }
+    __syncwarp();
+  }
+
+  // place_pod (allocator.py:85-108): join the first same-sm partition with headroom, else
+  // append a new partition
+  __device__ void place(int p, int g) const {
+    uint64_t* P = parts(g);
+    const int n = w.g_nparts[g];
+    const int s = w.p_s[p], q = w.p_q[p];
+    int pos = 1 << 30;
+    for (int i = lane; i < n; i += 32)
+      if (part_sm(P[i]) == s && 100 - part_alloc(P[i]) >= q) pos = min(pos, i);
+    for (int o = 16; o > 0; o >>= 1) pos = min(pos, __shfl_xor_sync(0xffffffffu, pos, o));
+    __syncwarp();
+    if (lane == 0) {
+      if (pos == (1 << 30)) {
+        if (n >= kPartCap || w.g_freesm[g] < s) {
+          set_err(w, RAPP_E_PLACEMENT, -1);
+        } else {
+          const uint32_t uid = w.g_nextuid[g]++;
+          P[n] = part_pack(s, q, 1, uid);
+          w.g_nparts[g] = n + 1;
+          w.g_freesm[g] -= s;
+          w.p_puid[p] = uid;
+        }
+      } else {
+        const uint64_t e = P[pos];
+        P[pos] = part_pack(part_sm(e), part_alloc(e) + q, part_npods(e) + 1, part_uid(e));
+        w.p_puid[p] = part_uid(e);
+      }
+      w.p_gpu[p] = g;
+      w.g_npods[g] += 1;
+      w.g_hgo[g] += s * q;
+    }
+    __syncwarp();
+  }
+
+  // release_pod (allocator.py:128-139): an emptied partition leaves the list (list.remove)
+  __device__ void release(int p) const {
+    const int g = w.p_gpu[p];
+    const int pos = find_part(g, w.p_puid[p]);
+    __syncwarp();
+    if (lane == 0) {
+      uint64_t* P = parts(g);
+      const uint64_t e = P[pos];
+      const int np = part_npods(e) - 1;
+      if (np == 0) {
+        const int n = w.g_nparts[g];
+        for (int i = pos; i + 1 < n; ++i) P[i] = P[i + 1];
+        w.g_nparts[g] = n - 1;
+        w.g_freesm[g] += part_sm(e);
+      } else {
+        P[pos] = part_pack(part_sm(e), part_alloc(e) - w.p_q[p], np, part_uid(e));
+      }
+      w.g_npods[g] -= 1;
+      w.g_hgo[g] -= w.p_s[p] * w.p_q[p];
+      w.p_state[p] = kDead;
+      // drop from its function's pod list
+      const int f = w.p_fn[p];
+      if (f >= 0) {
+        int* L = w.fn_pods + f * kMaxPods;
+        const int n2 = w.fn_npods[f];
+        for (int i = 0; i < n2; ++i)
+          if (L[i] == p) {
+            L[i] = L[n2 - 1];
+            break;
+          }
+        w.fn_npods[f] = n2 - 1;
+      }
+    }
+    __syncwarp();
+  }
+
+  __device__ void emit(int f, int kind, int b, int s, int q, int pod, int gpu, int rel) const {
+    if (lane == 0) {
+      const int i = (*w.n_actions)++;
+      w.actions[i] = rapp_action{f, kind, b, s, q, pod, gpu, rel};
+    }
+    __syncwarp();
+  }
+
+  // new COLD_STARTING pod pod-%06d (sim.py:337-340, 505-516)
+  __device__ int new_pod(int f, int b, int s, int q, double now) const {
+    int p = 0;
+    if (lane == 0) {
+      p = (*w.n_pods)++;
+      if (p >= w.pod_cap || w.fn_npods[f] >= kMaxPods) {
+        set_err(w, RAPP_E_ARG, f);
+        p = -1;
+      } else {
+        const int64_t c = (*w.counter)++;
+        char buf[32] = {0};
+        const char* pre = "pod-";
+        int len = 0;
+        for (; pre[len]; ++len) buf[len] = pre[len];
+        char dig[24];
+        int nd = 0;
+        int64_t v = c;
+        do {
+          dig[nd++] = char('0' + v % 10);
+          v /= 10;
+        } while (v > 0);
+        for (int k = nd; k < 6; ++k) buf[len++] = '0';
+        while (nd > 0) buf[len++] = dig[--nd];
+        PodId id;
+        for (int i = 0; i < 4; ++i) {
+          uint64_t x = 0;
+          for (int k = 0; k < 8; ++k) x = (x << 8) | uint8_t(buf[i * 8 + k]);
+          id.w[i] = x;
+        }
+        w.p_id[p] = id;
+        w.p_fn[p] = f;
+        w.p_b[p] = b;
+        w.p_s[p] = s;
+        w.p_q[p] = q;
+        w.p_state[p] = kCold;
+        w.p_ready[p] = __dadd_rn(now, w.cold_start);
+        w.fn_pods[f * kMaxPods + w.fn_npods[f]++] = p;
+      }
+    }
+    p = __shfl_sync(0xffffffffu, p, 0);
+    return p;
+  }
+
+  // lowest (occupancy, rank) among used GPUs (autoscaler.py:139-141); occupancy compares
+  // as the integer sum(sm*quota): /10000.0 is monotone and injective on 0..10000
+  __device__ int argmin_used() const {
+    long long best = LLONG_MAX;
+    for (int g = lane; g < w.G; g += 32)
+      if (w.g_npods[g] > 0) {
+        const long long k = (long long)w.g_hgo[g] << 32 | g;
+        best = k < best ? k : best;
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long x = __shfl_xor_sync(0xffffffffu, best, o);
+      best = x < best ? x : best;
+    }
+    return best == LLONG_MAX ? -1 : int(best & 0xFFFFFFFF);
+  }
+
+  __device__ int first_free() const {
+    int best = 1 << 30;
+    for (int g = lane; g < w.G; g += 32)
+      if (w.g_npods[g] == 0) best = min(best, g);
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    return best == (1 << 30) ? -1 : best;
+  }
+
+  // max_avail_quota_and_sm (allocator.py:26-52): max of (sm*hr, sm, join=1) over
+  // partitions with headroom (first wins ties), then (free*100, free, 0) if strictly greater
+  __device__ void best_slot(int g, int& sm, int& q) const {
+    const uint64_t* P = parts(g);
+    const int n = w.g_nparts[g];
+    // key: prod (15 bits) | sm (8) | (255 - pos) (8): max key = max (prod, sm), first pos
+    long long best = -1;
+    for (int i = lane; i < n; i += 32) {
+      const int hr = 100 - part_alloc(P[i]);
+      if (hr > 0) {
+        const long long k = ((long long)(part_sm(P[i]) * hr) << 16) |
+                            ((long long)part_sm(P[i]) << 8) | (255 - i);
+        best = k > best ? k : best;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long x = __shfl_xor_sync(0xffffffffu, best, o);
+      best = x > best ? x : best;
+    }
+    sm = 0;
+    q = 0;
+    long long bprod = -1, bsm = -1, bjoin = -1;
+    if (best >= 0) {
+      const int pos = 255 - int(best & 0xFF);
+      sm = part_sm(P[pos]);
+      q = 100 - part_alloc(P[pos]);
+      bprod = (long long)sm * q;
+      bsm = sm;
+      bjoin = 1;
+    }
+    const int free_sm = w.g_freesm[g];
+    if (free_sm > 0) {
+      const long long fp = (long long)free_sm * 100;
+      const bool greater = best < 0 || fp > bprod || (fp == bprod && (free_sm > bsm ||
+                           (free_sm == bsm && 0 > bjoin)));
+      if (greater) {
+        sm = free_sm;
+        q = 100;
+      }
+    }
+  }
+
+  // most_efficient_config(target) via the key-sorted prefix-max index: the first lattice
+  // point (in (s*q, s, q, b) order) with prefix max >= min(target, max rps)
+  __device__ void mec(int f, double target, int& b, int& s, int& q) const {
+    const double* pm = w.pmax + w.fn_lat_off[f];
+    const int64_t L = w.fn_lat_len[f];
+    const double top = pm[L - 1];
+    const double t = target <= top ? target : top;  // target > top -> max-rps fallback
+    // 32-ary search for the first index with pm[i] >= t (pm non-decreasing, pm[L-1] >= t):
+    // invariant: the answer lies in [lo, hi]; probes past hi count as ">= t"
+    int64_t lo = 0, hi = L - 1;
+    while (hi - lo > 31) {
+      const int64_t step = (hi - lo + 31) / 32;
+      const int64_t probe = lo + step * lane;
+      const bool ge = probe > hi || pm[probe] >= t;
+      const unsigned mask = __ballot_sync(0xffffffffu, ge);
+      if (mask == 0) {
+        lo = lo + step * 31 + 1;
+      } else {
+        const int first = __ffs(mask) - 1;
+        if (first == 0) {
+          hi = lo;
+        } else {
+          const int64_t ph = lo + step * first;
+          lo = lo + step * (first - 1) + 1;
+          hi = ph < hi ? ph : hi;
+        }
+      }
+    }
+    const int64_t probe = lo + lane;
+    const bool ge = probe > hi || pm[probe] >= t;
+    const unsigned mask = __ballot_sync(0xffffffffu, ge);
+    const int64_t idx = lo + (__ffs(mask) - 1);
+    const int nb = w.fn_nb[f];
+    const int pair = w.pairs[w.fn_pairs_off[f] + int(idx / nb)];
+    const TableDesc td = w.tds[w.fn_table[f]];
+    b = int(w.blist[w.fn_boff[f] + idx % nb]);
+    s = int(w.pool[td.off + td.os + (pair >> 16)]);
+    q = pair & 0xFFFF;
+  }
+
+  __device__ void scale_up(int f, double now) const {
+    const int d = w.delta;
+    double gap = w.gap0[f];
+    const int m = w.nsorted[f];
+    const int* srt = w.sorted + f * kMaxPods;
+    const double* rows = w.rows + int64_t(f) * kMaxPods * kRow;
+    // vertical first, largest sm first (autoscaler.py:115-133)
+    for (int j = 0; j < m; ++j) {
+      if (!(gap > 0.0)) break;
+      const int p = srt[j];
+      if (w.p_state[p] != kRunning) continue;
+      const int g = w.p_gpu[p];
+      const int pos = find_part(g, w.p_puid[p]);
+      const int q0 = w.p_q[p];
+      const int avail = q0 + (100 - part_alloc(parts(g)[pos]));
+      const int kd = w.row_kd[f * kMaxPods + j];
+      const double* row = rows + j * kRow + kd;  // row[k] = thr at q0 + k*d
+      const double cur = row[0];
+      // k* = first k >= 0 with q0+(k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0
+      int kstar = -1;
+      for (int base = 0; kstar < 0; base += 32) {
+        const int k = base + lane;
+        bool stop;
+        if (q0 + (k + 1) * d > avail) {
+          stop = true;
+        } else {
+          const double gain = k == 0 ? 0.0 : __dsub_rn(row[k], cur);
+          stop = !(__dsub_rn(gap, gain) > 0.0);
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, stop);
+        if (mask) kstar = base + __ffs(mask) - 1;
+      }
+      if (kstar > 0) {
+        const int nq = q0 + kstar * d;
+        const double gain = __dsub_rn(row[kstar], cur);
+        change_quota(p, nq);
+        emit(f, kVUp, w.p_b[p], w.p_s[p], nq, p, g, 0);
+        gap = __dsub_rn(gap, gain);
+      }
+    }
+    const int bref = w.bref[f];
+    // one pod on the used GPU with the lowest occupancy (autoscaler.py:137-152)
+    if (gap > 0.0) {
+      const int g = argmin_used();
+      if (g >= 0) {
+        int sm, qmax;
+        best_slot(g, sm, qmax);
+        if (sm > 0 && qmax > 0) {
+          if (!batch_ok(w, f, bref)) {
+            if (lane == 0) set_err(w, RAPP_E_VALUE, f);
+            return;
+          }
+          const double* T = w.tgrid + (int64_t(f) * 100 + (sm - 1)) * 100;
+          const double cmax = T[qmax - 1];
+          if (cmax > gap) {
+            // _covering_quota (autoscaler.py:168-175): first multiple of d <= qmax with
+            // throughput >= gap, else qmax
+            int quota = qmax;
+            for (int base = 0; base * d < qmax; base += 32) {
+              const int qq = (base + lane + 1) * d;
+              const bool hit = qq <= qmax && T[qq - 1] >= gap;
+              const unsigned mask = __ballot_sync(0xffffffffu, hit);
+              if (mask) {
+                quota = (base + __ffs(mask)) * d;
+                break;
+              }
+            }
+            const int p = new_pod(f, bref, sm, quota, now);
+            if (p < 0) return;
+            place(p, g);
+            emit(f, kHUp, bref, sm, quota, p, g, 0);
+            gap = __dsub_rn(gap, T[quota - 1]);
+          }
+        }
+      }
+    }
+    // one pod on a fresh GPU at the most cost-efficient configuration (autoscaler.py:155-165)
+    if (gap > 0.0) {
+      const int g = first_free();
+      if (g >= 0) {
+        int b, s, q;
+        mec(f, gap, b, s, q);
+        const int p = new_pod(f, b, s, q, now);
+        if (p < 0) return;
+        place(p, g);
+        emit(f, kHUp, b, s, q, p, g, 0);
+      }
+    }
+  }
+
+  __device__ void scale_down(int f, double now) const {
+    const int na = w.ndown[f];
+    const DownAct* acts = w.down + f * kMaxPods;
+    for (int i = 0; i < na; ++i) {
+      const DownAct a = acts[i];
+      const int p = a.pod;
+      const int g = w.p_gpu[p];
+      if (a.kind == kVDown) {
+        change_quota(p, a.quota);
+        emit(f, kVDown, w.p_b[p], w.p_s[p], a.quota, p, g, 0);
+      } else {
+        const int b = w.p_b[p], s = w.p_s[p];
+        const bool idle = w.p_idle[p] != 0;
+        if (lane == 0) w.p_state[p] = kDraining;
+        __syncwarp();
+        if (idle) release(p);
+        emit(f, kHDown, b, s, 0, p, g, idle ? 1 : 0);
+      }
+    }
+    if (lane == 0 && w.stamp[f]) w.last_down[f] = now;
+    __syncwarp();
+  }
+};
+
+__global__ void __launch_bounds__(32) k_tick_commit(World w, double now) {
+  Commit c{w, int(threadIdx.x & 31)};
+  for (int f = 0; f < w.F; ++f) {
+    if (*(volatile int32_t*)w.err) return;
+    const int cls = w.cls[f];
+    if (cls == kUp)
+      c.scale_up(f, now);
+    else if (cls == kDown)
+      c.scale_down(f, now);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// prefix-max index for the fresh-GPU search (built once; tables are immutable)
+// ---------------------------------------------------------------------------------------
+__global__ void k_index_rps(World w, int f0) {
+  const int f = f0 + blockIdx.y;
+  if (f >= w.F) return;
+  const int64_t L = w.fn_lat_len[f];
+  const int nb = w.fn_nb[f];
+  const TableDesc td = w.tds[w.fn_table[f]];
+  double* out = const_cast<double*>(w.pmax) + w.fn_lat_off[f];
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int pair = w.pairs[w.fn_pairs_off[f] + int(i / nb)];
+    const double b = w.blist[w.fn_boff[f] + i % nb];
+    const double s = w.pool[td.off + td.os + (pair >> 16)];
+    const double q = double(pair & 0xFFFF);
+    out[i] = thr_at(w, f, b, s, q);
+  }
+}
+
+// in-place inclusive prefix max per function (one CTA per function, chunked scan)
+__global__ void k_index_scan(World w, int f0) {
+  const int f = f0 + blockIdx.x;
+  if (f >= w.F) return;
+  const int64_t L = w.fn_lat_len[f];
+  double* a = const_cast<double*>(w.pmax) + w.fn_lat_off[f];
+  __shared__ double s_carry;
+  __shared__ double s_warp[32];
+  if (threadIdx.x == 0) s_carry = -INFINITY;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t base = 0; base < L; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    double v = i < L ? a[i] : -INFINITY;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double x = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v = x > v ? x : v;
+    }
+    if (lane == 31) s_warp[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      double x = lane < nw ? s_warp[lane] : -INFINITY;
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = y > x ? y : x;
+      }
+      if (lane < nw) s_warp[lane] = x;
+    }
+    __syncthreads();
+    const double carry = s_carry;
+    if (wid > 0) v = s_warp[wid - 1] > v ? s_warp[wid - 1] : v;
+    v = carry > v ? carry : v;
+    if (i < L) a[i] = v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = v;
+    __syncthreads();
+  }
+}
+
+}  // namespace rapp
+
+using namespace rapp;
+
+struct rapp_tick {
+  rapp_ctx* ctx = nullptr;
+  World w{};
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+  // staging for the host API
+  int64_t* d_arrivals = nullptr;
+  uint8_t* d_idle = nullptr;
+  double* d_pred_in = nullptr;
+  int32_t* h_count = nullptr;  // pinned
+};
+
+namespace rapp {
+
+template <typename T>
+static int dev_alloc(rapp_tick* t, T** p, size_t n) {
+  void* q = nullptr;
+  RAPP_CUDA(cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T)));
+  RAPP_CUDA(cudaMemset(q, 0, std::max<size_t>(1, n) * sizeof(T)));
+  t->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return RAPP_OK;
+}
+
+template <typename T>
+static int dev_upload(rapp_tick* t, T** p, const std::vector<T>& v) {
+  int rc = dev_alloc(t, p, v.size());
+  if (rc) return rc;
+  if (!v.empty()) RAPP_CUDA(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return RAPP_OK;
+}
+
+static PodId pack_id(const char* s) {
+  PodId id;
+  for (int i = 0; i < 4; ++i) {
+    uint64_t x = 0;
+    for (int k = 0; k < 8; ++k) x = (x << 8) | uint8_t(s[i * 8 + k]);
+    id.w[i] = x;
+  }
+  return id;
+}
+
+static void unpack_id(const PodId& id, char* s) {
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 8; ++k) s[i * 8 + k] = char((id.w[i] >> (8 * (7 - k))) & 0xFF);
+}
+
+static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uint8_t* d_idle,
+                       const double* d_pred, cudaStream_t st) {
+  World w = t->w;
+  w.p_idle = d_idle;
+  k_tick_prologue<<<std::max(1, std::min(1024, (w.pod_cap + 255) / 256)), 256, 0, st>>>(w, now);
+  RAPP_LAUNCHED();
+  if (w.F > 0) {
+    k_tick_phase_a<<<(w.F + 7) / 8, 256, 0, st>>>(w, now, d_arr, d_pred);
+    RAPP_LAUNCHED();
+    k_tick_grid<<<w.F * 100, 128, 0, st>>>(w);
+    RAPP_LAUNCHED();
+    k_tick_commit<<<1, 32, 0, st>>>(w, now);
+    RAPP_LAUNCHED();
+  }
+  return RAPP_OK;
+}
+
+}  // namespace rapp
+
+extern "C" {
+
+int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns,
+                     const rapp_fn_desc* fns, const int64_t* batch_lattice, int64_t n_gpus,
+                     const int64_t* part_off, const int32_t* part_sm, const int32_t* part_alloc,
+                     int64_t n_pods, const rapp_pod_desc* pods, int64_t pod_counter,
+                     rapp_tick** out) {
+  if (!ctx || !cfg || !out || n_fns < 0 || n_gpus < 0 || n_pods < 0) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  if (cfg->delta_iq < 1 || cfg->delta_iq > 100) {
+    set_error("delta_iq %d outside [1, 100]", cfg->delta_iq);
+    return RAPP_E_VALUE;
+  }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  std::unique_ptr<rapp_tick> t(new rapp_tick());
+  t->ctx = ctx;
+  RAPP_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  World& w = t->w;
+  w.alpha = cfg->alpha;
+  w.beta = cfg->beta;
+  w.cooldown = cfg->cooldown_ms;
+  w.r_min = cfg->r_min;
+  w.interval_s = cfg->interval_s;
+  w.cold_start = cfg->cold_start_ms;
+  w.kA = cfg->kal_A;
+  w.kQ = cfg->kal_Q;
+  w.kH = cfg->kal_H;
+  w.kD = cfg->kal_D;
+  w.kP0 = cfg->kal_P0;
+  w.delta = cfg->delta_iq;
+  const int F = (int)n_fns, G = (int)n_gpus;
+  w.F = F;
+  w.G = G;
+  // ---- functions, tables, search index ----
+  std::vector<int32_t> fn_table(F), fn_nb(F), fn_init(F), fn_npods(F, 0), fn_pairs_off(F),
+      fn_npairs(F);
+  std::vector<double> fn_min(F), kR(F), kP(F), last(F), blist;
+  std::vector<int64_t> fn_boff(F), fn_lat_off(F), fn_lat_len(F);
+  std::vector<int32_t> pairs;
+  std::vector<std::pair<std::vector<double>, int32_t>> shape_cache;  // (sms, ..) -> offset
+  int64_t lat_total = 0;
+  const int d = cfg->delta_iq;
+  const int nQ = 100 / d;
+  for (int f = 0; f < F; ++f) {
+    const rapp_fn_desc& fd = fns[f];
+    if (fd.table_id < 0 || fd.table_id >= (int32_t)ctx->tables.size()) {
+      set_error("function %d: unknown table id %d", f, fd.table_id);
+      return RAPP_E_ARG;
+    }
+    const TableDesc& td = ctx->tables[fd.table_id];
+    if (!td.sm_keyable) {
+      set_error("function %d: sm axis must hold integers in [0, 2^24)", f);
+      return RAPP_E_ARG;
+    }
+    fn_table[f] = fd.table_id;
+    fn_min[f] = fd.min_rps;
+    fn_init[f] = fd.kal_init;
+    kR[f] = fd.kal_R;
+    kP[f] = fd.kal_P;
+    last[f] = fd.last_down_ms;
+    fn_nb[f] = (int32_t)fd.lattice_len;
+    fn_boff[f] = (int64_t)blist.size();
+    if (fd.lattice_len < 1) {
+      set_error("function %d: empty batch lattice", f);
+      return RAPP_E_ARG;
+    }
+    for (int64_t i = 0; i < fd.lattice_len; ++i) blist.push_back((double)batch_lattice[fd.lattice_off + i]);
+    // (s, q) pairs of the lattice in key order (s*q, s, q); batches vary fastest
+    std::vector<double> sms((size_t)td.ns);
+    RAPP_CUDA(cudaMemcpy(sms.data(), ctx->d_pool + td.off + td.os, sms.size() * 8,
+                         cudaMemcpyDeviceToHost));
+    int32_t off = -1;
+    for (auto& sc : shape_cache)
+      if (sc.first == sms) off = sc.second;
+    if (off < 0) {
+      std::vector<std::array<int64_t, 4>> keys;
+      for (int si = 0; si < td.ns; ++si)
+        for (int qi = 1; qi <= nQ; ++qi) {
+          const int64_t s = (int64_t)sms[si], q = (int64_t)qi * d;
+          keys.push_back({s * q, s, q, (int64_t)si});
+        }
+      std::sort(keys.begin(), keys.end());
+      off = (int32_t)pairs.size();
+      for (auto& k : keys) pairs.push_back(int32_t(k[3] << 16 | k[2]));
+      shape_cache.push_back({sms, off});
+    }
+    fn_pairs_off[f] = off;
+    fn_npairs[f] = td.ns * nQ;
+    fn_lat_off[f] = lat_total;
+    fn_lat_len[f] = (int64_t)td.ns * nQ * fd.lattice_len;
+    lat_total += fn_lat_len[f];
+  }
+  int rc;
+#define UP(ptr, vec) \
+  if ((rc = dev_upload(t.get(), &ptr, vec))) return rc;
+  {
+    int32_t *a;
+    double *b;
+    int64_t *c;
+    UP(a, fn_table) w.fn_table = a;
+    UP(b, fn_min) w.fn_min_rps = b;
+    UP(c, fn_lat_off) w.fn_lat_off = c;
+    UP(c, fn_lat_len) w.fn_lat_len = c;
+    UP(a, fn_nb) w.fn_nb = a;
+    UP(c, fn_boff) w.fn_boff = c;
+    UP(b, blist) w.blist = b;
+    UP(a, fn_pairs_off) w.fn_pairs_off = a;
+    UP(a, fn_npairs) w.fn_npairs = a;
+    UP(a, pairs) w.pairs = a;
+    UP(w.k_init, fn_init)
+    UP(w.k_R, kR)
+    UP(w.k_P, kP)
+    UP(w.last_down, last)
+    double* pm;
+    if ((rc = dev_alloc(t.get(), &pm, (size_t)lat_total))) return rc;
+    w.pmax = pm;
+  }
+  // ---- GPUs and partitions ----
+  std::vector<int32_t> g_npods(G, 0), g_hgo(G, 0), g_nparts(G, 0), g_free(G, 100);
+  std::vector<uint32_t> g_uid(G, 0);
+  std::vector<uint64_t> g_parts((size_t)G * kPartCap, 0);
+  for (int g = 0; g < G; ++g) {
+    const int64_t n = part_off[g + 1] - part_off[g];
+    if (n > kPartCap) {
+      set_error("GPU %d holds %lld partitions (> %d)", g, (long long)n, kPartCap);
+      return RAPP_E_INVARIANT;
+    }
+    g_nparts[g] = (int32_t)n;
+    g_uid[g] = (uint32_t)n;
+    for (int64_t i = 0; i < n; ++i) {
+      const int sm = part_sm[part_off[g] + i], al = part_alloc[part_off[g] + i];
+      g_parts[(size_t)g * kPartCap + i] = part_pack(sm, al, 0, (uint32_t)i);
+      g_free[g] -= sm;
+    }
+  }
+  // ---- pods ----
+  const int cap = (int)(n_pods + 2 * (int64_t)F * 64 + 1024);  // room for many ticks of growth
+  w.pod_cap = cap;
+  std::vector<int32_t> p_fn(cap, -1), p_b(cap, 0), p_s(cap, 0), p_q(cap, 0), p_gpu(cap, 0),
+      p_state(cap, kDead), fn_pods((size_t)F * kMaxPods, 0);
+  std::vector<uint32_t> p_puid(cap, 0);
+  std::vector<double> p_ready(cap, 0.0);
+  std::vector<PodId> p_id(cap, PodId{{0, 0, 0, 0}});
+  for (int64_t i = 0; i < n_pods; ++i) {
+    const rapp_pod_desc& pd = pods[i];
+    if (pd.gpu < 0 || pd.gpu >= G) {
+      set_error("pod %lld: GPU rank %d out of range", (long long)i, pd.gpu);
+      return RAPP_E_INVARIANT;
+    }
+    const int g = pd.gpu;
+    if (pd.part < 0 || pd.part >= g_nparts[g]) {
+      set_error("pod %lld: partition %d out of range", (long long)i, pd.part);
+      return RAPP_E_INVARIANT;
+    }
+    uint64_t& e = g_parts[(size_t)g * kPartCap + pd.part];
+    e = part_pack(rapp::part_sm(e), rapp::part_alloc(e), part_npods(e) + 1, part_uid(e));
+    p_fn[i] = pd.fn;
+    p_b[i] = pd.batch;
+    p_s[i] = pd.sm;
+    p_q[i] = pd.quota;
+    p_gpu[i] = g;
+    p_puid[i] = part_uid(e);
+    p_state[i] = pd.state;
+    p_ready[i] = pd.ready_at_ms;
+    p_id[i] = pack_id(pd.id);
+    g_npods[g] += 1;
+    g_hgo[g] += pd.sm * pd.quota;
+    if (pd.fn >= 0) {
+      if (pd.fn >= F || fn_npods[pd.fn] >= kMaxPods) {
+        set_error("function %d: more than %d pods", pd.fn, kMaxPods);
+        return RAPP_E_ARG;
+      }
+      fn_pods[(size_t)pd.fn * kMaxPods + fn_npods[pd.fn]++] = (int32_t)i;
+    }
+  }
+  UP(w.g_npods, g_npods)
+  UP(w.g_hgo, g_hgo)
+  UP(w.g_nparts, g_nparts)
+  UP(w.g_freesm, g_free)
+  UP(w.g_nextuid, g_uid)
+  UP(w.g_parts, g_parts)
+  UP(w.p_fn, p_fn)
+  UP(w.p_b, p_b)
+  UP(w.p_s, p_s)
+  UP(w.p_q, p_q)
+  UP(w.p_gpu, p_gpu)
+  UP(w.p_puid, p_puid)
+  UP(w.p_state, p_state)
+  UP(w.p_ready, p_ready)
+  UP(w.p_id, p_id)
+  UP(w.fn_npods, fn_npods)
+  UP(w.fn_pods, fn_pods)
+#undef UP
+  {
+    std::vector<int32_t> np(1, (int32_t)n_pods);
+    if ((rc = dev_upload(t.get(), &w.n_pods, np))) return rc;
+    std::vector<int64_t> ctr(1, pod_counter);
+    if ((rc = dev_upload(t.get(), &w.counter, ctr))) return rc;
+  }
+  w.tds = ctx->d_desc;
+  w.pool = ctx->d_pool;
+  // scratch / outputs
+  const size_t FP = (size_t)std::max(F, 1);
+  if ((rc = dev_alloc(t.get(), &w.obs, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.pred, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.cls, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.gap0, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.nsorted, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.sorted, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.row_kd, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.rows, FP * kMaxPods * kRow))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.bref, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.tgrid, FP * 100 * 100))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.ndown, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.down, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.stamp, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.actions, FP * (kMaxPods + 4)))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.n_actions, 1))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.err, 1))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.err_fn, 1))) return rc;
+  if ((rc = dev_alloc(t.get(), &t->d_arrivals, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &t->d_idle, (size_t)cap))) return rc;
+  if ((rc = dev_alloc(t.get(), &t->d_pred_in, FP))) return rc;
+  RAPP_CUDA(cudaMallocHost(&t->h_count, 4 * sizeof(int32_t)));
+  // build the fresh-GPU search index
+  for (int f0 = 0; f0 < F; f0 += 32768) {
+    const int nf = std::min(F - f0, 32768);
+    k_index_rps<<<dim3(64, nf), 256, 0, t->stream>>>(w, f0);
+    RAPP_LAUNCHED();
+    k_index_scan<<<nf, 1024, 0, t->stream>>>(w, f0);
+    RAPP_LAUNCHED();
+  }
+  RAPP_CUDA(cudaStreamSynchronize(t->stream));
+  *out = t.release();
+  return RAPP_OK;
+}
+
+int rapp_tick_destroy(rapp_tick* t) {
+  if (!t) return RAPP_OK;
+  cudaSetDevice(t->ctx->device);
+  cudaStreamSynchronize(t->stream);
+  for (void* p : t->allocs) cudaFree(p);
+  if (t->h_count) cudaFreeHost(t->h_count);
+  cudaStreamDestroy(t->stream);
+  delete t;
+  return RAPP_OK;
+}
+
+int rapp_tick_pod_count(rapp_tick* t, int64_t* n) {
+  if (!t || !n) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  int32_t v = 0;
+  RAPP_CUDA(cudaMemcpy(&v, t->w.n_pods, sizeof v, cudaMemcpyDeviceToHost));
+  *n = v;
+  return RAPP_OK;
+}
+
+static int tick_error(rapp_tick* t) {
+  int32_t e[2] = {0, 0};
+  RAPP_CUDA(cudaMemcpy(&e[0], t->w.err, 4, cudaMemcpyDeviceToHost));
+  RAPP_CUDA(cudaMemcpy(&e[1], t->w.err_fn, 4, cudaMemcpyDeviceToHost));
+  if (e[0] == RAPP_OK) return RAPP_OK;
+  switch (e[0]) {
+    case RAPP_E_VALUE: set_error("function %d: batch outside table range", e[1]); break;
+    case RAPP_E_DEGENERATE: set_error("function %d: H*P'*H + D == 0", e[1]); break;
+    case RAPP_E_PLACEMENT: set_error("placement rejected (invariant broken)"); break;
+    default: set_error("function %d: pod capacity exceeded", e[1]); break;
+  }
+  return e[0];
+}
+
+int rapp_tick_run_dev(rapp_tick* t, double now_ms, const int64_t* d_arrivals,
+                      const uint8_t* d_idle, void* stream) {
+  if (!t) {
+    set_error("null tick");
+    return RAPP_E_ARG;
+  }
+  RAPP_CUDA(cudaSetDevice(t->ctx->device));
+  return launch_tick(t, now_ms, d_arrivals, d_idle, nullptr, (cudaStream_t)stream);
+}
+
+int rapp_tick_outputs_dev(rapp_tick* t, const rapp_action** a, const int32_t** c,
+                          const double** o, const double** p) {
+  if (!t) {
+    set_error("null tick");
+    return RAPP_E_ARG;
+  }
+  if (a) *a = t->w.actions;
+  if (c) *c = t->w.n_actions;
+  if (o) *o = t->w.obs;
+  if (p) *p = t->w.pred;
+  return RAPP_OK;
+}
+
+int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const uint8_t* idle,
+                  const double* predicted_in, rapp_action* actions, int64_t max_actions,
+                  int64_t* n_actions, double* observed_out, double* predicted_out) {
+  if (!t || !arrivals || !n_actions) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  RAPP_CUDA(cudaSetDevice(t->ctx->device));
+  World& w = t->w;
+  cudaStream_t st = t->stream;
+  const size_t F = (size_t)w.F;
+  int32_t np = 0;
+  RAPP_CUDA(cudaMemcpyAsync(&np, w.n_pods, 4, cudaMemcpyDeviceToHost, st));
+  if (F) RAPP_CUDA(cudaMemcpyAsync(t->d_arrivals, arrivals, F * 8, cudaMemcpyHostToDevice, st));
+  RAPP_CUDA(cudaStreamSynchronize(st));
+  if (idle && np) RAPP_CUDA(cudaMemcpyAsync(t->d_idle, idle, (size_t)np, cudaMemcpyHostToDevice, st));
+  if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
+  if (predicted_in && F)
+    RAPP_CUDA(cudaMemcpyAsync(t->d_pred_in, predicted_in, F * 8, cudaMemcpyHostToDevice, st));
+  int rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr, st);
+  if (rc) return rc;
+  RAPP_CUDA(cudaMemcpyAsync(t->h_count, w.n_actions, 4, cudaMemcpyDeviceToHost, st));
+  RAPP_CUDA(cudaStreamSynchronize(st));
+  if ((rc = tick_error(t))) return rc;
+  const int64_t n = t->h_count[0];
+  *n_actions = n;
+  if (n > max_actions) {
+    set_error("action buffer too small (%lld > %lld)", (long long)n, (long long)max_actions);
+    return RAPP_E_ARG;
+  }
+  if (n && actions)
+    RAPP_CUDA(cudaMemcpyAsync(actions, w.actions, (size_t)n * sizeof(rapp_action),
+                              cudaMemcpyDeviceToHost, st));
+  if (observed_out && F) RAPP_CUDA(cudaMemcpyAsync(observed_out, w.obs, F * 8, cudaMemcpyDeviceToHost, st));
+  if (predicted_out && F) RAPP_CUDA(cudaMemcpyAsync(predicted_out, w.pred, F * 8, cudaMemcpyDeviceToHost, st));
+  RAPP_CUDA(cudaStreamSynchronize(st));
+  return RAPP_OK;
+}
+
+int rapp_tick_read_pods(rapp_tick* t, rapp_pod_desc* out, int64_t cap, int64_t* n) {
+  if (!t || !n) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  World& w = t->w;
+  int32_t np = 0;
+  RAPP_CUDA(cudaMemcpy(&np, w.n_pods, 4, cudaMemcpyDeviceToHost));
+  *n = np;
+  if (!out) return RAPP_OK;
+  if (np > cap) {
+    set_error("pod buffer too small");
+    return RAPP_E_ARG;
+  }
+  std::vector<int32_t> fn(np), b(np), s(np), q(np), g(np), st(np);
+  std::vector<uint32_t> puid(np);
+  std::vector<double> rd(np);
+  std::vector<PodId> id(np);
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+  };
+  if (np) {
+    RAPP_CUDA(cp(fn.data(), w.p_fn, np * 4));
+    RAPP_CUDA(cp(b.data(), w.p_b, np * 4));
+    RAPP_CUDA(cp(s.data(), w.p_s, np * 4));
+    RAPP_CUDA(cp(q.data(), w.p_q, np * 4));
+    RAPP_CUDA(cp(g.data(), w.p_gpu, np * 4));
+    RAPP_CUDA(cp(st.data(), w.p_state, np * 4));
+    RAPP_CUDA(cp(puid.data(), w.p_puid, np * 4));
+    RAPP_CUDA(cp(rd.data(), w.p_ready, np * 8));
+    RAPP_CUDA(cp(id.data(), w.p_id, np * sizeof(PodId)));
+  }
+  // partition positions from uids
+  std::vector<uint64_t> parts((size_t)w.G * kPartCap);
+  std::vector<int32_t> nparts(w.G);
+  if (w.G) {
+    RAPP_CUDA(cp(parts.data(), w.g_parts, parts.size() * 8));
+    RAPP_CUDA(cp(nparts.data(), w.g_nparts, w.G * 4));
+  }
+  for (int i = 0; i < np; ++i) {
+    rapp_pod_desc& o = out[i];
+    memset(&o, 0, sizeof o);
+    o.fn = fn[i];
+    o.batch = b[i];
+    o.sm = s[i];
+    o.quota = q[i];
+    o.gpu = g[i];
+    o.state = st[i];
+    o.ready_at_ms = rd[i];
+    o.part = -1;
+    if (st[i] != kDead)
+      for (int k = 0; k < nparts[g[i]]; ++k)
+        if (part_uid(parts[(size_t)g[i] * kPartCap + k]) == puid[i]) {
+          o.part = k;
+          break;
+        }
+    unpack_id(id[i], o.id);
+  }
+  return RAPP_OK;
+}
+
+int rapp_tick_read_fns(rapp_tick* t, rapp_fn_desc* out) {
+  if (!t || !out) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  World& w = t->w;
+  const int F = w.F;
+  std::vector<int32_t> init(F);
+  std::vector<double> R(F), P(F), last(F);
+  if (F) {
+    RAPP_CUDA(cudaMemcpy(init.data(), w.k_init, F * 4, cudaMemcpyDeviceToHost));
+    RAPP_CUDA(cudaMemcpy(R.data(), w.k_R, F * 8, cudaMemcpyDeviceToHost));
+    RAPP_CUDA(cudaMemcpy(P.data(), w.k_P, F * 8, cudaMemcpyDeviceToHost));
+    RAPP_CUDA(cudaMemcpy(last.data(), w.last_down, F * 8, cudaMemcpyDeviceToHost));
+  }
+  for (int f = 0; f < F; ++f) {
+    out[f].kal_init = init[f];
+    out[f].kal_R = R[f];
+    out[f].kal_P = P[f];
+    out[f].last_down_ms = last[f];
+  }
+  return RAPP_OK;
+}
+
+int rapp_tick_read_parts(rapp_tick* t, int64_t* part_off, int32_t* psm, int32_t* palloc,
+                         int32_t* pnpods, int64_t cap) {
+  if (!t || !part_off) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  World& w = t->w;
+  std::vector<uint64_t> parts((size_t)w.G * kPartCap);
+  std::vector<int32_t> nparts(w.G);
+  if (w.G) {
+    RAPP_CUDA(cudaMemcpy(parts.data(), w.g_parts, parts.size() * 8, cudaMemcpyDeviceToHost));
+    RAPP_CUDA(cudaMemcpy(nparts.data(), w.g_nparts, w.G * 4, cudaMemcpyDeviceToHost));
+  }
+  int64_t k = 0;
+  part_off[0] = 0;
+  for (int g = 0; g < w.G; ++g) {
+    for (int i = 0; i < nparts[g]; ++i) {
+      if (k < cap) {
+        const uint64_t e = parts[(size_t)g * kPartCap + i];
+        if (psm) psm[k] = part_sm(e);
+        if (palloc) palloc[k] = part_alloc(e);
+        if (pnpods) pnpods[k] = part_npods(e);
+      }
+      ++k;
+    }
+    part_off[g + 1] = k;
+  }
+  return RAPP_OK;
+}
+
+int rapp_tick_counter(rapp_tick* t, int64_t* c) {
+  if (!t || !c) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  RAPP_CUDA(cudaMemcpy(c, t->w.counter, 8, cudaMemcpyDeviceToHost));
+  return RAPP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+"""Batched scaler tick on the B200: the drop-in for SimulationEngine._handle_scaler.
+
+`TickEngine` uploads a scaler world — functions in sorted-id order with their perf tables,
+the cluster (GPUs in sorted-id order, partition lists in insertion order, pods), Kalman
+states and scale-down stamps — and runs whole ticks on the device (rapp_tick_run,
+include/rapp_b200.h).  One tick reproduces, function by function in sorted order,
+hs/sim.py:470-491: observed = arrivals / interval; Kalman (hs/kalman.py:45-62);
+Autoscaler.scale (hs/autoscaler.py:73-234); apply (hs/sim.py:493-525: change_quota, a new
+COLD_STARTING `pod-%06d` placed on its GPU, DRAINING with immediate release when idle).
+The device state persists across ticks; `sync_host()` / `apply_to_host=True` keep a host
+ClusterState in step when a caller needs the Python objects.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Mapping, Optional, Sequence
+
+import numpy as np
+
+from . import _lib, allocator
+from .core import ActionKind, PodInstance, PodState, ScalingAction
+from .errors import ConfigError, FilterDegenerateError, InvariantViolation
+
+KINDS = (ActionKind.VERTICAL_UP, ActionKind.VERTICAL_DOWN, ActionKind.HORIZONTAL_UP,
+         ActionKind.HORIZONTAL_DOWN)
+_STATE_CODE = {PodState.COLD_STARTING: 0, PodState.RUNNING: 1, PodState.DRAINING: 2}
+_CODE_STATE = {0: PodState.COLD_STARTING, 1: PodState.RUNNING, 2: PodState.DRAINING}
+
+
+class ScalerConfigC(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double),
+                ("cooldown_ms", ctypes.c_double), ("r_min", ctypes.c_double),
+                ("delta_iq", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("interval_s", ctypes.c_double), ("cold_start_ms", ctypes.c_double),
+                ("kal_A", ctypes.c_double), ("kal_Q", ctypes.c_double),
+                ("kal_H", ctypes.c_double), ("kal_D", ctypes.c_double),
+                ("kal_P0", ctypes.c_double)]
+
+
+FN_DTYPE = np.dtype([("table_id", "<i4"), ("_pad", "<i4"), ("min_rps", "<f8"),
+                     ("lattice_off", "<i8"), ("lattice_len", "<i8"), ("kal_init", "<i4"),
+                     ("_pad2", "<i4"), ("kal_R", "<f8"), ("kal_P", "<f8"),
+                     ("last_down_ms", "<f8")])
+POD_DTYPE = np.dtype([("fn", "<i4"), ("batch", "<i4"), ("sm", "<i4"), ("quota", "<i4"),
+                      ("gpu", "<i4"), ("part", "<i4"), ("state", "<i4"), ("_pad", "<i4"),
+                      ("ready_at_ms", "<f8"), ("id", "S32")])
+ACTION_DTYPE = np.dtype([("fn", "<i4"), ("kind", "<i4"), ("batch", "<i4"), ("sm", "<i4"),
+                         ("quota", "<i4"), ("pod", "<i4"), ("gpu", "<i4"),
+                         ("released", "<i4")])
+assert FN_DTYPE.itemsize == 64 and POD_DTYPE.itemsize == 72 and ACTION_DTYPE.itemsize == 32
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if a.size else None
+
+
+def _state_code(state) -> int:
+    if isinstance(state, str):
+        state = PodState(state)
+    return _STATE_CODE[PodState(state.value)]
+
+
+@dataclass
+class TickResult:
+    actions: list[ScalingAction]      # reference-shaped (horizontal_up carries pod_id None)
+    pod_ids: list[str]                # pod each action refers to (new pods: their new id)
+    released: list[bool]              # horizontal_down of an idle pod: released at once
+    observed: dict[str, float]
+    predicted: dict[str, float]
+    raw: np.ndarray = field(repr=False, default=None)
+
+
+class TickEngine:
+    """Device-resident scaler world; `tick()` runs one _handle_scaler for all functions."""
+
+    def __init__(self, functions: Sequence, tables: Mapping, cluster, scaler_config, *,
+                 kalman_params: Optional[dict] = None, scaler_interval_ms: float = 2000.0,
+                 cold_start_ms: float = 5000.0, pod_counter: int = 0,
+                 kalman_states: Optional[Mapping] = None,
+                 last_scale_down: Optional[Mapping[str, float]] = None,
+                 promote_cold: bool = True, device: Optional[int] = None):
+        from .perf import PerfTable
+        self.cluster = cluster
+        self.config = scaler_config
+        self.functions = {f.function_id: f for f in functions}
+        self.fids = sorted(self.functions)
+        self.fidx = {fid: i for i, fid in enumerate(self.fids)}
+        kp = dict(kalman_params or {})
+        kal = {"A": kp.get("A", 1.0), "Q": kp.get("Q", 4.0), "H": kp.get("H", 1.0),
+               "D": kp.get("D", 16.0), "P0": kp.get("P0", 1.0)}
+        self.interval_ms = float(scaler_interval_ms)
+        self.cold_start_ms = float(cold_start_ms)
+        # tables and batch lattices (most_efficient_config's _batch_lattice rule)
+        ctx = None
+        fn_arr = np.zeros(len(self.fids), dtype=FN_DTYPE)
+        lattice: list[int] = []
+        for i, fid in enumerate(self.fids):
+            f = self.functions[fid]
+            ref = f.perf_table_ref or fid
+            table = tables.get(ref)
+            if table is None:
+                raise ConfigError(f"missing perf table {ref!r} for {fid}")
+            if not isinstance(table, PerfTable):
+                raise ConfigError(f"table {ref!r} must be a paper_2505_01968_b200 PerfTable")
+            c, tid = table.device_table()
+            if ctx is None:
+                ctx = c
+            elif c is not ctx:
+                raise ConfigError("all tables of a TickEngine must share one device")
+            bl = table._batch_lattice(f.allowed_batches or None)
+            fn_arr[i]["table_id"] = tid
+            fn_arr[i]["min_rps"] = math.nan if f.min_rps is None else float(f.min_rps)
+            fn_arr[i]["lattice_off"] = len(lattice)
+            fn_arr[i]["lattice_len"] = len(bl)
+            lattice.extend(bl)
+            st = (kalman_states or {}).get(fid)
+            if st is not None:
+                fn_arr[i]["kal_init"] = 1
+                fn_arr[i]["kal_R"] = st.R
+                fn_arr[i]["kal_P"] = st.P
+            ld = (last_scale_down or {}).get(fid)
+            fn_arr[i]["last_down_ms"] = -math.inf if ld is None else float(ld)
+        self.ctx = ctx or _lib.Context.get(device)
+        # GPUs in sorted-id order; partitions in list order
+        self.gids = sorted(cluster.gpus)
+        self.grank = {g: i for i, g in enumerate(self.gids)}
+        part_off, psm, palloc = [0], [], []
+        where = {}
+        for g in self.gids:
+            for pos, part in enumerate(cluster.gpus[g].partitions):
+                psm.append(part.sm_percent)
+                palloc.append(part.quota_allocated)
+                for pid in part.resident_pods:
+                    where[pid] = pos
+            part_off.append(len(psm))
+        # pods
+        self.pod_ids: list[str] = []
+        self.pod_fids: list[str] = []
+        pods = np.zeros(len(cluster.pods), dtype=POD_DTYPE)
+        for i, pod in enumerate(cluster.pods.values()):
+            raw = pod.pod_id.encode("utf-8")
+            if len(raw) > 32 or b"\x00" in raw:
+                raise ConfigError(f"pod id {pod.pod_id!r}: at most 32 UTF-8 bytes, no NUL")
+            if pod.pod_id not in where:
+                raise InvariantViolation(f"pod {pod.pod_id} is not resident on a partition")
+            pods[i] = (self.fidx.get(pod.function_id, -1), pod.batch, pod.sm_percent,
+                       pod.quota_percent, self.grank[pod.gpu_id], where[pod.pod_id],
+                       _state_code(pod.state), 0,
+                       float(getattr(pod, "ready_at_ms", 0.0)) if promote_cold else math.inf,
+                       raw)
+            self.pod_ids.append(pod.pod_id)
+            self.pod_fids.append(pod.function_id)
+        self.counter = int(pod_counter)
+        cfg = ScalerConfigC(scaler_config.alpha, scaler_config.beta, scaler_config.cooldown_ms,
+                            scaler_config.r_min, scaler_config.delta_iq, 0,
+                            self.interval_ms / 1000.0, self.cold_start_ms, kal["A"], kal["Q"],
+                            kal["H"], kal["D"], kal["P0"])
+        lat = np.asarray(lattice if lattice else [0], dtype=np.int64)
+        po = np.asarray(part_off, dtype=np.int64)
+        ps = np.asarray(psm if psm else [0], dtype=np.int32)
+        pa = np.asarray(palloc if palloc else [0], dtype=np.int32)
+        h = _lib.c_vp()
+        _lib.check(_lib.load().rapp_tick_create(
+            self.ctx.handle, ctypes.byref(cfg), len(self.fids), _ptr(fn_arr), _lib.i64ptr(lat),
+            len(self.gids), _lib.i64ptr(po), _lib.i32ptr(ps), _lib.i32ptr(pa), len(pods),
+            _ptr(pods), self.counter, ctypes.byref(h)), "TickEngine")
+        self._h = h
+        self._act_buf = np.zeros(max(64, len(self.fids) * 36), dtype=ACTION_DTYPE)
+        self._obs = np.zeros(max(1, len(self.fids)))
+        self._pred = np.zeros(max(1, len(self.fids)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.rapp_tick_destroy(h)
+
+    # -- one tick -----------------------------------------------------------------------
+
+    def tick(self, now_ms: float, arrivals, idle=None, *, predicted=None,
+             apply_to_host: bool = False) -> TickResult:
+        """arrivals: {fid: count} or a sequence in sorted-fid order.  idle: pod ids with no
+        queued / in-service work (None: every pod is idle).  predicted: {fid: rps} to skip
+        the Kalman step (Autoscaler.scale semantics)."""
+        lib = _lib.load()
+        F = len(self.fids)
+        if isinstance(arrivals, Mapping):
+            arr = np.array([int(arrivals.get(f, 0)) for f in self.fids], dtype=np.int64)
+        else:
+            arr = np.ascontiguousarray(arrivals, dtype=np.int64)
+        if arr.shape != (F,):
+            raise ValueError(f"expected {F} arrival counts")
+        if np.any(arr < 0):
+            raise ValueError("observed_rps must be non-negative")
+        n = len(self.pod_ids)
+        if idle is None:
+            idle_arr = np.ones(max(1, n), dtype=np.uint8)
+        else:
+            idle_set = set(idle)
+            idle_arr = np.fromiter((pid in idle_set for pid in self.pod_ids), dtype=np.uint8,
+                                   count=n) if n else np.zeros(1, dtype=np.uint8)
+        pred_in = None
+        if predicted is not None:
+            pred_in = np.array([float(predicted[f]) for f in self.fids], dtype=np.float64)
+        nact = ctypes.c_int64()
+        rc = lib.rapp_tick_run(self._h, float(now_ms), _lib.i64ptr(arr) if F else None,
+                               _ptr(idle_arr), _ptr(pred_in) if pred_in is not None else None,
+                               _ptr(self._act_buf), len(self._act_buf), ctypes.byref(nact),
+                               _ptr(self._obs), _ptr(self._pred))
+        if rc == _lib.RAPP_E_DEGENERATE:
+            raise FilterDegenerateError("H*P'*H + D == 0")
+        _lib.check(rc, "tick")
+        raw = self._act_buf[:nact.value].copy()
+        res = self._decode(raw)
+        if apply_to_host:
+            self._apply_host(res, float(now_ms))
+        return res
+
+    def _decode(self, raw: np.ndarray) -> TickResult:
+        actions, pod_ids, released = [], [], []
+        for a in raw:
+            fid = self.fids[a["fn"]]
+            kind = KINDS[a["kind"]]
+            gpu = self.gids[a["gpu"]]
+            if kind is ActionKind.HORIZONTAL_UP:
+                pid = f"pod-{self.counter:06d}"
+                self.counter += 1
+                assert a["pod"] == len(self.pod_ids), "device pod index out of step"
+                self.pod_ids.append(pid)
+                self.pod_fids.append(fid)
+                actions.append(ScalingAction(fid, kind, int(a["batch"]), int(a["sm"]),
+                                             int(a["quota"]), None, gpu))
+            else:
+                pid = self.pod_ids[a["pod"]]
+                actions.append(ScalingAction(fid, kind, int(a["batch"]), int(a["sm"]),
+                                             int(a["quota"]), pid, gpu))
+            pod_ids.append(pid)
+            released.append(bool(a["released"]))
+        obs = {f: float(self._obs[i]) for i, f in enumerate(self.fids)}
+        pred = {f: float(self._pred[i]) for i, f in enumerate(self.fids)}
+        return TickResult(actions, pod_ids, released, obs, pred, raw)
+
+    def _apply_host(self, res: TickResult, now: float) -> None:
+        """Cluster effects of hs/sim.py:493-525 on the host snapshot (promotions first)."""
+        cl = self.cluster
+        for pod in cl.pods.values():
+            if PodState(pod.state.value) is PodState.COLD_STARTING and pod.ready_at_ms <= now:
+                pod.state = type(pod.state)("running")
+        cl.clock_ms = now
+        for act, pid, rel in zip(res.actions, res.pod_ids, res.released):
+            if act.kind in (ActionKind.VERTICAL_UP, ActionKind.VERTICAL_DOWN):
+                allocator.change_quota(cl, pid, act.quota_percent)
+            elif act.kind is ActionKind.HORIZONTAL_UP:
+                pod = PodInstance(pid, act.function_id, act.batch, act.sm_percent,
+                                  act.quota_percent, act.gpu_id, state=PodState.COLD_STARTING,
+                                  ready_at_ms=now + self.cold_start_ms)
+                allocator.place_pod(cl, pod, act.gpu_id)
+            else:
+                pod = cl.pods[pid]
+                pod.state = type(pod.state)("draining")
+                if rel:
+                    allocator.release_pod(cl, pid)
+
+    # -- device state readback --------------------------------------------------------------
+
+    def read_pods(self) -> np.ndarray:
+        lib = _lib.load()
+        n = ctypes.c_int64()
+        _lib.check(lib.rapp_tick_read_pods(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros(max(1, n.value), dtype=POD_DTYPE)
+        _lib.check(lib.rapp_tick_read_pods(self._h, _ptr(out), len(out), ctypes.byref(n)))
+        return out[:n.value]
+
+    def read_partitions(self) -> dict[str, list[tuple[int, int, int]]]:
+        lib = _lib.load()
+        off = np.zeros(len(self.gids) + 1, dtype=np.int64)
+        cap = 100 * max(1, len(self.gids))
+        sm = np.zeros(cap, dtype=np.int32)
+        al = np.zeros(cap, dtype=np.int32)
+        npd = np.zeros(cap, dtype=np.int32)
+        _lib.check(lib.rapp_tick_read_parts(self._h, _lib.i64ptr(off), _lib.i32ptr(sm),
+                                            _lib.i32ptr(al), _lib.i32ptr(npd), cap))
+        return {g: [(int(sm[k]), int(al[k]), int(npd[k])) for k in range(off[i], off[i + 1])]
+                for i, g in enumerate(self.gids)}
+
+    def read_functions(self) -> np.ndarray:
+        out = np.zeros(max(1, len(self.fids)), dtype=FN_DTYPE)
+        _lib.check(_lib.load().rapp_tick_read_fns(self._h, _ptr(out)))
+        return out[:len(self.fids)]
+
+    def device_cluster_dict(self) -> dict:
+        """{gpus: [{id, partitions: [{sm, alloc, npods}]}], pods: sorted rows} — the device
+        world in the same shape tests use for host snapshots (residents by count)."""
+        pods = self.read_pods()
+        rows = []
+        for i, p in enumerate(pods):
+            if p["state"] < 0:
+                continue
+            rows.append([self.pod_ids[i], self.pod_fids[i],
+                         int(p["batch"]), int(p["sm"]), int(p["quota"]), self.gids[p["gpu"]],
+                         _CODE_STATE[int(p["state"])].value])
+        return {"partitions": self.read_partitions(), "pods": sorted(rows, key=str)}

@@ -1,0 +1,162 @@
+"""The batched device tick vs the real reference (golden decisions and ticks) and vs the
+scaler oracle on config-4-sized ticks.  Mirrors pkg/tests/test_autoscaler.py,
+test_acceptance.py C2 and the sim's per-tick loop (hs/sim.py:470-491)."""
+
+import copy
+import random
+
+import numpy as np
+import pytest
+
+from oracle import scaler_oracle as so
+
+from .conftest import golden_table_arrays, load_golden
+from .golden_io import (cluster_from, cluster_to, function_from, fx, golden_cluster_to,
+                        make_part, make_pod, surface_tables)
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg_obj(c):
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    a, b, d, cd, rmin = c
+    return ScalerConfig(alpha=fx(a), beta=fx(b), delta_iq=d, cooldown_ms=fx(cd), r_min=fx(rmin))
+
+
+def _acts(actions):
+    return [[a.function_id, a.kind.value, a.batch, a.sm_percent, a.quota_percent, a.pod_id,
+             a.gpu_id] for a in actions]
+
+
+def test_scale_matches_reference_golden():
+    """Every single-function decision of the reference (1,610 cases incl. the six
+    hand-traced conformance scenarios and the three randomized loops)."""
+    from paper_2505_01968_b200 import PerfTable
+    from paper_2505_01968_b200.autoscaler import Autoscaler
+    g = load_golden("scale.json")
+    t = g["table"]
+    b, s, q, v = golden_table_arrays(t)
+    table = PerfTable(t["function_id"], t["batches"], t["sms"], t["quotas"], v)
+    fn = function_from(g["function"])
+    for case in g["cases"]:
+        sc = Autoscaler(_cfg_obj(case["cfg"]), {"conf-fn": table})
+        if case["last_down"] is not None:
+            sc._last_scale_down["conf-fn"] = fx(case["last_down"])
+        cluster = cluster_from(case["cluster"])
+        got = _acts(sc.scale(fn, cluster, fx(case["rate"])))
+        assert got == case["actions"], case["name"]
+        want_stamp = fx(case["stamp"])
+        assert sc._last_scale_down.get("conf-fn") == want_stamp, case["name"]
+        assert cluster_to(cluster) == golden_cluster_to(case["cluster"]), case["name"]
+
+
+def _engine_for_run(run, apply_to_host=True):
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    fns = [function_from(f) for f in run["functions"]]
+    tables = surface_tables(run["tables"], fns)
+    cluster = cluster_from(run["initial"])
+    cfg = ScalerConfig(alpha=fx(run["alpha"]), beta=fx(run["beta"]), delta_iq=run["delta"],
+                       cooldown_ms=fx(run["cooldown_ms"]), r_min=fx(run["r_min"]))
+    kal = {k: fx(v) for k, v in run["kalman"].items()}
+    eng = TickEngine(fns, tables, cluster, cfg, kalman_params=kal,
+                     scaler_interval_ms=fx(run["interval_ms"]),
+                     cold_start_ms=fx(run["cold_start_ms"]), pod_counter=run["pod_counter0"])
+    return eng, fns, cluster
+
+
+def test_ticks_match_reference_golden():
+    """Multi-tick runs of the reference's _handle_scaler (Kalman, decisions, apply with new
+    pod ids, releases of idle drained pods, cold-start promotion), 0-ulp rates."""
+    g = load_golden("tick.json")
+    for run in g["runs"]:
+        eng, fns, cluster = _engine_for_run(run)
+        fids = [f["id"] for f in run["functions"]]
+        for t in run["ticks"]:
+            res = eng.tick(fx(t["now"]), t["arrivals"], idle=set(t["idle"]), apply_to_host=True)
+            assert _acts(res.actions) == [list(a) for a in t["actions"]]
+            assert [a for a, k in zip(res.pod_ids, res.actions)
+                    if k.kind.value == "horizontal_up"] == t["new_pods"]
+            assert [res.observed[f] for f in fids] == [fx(x) for x in t["observed"]]
+            assert [res.predicted[f] for f in fids] == [fx(x) for x in t["predicted"]]
+            cluster.validate()
+        assert cluster_to(cluster) == golden_cluster_to(run["final"])
+        # the device world agrees with the host mirror
+        dev = eng.device_cluster_dict()
+        host = cluster_to(cluster)
+        assert dev["pods"] == sorted(host["pods"], key=str)
+        for gpu in host["gpus"]:
+            assert [(p["sm"], p["alloc"], len(p["residents"])) for p in gpu["partitions"]] == \
+                dev["partitions"][gpu["id"]]
+
+
+def _oracle_ticks(fns, tables, cluster, cfg, nticks, seed, interval_ms=2000.0,
+                  cold_start_ms=5000.0, kal=None):
+    """Runs the oracle and the device engine side by side on the same inputs."""
+    from paper_2505_01968_b200.tick import TickEngine
+    import bench
+    kal = kal or {"A": 1.0, "Q": 4.0, "H": 1.0, "D": 16.0, "P0": 1.0}
+    eng = TickEngine(fns, tables, copy.deepcopy(cluster), cfg, kalman_params=kal,
+                     scaler_interval_ms=interval_ms, cold_start_ms=cold_start_ms,
+                     pod_counter=len(cluster.pods))
+    ocl = copy.deepcopy(cluster)
+    otables = {k: so.OTable(t) for k, t in tables.items()}
+    ocfg = {"alpha": cfg.alpha, "beta": cfg.beta, "delta": cfg.delta_iq,
+            "cooldown_ms": cfg.cooldown_ms, "r_min": cfg.r_min}
+    okal = {k: v for k, v in kal.items() if k != "P0"}
+    kstate, last_down = {}, {}
+    counter = len(cluster.pods)
+    functions = {f.function_id: f for f in fns}
+    caps = {f.function_id: otables[f.function_id].thr(8, 20, 20) for f in fns}
+    rng = random.Random(seed)
+    n_actions = 0
+    for k in range(nticks):
+        now = interval_ms * (k + 1)
+        swing = (1.0, 1.5, 0.2, 2.0, 0.05)[k % 5]
+        arrivals = bench.config4_arrivals(fns, caps, rng, interval_ms / 1000.0, 0.0, 3.0 * swing)
+        idle = {pid for pid in eng.pod_ids if rng.random() < 0.7}
+        acts, obs, pred, counter = so.tick(ocfg, functions, otables, ocl, now, interval_ms,
+                                           arrivals, idle, kstate, okal, kal["P0"], last_down,
+                                           counter, make_pod, make_part,
+                                           cold_start_ms=cold_start_ms)
+        res = eng.tick(now, arrivals, idle=idle)
+        got = [[a.function_id, a.kind.value, a.batch, a.sm_percent, a.quota_percent, pid,
+                a.gpu_id] for a, pid in zip(res.actions, res.pod_ids)]
+        assert got == [list(a) for a in acts], f"tick {k}"
+        assert res.predicted == pred and res.observed == obs
+        n_actions += len(acts)
+    dev = eng.device_cluster_dict()
+    assert dev["pods"] == sorted(cluster_to(ocl)["pods"], key=str)
+    return n_actions
+
+
+def test_config4_ticks_vs_oracle():
+    """1,000 functions on 400 GPUs (config 4), five ticks with swinging load."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    fns, tables, cluster, _ = bench.make_config4_world(1000, 400, seed=0)
+    n = _oracle_ticks(fns, tables, cluster, ScalerConfig(), 5, seed=1)
+    assert n > 1000
+
+
+@pytest.mark.parametrize("delta,ngpu,nfn", [(1, 50, 60), (7, 30, 80), (25, 200, 150),
+                                            (10, 12, 40)])
+def test_random_worlds_vs_oracle(delta, ngpu, nfn):
+    """Quota steps 1..25, crowded and sparse clusters (fresh-GPU branch, releases)."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    fns, tables, cluster, _ = bench.make_config4_world(nfn, ngpu, seed=delta)
+    cfg = ScalerConfig(alpha=0.85, beta=0.4, delta_iq=delta, cooldown_ms=1000.0, r_min=1.0)
+    _oracle_ticks(fns, tables, cluster, cfg, 8, seed=delta, interval_ms=1000.0,
+                  cold_start_ms=1500.0)
+
+
+def test_full_grid_fresh_gpu_search_vs_oracle():
+    """Full-grid tables (32x91x100, delta 1): the fresh-GPU most_efficient_config runs on a
+    291,200-point lattice through the prefix-max index."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    fns, tables, cluster, _ = bench.make_config4_world(12, 40, seed=3, full_grid=True)
+    cfg = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=1, cooldown_ms=1000.0, r_min=1.0)
+    _oracle_ticks(fns, tables, cluster, cfg, 4, seed=5, interval_ms=1000.0,
+                  cold_start_ms=1500.0)
