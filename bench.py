@@ -432,6 +432,113 @@ def run_lattice(args, rank, world, local):
 
 
 # ----------------------------------------------------------------------------------------
+# tick workload (config 4): whole scaler ticks for 1,000 functions on 400 simulated GPUs
+# ----------------------------------------------------------------------------------------
+
+
+def run_tick(args, local, ticks=None, warmup=None, full_grid=False):
+    """Device µs per tick (CUDA events around rapp_tick_run_dev, inputs resident) and
+    end-to-end µs per tick through TickEngine.tick (H2D arrivals + idle flags, kernels,
+    D2H of the ordered action list and rates)."""
+    import ctypes
+    import torch
+    from paper_2505_01968_b200 import _lib
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    ticks = ticks or args.ticks
+    warmup = warmup if warmup is not None else 3
+    dev = torch.device("cuda", local)
+    fns, tables, cluster, caps = make_config4_world(1000, 400, seed=0, full_grid=full_grid,
+                                                    device=local)
+    cfg = ScalerConfig(delta_iq=1 if full_grid else 10)
+    interval_ms = 2000.0
+    rng = random.Random(0)
+
+    def arrivals_for(k):
+        swing = (1.0, 1.5, 0.2, 2.0, 0.05)[k % 5]
+        a = config4_arrivals(fns, caps, rng, interval_ms / 1000.0, 0.0, 3.0 * swing)
+        return np.array([a[f.function_id] for f in sorted(fns, key=lambda f: f.function_id)],
+                        dtype=np.int64)
+
+    import copy
+    cluster0 = copy.deepcopy(cluster)
+    t0 = time.perf_counter()
+    eng = TickEngine(fns, tables, cluster, cfg, scaler_interval_ms=interval_ms,
+                     cold_start_ms=5000.0, pod_counter=len(cluster.pods), device=local)
+    build_s = time.perf_counter() - t0
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(dev)
+    total = warmup + ticks
+    d_arr = [torch.from_numpy(arrivals_for(k)).to(dev) for k in range(total)]
+    d_idle = torch.ones(1 << 20, dtype=torch.uint8, device=dev)
+    pa, pc = _lib.c_vp(), _lib.c_vp()
+    _lib.check(lib.rapp_tick_outputs_dev(eng._h, ctypes.byref(pa), ctypes.byref(pc), None, None))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(total)]
+    launches0 = _lib.launch_count()
+    for k in range(total):
+        evs[k][0].record(stream)
+        _lib.check(lib.rapp_tick_run_dev(eng._h, interval_ms * (k + 1), d_arr[k].data_ptr(),
+                                         d_idle.data_ptr(), stream.cuda_stream))
+        evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = (_lib.launch_count() - launches0) // total
+    dev_us = [evs[k][0].elapsed_time(evs[k][1]) * 1000.0 for k in range(warmup, total)]
+    # end-to-end through the public host API (each tick: H2D inputs, kernels, D2H results)
+    eng2 = TickEngine(fns, tables, cluster0, cfg, scaler_interval_ms=interval_ms,
+                      cold_start_ms=5000.0, pod_counter=len(cluster0.pods), device=local)
+    rng = random.Random(0)
+    host_arr = [arrivals_for(k) for k in range(total)]
+    e2e_us, acts = [], []
+    for k in range(total):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        res = eng2.tick(interval_ms * (k + 1), host_arr[k], idle=None)
+        e2e_us.append((time.perf_counter() - t1) * 1e6)
+        acts.append(len(res.actions))
+    e2e_us = e2e_us[warmup:]
+    acts = acts[warmup:]
+    return {"functions": 1000, "gpus_simulated": 400, "grid": "32x91x100, delta 1" if full_grid
+            else "6x10x10, delta 10", "ticks": ticks,
+            "device_us_median": float(np.median(dev_us)), "device_us_max": float(np.max(dev_us)),
+            "e2e_us_median": float(np.median(e2e_us)), "e2e_us_max": float(np.max(e2e_us)),
+            "actions_per_tick_mean": float(np.mean(acts)), "launches_per_tick": int(launches),
+            "world_build_s": round(build_s, 3),
+            "e2e_api": "TickEngine.tick (rapp_tick_run: H2D arrivals+idle, D2H actions+rates)"}
+
+
+def tick_cpu_baseline(args, nticks=2):
+    """The scaler oracle (pure-Python restatement of the reference tick, oracle/) on one
+    host core for the same config-4 world: seconds per tick.  The reference itself spends
+    ~44 s/tick here (>98% in copy.deepcopy); the restatement copies less."""
+    import copy
+    from oracle import scaler_oracle as so
+    from paper_2505_01968_b200.core import PodInstance, PodState, SmPartition
+    fns, tables, cluster, caps = make_config4_world(1000, 400, seed=0)
+    otables = {k: so.OTable(t) for k, t in tables.items()}
+    cfg = {"alpha": 0.9, "beta": 0.5, "delta": 10, "cooldown_ms": 30000.0, "r_min": 1.0}
+    kal = {"A": 1.0, "Q": 4.0, "H": 1.0, "D": 16.0}
+    functions = {f.function_id: f for f in fns}
+    rng = random.Random(0)
+    kstate, last_down, counter = {}, {}, len(cluster.pods)
+    times = []
+    for k in range(nticks):
+        swing = (1.0, 1.5, 0.2, 2.0, 0.05)[k % 5]
+        arr = config4_arrivals(fns, caps, rng, 2.0, 0.0, 3.0 * swing)
+        t0 = time.perf_counter()
+        _, _, _, counter = so.tick(
+            cfg, functions, otables, cluster, 2000.0 * (k + 1), 2000.0, arr, set(cluster.pods),
+            kstate, kal, 1.0, last_down, counter,
+            lambda pid, fid, b, s, q, g: PodInstance(pid, fid, b, s, q, g,
+                                                     state=PodState.COLD_STARTING),
+            lambda sm: SmPartition(sm), cold_start_ms=5000.0)
+        times.append(time.perf_counter() - t0)
+    return {"value": float(np.median(times)) * 1e6, "unit": "us/tick", "cores": 1,
+            "kind": "port", "sample": f"{nticks} config-4 ticks of oracle/scaler_oracle.py "
+            "(1,000 functions, 400 GPUs)"}
+
+
+# ----------------------------------------------------------------------------------------
 # CPU baseline / reference arm: the reference's own compiled kernel on all host cores
 # ----------------------------------------------------------------------------------------
 
@@ -502,7 +609,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["stream", "lattice"], default="stream")
+    ap.add_argument("--workload", choices=["stream", "lattice", "tick"], default="stream")
+    ap.add_argument("--ticks", type=int, default=50)
+    ap.add_argument("--full-grid", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--queries", type=int, default=QUERIES_PER_MODEL)
     ap.add_argument("--functions", type=int, default=3125)
     ap.add_argument("--no-e2e", action="store_true")
@@ -531,6 +641,21 @@ def main():
         return
 
     rank, world, local = dist_init(args.gpus)
+    if args.workload == "tick":
+        tick = run_tick(args, local, full_grid=args.full_grid)
+        if rank == 0:
+            line = {"metric": METRIC, "value": tick["device_us_median"], "unit": "us/tick",
+                    "n_gpus": world, "steps": tick["ticks"], "warmup": 3,
+                    "ms_per_step": tick["device_us_median"] / 1000.0, "higher_is_better": False,
+                    "scaling": "replicas", "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic", "config": {"workload": "config4 tick: " + tick["grid"]},
+                    "e2e": {"value": tick["e2e_us_median"], "unit": "us/tick",
+                            "h2d_bytes_per_step": 1000 * 8 + 1000,
+                            "d2h_bytes_per_step": "actions (32 B each) + 2 x 8 KB rates"},
+                    "tick": tick, "cpu_baseline": tick_cpu_baseline(args),
+                    "gpu_launches": tick["launches_per_tick"] * tick["ticks"], "impl": "ours"}
+            print(json.dumps(line))
+        return
     res = (run_stream if args.workload == "stream" else run_lattice)(args, rank, world, local)
     if rank != 0:
         if world > 1:
@@ -547,6 +672,11 @@ def main():
             "dtype": res["dtype"], "data": "synthetic", "config": res["config"],
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
             "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours"}
+    if world == 1 and args.workload == "stream" and not args.no_extra:
+        # the second half of the metric ("scaling decisions/tick latency") and config 5
+        extra = {"tick_config4": run_tick(args, local, ticks=20)}
+        extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
+        line["extra"] = extra
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
