@@ -380,14 +380,19 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
 // ---------------------------------------------------------------------------------------
 // phase A2: throughput(batch_ref, sm, q) for sm, q in 1..100 of every scale-up function
 // ---------------------------------------------------------------------------------------
+// Only the quota multiples of delta are tabulated (the covering-quota scan reads those);
+// c_max at an off-step q_max is evaluated on demand by the commit warp.
 __global__ void k_tick_grid(World w) {
-  const int f = blockIdx.x / 100, sm = blockIdx.x % 100 + 1;
+  const int f = blockIdx.x;
   if (w.cls[f] != kUp) return;
   const int b = w.bref[f];
   if (!batch_ok(w, f, b)) return;  // phase B raises if the value is ever needed
-  for (int q = threadIdx.x + 1; q <= 100; q += blockDim.x)
+  const int d = w.delta, nq = 100 / d;
+  for (int i = threadIdx.x; i < 100 * nq; i += blockDim.x) {
+    const int sm = i / nq + 1, q = (i % nq + 1) * d;
     w.tgrid[(int64_t(f) * 100 + (sm - 1)) * 100 + (q - 1)] =
         thr_at(w, f, double(b), double(sm), double(q));
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -710,7 +715,13 @@ struct Commit {
             return;
           }
           const double* T = w.tgrid + (int64_t(f) * 100 + (sm - 1)) * 100;
-          const double cmax = T[qmax - 1];
+          double cmax;
+          if (qmax % d == 0) {
+            cmax = T[qmax - 1];
+          } else {  // max_quota_capability at an off-step quota (autoscaler.py:144)
+            cmax = lane == 0 ? thr_at(w, f, double(bref), double(sm), double(qmax)) : 0.0;
+            cmax = __shfl_sync(0xffffffffu, cmax, 0);
+          }
           if (cmax > gap) {
             // _covering_quota (autoscaler.py:168-175): first multiple of d <= qmax with
             // throughput >= gap, else qmax
@@ -728,7 +739,7 @@ struct Commit {
             if (p < 0) return;
             place(p, g);
             emit(f, kHUp, bref, sm, quota, p, g, 0);
-            gap = __dsub_rn(gap, T[quota - 1]);
+            gap = __dsub_rn(gap, quota % d == 0 ? T[quota - 1] : cmax);  // quota == qmax
           }
         }
       }
@@ -771,15 +782,58 @@ struct Commit {
   }
 };
 
-__global__ void __launch_bounds__(32) k_tick_commit(World w, double now) {
-  Commit c{w, int(threadIdx.x & 31)};
-  for (int f = 0; f < w.F; ++f) {
-    if (*(volatile int32_t*)w.err) return;
-    const int cls = w.cls[f];
-    if (cls == kUp)
-      c.scale_up(f, now);
-    else if (cls == kDown)
-      c.scale_down(f, now);
+// One warp.  The per-GPU summaries (pod count, occupancy, partition count, free SM share,
+// next partition uid) live in shared memory for the whole tick when they fit: the
+// used-GPU argmin and the first-free scan then read shared memory only.  Function classes
+// are fetched 32 at a time and only active functions are visited, in sorted order.
+__global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int smem_g) {
+  extern __shared__ int32_t sg[];
+  const int lane = threadIdx.x & 31;
+  World v = w;
+  const int G = w.G;
+  if (smem_g) {
+    for (int g = lane; g < G; g += 32) {
+      sg[g] = w.g_npods[g];
+      sg[G + g] = w.g_hgo[g];
+      sg[2 * G + g] = w.g_nparts[g];
+      sg[3 * G + g] = w.g_freesm[g];
+      sg[4 * G + g] = int32_t(w.g_nextuid[g]);
+    }
+    v.g_npods = sg;
+    v.g_hgo = sg + G;
+    v.g_nparts = sg + 2 * G;
+    v.g_freesm = sg + 3 * G;
+    v.g_nextuid = reinterpret_cast<uint32_t*>(sg + 4 * G);
+    __syncwarp();
+  }
+  Commit c{v, lane};
+  bool stop = false;
+  for (int base = 0; base < w.F && !stop; base += 32) {
+    const int mine = base + lane < w.F ? w.cls[base + lane] : kNone;
+    unsigned act = __ballot_sync(0xffffffffu, mine != kNone);
+    while (act) {
+      const int i = __ffs(act) - 1;
+      act &= act - 1;
+      const int cls = __shfl_sync(0xffffffffu, mine, i);
+      if (cls == kUp)
+        c.scale_up(base + i, now);
+      else
+        c.scale_down(base + i, now);
+      if (*(volatile int32_t*)w.err) {
+        stop = true;
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  if (smem_g) {
+    for (int g = lane; g < G; g += 32) {
+      w.g_npods[g] = sg[g];
+      w.g_hgo[g] = sg[G + g];
+      w.g_nparts[g] = sg[2 * G + g];
+      w.g_freesm[g] = sg[3 * G + g];
+      w.g_nextuid[g] = uint32_t(sg[4 * G + g]);
+    }
   }
 }
 
@@ -902,9 +956,14 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
   if (w.F > 0) {
     k_tick_phase_a<<<(w.F + 7) / 8, 256, 0, st>>>(w, now, d_arr, d_pred);
     RAPP_LAUNCHED();
-    k_tick_grid<<<w.F * 100, 128, 0, st>>>(w);
+    k_tick_grid<<<w.F, 256, 0, st>>>(w);
     RAPP_LAUNCHED();
-    k_tick_commit<<<1, 32, 0, st>>>(w, now);
+    const size_t gbytes = size_t(5) * w.G * sizeof(int32_t);
+    const int smem_g = gbytes <= 200 * 1024 ? 1 : 0;
+    if (smem_g && gbytes > 48 * 1024)
+      RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)gbytes));
+    k_tick_commit<<<1, 32, smem_g ? gbytes : 0, st>>>(w, now, smem_g);
     RAPP_LAUNCHED();
   }
   return RAPP_OK;
