@@ -401,8 +401,25 @@ __global__ void k_tick_grid(World w) {
 struct Commit {
   const World& w;
   int lane;
+  // partition lists of GPUs with at most `ps` partitions live in shared memory for the
+  // whole commit (sp[g*ps ...]); a GPU that has or grows beyond ps uses its global row
+  uint64_t* sp;
+  uint8_t* ovf;
+  int ps;
+  int* nact;  // shared-memory action counter
 
-  __device__ uint64_t* parts(int g) const { return w.g_parts + int64_t(g) * kPartCap; }
+  __device__ uint64_t* parts(int g) const {
+    return ovf[g] ? w.g_parts + int64_t(g) * kPartCap : sp + int64_t(g) * ps;
+  }
+
+  // before appending entry n to GPU g: move a full shared-memory list to global memory
+  __device__ void make_room(int g, int n) const {
+    if (!ovf[g] && n >= ps) {
+      uint64_t* dst = w.g_parts + int64_t(g) * kPartCap;
+      for (int i = 0; i < n; ++i) dst[i] = sp[int64_t(g) * ps + i];
+      ovf[g] = 1;
+    }
+  }
 
   // position of the partition with this uid on GPU g (partition_of, core.py:148-158)
   __device__ int find_part(int g, uint32_t uid) const {
@@ -451,6 +468,8 @@ struct Commit {
         if (n >= kPartCap || w.g_freesm[g] < s) {
           set_err(w, RAPP_E_PLACEMENT, -1);
         } else {
+          make_room(g, n);
+          P = parts(g);
           const uint32_t uid = w.g_nextuid[g]++;
           P[n] = part_pack(s, q, 1, uid);
           w.g_nparts[g] = n + 1;
@@ -507,7 +526,7 @@ struct Commit {
 
   __device__ void emit(int f, int kind, int b, int s, int q, int pod, int gpu, int rel) const {
     if (lane == 0) {
-      const int i = (*w.n_actions)++;
+      const int i = (*nact)++;
       w.actions[i] = rapp_action{f, kind, b, s, q, pod, gpu, rel};
     }
     __syncwarp();
@@ -786,11 +805,23 @@ struct Commit {
 // next partition uid) live in shared memory for the whole tick when they fit: the
 // used-GPU argmin and the first-free scan then read shared memory only.  Function classes
 // are fetched 32 at a time and only active functions are visited, in sorted order.
-__global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int smem_g) {
-  extern __shared__ int32_t sg[];
+__global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int smem_g, int ps) {
+  extern __shared__ __align__(16) int32_t sg[];
+  __shared__ int s_nact;
   const int lane = threadIdx.x & 31;
   World v = w;
   const int G = w.G;
+  // shared layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)][ovf G bytes]
+  uint64_t* sp = reinterpret_cast<uint64_t*>(sg + ((5 * G + 1) & ~1));
+  uint8_t* ovf = reinterpret_cast<uint8_t*>(sp + int64_t(G) * ps);
+  if (lane == 0) s_nact = 0;
+  for (int g = lane; g < G; g += 32) {
+    const int n = w.g_nparts[g];
+    const bool cached = n <= ps && ps > 0;
+    ovf[g] = cached ? 0 : 1;
+    if (cached)
+      for (int i = 0; i < n; ++i) sp[int64_t(g) * ps + i] = w.g_parts[int64_t(g) * kPartCap + i];
+  }
   if (smem_g) {
     for (int g = lane; g < G; g += 32) {
       sg[g] = w.g_npods[g];
@@ -806,7 +837,8 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
     v.g_nextuid = reinterpret_cast<uint32_t*>(sg + 4 * G);
     __syncwarp();
   }
-  Commit c{v, lane};
+  __syncwarp();
+  Commit c{v, lane, sp, ovf, ps, &s_nact};
   bool stop = false;
   for (int base = 0; base < w.F && !stop; base += 32) {
     const int mine = base + lane < w.F ? w.cls[base + lane] : kNone;
@@ -826,6 +858,12 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
     }
   }
   __syncwarp();
+  if (lane == 0) *w.n_actions = s_nact;
+  for (int g = lane; g < G; g += 32)
+    if (!ovf[g]) {
+      const int n = v.g_nparts[g];
+      for (int i = 0; i < n; ++i) w.g_parts[int64_t(g) * kPartCap + i] = sp[int64_t(g) * ps + i];
+    }
   if (smem_g) {
     for (int g = lane; g < G; g += 32) {
       w.g_npods[g] = sg[g];
@@ -958,12 +996,18 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     RAPP_LAUNCHED();
     k_tick_grid<<<w.F, 256, 0, st>>>(w);
     RAPP_LAUNCHED();
-    const size_t gbytes = size_t(5) * w.G * sizeof(int32_t);
-    const int smem_g = gbytes <= 200 * 1024 ? 1 : 0;
-    if (smem_g && gbytes > 48 * 1024)
-      RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)gbytes));
-    k_tick_commit<<<1, 32, smem_g ? gbytes : 0, st>>>(w, now, smem_g);
+    // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
+    // per GPU + overflow flags, within ~200 KB
+    const size_t budget = 200 * 1024;
+    const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
+    const int smem_g = gbytes + size_t(w.G) <= budget ? 1 : 0;
+    int ps = 0;
+    if (smem_g)
+      ps = (int)std::min<size_t>(12, (budget - gbytes - size_t(w.G)) / (8 * std::max(1, w.G)));
+    const size_t bytes = gbytes + size_t(w.G) * ps * 8 + size_t(w.G) + 16;
+    RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(bytes, 48 * 1024)));
+    k_tick_commit<<<1, 32, bytes, st>>>(w, now, smem_g, ps);
     RAPP_LAUNCHED();
   }
   return RAPP_OK;
