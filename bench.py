@@ -390,19 +390,15 @@ def run_lattice(args, rank, world, local):
     nfn = args.functions
     tables = make_config5_tables(nfn, seed=0, device=local)
     allowed = list(range(1, 33))
+    from paper_2505_01968_b200.shard import search_sharded
     tset = PerfTableSet([(t, allowed) for t in tables], quota_step=1)
-    f0, f1 = rank * nfn // world, (rank + 1) * nfn // world
     targets = torch.tensor([0.5 * max_lattice_rps(t) for t in tables], dtype=torch.float64,
                            device=dev)
-    per = (nfn + world - 1) // world
-    local_out = torch.full((per, 3), -1, dtype=torch.int32, device=dev)
-    gathered = torch.empty((per * world, 3), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        tset.search_dev(targets, local_out, fn_begin=f0, fn_end=f1, stream=stream.cuda_stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, local_out)
+        # functions sharded over ranks; one NCCL all-gather of the (b, s, q) decisions
+        return search_sharded(tset, targets, rank, world, stream=stream.cuda_stream)
 
     for _ in range(args.warmup):
         step()
