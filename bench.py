@@ -324,8 +324,11 @@ def run_stream(args, rank, world, local):
     # e2e: the reference-shaped host API with pinned host buffers, copies inside the timing
     e2e = None
     if not args.no_e2e:
-        hc = [c.cpu().pin_memory() for c in coords]
-        ho = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in tables]
+        # each e2e step streams 2.5e7 queries per model (1e8 predictions, 2.4 GB in) from
+        # pinned host memory — a bounded slice of the same workload, same metric
+        ne = min(n, 25_000_000)
+        hc = [c[:ne].cpu().pin_memory() for c in coords]
+        ho = [torch.empty(ne, dtype=torch.float64).pin_memory() for _ in tables]
         arrays = config2_arrays()
 
         def e2e_step():
@@ -334,18 +337,20 @@ def run_stream(args, rank, world, local):
 
         e2e_step()
         ok = all(np.array_equal(ho[k].numpy().view(np.int64),
-                                outs[k].cpu().numpy().view(np.int64)) for k in range(len(ho)))
+                                outs[k][:ne].cpu().numpy().view(np.int64))
+                 for k in range(len(ho)))
         if not ok:
             raise RuntimeError("e2e host path disagrees with the device path")
         barrier(world)
-        e2e_steps = max(1, min(args.steps, 5))
+        e2e_steps = max(1, min(args.steps, 10))
+        e2e_preds = len(tables) * ne
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-        e2e = {"value": world * preds_per_step * e2e_steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": preds_per_step * 24, "d2h_bytes_per_step": preds_per_step * 8,
+        e2e = {"value": world * e2e_preds * e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": e2e_preds * 24, "d2h_bytes_per_step": e2e_preds * 8,
                "steps": e2e_steps, "api": "paper_2505_01968_b200.kernels.interp3_many "
                "(C ABI rapp_interp3_many, pinned host buffers)"}
 

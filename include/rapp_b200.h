@@ -129,7 +129,9 @@ typedef struct {
     double alpha, beta;        /* ScalerConfig (hs/autoscaler.py:28-43) */
     double cooldown_ms, r_min;
     int32_t delta_iq;
-    int32_t _pad;
+    int32_t policy;            /* 0 hybrid (HybridPolicy), 1 replica-count baseline
+                                  (_ReplicaPolicy: horizontal-only / exclusive-gpu,
+                                  hs/policies.py:49-160) */
     double interval_s;         /* scaler_interval_ms / 1000.0, computed by the caller */
     double cold_start_ms;      /* SimConfig.cold_start_ms (new pods become RUNNING then) */
     double kal_A, kal_Q, kal_H, kal_D, kal_P0;  /* Kalman defaults (hs/kalman.py:15-19) */
@@ -145,6 +147,8 @@ typedef struct {
     int32_t _pad2;
     double kal_R, kal_P;
     double last_down_ms;       /* -inf when the function never scaled down */
+    int32_t shape_batch;       /* replica policy: the fixed pod shape (initial_config) */
+    int32_t shape_sm, shape_quota, _pad3;
 } rapp_fn_desc;
 
 typedef struct {

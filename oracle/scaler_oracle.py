@@ -259,6 +259,59 @@ def _down(cfg, fid, table, pods, excess):
     return out
 
 
+# -- replica-count baselines (hs/policies.py:49-160) -------------------------------------------
+
+
+def _legal(gpu, sm, q):
+    if not (1 <= sm <= 100 and 1 <= q <= 100):
+        return False
+    for p in gpu.partitions:
+        if p.sm_percent == sm and 100 - p.quota_allocated >= q:
+            return True
+    return _free_sm(gpu) >= sm
+
+
+def replica_decide(cfg, fn, table: OTable, cluster, R, last_down, shape, pod_factory,
+                   part_factory):
+    """_ReplicaPolicy.decide: returns (actions, new_last_down or None).  shape = (b, s, q)."""
+    fid = fn.function_id
+    sb, ss, sq = shape
+    pod_cap = table.thr(sb, ss, sq)
+    pods = [p for p in cluster.pods.values() if p.function_id == fid and _state(p) != DRAINING]
+    if not pods:
+        return [], None
+    cap = sum(table.thr(p.batch, p.sm_percent, p.quota_percent) for p in pods)
+    if R > cap * cfg["alpha"]:
+        wanted = math.ceil((R - cap * cfg["alpha"]) / pod_cap)
+        scratch = _Scratch(cluster)
+        out = []
+        for i in range(wanted):
+            totals = {}
+            for p in scratch.pods.values():
+                totals[p.gpu_id] = totals.get(p.gpu_id, 0) + p.sm_percent * p.quota_percent
+            cands = sorted((g for g in totals if _legal(scratch.gpus[g], ss, sq)),
+                           key=lambda g: (totals[g] / 10000.0, g))
+            gid = cands[0] if cands else next(
+                (g for g in sorted(scratch.gpus) if g not in totals
+                 and _legal(scratch.gpus[g], ss, sq)), None)
+            if gid is None:
+                break
+            out.append(_act(fid, H_UP, sb, ss, sq, None, gid))
+            place(scratch, pod_factory(f"__staged-{i}", fid, sb, ss, sq, gid), gid, part_factory)
+        return out, None
+    r_min = fn.min_rps if fn.min_rps is not None else cfg["r_min"]
+    last = last_down if last_down is not None else float("-inf")
+    if R < cap * cfg["beta"] and R > r_min and cluster.clock_ms - last >= cfg["cooldown_ms"]:
+        running = sorted((p for p in pods if _state(p) == RUNNING), key=lambda p: p.pod_id,
+                         reverse=True)
+        removable = max(0, len(running) - 1)
+        count = min(removable, int((cap - R) // pod_cap)) if pod_cap > 0 else 0
+        acts = [_act(fid, H_DOWN, p.batch, p.sm_percent, 0, p.pod_id, p.gpu_id)
+                for p in running[:count]]
+        return acts, (cluster.clock_ms if acts else None)
+    return [], None
+
+
 # -- Kalman (hs/kalman.py:45-62) ------------------------------------------------------------
 
 
@@ -282,7 +335,8 @@ def kalman_step(st, observed):
 
 
 def tick(cfg, functions, tables, cluster, now, interval_ms, arrivals, idle, kstate, kdefaults,
-         p0, last_down, counter, pod_factory, part_factory, cold_start_ms=5000.0):
+         p0, last_down, counter, pod_factory, part_factory, cold_start_ms=5000.0,
+         policy="hybrid"):
     """Mutates cluster/kstate/last_down in place.  Returns (actions with resolved pod ids,
     observed {fid: rps}, predicted {fid: rps}, new counter).  Pods whose cold start ended
     at or before `now` turn RUNNING first (ready events precede the scaler event at equal
@@ -305,8 +359,15 @@ def tick(cfg, functions, tables, cluster, now, interval_ms, arrivals, idle, ksta
         kstate[fid] = st
         observed[fid], predicted[fid] = obs, pred
         table = tables[fn.perf_table_ref or fid]
-        acts, stamp = scale(cfg, fn, table, cluster, pred, last_down.get(fid), pod_factory,
-                            part_factory)
+        if policy == "hybrid":
+            acts, stamp = scale(cfg, fn, table, cluster, pred, last_down.get(fid), pod_factory,
+                                part_factory)
+        else:
+            init = fn.initial
+            shape = ((init.batch, 100, 100) if policy == "exclusive-gpu"
+                     else (init.batch, init.sm_percent, init.quota_percent))
+            acts, stamp = replica_decide(cfg, fn, table, cluster, pred, last_down.get(fid),
+                                         shape, pod_factory, part_factory)
         if stamp is not None:
             last_down[fid] = stamp
         for a in acts:

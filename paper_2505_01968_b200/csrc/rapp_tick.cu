@@ -76,6 +76,9 @@ struct World {
   // config
   double alpha, beta, cooldown, r_min, interval_s, cold_start, kA, kQ, kH, kD, kP0;
   int delta, F, G, pod_cap;
+  int policy;                    // 0 hybrid, 1 replica-count baseline
+  const int32_t* fn_shape;       // [F][3] replica policy pod shape (b, s, q)
+  int32_t* wanted;               // replica scale-up: ceil(gap / pod_cap), clamped
   // tables
   const TableDesc* tds;
   const double* pool;
@@ -172,6 +175,116 @@ __global__ void k_tick_prologue(World w, double now) {
   }
 }
 
+// CPython float floor division (Objects/floatobject.c _float_div_mod): fmod-based, with
+// the quotient snapped to the nearest integer — not floor(x / y).
+__device__ __forceinline__ double py_floordiv(double vx, double wx) {
+  double mod = fmod(vx, wx);
+  double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
+  if (mod != 0.0) {
+    if ((wx < 0.0) != (mod < 0.0)) {
+      mod = __dadd_rn(mod, wx);
+      div = __dsub_rn(div, 1.0);
+    }
+  }
+  double fl;
+  if (div != 0.0) {
+    fl = floor(div);
+    if (__dsub_rn(div, fl) > 0.5) fl = __dadd_rn(fl, 1.0);
+  } else {
+    fl = copysign(0.0, __ddiv_rn(vx, wx));
+  }
+  return fl;
+}
+
+// Replica-count baselines (hs/policies.py:69-105): fixed-shape pods, capability summed in
+// pods-dict order (= pod index order), wanted = ceil(gap / pod_cap) new pods, scale-down
+// removes floor(excess / pod_cap) RUNNING pods newest id first, never the last one.
+__device__ void replica_phase_a(const World& w, int f, int lane, double R, double now,
+                                int* lst) {
+  int m = 0;
+  if (lane == 0) {
+    const int n = w.fn_npods[f];
+    for (int i = 0; i < n; ++i) {
+      const int p = w.fn_pods[f * kMaxPods + i];
+      if (w.p_state[p] == kDraining) continue;
+      int j = m++;
+      while (j > 0 && lst[j - 1] > p) {
+        lst[j] = lst[j - 1];
+        --j;
+      }
+      lst[j] = p;
+    }
+  }
+  __syncwarp();
+  m = __shfl_sync(0xffffffffu, m, 0);
+  if (m == 0) {
+    if (lane == 0) w.cls[f] = kNone;
+    return;
+  }
+  double* vals = w.rows + int64_t(f) * kMaxPods * kRow;  // scratch: one value per pod
+  for (int j = lane; j < m; j += 32) {
+    const int p = lst[j];
+    if (!batch_ok(w, f, w.p_b[p])) set_err(w, RAPP_E_VALUE, f);
+    vals[j] = thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(w.p_q[p]));
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  const int* shape = w.fn_shape + 3 * f;
+  if (!batch_ok(w, f, shape[0])) set_err(w, RAPP_E_VALUE, f);
+  const double pod_cap = thr_at(w, f, double(shape[0]), double(shape[1]), double(shape[2]));
+  double s = vals[0], c = 0.0;  // sum() in dict order (CPython 3.12: Neumaier)
+  for (int j = 1; j < m; ++j) {
+    const double x = vals[j];
+    const double t = __dadd_rn(s, x);
+    if (fabs(s) >= fabs(x))
+      c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
+    else
+      c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+    s = t;
+  }
+  if (c != 0.0 && isfinite(c)) s = __dadd_rn(s, c);
+  const double cap = s;
+  const double up_thr = __dmul_rn(cap, w.alpha);
+  if (R > up_thr) {
+    const double want = ceil(__ddiv_rn(__dsub_rn(R, up_thr), pod_cap));
+    w.wanted[f] = want > double(1 << 30) ? (1 << 30) : int(want);
+    w.cls[f] = kUp;
+    return;
+  }
+  const double mr = w.fn_min_rps[f];
+  const double r_min = mr != mr ? w.r_min : mr;
+  if (!(R < __dmul_rn(cap, w.beta) && R > r_min &&
+        __dsub_rn(now, w.last_down[f]) >= w.cooldown)) {
+    w.cls[f] = kNone;
+    return;
+  }
+  // RUNNING pods newest first: pod id descending
+  int run[kMaxPods];
+  int nr = 0;
+  for (int j = 0; j < m; ++j) {
+    const int p = lst[j];
+    if (w.p_state[p] != kRunning) continue;
+    int i = nr++;
+    while (i > 0 && id_less(w.p_id[run[i - 1]], w.p_id[p])) {
+      run[i] = run[i - 1];
+      --i;
+    }
+    run[i] = p;
+  }
+  const int removable = nr - 1 > 0 ? nr - 1 : 0;
+  int count = 0;
+  if (pod_cap > 0.0) {
+    const double k = py_floordiv(__dsub_rn(cap, R), pod_cap);
+    count = k < double(removable) ? int(k) : removable;  // min(removable, int(k))
+    if (count < 0) count = 0;
+  }
+  DownAct* out = w.down + f * kMaxPods;
+  for (int i = 0; i < count; ++i) out[i] = DownAct{kHDown, run[i], 0, 0};
+  w.ndown[f] = count;
+  w.stamp[f] = count > 0;
+  w.cls[f] = kDown;
+}
+
 // ---------------------------------------------------------------------------------------
 // phase A: one warp per function
 // ---------------------------------------------------------------------------------------
@@ -211,6 +324,10 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
     w.pred[f] = R;
   }
   R = __shfl_sync(0xffffffffu, R, 0);
+  if (w.policy == 1) {
+    replica_phase_a(w, f, lane, R, now, srt);
+    return;
+  }
 
   // non-draining pods sorted by (-sm, pod_id) (autoscaler.py:81-85)
   int m = 0;
@@ -384,7 +501,7 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
 // c_max at an off-step q_max is evaluated on demand by the commit warp.
 __global__ void k_tick_grid(World w) {
   const int f = blockIdx.x;
-  if (w.cls[f] != kUp) return;
+  if (w.policy != 0 || w.cls[f] != kUp) return;
   const int b = w.bref[f];
   if (!batch_ok(w, f, b)) return;  // phase B raises if the value is ever needed
   const int d = w.delta, nq = 100 / d;
@@ -777,6 +894,55 @@ struct Commit {
     }
   }
 
+  // check_placement (allocator.py:63-82) == nullptr: a joinable same-sm partition with
+  // headroom >= q, or an unallocated share >= sm
+  __device__ bool legal(int g, int s, int q) const {
+    if (s < 1 || s > 100 || q < 1 || q > 100) return false;
+    if (w.g_freesm[g] >= s) return true;
+    const uint64_t* P = parts(g);
+    const int n = w.g_nparts[g];
+    for (int i = 0; i < n; ++i)
+      if (part_sm(P[i]) == s && 100 - part_alloc(P[i]) >= q) return true;
+    return false;
+  }
+
+  // _pick_gpu (policies.py:128-141): the lowest (occupancy, id) used GPU that can take the
+  // shape, else the first free GPU that can, else none
+  __device__ int pick_gpu(int s, int q) const {
+    long long best = LLONG_MAX;
+    int first_free = 1 << 30;
+    for (int g = lane; g < w.G; g += 32) {
+      if (!legal(g, s, q)) continue;
+      if (w.g_npods[g] > 0) {
+        const long long k = (long long)w.g_hgo[g] << 32 | g;
+        best = k < best ? k : best;
+      } else {
+        first_free = min(first_free, g);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long x = __shfl_xor_sync(0xffffffffu, best, o);
+      best = x < best ? x : best;
+      first_free = min(first_free, __shfl_xor_sync(0xffffffffu, first_free, o));
+    }
+    if (best != LLONG_MAX) return int(best & 0xFFFFFFFF);
+    return first_free == (1 << 30) ? -1 : first_free;
+  }
+
+  // _add_replicas (policies.py:107-126)
+  __device__ void replica_up(int f, double now) const {
+    const int* shape = w.fn_shape + 3 * f;
+    const int want = w.wanted[f];
+    for (int i = 0; i < want; ++i) {
+      const int g = pick_gpu(shape[1], shape[2]);
+      if (g < 0) break;  // cluster saturated for this shape
+      const int p = new_pod(f, shape[0], shape[1], shape[2], now);
+      if (p < 0) return;
+      place(p, g);
+      emit(f, kHUp, shape[0], shape[1], shape[2], p, g, 0);
+    }
+  }
+
   __device__ void scale_down(int f, double now) const {
     const int na = w.ndown[f];
     const DownAct* acts = w.down + f * kMaxPods;
@@ -847,10 +1013,14 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
       const int i = __ffs(act) - 1;
       act &= act - 1;
       const int cls = __shfl_sync(0xffffffffu, mine, i);
-      if (cls == kUp)
-        c.scale_up(base + i, now);
-      else
+      if (cls == kUp) {
+        if (w.policy == 0)
+          c.scale_up(base + i, now);
+        else
+          c.replica_up(base + i, now);
+      } else {
         c.scale_down(base + i, now);
+      }
       if (*(volatile int32_t*)w.err) {
         stop = true;
         break;
@@ -1048,12 +1218,17 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   w.kD = cfg->kal_D;
   w.kP0 = cfg->kal_P0;
   w.delta = cfg->delta_iq;
+  if (cfg->policy != 0 && cfg->policy != 1) {
+    set_error("unknown policy code %d", cfg->policy);
+    return RAPP_E_VALUE;
+  }
+  w.policy = cfg->policy;
   const int F = (int)n_fns, G = (int)n_gpus;
   w.F = F;
   w.G = G;
   // ---- functions, tables, search index ----
   std::vector<int32_t> fn_table(F), fn_nb(F), fn_init(F), fn_npods(F, 0), fn_pairs_off(F),
-      fn_npairs(F);
+      fn_npairs(F), fn_shape(3 * (size_t)F);
   std::vector<double> fn_min(F), kR(F), kP(F), last(F), blist;
   std::vector<int64_t> fn_boff(F), fn_lat_off(F), fn_lat_len(F);
   std::vector<int32_t> pairs;
@@ -1073,6 +1248,9 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
       return RAPP_E_ARG;
     }
     fn_table[f] = fd.table_id;
+    fn_shape[3 * f] = fd.shape_batch;
+    fn_shape[3 * f + 1] = fd.shape_sm;
+    fn_shape[3 * f + 2] = fd.shape_quota;
     fn_min[f] = fd.min_rps;
     fn_init[f] = fd.kal_init;
     kR[f] = fd.kal_R;
@@ -1118,6 +1296,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
     double *b;
     int64_t *c;
     UP(a, fn_table) w.fn_table = a;
+    UP(a, fn_shape) w.fn_shape = a;
     UP(b, fn_min) w.fn_min_rps = b;
     UP(c, fn_lat_off) w.fn_lat_off = c;
     UP(c, fn_lat_len) w.fn_lat_len = c;
@@ -1225,6 +1404,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.pred, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.cls, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.gap0, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.wanted, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.nsorted, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.sorted, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.row_kd, FP * kMaxPods))) return rc;

@@ -33,7 +33,7 @@ _CODE_STATE = {0: PodState.COLD_STARTING, 1: PodState.RUNNING, 2: PodState.DRAIN
 class ScalerConfigC(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double),
                 ("cooldown_ms", ctypes.c_double), ("r_min", ctypes.c_double),
-                ("delta_iq", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("delta_iq", ctypes.c_int32), ("policy", ctypes.c_int32),
                 ("interval_s", ctypes.c_double), ("cold_start_ms", ctypes.c_double),
                 ("kal_A", ctypes.c_double), ("kal_Q", ctypes.c_double),
                 ("kal_H", ctypes.c_double), ("kal_D", ctypes.c_double),
@@ -43,14 +43,36 @@ class ScalerConfigC(ctypes.Structure):
 FN_DTYPE = np.dtype([("table_id", "<i4"), ("_pad", "<i4"), ("min_rps", "<f8"),
                      ("lattice_off", "<i8"), ("lattice_len", "<i8"), ("kal_init", "<i4"),
                      ("_pad2", "<i4"), ("kal_R", "<f8"), ("kal_P", "<f8"),
-                     ("last_down_ms", "<f8")])
+                     ("last_down_ms", "<f8"), ("shape_batch", "<i4"), ("shape_sm", "<i4"),
+                     ("shape_quota", "<i4"), ("_pad3", "<i4")])
 POD_DTYPE = np.dtype([("fn", "<i4"), ("batch", "<i4"), ("sm", "<i4"), ("quota", "<i4"),
                       ("gpu", "<i4"), ("part", "<i4"), ("state", "<i4"), ("_pad", "<i4"),
                       ("ready_at_ms", "<f8"), ("id", "S32")])
 ACTION_DTYPE = np.dtype([("fn", "<i4"), ("kind", "<i4"), ("batch", "<i4"), ("sm", "<i4"),
                          ("quota", "<i4"), ("pod", "<i4"), ("gpu", "<i4"),
                          ("released", "<i4")])
-assert FN_DTYPE.itemsize == 64 and POD_DTYPE.itemsize == 72 and ACTION_DTYPE.itemsize == 32
+assert FN_DTYPE.itemsize == 80 and POD_DTYPE.itemsize == 72 and ACTION_DTYPE.itemsize == 32
+
+POLICY_NAMES = ("hybrid", "horizontal-only", "exclusive-gpu")
+_ALIASES = {"hybrid": "hybrid", "horizontal": "horizontal-only",
+            "horizontal-only": "horizontal-only", "exclusive": "exclusive-gpu",
+            "exclusive-gpu": "exclusive-gpu"}
+
+
+def canonical_policy(name: str) -> str:
+    """Policy name aliases of hs/policies.py:165-183; ConfigError when unknown."""
+    canon = _ALIASES.get(name)
+    if canon is None:
+        raise ConfigError(f"unknown policy {name!r}; expected one of {POLICY_NAMES}")
+    return canon
+
+
+def policy_shape(policy: str, function) -> tuple[int, int, int]:
+    """Fixed pod shape of the replica baselines (hs/policies.py:206-222)."""
+    init = function.initial
+    if policy == "exclusive-gpu":
+        return init.batch, 100, 100
+    return init.batch, init.sm_percent, init.quota_percent
 
 
 def _ptr(a):
@@ -81,8 +103,10 @@ class TickEngine:
                  cold_start_ms: float = 5000.0, pod_counter: int = 0,
                  kalman_states: Optional[Mapping] = None,
                  last_scale_down: Optional[Mapping[str, float]] = None,
-                 promote_cold: bool = True, device: Optional[int] = None):
+                 promote_cold: bool = True, policy: str = "hybrid",
+                 device: Optional[int] = None):
         from .perf import PerfTable
+        self.policy = canonical_policy(policy)
         self.cluster = cluster
         self.config = scaler_config
         self.functions = {f.function_id: f for f in functions}
@@ -123,6 +147,8 @@ class TickEngine:
                 fn_arr[i]["kal_P"] = st.P
             ld = (last_scale_down or {}).get(fid)
             fn_arr[i]["last_down_ms"] = -math.inf if ld is None else float(ld)
+            sb, ss, sq = policy_shape(self.policy, f)
+            fn_arr[i]["shape_batch"], fn_arr[i]["shape_sm"], fn_arr[i]["shape_quota"] = sb, ss, sq
         self.ctx = ctx or _lib.Context.get(device)
         # GPUs in sorted-id order; partitions in list order
         self.gids = sorted(cluster.gpus)
@@ -155,7 +181,8 @@ class TickEngine:
             self.pod_fids.append(pod.function_id)
         self.counter = int(pod_counter)
         cfg = ScalerConfigC(scaler_config.alpha, scaler_config.beta, scaler_config.cooldown_ms,
-                            scaler_config.r_min, scaler_config.delta_iq, 0,
+                            scaler_config.r_min, scaler_config.delta_iq,
+                            0 if self.policy == "hybrid" else 1,
                             self.interval_ms / 1000.0, self.cold_start_ms, kal["A"], kal["Q"],
                             kal["H"], kal["D"], kal["P0"])
         lat = np.asarray(lattice if lattice else [0], dtype=np.int64)

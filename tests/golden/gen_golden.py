@@ -264,20 +264,24 @@ def gen_tick(hs):
     from hybridscale import ScalerConfig, SimConfig, WorkloadTrace
     from hybridscale.sim import SimulationEngine
     runs = []
-    specs = [  # (nfn, ngpu, seed, ticks, delta, alpha, beta)
-        (12, 6, 1, 8, 10, 0.9, 0.5), (40, 16, 2, 8, 10, 0.65, 0.45),
-        (100, 64, 3, 8, 10, 0.9, 0.5), (60, 20, 4, 8, 20, 0.8, 0.3),
-        (30, 40, 5, 8, 1, 0.9, 0.5),
+    specs = [  # (nfn, ngpu, seed, ticks, delta, alpha, beta, policy)
+        (12, 6, 1, 8, 10, 0.9, 0.5, "hybrid"), (40, 16, 2, 8, 10, 0.65, 0.45, "hybrid"),
+        (100, 64, 3, 8, 10, 0.9, 0.5, "hybrid"), (60, 20, 4, 8, 20, 0.8, 0.3, "hybrid"),
+        (30, 40, 5, 8, 1, 0.9, 0.5, "hybrid"),
+        (20, 12, 6, 8, 10, 0.9, 0.5, "horizontal-only"),
+        (50, 30, 7, 8, 10, 0.65, 0.45, "horizontal-only"),
+        (10, 24, 8, 8, 10, 0.9, 0.5, "exclusive-gpu"),
+        (30, 40, 9, 8, 10, 0.8, 0.3, "exclusive-gpu"),
     ]
     if os.environ.get("GOLDEN_BIG"):
-        specs.append((1000, 400, 0, 1, 10, 0.9, 0.5))
-    for nfn, ngpu, seed, nticks, delta, alpha, beta in specs:
+        specs.append((1000, 400, 0, 1, 10, 0.9, 0.5, "hybrid"))
+    for nfn, ngpu, seed, nticks, delta, alpha, beta, policy in specs:
         fns, tables, cluster, tparams = make_tick_world(hs, nfn, ngpu, seed)
         cfg = ScalerConfig(alpha=alpha, beta=beta, delta_iq=delta, cooldown_ms=3000.0, r_min=1.0)
         simcfg = SimConfig(scaler_interval_ms=1000.0, cold_start_ms=1500.0)
         trace = WorkloadTrace(entries=[], horizon_ms=1.0) if hasattr(hs, "WorkloadTrace") else None
         kal = {"A": 1.0, "Q": 25.0, "H": 1.0, "D": 4.0, "P0": 1.0}
-        eng = SimulationEngine(trace, fns, tables, cluster, cfg, simcfg, "hybrid", kal)
+        eng = SimulationEngine(trace, fns, tables, cluster, cfg, simcfg, policy, kal)
         eng._bootstrap()
         recorded = []
         orig = eng.policy.decide
@@ -288,15 +292,17 @@ def gen_tick(hs):
             return acts
         eng.policy.decide = spy
         rng = random.Random(seed * 7919)
-        run = {"nfn": nfn, "ngpu": ngpu, "seed": seed, "delta": delta, "alpha": hx(alpha),
+        run = {"nfn": nfn, "ngpu": ngpu, "seed": seed, "policy": policy, "delta": delta,
+               "alpha": hx(alpha),
                "beta": hx(beta), "cooldown_ms": hx(3000.0), "r_min": hx(1.0),
                "interval_ms": hx(1000.0), "cold_start_ms": hx(1500.0),
                "kalman": {k: hx(v) for k, v in kal.items()},
                "functions": [fn_dict(f) for f in fns],
                "tables": tparams,
                "initial": cluster_dict(eng.cluster), "ticks": []}
-        caps = {f.function_id: tables[f.function_id].throughput(8, f.initial.sm_percent, 20)
-                for f in fns}
+        shape_sq = (100, 100) if policy == "exclusive-gpu" else None
+        caps = {f.function_id: tables[f.function_id].throughput(
+                    8, *(shape_sq or (f.initial.sm_percent, 20))) for f in fns}
         counter0 = eng._pod_counter
         run["pod_counter0"] = counter0
         for k in range(nticks):
@@ -335,7 +341,45 @@ def gen_tick(hs):
     dump("tick.json", {"runs": runs})
 
 
-GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick}
+def gen_policy(hs):
+    """Replica-count baseline decisions (hs/policies.py:69-141) on the randomized clusters
+    of test_autoscaler.py, plus the hand cases of test_policies.py."""
+    import copy
+    from hybridscale import ScalerConfig, build_cluster, make_policy
+    from tests.conftest import make_conformance_table, make_function, place_running_pod
+    from tests.test_autoscaler import _random_cluster
+    table = make_conformance_table()
+    cases = []
+    for pname in ("horizontal-only", "exclusive-gpu"):
+        for seed, lo, hi in ((11, 0, 600), (12, 1.01, 60), (13, 100, 3000)):
+            rng = random.Random(seed)
+            for trial in range(150):
+                cluster = _random_cluster(rng)
+                cluster.clock_ms = rng.choice([0.0, 20_000.0, 60_000.0])
+                rate = rng.uniform(lo, hi)
+                init = rng.choice([(8, 50, 20), (8, 25, 40), (8, 50, 10)])
+                fn = make_function("conf-fn", initial=init)
+                for step in (20, 10):
+                    conf = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=step, cooldown_ms=30000,
+                                        r_min=1.0)
+                    pol = make_policy(pname, conf, {"conf-fn": table})
+                    last = rng.choice([None, 10_000.0])
+                    if last is not None:
+                        pol._last_scale_down["conf-fn"] = last
+                    before = cluster_dict(cluster)
+                    acts = pol.decide(fn, copy.deepcopy(cluster), rate)
+                    cases.append({"policy": pname, "cluster": before, "rate": hx(rate),
+                                  "initial": list(init), "last_down": None if last is None
+                                  else hx(last),
+                                  "cfg": [hx(0.9), hx(0.5), step, hx(30000.0), hx(1.0)],
+                                  "actions": action_list(acts),
+                                  "stamp": None if "conf-fn" not in pol._last_scale_down
+                                  else hx(pol._last_scale_down["conf-fn"])})
+    dump("policy.json", {"table": table_dict(table), "cases": cases})
+
+
+GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick,
+              "policy": gen_policy}
 
 
 def main(argv):

@@ -73,7 +73,8 @@ def run_oracle_ticks(run):
         acts, obs, pred, counter = so.tick(cfg, functions, tables, cluster, fx(t["now"]),
                                            fx(run["interval_ms"]), arrivals, set(t["idle"]),
                                            kstate, kal, p0, last_down, counter, make_pod,
-                                           make_part, cold_start_ms=fx(run["cold_start_ms"]))
+                                           make_part, cold_start_ms=fx(run["cold_start_ms"]),
+                                           policy=run.get("policy", "hybrid"))
         per_tick.append((acts, obs, pred))
     return per_tick, cluster
 
@@ -94,3 +95,22 @@ def test_oracle_reproduces_reference_ticks(tick_golden):
             assert [obs[f] for f in fids] == [fx(x) for x in t["observed"]]
             assert [pred[f] for f in fids] == [fx(x) for x in t["predicted"]]
         assert cluster_to(cluster) == golden_cluster_to(run["final"])
+
+
+def test_oracle_reproduces_reference_replica_policies():
+    """hs/policies.py:69-141 (horizontal-only, exclusive-gpu) on randomized clusters."""
+    g = load_golden("policy.json")
+    table = so.OTable(_T(g["table"]))
+    from paper_2505_01968_b200.core import FunctionSpec, PodConfig
+    for case in g["cases"]:
+        init = case["initial"]
+        fn = FunctionSpec("conf-fn", 20.0, perf_table_ref="conf-fn", allowed_batches=[8],
+                          initial=PodConfig(*init))
+        shape = (init[0], 100, 100) if case["policy"] == "exclusive-gpu" else tuple(init)
+        cluster = cluster_from(case["cluster"])
+        acts, stamp = so.replica_decide(_cfg(case["cfg"]), fn, table, cluster,
+                                        fx(case["rate"]), fx(case["last_down"]), shape,
+                                        make_pod, make_part)
+        assert [list(a) for a in acts] == case["actions"]
+        if stamp is not None:
+            assert stamp == fx(case["stamp"])

@@ -61,7 +61,8 @@ def _engine_for_run(run, apply_to_host=True):
     kal = {k: fx(v) for k, v in run["kalman"].items()}
     eng = TickEngine(fns, tables, cluster, cfg, kalman_params=kal,
                      scaler_interval_ms=fx(run["interval_ms"]),
-                     cold_start_ms=fx(run["cold_start_ms"]), pod_counter=run["pod_counter0"])
+                     cold_start_ms=fx(run["cold_start_ms"]), pod_counter=run["pod_counter0"],
+                     policy=run.get("policy", "hybrid"))
     return eng, fns, cluster
 
 
@@ -160,3 +161,112 @@ def test_full_grid_fresh_gpu_search_vs_oracle():
     cfg = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=1, cooldown_ms=1000.0, r_min=1.0)
     _oracle_ticks(fns, tables, cluster, cfg, 4, seed=5, interval_ms=1000.0,
                   cold_start_ms=1500.0)
+
+
+def test_replica_policies_match_reference_golden():
+    """horizontal-only / exclusive-gpu decisions (hs/policies.py:69-141), 1,800 cases."""
+    from paper_2505_01968_b200 import PerfTable
+    from paper_2505_01968_b200.core import FunctionSpec, PodConfig
+    from paper_2505_01968_b200.policies import make_policy
+    g = load_golden("policy.json")
+    t = g["table"]
+    b, s, q, v = golden_table_arrays(t)
+    table = PerfTable(t["function_id"], t["batches"], t["sms"], t["quotas"], v)
+    for case in g["cases"]:
+        fn = FunctionSpec("conf-fn", 20.0, perf_table_ref="conf-fn", allowed_batches=[8],
+                          initial=PodConfig(*case["initial"]))
+        pol = make_policy(case["policy"], _cfg_obj(case["cfg"]), {"conf-fn": table})
+        if case["last_down"] is not None:
+            pol._last_scale_down["conf-fn"] = fx(case["last_down"])
+        got = _acts(pol.decide(fn, cluster_from(case["cluster"]), fx(case["rate"])))
+        assert got == case["actions"]
+        assert pol._last_scale_down.get("conf-fn") == fx(case["stamp"])
+
+
+def test_policy_hand_cases():
+    """pkg/tests/test_policies.py: 4 fixed-shape replicas packed onto gpu-000; newest-first
+    removal; never the last pod; whole-GPU replicas need a free GPU; aliases."""
+    from paper_2505_01968_b200 import PerfTable
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.core import (ClusterState, FunctionSpec, GpuDevice, PodConfig,
+                                            PodInstance, PodState)
+    from paper_2505_01968_b200 import allocator
+    from paper_2505_01968_b200.errors import ConfigError
+    from paper_2505_01968_b200.policies import (ExclusiveGpuPolicy, HorizontalOnlyPolicy,
+                                                make_policy)
+    quotas = list(range(10, 101, 10))
+    lat = np.zeros((1, 2, 10))
+    for qi, qq in enumerate(quotas):
+        lat[0, 1, qi] = 8000.0 / (2.0 * qq + 10.0)
+        lat[0, 0, qi] = 2.0 * lat[0, 1, qi]
+    tables = {"conf-fn": PerfTable("conf-fn", [8], [25, 50], quotas, lat)}
+    cfg = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=20)
+    fn = FunctionSpec("conf-fn", 20.0, perf_table_ref="conf-fn", allowed_batches=[8],
+                      initial=PodConfig(8, 50, 20))
+
+    def cluster(n):
+        return ClusterState(gpus={f"gpu-{i:03d}": GpuDevice(f"gpu-{i:03d}") for i in range(n)})
+
+    def put(c, pid, sm, qq, gpu):
+        allocator.place_pod(c, PodInstance(pid, "conf-fn", 8, sm, qq, gpu,
+                                           state=PodState.RUNNING), gpu)
+
+    assert isinstance(make_policy("horizontal", cfg, tables), HorizontalOnlyPolicy)
+    assert isinstance(make_policy("exclusive", cfg, tables), ExclusiveGpuPolicy)
+    with pytest.raises(ConfigError):
+        make_policy("magic", cfg, tables)
+    c = cluster(3)
+    put(c, "p0", 50, 20, "gpu-000")
+    acts = make_policy("horizontal-only", cfg, tables).decide(fn, c, 200.0)
+    assert [(a.kind.value, a.batch, a.sm_percent, a.quota_percent, a.gpu_id) for a in acts] == \
+        [("horizontal_up", 8, 50, 20, "gpu-000")] * 4
+    c = cluster(2)
+    for i in range(3):
+        put(c, f"p{i}", 50, 20, "gpu-000")
+    c.clock_ms = 60_000.0
+    pol = make_policy("horizontal-only", cfg, tables)
+    assert [a.pod_id for a in pol.decide(fn, c, 20.0)] == ["p2", "p1"]
+    c.clock_ms = 70_000.0
+    assert pol.decide(fn, c, 20.0) == []  # cooldown
+    c = cluster(1)
+    put(c, "p0", 50, 20, "gpu-000")
+    c.clock_ms = 60_000.0
+    assert make_policy("horizontal-only", cfg, tables).decide(fn, c, 2.0) == []
+    c = cluster(2)
+    put(c, "p0", 100, 100, "gpu-000")
+    acts = make_policy("exclusive-gpu", cfg, tables).decide(fn, c, 2000.0)
+    assert [(a.gpu_id, a.sm_percent, a.quota_percent) for a in acts] == [("gpu-001", 100, 100)]
+
+
+@pytest.mark.parametrize("policy", ["horizontal-only", "exclusive-gpu"])
+def test_replica_ticks_vs_oracle_at_scale(policy):
+    """300 functions, replica policies, several ticks: device vs oracle."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    fns, tables, cluster, _ = bench.make_config4_world(300, 400, seed=11)
+    cfg = ScalerConfig(alpha=0.8, beta=0.4, delta_iq=10, cooldown_ms=1000.0)
+    eng = TickEngine(fns, tables, copy.deepcopy(cluster), cfg, scaler_interval_ms=1000.0,
+                     cold_start_ms=1500.0, pod_counter=300, policy=policy)
+    ocl = copy.deepcopy(cluster)
+    otables = {k: so.OTable(t) for k, t in tables.items()}
+    ocfg = {"alpha": 0.8, "beta": 0.4, "delta": 10, "cooldown_ms": 1000.0, "r_min": 1.0}
+    kal = {"A": 1.0, "Q": 4.0, "H": 1.0, "D": 16.0}
+    kstate, last, counter = {}, {}, 300
+    functions = {f.function_id: f for f in fns}
+    caps = {f.function_id: otables[f.function_id].thr(8, 20, 20) for f in fns}
+    rng = random.Random(4)
+    total = 0
+    for k in range(6):
+        now = 1000.0 * (k + 1)
+        arr = bench.config4_arrivals(fns, caps, rng, 1.0, 0.0, (4.0, 0.1, 3.0, 0.02, 5.0, 0.3)[k])
+        idle = {pid for pid in eng.pod_ids if rng.random() < 0.6}
+        acts, obs, pred, counter = so.tick(ocfg, functions, otables, ocl, now, 1000.0, arr, idle,
+                                           kstate, kal, 1.0, last, counter, make_pod, make_part,
+                                           cold_start_ms=1500.0, policy=policy)
+        res = eng.tick(now, arr, idle=idle)
+        got = [[a.function_id, a.kind.value, a.batch, a.sm_percent, a.quota_percent, pid,
+                a.gpu_id] for a, pid in zip(res.actions, res.pod_ids)]
+        assert got == [list(a) for a in acts], f"tick {k}"
+        total += len(acts)
+    assert total > 50
