@@ -41,7 +41,7 @@
 
 namespace rapp {
 
-constexpr int kMaxPods = 32;   // pods per managed function
+constexpr int kMaxPods = 128;  // pods per managed function (RAPP_E_ARG beyond)
 constexpr int kPartCap = 100;  // partitions per GPU (each >= 1 SM%, sum <= 100)
 constexpr int kRow = 101;      // quota steps per pod row
 constexpr int kCold = 0, kRunning = 1, kDraining = 2, kDead = -1;
