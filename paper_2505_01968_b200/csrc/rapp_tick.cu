@@ -130,6 +130,10 @@ struct World {
   int32_t* row_kd;               // [F][kMaxPods] index of q0 inside the row
   double* rows;                  // [F][kMaxPods][kRow] throughput at q0 + k*delta
   int32_t* bref;                 // batch of sorted[0]
+  // speculative vertical walk against tick-start headroom (phase A), per sorted pod:
+  int32_t* spec_avail;           // [F][kMaxPods] avail the walk assumed (-1: not walked)
+  int32_t* spec_k;               // [F][kMaxPods] steps taken
+  double* spec_gain;             // [F][kMaxPods] gain of those steps
   double* tgrid;                 // [F][100][100] throughput(bref, sm, q)
   int32_t* ndown;
   DownAct* down;                 // [F][kMaxPods]
@@ -412,7 +416,42 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
         rows[j * kRow + kd + k] =
             thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 + k * d));
     }
-    if (lane == 0) w.cls[f] = kUp;
+    __syncwarp();
+    if (lane == 0) {
+      // Speculate the vertical walk (autoscaler.py:115-133) with the tick-start headroom
+      // of each pod's partition.  The walk of pod j depends only on that headroom and on
+      // the gap left by pods 0..j-1 of this function, so phase B reuses it verbatim while
+      // every headroom it observes equals the one assumed here.
+      double gap = w.gap0[f];
+      for (int j = 0; j < m; ++j) {
+        w.spec_avail[f * kMaxPods + j] = -1;
+        if (!(gap > 0.0)) continue;
+        const int p = srt[j];
+        if (w.p_state[p] != kRunning) continue;
+        const int g = w.p_gpu[p];
+        const uint64_t* P = w.g_parts + int64_t(g) * kPartCap;
+        int alloc = 100;
+        for (int i = 0; i < w.g_nparts[g]; ++i)
+          if (part_uid(P[i]) == w.p_puid[p]) {
+            alloc = part_alloc(P[i]);
+            break;
+          }
+        const int q0 = w.p_q[p];
+        const int avail = q0 + (100 - alloc);
+        const double* row = rows + j * kRow + w.row_kd[f * kMaxPods + j];
+        int k = 0;
+        double gain = 0.0;
+        while (q0 + (k + 1) * d <= avail && __dsub_rn(gap, gain) > 0.0) {
+          ++k;
+          gain = __dsub_rn(row[k], row[0]);
+        }
+        w.spec_avail[f * kMaxPods + j] = avail;
+        w.spec_k[f * kMaxPods + j] = k;
+        w.spec_gain[f * kMaxPods + j] = gain;
+        if (k > 0) gap = __dsub_rn(gap, gain);
+      }
+      w.cls[f] = kUp;
+    }
     return;
   }
   if (cls != kDown) {
@@ -805,6 +844,7 @@ struct Commit {
     const int* srt = w.sorted + f * kMaxPods;
     const double* rows = w.rows + int64_t(f) * kMaxPods * kRow;
     // vertical first, largest sm first (autoscaler.py:115-133)
+    bool spec_ok = true;
     for (int j = 0; j < m; ++j) {
       if (!(gap > 0.0)) break;
       const int p = srt[j];
@@ -813,26 +853,33 @@ struct Commit {
       const int pos = find_part(g, w.p_puid[p]);
       const int q0 = w.p_q[p];
       const int avail = q0 + (100 - part_alloc(parts(g)[pos]));
-      const int kd = w.row_kd[f * kMaxPods + j];
-      const double* row = rows + j * kRow + kd;  // row[k] = thr at q0 + k*d
-      const double cur = row[0];
-      // k* = first k >= 0 with q0+(k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0
       int kstar = -1;
-      for (int base = 0; kstar < 0; base += 32) {
-        const int k = base + lane;
-        bool stop;
-        if (q0 + (k + 1) * d > avail) {
-          stop = true;
-        } else {
-          const double gain = k == 0 ? 0.0 : __dsub_rn(row[k], cur);
-          stop = !(__dsub_rn(gap, gain) > 0.0);
+      double gain = 0.0;
+      if (spec_ok && w.spec_avail[f * kMaxPods + j] == avail) {
+        kstar = w.spec_k[f * kMaxPods + j];  // the walk phase A did with this headroom
+        gain = w.spec_gain[f * kMaxPods + j];
+      } else {
+        spec_ok = false;  // later pods start from a different gap: walk them here
+        const int kd = w.row_kd[f * kMaxPods + j];
+        const double* row = rows + j * kRow + kd;  // row[k] = thr at q0 + k*d
+        const double cur = row[0];
+        // k* = first k >= 0 with q0+(k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0
+        for (int base = 0; kstar < 0; base += 32) {
+          const int k = base + lane;
+          bool stop;
+          if (q0 + (k + 1) * d > avail) {
+            stop = true;
+          } else {
+            const double gk = k == 0 ? 0.0 : __dsub_rn(row[k], cur);
+            stop = !(__dsub_rn(gap, gk) > 0.0);
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, stop);
+          if (mask) kstar = base + __ffs(mask) - 1;
         }
-        const unsigned mask = __ballot_sync(0xffffffffu, stop);
-        if (mask) kstar = base + __ffs(mask) - 1;
+        if (kstar > 0) gain = __dsub_rn(row[kstar], cur);
       }
       if (kstar > 0) {
         const int nq = q0 + kstar * d;
-        const double gain = __dsub_rn(row[kstar], cur);
         change_quota(p, nq);
         emit(f, kVUp, w.p_b[p], w.p_s[p], nq, p, g, 0);
         gap = __dsub_rn(gap, gain);
@@ -1410,6 +1457,9 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.row_kd, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.rows, FP * kMaxPods * kRow))) return rc;
   if ((rc = dev_alloc(t.get(), &w.bref, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.spec_avail, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.spec_k, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.spec_gain, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.tgrid, FP * 100 * 100))) return rc;
   if ((rc = dev_alloc(t.get(), &w.ndown, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.down, FP * kMaxPods))) return rc;
