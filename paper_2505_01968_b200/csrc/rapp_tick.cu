@@ -837,27 +837,78 @@ struct Commit {
     q = pair & 0xFFFF;
   }
 
-  __device__ void scale_up(int f, double now) const {
+  // Function header + first sorted pod, prefetched for 32 functions at once by the commit
+  // loop (nothing here can change before the function's own turn in the tick).
+  struct Pre {
+    double gap0, sg0;
+    int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref;
+    uint32_t uid0;
+  };
+
+  __device__ Pre prefetch(int f) const {
+    Pre r{};
+    r.p0 = -1;
+    if (f < w.F && w.cls[f] == kUp && w.policy == 0) {
+      r.gap0 = w.gap0[f];
+      r.m = w.nsorted[f];
+      r.bref = w.bref[f];
+      r.sav0 = w.spec_avail[f * kMaxPods];
+      r.sk0 = w.spec_k[f * kMaxPods];
+      r.sg0 = w.spec_gain[f * kMaxPods];
+      r.p0 = r.m > 0 ? w.sorted[f * kMaxPods] : -1;
+      if (r.p0 >= 0) {
+        const int p = r.p0;
+        r.st0 = w.p_state[p];
+        r.gpu0 = w.p_gpu[p];
+        r.uid0 = w.p_puid[p];
+        r.q0 = w.p_q[p];
+        r.b0 = w.p_b[p];
+        r.s0 = w.p_s[p];
+      }
+    }
+    return r;
+  }
+
+  __device__ static Pre bcast(const Pre& x, int src) {
+    Pre r;
+    r.gap0 = __shfl_sync(0xffffffffu, x.gap0, src);
+    r.sg0 = __shfl_sync(0xffffffffu, x.sg0, src);
+    r.m = __shfl_sync(0xffffffffu, x.m, src);
+    r.p0 = __shfl_sync(0xffffffffu, x.p0, src);
+    r.st0 = __shfl_sync(0xffffffffu, x.st0, src);
+    r.gpu0 = __shfl_sync(0xffffffffu, x.gpu0, src);
+    r.q0 = __shfl_sync(0xffffffffu, x.q0, src);
+    r.b0 = __shfl_sync(0xffffffffu, x.b0, src);
+    r.s0 = __shfl_sync(0xffffffffu, x.s0, src);
+    r.sav0 = __shfl_sync(0xffffffffu, x.sav0, src);
+    r.sk0 = __shfl_sync(0xffffffffu, x.sk0, src);
+    r.bref = __shfl_sync(0xffffffffu, x.bref, src);
+    r.uid0 = __shfl_sync(0xffffffffu, x.uid0, src);
+    return r;
+  }
+
+  __device__ void scale_up(int f, double now, const Pre& pre) const {
     const int d = w.delta;
-    double gap = w.gap0[f];
-    const int m = w.nsorted[f];
+    double gap = pre.gap0;
+    const int m = pre.m;
     const int* srt = w.sorted + f * kMaxPods;
     const double* rows = w.rows + int64_t(f) * kMaxPods * kRow;
     // vertical first, largest sm first (autoscaler.py:115-133)
     bool spec_ok = true;
     for (int j = 0; j < m; ++j) {
       if (!(gap > 0.0)) break;
-      const int p = srt[j];
-      if (w.p_state[p] != kRunning) continue;
-      const int g = w.p_gpu[p];
-      const int pos = find_part(g, w.p_puid[p]);
-      const int q0 = w.p_q[p];
+      const int p = j == 0 ? pre.p0 : srt[j];
+      if ((j == 0 ? pre.st0 : w.p_state[p]) != kRunning) continue;
+      const int g = j == 0 ? pre.gpu0 : w.p_gpu[p];
+      const int pos = find_part(g, j == 0 ? pre.uid0 : w.p_puid[p]);
+      const int q0 = j == 0 ? pre.q0 : w.p_q[p];
       const int avail = q0 + (100 - part_alloc(parts(g)[pos]));
       int kstar = -1;
       double gain = 0.0;
-      if (spec_ok && w.spec_avail[f * kMaxPods + j] == avail) {
-        kstar = w.spec_k[f * kMaxPods + j];  // the walk phase A did with this headroom
-        gain = w.spec_gain[f * kMaxPods + j];
+      const int sav = j == 0 ? pre.sav0 : w.spec_avail[f * kMaxPods + j];
+      if (spec_ok && sav == avail) {
+        kstar = j == 0 ? pre.sk0 : w.spec_k[f * kMaxPods + j];  // phase A's walk
+        gain = j == 0 ? pre.sg0 : w.spec_gain[f * kMaxPods + j];
       } else {
         spec_ok = false;  // later pods start from a different gap: walk them here
         const int kd = w.row_kd[f * kMaxPods + j];
@@ -881,11 +932,11 @@ struct Commit {
       if (kstar > 0) {
         const int nq = q0 + kstar * d;
         change_quota(p, nq);
-        emit(f, kVUp, w.p_b[p], w.p_s[p], nq, p, g, 0);
+        emit(f, kVUp, j == 0 ? pre.b0 : w.p_b[p], j == 0 ? pre.s0 : w.p_s[p], nq, p, g, 0);
         gap = __dsub_rn(gap, gain);
       }
     }
-    const int bref = w.bref[f];
+    const int bref = pre.bref;
     // one pod on the used GPU with the lowest occupancy (autoscaler.py:137-152)
     if (gap > 0.0) {
       const int g = argmin_used();
@@ -1055,6 +1106,7 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
   bool stop = false;
   for (int base = 0; base < w.F && !stop; base += 32) {
     const int mine = base + lane < w.F ? w.cls[base + lane] : kNone;
+    const Commit::Pre pre = c.prefetch(base + lane);
     unsigned act = __ballot_sync(0xffffffffu, mine != kNone);
     while (act) {
       const int i = __ffs(act) - 1;
@@ -1062,7 +1114,7 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
       const int cls = __shfl_sync(0xffffffffu, mine, i);
       if (cls == kUp) {
         if (w.policy == 0)
-          c.scale_up(base + i, now);
+          c.scale_up(base + i, now, Commit::bcast(pre, i));
         else
           c.replica_up(base + i, now);
       } else {
