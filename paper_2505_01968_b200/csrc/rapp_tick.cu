@@ -1216,7 +1216,8 @@ struct rapp_tick {
   int64_t* d_arrivals = nullptr;
   uint8_t* d_idle = nullptr;
   double* d_pred_in = nullptr;
-  int32_t* h_count = nullptr;  // pinned
+  int32_t* h_count = nullptr;  // pinned: n_actions, err, err_fn
+  int64_t h_npods = 0;         // pods created so far (host copy of w.n_pods)
 };
 
 namespace rapp {
@@ -1524,6 +1525,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &t->d_idle, (size_t)cap))) return rc;
   if ((rc = dev_alloc(t.get(), &t->d_pred_in, FP))) return rc;
   RAPP_CUDA(cudaMallocHost(&t->h_count, 4 * sizeof(int32_t)));
+  t->h_npods = n_pods;
   // build the fresh-GPU search index
   for (int f0 = 0; f0 < F; f0 += 32768) {
     const int nf = std::min(F - f0, 32768);
@@ -1580,6 +1582,7 @@ int rapp_tick_run_dev(rapp_tick* t, double now_ms, const int64_t* d_arrivals,
     return RAPP_E_ARG;
   }
   RAPP_CUDA(cudaSetDevice(t->ctx->device));
+  t->h_npods = -1;  // the host no longer knows the pod count without a read-back
   return launch_tick(t, now_ms, d_arrivals, d_idle, nullptr, (cudaStream_t)stream);
 }
 
@@ -1608,31 +1611,53 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
   World& w = t->w;
   cudaStream_t st = t->stream;
   const size_t F = (size_t)w.F;
-  int32_t np = 0;
-  RAPP_CUDA(cudaMemcpyAsync(&np, w.n_pods, 4, cudaMemcpyDeviceToHost, st));
+  if (t->h_npods < 0) {  // after device-only ticks
+    int32_t v = 0;
+    RAPP_CUDA(cudaStreamSynchronize(st));
+    RAPP_CUDA(cudaMemcpy(&v, w.n_pods, 4, cudaMemcpyDeviceToHost));
+    t->h_npods = v;
+  }
+  const int64_t np = t->h_npods;  // tracked on the host: no round trip before the launch
   if (F) RAPP_CUDA(cudaMemcpyAsync(t->d_arrivals, arrivals, F * 8, cudaMemcpyHostToDevice, st));
-  RAPP_CUDA(cudaStreamSynchronize(st));
   if (idle && np) RAPP_CUDA(cudaMemcpyAsync(t->d_idle, idle, (size_t)np, cudaMemcpyHostToDevice, st));
   if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
   if (predicted_in && F)
     RAPP_CUDA(cudaMemcpyAsync(t->d_pred_in, predicted_in, F * 8, cudaMemcpyHostToDevice, st));
   int rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr, st);
   if (rc) return rc;
+  // one synchronisation for the usual case: count, status, rates and the first actions
   RAPP_CUDA(cudaMemcpyAsync(t->h_count, w.n_actions, 4, cudaMemcpyDeviceToHost, st));
+  RAPP_CUDA(cudaMemcpyAsync(t->h_count + 1, w.err, 4, cudaMemcpyDeviceToHost, st));
+  RAPP_CUDA(cudaMemcpyAsync(t->h_count + 2, w.err_fn, 4, cudaMemcpyDeviceToHost, st));
+  const int64_t spec = actions ? std::min<int64_t>(max_actions, 1024) : 0;
+  if (spec > 0)
+    RAPP_CUDA(cudaMemcpyAsync(actions, w.actions, (size_t)spec * sizeof(rapp_action),
+                              cudaMemcpyDeviceToHost, st));
+  if (observed_out && F) RAPP_CUDA(cudaMemcpyAsync(observed_out, w.obs, F * 8, cudaMemcpyDeviceToHost, st));
+  if (predicted_out && F) RAPP_CUDA(cudaMemcpyAsync(predicted_out, w.pred, F * 8, cudaMemcpyDeviceToHost, st));
   RAPP_CUDA(cudaStreamSynchronize(st));
-  if ((rc = tick_error(t))) return rc;
+  if (t->h_count[1] != RAPP_OK) {
+    if ((rc = tick_error(t))) return rc;
+  }
   const int64_t n = t->h_count[0];
   *n_actions = n;
   if (n > max_actions) {
     set_error("action buffer too small (%lld > %lld)", (long long)n, (long long)max_actions);
     return RAPP_E_ARG;
   }
-  if (n && actions)
-    RAPP_CUDA(cudaMemcpyAsync(actions, w.actions, (size_t)n * sizeof(rapp_action),
-                              cudaMemcpyDeviceToHost, st));
-  if (observed_out && F) RAPP_CUDA(cudaMemcpyAsync(observed_out, w.obs, F * 8, cudaMemcpyDeviceToHost, st));
-  if (predicted_out && F) RAPP_CUDA(cudaMemcpyAsync(predicted_out, w.pred, F * 8, cudaMemcpyDeviceToHost, st));
-  RAPP_CUDA(cudaStreamSynchronize(st));
+  if (actions && n > spec) {
+    RAPP_CUDA(cudaMemcpyAsync(actions + spec, w.actions + spec,
+                              (size_t)(n - spec) * sizeof(rapp_action), cudaMemcpyDeviceToHost,
+                              st));
+    RAPP_CUDA(cudaStreamSynchronize(st));
+  }
+  if (actions) {
+    for (int64_t i = 0; i < n; ++i) t->h_npods += actions[i].kind == kHUp;
+  } else {
+    int32_t v = 0;
+    RAPP_CUDA(cudaMemcpy(&v, w.n_pods, 4, cudaMemcpyDeviceToHost));
+    t->h_npods = v;
+  }
   return RAPP_OK;
 }
 

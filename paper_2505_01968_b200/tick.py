@@ -85,14 +85,45 @@ def _state_code(state) -> int:
     return _STATE_CODE[PodState(state.value)]
 
 
-@dataclass
 class TickResult:
-    actions: list[ScalingAction]      # reference-shaped (horizontal_up carries pod_id None)
-    pod_ids: list[str]                # pod each action refers to (new pods: their new id)
-    released: list[bool]              # horizontal_down of an idle pod: released at once
-    observed: dict[str, float]
-    predicted: dict[str, float]
-    raw: np.ndarray = field(repr=False, default=None)
+    """One tick's output.  `raw` holds the packed action records (rapp_action) in
+    emission order and `observed_rps`/`predicted_rps` the per-function rates in sorted
+    function order; the reference-shaped views below are built on first access."""
+
+    def __init__(self, engine, raw, obs, pred, pod_ids):
+        self.raw = raw
+        self.observed_rps = obs
+        self.predicted_rps = pred
+        self.pod_ids = pod_ids          # pod each action refers to (new pods: new id)
+        self._engine = engine
+        self._actions = None
+
+    @property
+    def actions(self) -> list[ScalingAction]:
+        """Reference-shaped actions (horizontal_up carries pod_id None)."""
+        if self._actions is None:
+            e = self._engine
+            out = []
+            for a, pid in zip(self.raw.tolist(), self.pod_ids):
+                kind = KINDS[a[1]]
+                out.append(ScalingAction(e.fids[a[0]], kind, a[2], a[3], a[4],
+                                         None if kind is ActionKind.HORIZONTAL_UP else pid,
+                                         e.gids[a[6]]))
+            self._actions = out
+        return self._actions
+
+    @property
+    def released(self) -> list[bool]:
+        """horizontal_down of an idle pod: released at once."""
+        return [bool(x) for x in self.raw["released"]]
+
+    @property
+    def observed(self) -> dict[str, float]:
+        return dict(zip(self._engine.fids, self.observed_rps.tolist()))
+
+    @property
+    def predicted(self) -> dict[str, float]:
+        return dict(zip(self._engine.fids, self.predicted_rps.tolist()))
 
 
 class TickEngine:
@@ -219,11 +250,13 @@ class TickEngine:
             arr = np.ascontiguousarray(arrivals, dtype=np.int64)
         if arr.shape != (F,):
             raise ValueError(f"expected {F} arrival counts")
-        if np.any(arr < 0):
+        if F and arr.min() < 0:
             raise ValueError("observed_rps must be non-negative")
         n = len(self.pod_ids)
         if idle is None:
-            idle_arr = np.ones(max(1, n), dtype=np.uint8)
+            if getattr(self, "_all_idle", None) is None or len(self._all_idle) < max(1, n):
+                self._all_idle = np.ones(max(1024, 2 * n), dtype=np.uint8)
+            idle_arr = self._all_idle
         else:
             idle_set = set(idle)
             idle_arr = np.fromiter((pid in idle_set for pid in self.pod_ids), dtype=np.uint8,
@@ -240,34 +273,30 @@ class TickEngine:
             raise FilterDegenerateError("H*P'*H + D == 0")
         _lib.check(rc, "tick")
         raw = self._act_buf[:nact.value].copy()
-        res = self._decode(raw)
+        res = self._bookkeep(raw)
         if apply_to_host:
             self._apply_host(res, float(now_ms))
         return res
 
-    def _decode(self, raw: np.ndarray) -> TickResult:
-        actions, pod_ids, released = [], [], []
-        for a in raw:
-            fid = self.fids[a["fn"]]
-            kind = KINDS[a["kind"]]
-            gpu = self.gids[a["gpu"]]
-            if kind is ActionKind.HORIZONTAL_UP:
+    def _bookkeep(self, raw: np.ndarray) -> TickResult:
+        """Names the pods the device created (pod-%06d in apply order, like the sim's
+        counter) and maps every action to its pod id."""
+        pods = raw["pod"].tolist()
+        kinds = raw["kind"].tolist()
+        fns = raw["fn"].tolist()
+        pod_ids = []
+        for p, k, f in zip(pods, kinds, fns):
+            if k == 2:  # horizontal_up: a new pod at the next device index
+                assert p == len(self.pod_ids), "device pod index out of step"
                 pid = f"pod-{self.counter:06d}"
                 self.counter += 1
-                assert a["pod"] == len(self.pod_ids), "device pod index out of step"
                 self.pod_ids.append(pid)
-                self.pod_fids.append(fid)
-                actions.append(ScalingAction(fid, kind, int(a["batch"]), int(a["sm"]),
-                                             int(a["quota"]), None, gpu))
+                self.pod_fids.append(self.fids[f])
             else:
-                pid = self.pod_ids[a["pod"]]
-                actions.append(ScalingAction(fid, kind, int(a["batch"]), int(a["sm"]),
-                                             int(a["quota"]), pid, gpu))
+                pid = self.pod_ids[p]
             pod_ids.append(pid)
-            released.append(bool(a["released"]))
-        obs = {f: float(self._obs[i]) for i, f in enumerate(self.fids)}
-        pred = {f: float(self._pred[i]) for i, f in enumerate(self.fids)}
-        return TickResult(actions, pod_ids, released, obs, pred, raw)
+        return TickResult(self, raw, self._obs[:len(self.fids)].copy(),
+                          self._pred[:len(self.fids)].copy(), pod_ids)
 
     def _apply_host(self, res: TickResult, now: float) -> None:
         """Cluster effects of hs/sim.py:493-525 on the host snapshot (promotions first)."""
