@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(kSearchThreads)
   double* sThr = p;                p += nB;
   double* sB = p;                  p += nB;
   int2* sI = (int2*)p;             p += nB;
-  unsigned long long* sMin = (unsigned long long*)p;
+  unsigned long long* sMin = (unsigned long long*)p;  p += nB;
+  double2* sTT = (double2*)p;      p += 2 * nB;  // (tb, threshold) per batch entry
+  int4* sSeg = (int4*)p;           p += 2 * nB;  // runs of entries sharing a row bracket
+  __shared__ int s_nseg;
 
   // per-axis brackets, once per CTA (locate semantics, _grid_cy.pyx:9-33)
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -170,9 +173,24 @@ __global__ void __launch_bounds__(kSearchThreads)
     sI[i] = make_int2(lo, hi);
     sB[i] = b;
     sThr[i] = thr_g[fd.boff + i];
+    sTT[i] = make_double2(t, sThr[i]);
     if (MINLAT) sMin[i] = 0x7FF0000000000000ull;
   }
   __syncthreads();
+  // batch entries are sorted, so entries bracketed by the same table rows (i0, i1) are
+  // consecutive: one segment per bracket, its two row values computed once per (s, q)
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int i = 0; i < nB; ++i) {
+      if (i == 0 || sI[i].x != sI[i - 1].x || sI[i].y != sI[i - 1].y)
+        sSeg[n++] = make_int4(sI[i].x, sI[i].y, i, i + 1);
+      else
+        sSeg[n - 1].w = i + 1;
+    }
+    s_nseg = n;
+  }
+  __syncthreads();
+  const int nseg = s_nseg;
 
   const double target = targets[f];
   const int pairs = ns * nQ;
@@ -203,25 +221,23 @@ __global__ void __launch_bounds__(kSearchThreads)
       cb = c;
       return c;
     };
-    int found = -1;
-    for (int g = 0; g < nB; g += 32) {
-      uint32_t mask = 0;
-      const int ge = min(nB, g + 32);
-      for (int bi = g; bi < ge; ++bi) {
-        const int2 ii = sI[bi];
-        const double c0 = row(ii.x);
-        const double c1 = row(ii.y);
-        const double lat = lerp_rn(c0, c1, sTb[bi]);
+    int found = 1 << 30;  // first feasible batch entry (entries ascend with b)
+    for (int sg = 0; sg < nseg; ++sg) {
+      const int4 S = sSeg[sg];
+      const double c0 = row(S.x);
+      const double c1 = S.y == S.x ? c0 : row(S.y);
+      for (int bi = S.z; bi < S.w; ++bi) {
+        const double2 tt = sTT[bi];
+        const double lat = lerp_rn(c0, c1, tt.x);  // the reference's final batch lerp
         if (MINLAT) {
           if (lat >= 0.0) atomicMin(&sMin[bi], (unsigned long long)__double_as_longlong(lat));
         } else {
-          const bool ok = lat > 0.0 ? (lat <= sThr[bi]) : (throughput(sB[bi], lat) >= target);
-          mask |= uint32_t(ok) << (bi - g);
+          const bool ok = lat > 0.0 ? (lat <= tt.y) : (throughput(sB[bi], lat) >= target);
+          found = ok && bi < found ? bi : found;
         }
       }
-      if (!MINLAT && found < 0 && mask) found = g + __ffs(mask) - 1;
     }
-    if (!MINLAT && found >= 0) {
+    if (!MINLAT && found < (1 << 30)) {
       const uint64_t s = uint64_t(sa[si]);
       const uint64_t q = uint64_t((qi + 1) * step);
       const unsigned long long k =
@@ -407,7 +423,7 @@ int rapp_mec_plan_create(rapp_ctx* ctx, int64_t nfn, const int32_t* table_of_fn,
     }
   pl->total_b = (int64_t)blist.size();
   pl->smem_table = max_seg * 8 <= kSearchSmemTable;
-  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 5 * max_nB;
+  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 10 * max_nB;
   pl->smem_bytes = (size_t)((pl->smem_table ? max_seg : 0) + brk) * 8;
   if (pl->smem_bytes > 200 * 1024) {
     set_error("lattice search shared-memory footprint %zu bytes too large", pl->smem_bytes);
