@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kSearchThreads)
   double* sB = p;                  p += nB;
   int2* sI = (int2*)p;             p += nB;
   unsigned long long* sMin = (unsigned long long*)p;  p += nB;
+  p += (p - smem) & 1;                           // 16-byte alignment for the vectors below
   double2* sTT = (double2*)p;      p += 2 * nB;  // (tb, threshold) per batch entry
   int4* sSeg = (int4*)p;           p += 2 * nB;  // runs of entries sharing a row bracket
   __shared__ int s_nseg;
@@ -423,7 +424,7 @@ int rapp_mec_plan_create(rapp_ctx* ctx, int64_t nfn, const int32_t* table_of_fn,
     }
   pl->total_b = (int64_t)blist.size();
   pl->smem_table = max_seg * 8 <= kSearchSmemTable;
-  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 10 * max_nB;
+  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 10 * max_nB + 2;
   pl->smem_bytes = (size_t)((pl->smem_table ? max_seg : 0) + brk) * 8;
   if (pl->smem_bytes > 200 * 1024) {
     set_error("lattice search shared-memory footprint %zu bytes too large", pl->smem_bytes);
