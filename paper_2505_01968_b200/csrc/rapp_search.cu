@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(kSearchThreads)
   }
   __syncthreads();
   const int nseg = s_nseg;
+  const bool pos_table = td.fast != 0;  // fast-path tables are finite and positive
 
   const double target = targets[f];
   const int pairs = ns * nQ;
@@ -227,12 +228,23 @@ __global__ void __launch_bounds__(kSearchThreads)
       const int4 S = sSeg[sg];
       const double c0 = row(S.x);
       const double c1 = S.y == S.x ? c0 : row(S.y);
-      for (int bi = S.z; bi < S.w; ++bi) {
-        const double2 tt = sTT[bi];
-        const double lat = lerp_rn(c0, c1, tt.x);  // the reference's final batch lerp
-        if (MINLAT) {
+      if (MINLAT) {
+        for (int bi = S.z; bi < S.w; ++bi) {
+          const double lat = lerp_rn(c0, c1, sTT[bi].x);
           if (lat >= 0.0) atomicMin(&sMin[bi], (unsigned long long)__double_as_longlong(lat));
-        } else {
+        }
+      } else if (pos_table) {
+        // finite positive grid (checked at upload): every interpolated latency is > 0, so
+        // `rps >= target` is exactly `lat <= threshold` — no division on this path
+        for (int bi = S.z; bi < S.w; ++bi) {
+          const double2 tt = sTT[bi];
+          const double lat = lerp_rn(c0, c1, tt.x);  // the reference's final batch lerp
+          found = lat <= tt.y && bi < found ? bi : found;
+        }
+      } else {
+        for (int bi = S.z; bi < S.w; ++bi) {
+          const double2 tt = sTT[bi];
+          const double lat = lerp_rn(c0, c1, tt.x);
           const bool ok = lat > 0.0 ? (lat <= tt.y) : (throughput(sB[bi], lat) >= target);
           found = ok && bi < found ? bi : found;
         }
