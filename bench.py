@@ -437,10 +437,11 @@ def run_lattice(args, rank, world, local):
 # ----------------------------------------------------------------------------------------
 
 
-def run_tick(args, local, ticks=None, warmup=None, full_grid=False):
+def run_tick(args, local, ticks=None, warmup=None, full_grid=False, nfn=1000, ngpu=400):
     """Device µs per tick (CUDA events around rapp_tick_run_dev, inputs resident) and
     end-to-end µs per tick through TickEngine.tick (H2D arrivals + idle flags, kernels,
-    D2H of the ordered action list and rates)."""
+    D2H of the ordered action list and rates).  Config 4: nfn=1000, ngpu=400; the
+    config-3 tick size is nfn=100, ngpu=64."""
     import ctypes
     import torch
     from paper_2505_01968_b200 import _lib
@@ -449,7 +450,7 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False):
     ticks = ticks or args.ticks
     warmup = warmup if warmup is not None else 3
     dev = torch.device("cuda", local)
-    fns, tables, cluster, caps = make_config4_world(1000, 400, seed=0, full_grid=full_grid,
+    fns, tables, cluster, caps = make_config4_world(nfn, ngpu, seed=0, full_grid=full_grid,
                                                     device=local)
     cfg = ScalerConfig(delta_iq=1 if full_grid else 10)
     interval_ms = 2000.0
@@ -499,7 +500,7 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False):
         acts.append(len(res.actions))
     e2e_us = e2e_us[warmup:]
     acts = acts[warmup:]
-    return {"functions": 1000, "gpus_simulated": 400, "grid": "32x91x100, delta 1" if full_grid
+    return {"functions": nfn, "gpus_simulated": ngpu, "grid": "32x91x100, delta 1" if full_grid
             else "6x10x10, delta 10", "ticks": ticks,
             "device_us_median": float(np.median(dev_us)), "device_us_max": float(np.max(dev_us)),
             "e2e_us_median": float(np.median(e2e_us)), "e2e_us_max": float(np.max(e2e_us)),
@@ -675,7 +676,8 @@ def main():
             "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours"}
     if world == 1 and args.workload == "stream" and not args.no_extra:
         # the second half of the metric ("scaling decisions/tick latency") and config 5
-        extra = {"tick_config4": run_tick(args, local, ticks=20)}
+        extra = {"tick_config4": run_tick(args, local, ticks=20),
+                 "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64)}
         extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
         line["extra"] = extra
     print(json.dumps(line))
