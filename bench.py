@@ -74,7 +74,7 @@ def config2_arrays():
     return out
 
 
-def make_config5_tables(n, seed=0, device=None):
+def make_config5_tables(n, seed=0, device=None, upload=True):
     """Config 5 tables: b=[1..32 pow2] x s=1..100 x q=10..100/10 per function, random
     gen_tables parameters (fixed~U(4,20), per_item~U(0.5,4),
     sm_floor~U(0.2,0.4)).  The lattice a search walks is B x table.sms x quota steps
@@ -88,8 +88,20 @@ def make_config5_tables(n, seed=0, device=None):
         fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
         tables.append(PerfTable(f"fn-{i:05d}", BATCHES, s, q,
                                 surface(fixed, per, floor, 1.0 - floor, BATCHES, s, q),
-                                device=device))
+                                device=device) if upload else
+                      _HostTable(BATCHES, s, q,
+                                 surface(fixed, per, floor, 1.0 - floor, BATCHES, s, q)))
     return tables
+
+
+class _HostTable:
+    """Axes + grid only (CPU-baseline workers never touch the device)."""
+
+    def __init__(self, b, s, q, lat):
+        self.batches = list(b)
+        self._b_axis, self._s_axis, self._q_axis = (np.asarray(a, dtype=np.float64)
+                                                    for a in (b, s, q))
+        self.latency_ms = lat
 
 
 def make_config4_world(nfn=1000, ngpu=400, seed=0, full_grid=False, device=None):
@@ -387,18 +399,50 @@ def load_traffic(n):
 # ----------------------------------------------------------------------------------------
 
 
+def lattice_fp64_ops(table, batches, step):
+    """FP64 operations K3 executes per lattice point of one function (algorithmic work of
+    the segment formulation, rapp_search.cu): per (s, q) pair 9 ops (three lerps of
+    sub/mul/add) for every distinct table row a batch segment brackets, 1 sub per segment,
+    and per point the final batch lerp (mul, add) plus the feasibility compare."""
+    from paper_2505_01968_b200.perf import PerfTable  # noqa: F401  (typing only)
+    ax = list(table._b_axis)
+    segs, rows = [], set()
+    for b in batches:
+        if b <= ax[0]:
+            br = (0, 0)
+        elif b >= ax[-1]:
+            br = (len(ax) - 1, len(ax) - 1)
+        else:
+            lo = max(i for i in range(len(ax)) if ax[i] <= b)
+            br = (lo, lo) if ax[lo] == b else (lo, lo + 1)
+        if not segs or segs[-1] != br:
+            segs.append(br)
+        rows.update(br)
+    per_pair = 9 * len(rows) + len(segs) + 3 * len(batches)
+    return per_pair / len(batches)
+
+
+def fp64_peak(local):
+    """Measured non-FMA FP64 instruction rate (ops/s) of this device (rapp_probe_fp64)."""
+    import ctypes
+    from paper_2505_01968_b200 import _lib
+    a, m = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.load().rapp_probe_fp64(int(local), ctypes.byref(a), ctypes.byref(m)))
+    return min(a.value, m.value)
+
+
 def run_lattice(args, rank, world, local):
+    import ctypes
     import torch
-    import torch.distributed as dist
     from paper_2505_01968_b200 import PerfTableSet, _lib
     dev = torch.device("cuda", local)
     nfn = args.functions
     tables = make_config5_tables(nfn, seed=0, device=local)
     allowed = list(range(1, 33))
-    from paper_2505_01968_b200.shard import search_sharded
+    from paper_2505_01968_b200.shard import search_sharded, shard_range
     tset = PerfTableSet([(t, allowed) for t in tables], quota_step=1)
-    targets = torch.tensor([0.5 * max_lattice_rps(t) for t in tables], dtype=torch.float64,
-                           device=dev)
+    host_targets = np.array([0.5 * max_lattice_rps(t) for t in tables], dtype=np.float64)
+    targets = torch.from_numpy(host_targets).to(dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -408,6 +452,8 @@ def run_lattice(args, rank, world, local):
     for _ in range(args.warmup):
         step()
     barrier(world)
+    lib = _lib.load()
+    _lib.check(lib.rapp_mec_plan_timing(tset._plan, 1))
     launches0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -419,17 +465,101 @@ def run_lattice(args, rank, world, local):
         torch.cuda.synchronize()
         clk.mark_end()
     launches = _lib.launch_count() - launches0
+    k_ms, k_n = ctypes.c_double(), ctypes.c_int64()
+    _lib.check(lib.rapp_mec_plan_kernel_time(tset._plan, ctypes.byref(k_ms), ctypes.byref(k_n)))
+    _lib.check(lib.rapp_mec_plan_timing(tset._plan, 0))
     barrier(world)
     ms = max_over_ranks(start.elapsed_time(end), world)
     points = tset.points
     value = points * args.steps / (ms / 1000.0)
+    # roofline of the dominant kernel (the K3 meet pass) against the measured FP64 rate
+    f0, f1 = shard_range(nfn, rank, world)
+    my_points = points * (f1 - f0) / nfn
+    ops_pt = lattice_fp64_ops(tables[0], allowed, 1)
+    kern_s = k_ms.value / 1000.0 / max(1, k_n.value)
+    achieved = my_points * ops_pt / kern_s / 1e12
+    peak = fp64_peak(local) / 1e12
+    roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(peak, 3),
+            "unit": "Tops/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "k_mec_lattice<meet> (rapp_search.cu)",
+            "peak_source": "measured: rapp_probe_fp64 (independent __dadd_rn/__dmul_rn chains "
+                           "on every SM, min of the two rates)",
+            "fp64_ops_per_point": round(ops_pt, 4),
+            "naive_fp64_ops_per_point": 30.30,
+            "kernel_ms_per_launch": round(kern_s * 1000.0, 4),
+            "kernel_share_of_step": round(k_ms.value / max(1e-9, start.elapsed_time(end)), 4),
+            "note": "the kernel is issue-bound (integer/select work beside the FP64 ops); "
+                    "HBM traffic is the tables once (48 KB/function)"}
+    # end to end through the public API: host targets -> H2D, search, D2H decisions
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(host_targets).pin_memory()
+        out_host = torch.empty((nfn, 3), dtype=torch.int32).pin_memory()
+        d_t = torch.empty_like(targets)
+
+        def e2e_step():
+            d_t.copy_(pinned, non_blocking=True)
+            res = search_sharded(tset, d_t, rank, world, stream=stream.cuda_stream)
+            out_host.copy_(res, non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nrep = max(3, args.steps // 2)
+        for _ in range(nrep):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = max_over_ranks((time.perf_counter() - t0) * 1000.0, world)
+        e2e = {"value": points * nrep / (dt / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": nfn * 8, "d2h_bytes_per_step": nfn * 12, "steps": nrep,
+               "api": "shard.search_sharded over PerfTableSet (C ABI rapp_mec_plan_run_dev), "
+                      "pinned host targets in, (b, s, q) decisions out"}
     cfg = {"workload": f"config5: {nfn} functions x 32 batches x 100 sm x 100 quota lattice "
            "(most_efficient_config, target 0.5 x max rps), tables 6x100x10",
            "points_per_step": points, "parallelism": f"functions sharded x{world}, NCCL "
-           "all-gather of decisions"}
-    return {"value": value, "ms": ms, "roofline": None, "e2e": None, "config": cfg,
+           "all-gather of decisions",
+           "l2": "tables 150 MB > 126 MB L2, each read once per step (no flush needed)"}
+    return {"value": value, "ms": ms, "roofline": roof, "e2e": e2e, "config": cfg,
             "launches": launches, "clocks": clk.summary(), "dtype": "f64",
             "scaling": "strong"}
+
+
+_LW = {}
+
+
+def _lattice_worker_init(nfn_sample):
+    from oracle.binding import load_oracle
+    load_oracle()
+    tables = make_config5_tables(nfn_sample, seed=0, device=None, upload=False)
+    _LW["work"] = [(t, 0.5 * max_lattice_rps(t)) for t in tables]
+
+
+def _lattice_worker_run(_):
+    from oracle.binding import or_most_efficient_config
+    for t, target in _LW["work"]:
+        or_most_efficient_config(t._b_axis, t._s_axis, t._q_axis, t.latency_ms, target, 1,
+                                 list(range(1, 33)))
+    return len(_LW["work"])
+
+
+def lattice_cpu_baseline(fn_per_proc=25, steps=3, procs=None):
+    """The C restatement of most_efficient_config (oracle/rapp_oracle.c; the reference's
+    search is Python, hs/perf.py:104-145, and cannot travel to the GPU box) over a process
+    pool: config-5 lattices per second of host time."""
+    import multiprocessing as mp
+    procs = procs or host_cores()
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs, initializer=_lattice_worker_init, initargs=(fn_per_proc,)) as pool:
+        pool.map(_lattice_worker_run, range(procs))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pool.map(_lattice_worker_run, range(procs))
+        dt = time.perf_counter() - t0
+    pts = steps * procs * fn_per_proc * 32 * 100 * 100
+    return {"value": pts / dt, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": f"{fn_per_proc} config-5 functions (32x100x100 lattice each) per process "
+                      f"per step, {procs} processes, {steps} steps ({pts} points, {dt:.2f} s)"}
 
 
 # ----------------------------------------------------------------------------------------
@@ -668,6 +798,8 @@ def main():
     if world == 1 and not args.no_cpu_baseline and args.workload == "stream":
         v, info = cpu_reference(steps=3, warmup=1)
         cpu = {"value": v, "unit": UNIT, **info}
+    if world == 1 and not args.no_cpu_baseline and args.workload == "lattice":
+        cpu = lattice_cpu_baseline()
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
             "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None,
@@ -679,6 +811,13 @@ def main():
         extra = {"tick_config4": run_tick(args, local, ticks=20),
                  "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64)}
         extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
+        largs = argparse.Namespace(**{**vars(args), "steps": 50, "functions": 3125})
+        lat = run_lattice(largs, rank, world, local)
+        extra["lattice_config5"] = {"value": lat["value"], "unit": UNIT,
+                                    "ms_per_step": lat["ms"] / largs.steps,
+                                    "roofline": lat["roofline"], "e2e": lat["e2e"],
+                                    "config": lat["config"],
+                                    "cpu_baseline": lattice_cpu_baseline()}
         line["extra"] = extra
     print(json.dumps(line))
     if world > 1:

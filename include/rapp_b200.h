@@ -117,6 +117,13 @@ int rapp_mec_plan_run_dev(rapp_mec_plan *plan, const double *d_targets, int64_t 
                           int64_t fn_end, int32_t *d_out_bsq, uint64_t *d_out_key,
                           void *stream);
 
+/* Measurement: when enabled (which also resets the record), every run brackets its meet
+ * pass — the fused lattice kernel K3 — with CUDA events on the run's stream;
+ * rapp_mec_plan_kernel_time synchronises them and returns the summed kernel time and the
+ * number of timed launches. */
+int rapp_mec_plan_timing(rapp_mec_plan *plan, int enable);
+int rapp_mec_plan_kernel_time(rapp_mec_plan *plan, double *total_ms, int64_t *launches);
+
 /* ---- batched scaler tick (hs/sim.py:470-491 driving hs/autoscaler.py:73-234) ---------
  * A device-resident scaler world: functions (in sorted-id order), their tables, the
  * cluster (GPUs in sorted-id order with their partition lists in insertion order, pods),
@@ -207,6 +214,11 @@ int rapp_tick_read_fns(rapp_tick *t, rapp_fn_desc *fns);
 int rapp_tick_read_parts(rapp_tick *t, int64_t *part_off, int32_t *part_sm,
                          int32_t *part_alloc, int32_t *part_npods, int64_t cap);
 int rapp_tick_counter(rapp_tick *t, int64_t *pod_counter);
+
+/* ---- measurement probes (bench.py; not on the product path) --------------------------
+ * Non-FMA FP64 instruction rate of `device` (independent __dadd_rn / __dmul_rn chains on
+ * every SM): the denominator of the lattice search's FP64 roofline. */
+int rapp_probe_fp64(int device, double *dadd_per_s, double *dmul_per_s);
 
 /* ---- kernel-launch accounting (evidence for bench.py's gpu_launches) ----------------- */
 int64_t rapp_launch_count(void);

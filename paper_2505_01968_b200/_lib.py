@@ -63,6 +63,9 @@ SIGNATURES = [
     ("rapp_mec_plan_points", ctypes.c_int, [c_vp, c_i64p]),
     ("rapp_mec_plan_run_dev", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp,
                                              c_vp, c_vp]),
+    ("rapp_mec_plan_timing", ctypes.c_int, [c_vp, ctypes.c_int]),
+    ("rapp_mec_plan_kernel_time", ctypes.c_int, [c_vp, c_dp, c_i64p]),
+    ("rapp_probe_fp64", ctypes.c_int, [ctypes.c_int, c_dp, c_dp]),
     ("rapp_tick_create", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_i64p,
                                         ctypes.c_int64, c_i64p, c_i32p, c_i32p, ctypes.c_int64,
                                         c_vp, ctypes.c_int64, ctypes.POINTER(c_vp)]),

@@ -316,6 +316,10 @@ struct rapp_mec_plan {
   unsigned long long* d_key = nullptr;
   double* d_target2 = nullptr;
   int32_t* d_fb = nullptr;
+  // optional per-launch timing of the meet pass (bench.py's roofline): event pairs
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // 2 per timed launch
+  size_t ev_used = 0;
 };
 
 namespace rapp {
@@ -350,11 +354,25 @@ static int run_plan(rapp_mec_plan* pl, const double* d_targets, int64_t f0, int6
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
   int rc;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (pl->timing) {
+    if (pl->ev_used + 2 > pl->ev.size()) {
+      pl->ev.resize(pl->ev.size() + 64, nullptr);
+      for (size_t i = pl->ev_used; i < pl->ev.size(); ++i) RAPP_CUDA(cudaEventCreate(&pl->ev[i]));
+    }
+    t0 = pl->ev[pl->ev_used++];
+    t1 = pl->ev[pl->ev_used++];
+    RAPP_CUDA(cudaEventRecord(t0, st));
+  }
   if (pl->smem_table) {
     if ((rc = launch_lattice<true, false, false>(pl, d_targets, f0, nf, chunks, st))) return rc;
-    if ((rc = launch_lattice<true, true, true>(pl, d_targets, f0, nf, chunks, st))) return rc;
   } else {
     if ((rc = launch_lattice<false, false, false>(pl, d_targets, f0, nf, chunks, st))) return rc;
+  }
+  if (t1) RAPP_CUDA(cudaEventRecord(t1, st));
+  if (pl->smem_table) {
+    if ((rc = launch_lattice<true, true, true>(pl, d_targets, f0, nf, chunks, st))) return rc;
+  } else {
     if ((rc = launch_lattice<false, true, true>(pl, d_targets, f0, nf, chunks, st))) return rc;
   }
   k_mec_fallback<<<hblocks, 32 * wpb, 0, st>>>(pl->d_fn, pl->d_blist, f0, f1, pl->d_key,
@@ -472,6 +490,7 @@ int rapp_mec_plan_destroy(rapp_mec_plan* pl) {
   cudaFree(pl->d_key);
   cudaFree(pl->d_target2);
   cudaFree(pl->d_fb);
+  for (cudaEvent_t e : pl->ev) cudaEventDestroy(e);
   delete pl;
   return RAPP_OK;
 }
@@ -482,6 +501,33 @@ int rapp_mec_plan_points(rapp_mec_plan* pl, int64_t* points) {
     return RAPP_E_ARG;
   }
   *points = pl->points;
+  return RAPP_OK;
+}
+
+int rapp_mec_plan_timing(rapp_mec_plan* pl, int enable) {
+  if (!pl) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  pl->timing = enable != 0;
+  pl->ev_used = 0;
+  return RAPP_OK;
+}
+
+int rapp_mec_plan_kernel_time(rapp_mec_plan* pl, double* total_ms, int64_t* launches) {
+  if (!pl || !total_ms || !launches) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  double sum = 0.0;
+  for (size_t i = 0; i + 1 < pl->ev_used; i += 2) {
+    RAPP_CUDA(cudaEventSynchronize(pl->ev[i + 1]));
+    float ms = 0.f;
+    RAPP_CUDA(cudaEventElapsedTime(&ms, pl->ev[i], pl->ev[i + 1]));
+    sum += ms;
+  }
+  *total_ms = sum;
+  *launches = (int64_t)(pl->ev_used / 2);
   return RAPP_OK;
 }
 
