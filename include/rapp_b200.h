@@ -88,6 +88,33 @@ int rapp_interp3_many_dev(rapp_ctx *ctx, int32_t table_id, const double *d_coord
 int rapp_interp3_many_host(rapp_ctx *ctx, int32_t table_id, const double *coords,
                            int64_t n, double *out);
 
+/* ---- perf-table ingest (load_table / validate_table_file, hs/perf.py:155-267) ----------
+ * Native row reader for the strict common CSV form: the exact header line, then
+ * `fid,int,int,int,float` rows with one function id, no quoting, padding, blank lines or
+ * non-ASCII bytes.  *regular = 1 and n_rows rows are written (cap >= rows) when the whole
+ * file has that form; otherwise *regular = 0 and the caller reads it with a full CSV reader
+ * (which also produces the reference's format-error messages). */
+int rapp_csv_parse(const char *buf, int64_t len, int64_t cap, int64_t *batch, int64_t *sm,
+                   int64_t *quota, double *latency, int64_t *n_rows, char *function_id,
+                   int64_t function_id_cap, int32_t *regular);
+
+/* Grid assembly and validation on the device.  Rows are (batch, sm, quota, latency) in file
+ * order.  Axes = sorted distinct values per column (hs/perf.py:209-211); a row whose cell
+ * already has an earlier row is a duplicate (perf.py:200-205); every empty cell is
+ * missing (perf.py:216-221); when none is missing every cell is checked for v <= 0 and for
+ * monotonicity along batch / sm / quota (perf.py:239-267).  Cell flag bits: 1 missing,
+ * 2 non_positive, 4 batch decreases, 8 sm increases, 16 quota increases. */
+typedef struct rapp_ingest rapp_ingest;
+int rapp_ingest_create(rapp_ctx *ctx, int64_t n_rows, const int64_t *batch, const int64_t *sm,
+                       const int64_t *quota, const double *latency, rapp_ingest **out);
+int rapp_ingest_shape(rapp_ingest *ing, int64_t *nb, int64_t *ns, int64_t *nq,
+                      int32_t *n_missing, int32_t *n_flagged, int32_t *n_duplicates);
+/* Host copies (any pointer may be NULL): axes (int64), grid (nb*ns*nq doubles, C order,
+ * 0.0 at missing cells), cell flags (nb*ns*nq bytes), per-row duplicate flags (n_rows). */
+int rapp_ingest_read(rapp_ingest *ing, int64_t *b_axis, int64_t *s_axis, int64_t *q_axis,
+                     double *grid, uint8_t *cell_flags, uint8_t *row_duplicate);
+int rapp_ingest_destroy(rapp_ingest *ing);
+
 /* ---- configuration search: most_efficient_config batched over functions --------------
  * hs/perf.py:104-145.  Function f searches table_of_fn[f] over the lattice
  *   B_f x table.sms x range(quota_step, 101, quota_step)

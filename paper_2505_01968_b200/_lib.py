@@ -55,6 +55,15 @@ SIGNATURES = [
                                              c_vp, c_vp]),
     ("rapp_interp3_many_host", ctypes.c_int, [c_vp, ctypes.c_int32, c_dp, ctypes.c_int64,
                                               c_dp]),
+    ("rapp_csv_parse", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, c_i64p,
+                                      c_i64p, c_i64p, c_dp, c_i64p, ctypes.c_char_p,
+                                      ctypes.c_int64, c_i32p]),
+    ("rapp_ingest_create", ctypes.c_int, [c_vp, ctypes.c_int64, c_i64p, c_i64p, c_i64p, c_dp,
+                                          ctypes.POINTER(c_vp)]),
+    ("rapp_ingest_shape", ctypes.c_int, [c_vp, c_i64p, c_i64p, c_i64p, c_i32p, c_i32p,
+                                         c_i32p]),
+    ("rapp_ingest_read", ctypes.c_int, [c_vp, c_i64p, c_i64p, c_i64p, c_dp, c_vp, c_vp]),
+    ("rapp_ingest_destroy", ctypes.c_int, [c_vp]),
     ("rapp_mec_batch", ctypes.c_int, [c_vp, ctypes.c_int64, c_i32p, c_dp, ctypes.c_int32,
                                       c_i64p, c_i64p, c_i64p]),
     ("rapp_mec_plan_create", ctypes.c_int, [c_vp, ctypes.c_int64, c_i32p, ctypes.c_int32,

@@ -378,8 +378,110 @@ def gen_policy(hs):
     dump("policy.json", {"table": table_dict(table), "cases": cases})
 
 
+# -- table ingest ----------------------------------------------------------------
+
+
+def ingest_cases():
+    """CSV texts covering the reference's ingest paths (hs/perf.py:155-267): valid tables
+    (strict form and csv-module form), duplicates, missing cells, non-positive and
+    non-monotone cells, NaN, and every format error class."""
+    H = "function_id,batch,sm_percent,quota_percent,latency_ms"
+    rng = random.Random(4242)
+    cases = {}
+
+    def rows_of(fid, bs, ss, qs, f):
+        return [(fid, b, s, q, f(b, s, q)) for b in bs for s in ss for q in qs]
+
+    def text(rows, header=H, sep="\n"):
+        return sep.join([header] + [",".join(str(x) for x in r) for r in rows]) + sep
+
+    def surf(b, s, q):
+        return (8.0 + 1.5 * b) * (0.35 + 0.65 * (100.0 / s)) * (100.0 / q)
+
+    for name in ("resnet50.csv", "bert-small.csv"):
+        cases["ref_" + name] = open(os.path.join(REF_PKG, "tables", name), encoding="utf-8").read()
+    base = rows_of("fn", [1, 2, 4, 8], [20, 50, 100], [10, 40, 70, 100], surf)
+    cases["valid"] = text(base)
+    shuffled = list(base)
+    rng.shuffle(shuffled)
+    cases["valid_shuffled"] = text(shuffled)
+    cases["valid_crlf"] = text(base, sep="\r\n")
+    cases["valid_padded"] = text([(" fn ", b, f" {s}", q, f" {v!r}") for fn, b, s, q, v in base])
+    cases["valid_quoted"] = H + "\n" + "".join(f'"fn",{b},{s},{q},"{v!r}"\n'
+                                                for _, b, s, q, v in base)
+    cases["valid_blank_lines"] = text(base[:5]) + "\n\n" + text(base[5:], header="")[1:]
+    cases["valid_float_forms"] = text([(fn, b, s, q, f"{v:.6e}" if i % 3 == 0 else
+                                        (f"+{v}" if i % 3 == 1 else repr(v)))
+                                       for i, (fn, b, s, q, v) in enumerate(base)])
+    cases["valid_no_trailing_newline"] = text(base)[:-1]
+    cases["valid_single_cell"] = text([("one", 4, 50, 50, 12.5)])
+    cases["valid_flat"] = text(rows_of("flat", [1, 2], [50, 100], [50, 100],
+                                       lambda b, s, q: 10.0))
+    cases["duplicate"] = text(base + [base[3], base[0], base[3]])
+    cases["duplicate_shuffled"] = text(shuffled[:20] + [shuffled[2]] + shuffled[20:] +
+                                       [shuffled[7]])
+    missing = list(base)
+    del missing[13]
+    del missing[-1]
+    cases["missing"] = text(missing)
+    cases["missing_and_bad"] = text([(fn, b, s, q, -v if i == 3 else v)
+                                     for i, (fn, b, s, q, v) in enumerate(missing)])
+    cases["non_positive"] = text([(fn, b, s, q, 0.0 if i == 5 else (-1.5 if i == 30 else v))
+                                  for i, (fn, b, s, q, v) in enumerate(base)])
+    cases["mono_batch"] = text([(fn, b, s, q, v / 10 if b == 4 else v) for fn, b, s, q, v in base])
+    cases["mono_sm"] = text([(fn, b, s, q, v * 3 if s == 100 and q == 40 else v)
+                             for fn, b, s, q, v in base])
+    cases["mono_quota"] = text([(fn, b, s, q, v * 9 if q == 70 else v) for fn, b, s, q, v in base])
+    cases["nan_and_inf"] = text([(fn, b, s, q, "nan" if i == 7 else ("inf" if i == 9 else v))
+                                 for i, (fn, b, s, q, v) in enumerate(base)])
+    cases["many_issues"] = text([(fn, b, s, q, (-v if i % 7 == 0 else v * (1 + (i % 5))))
+                                 for i, (fn, b, s, q, v) in enumerate(base)])
+    cases["bad_header"] = "nope,nope\n1,2\n"
+    cases["header_only"] = H + "\n"
+    cases["empty_file"] = ""
+    cases["mixed_ids"] = text(base[:10] + [("other",) + tuple(base[10][1:])] + base[11:])
+    cases["bad_int"] = text(base[:4] + [("fn", "x", 20, 10, 1.0)] + base[4:])
+    cases["bad_float"] = text(base[:4] + [("fn", 1, 20, 10, "fast")] + base[4:])
+    cases["short_row"] = H + "\n" + "fn,1,20\n" + text(base, header="")[1:]
+    cases["float_int_field"] = text(base[:2] + [("fn", "1.0", 20, 10, 1.0)] + base[2:])
+    cases["underscore_int"] = text([(fn, b, "1_00" if s == 100 else s, q, v)
+                                    for fn, b, s, q, v in base])
+    cases["negative_axes"] = text(rows_of("neg", [-4, 2], [-50, 100], [10, 20],
+                                          lambda b, s, q: 100.0 - b - s / 10.0 - q))
+    cases["big_batch_values"] = text(rows_of("big", [1, 10 ** 12], [50, 100], [10, 100],
+                                             lambda b, s, q: 5.0 + (b > 1) - s / 100.0 - q / 1000.0))
+    return cases
+
+
+def gen_ingest(hs):
+    import tempfile
+    from hybridscale import load_table, validate_table_file
+    from hybridscale.errors import TableFormatError
+    out = {}
+    tmp = tempfile.mkdtemp()
+    for name, body in ingest_cases().items():
+        path = os.path.join(tmp, "table.csv")
+        with open(path, "w", encoding="utf-8", newline="") as fh:
+            fh.write(body)
+        rep = validate_table_file(path)
+        rec = {"csv": body, "report": {
+            "function_id": rep.function_id, "batches": list(rep.batches), "sms": list(rep.sms),
+            "quotas": list(rep.quotas),
+            "issues": [[i.kind, i.message, list(i.coord) if i.coord else None]
+                       for i in rep.issues]}}
+        try:
+            t = load_table(path)
+            rec["load"] = {"ok": True, "table": table_dict(t)}
+        except TableFormatError as exc:
+            msg = str(exc)
+            assert msg.startswith(path + ": "), msg
+            rec["load"] = {"ok": False, "message": msg[len(path) + 2:]}
+        out[name] = rec
+    dump("ingest.json", out)
+
+
 GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick,
-              "policy": gen_policy}
+              "policy": gen_policy, "ingest": gen_ingest}
 
 
 def main(argv):
