@@ -71,6 +71,15 @@ __device__ int32_t* slot_of(const IngestDev& d, int a, int64_t key) {
   }
 }
 
+__global__ void k_ing_init(IngestDev d, uint32_t cap) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x)
+    for (int a = 0; a < 3; ++a) d.keys[a][i] = kEmptyKey;
+  if (blockIdx.x == 0 && threadIdx.x < 4) {
+    d.ndist[threadIdx.x] = 0;
+    d.counts[threadIdx.x] = 0;
+  }
+}
+
 __global__ void k_ing_insert(IngestDev d) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < d.n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -322,38 +331,54 @@ int rapp_ingest_create(rapp_ctx* ctx, int64_t n, const int64_t* batch, const int
   ing->ctx = ctx;
   ing->n = n;
   RAPP_CUDA(cudaSetDevice(ctx->device));
-  auto alloc = [&](void** p, size_t bytes) -> int {
-    RAPP_CUDA(cudaMalloc(p, bytes ? bytes : 8));
-    ing->allocs.push_back(*p);
-    return RAPP_OK;
-  };
   IngestDev& d = ing->d;
   d.n = n;
   uint32_t cap = 1;
   while (cap < 2 * uint64_t(n)) cap <<= 1;
   d.mask = cap - 1;
-  int rc;
+  // one device allocation for every per-row and per-slot array (cells come later)
+  const size_t per_axis = size_t(n) * 8 * 3 + size_t(cap) * 12;  // col, distinct, axis; keys, rank
+  const size_t bytes = 3 * per_axis + size_t(n) * 8 * 3 + size_t(n) + 1024;  // + rounding
+  char* base = nullptr;
+  RAPP_CUDA(cudaMalloc(&base, bytes));
+  ing->allocs.push_back(base);
+  char* cur = base;
+  auto take = [&](size_t b) {
+    char* r = cur;
+    cur += (b + 15) & ~size_t(15);
+    return r;
+  };
+  for (int a = 0; a < 3; ++a) d.col[a] = reinterpret_cast<const int64_t*>(take(size_t(n) * 8));
+  d.lat = reinterpret_cast<const double*>(take(size_t(n) * 8));
+  {  // columns + latencies staged in the device layout: one H2D copy
+    const size_t stride = ((size_t(n) * 8 + 15) & ~size_t(15)) / 8;  // take() rounding
+    std::vector<int64_t> staged(stride * 4);
+    for (int a = 0; a < 3; ++a) std::memcpy(staged.data() + stride * a, cols[a], size_t(n) * 8);
+    std::memcpy(staged.data() + stride * 3, lat, size_t(n) * 8);
+    RAPP_CUDA(cudaMemcpy((void*)d.col[0], staged.data(), stride * 32, cudaMemcpyHostToDevice));
+  }
   for (int a = 0; a < 3; ++a) {
-    if ((rc = alloc((void**)&d.col[a], n * 8))) return rc;
-    RAPP_CUDA(cudaMemcpy((void*)d.col[a], cols[a], n * 8, cudaMemcpyHostToDevice));
-    if ((rc = alloc((void**)&d.keys[a], size_t(cap) * 8))) return rc;
-    if ((rc = alloc((void**)&d.slot_rank[a], size_t(cap) * 4))) return rc;
-    if ((rc = alloc((void**)&d.distinct[a], n * 8))) return rc;
-    if ((rc = alloc((void**)&d.axis[a], n * 8))) return rc;
+    d.keys[a] = reinterpret_cast<unsigned long long*>(take(size_t(cap) * 8));
+    d.slot_rank[a] = reinterpret_cast<int32_t*>(take(size_t(cap) * 4));
+    d.distinct[a] = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
+    d.axis[a] = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
   }
-  {  // every hash slot starts empty (kEmptyKey)
-    std::vector<unsigned long long> empty(cap, kEmptyKey);
-    for (int a = 0; a < 3; ++a)
-      RAPP_CUDA(cudaMemcpy(d.keys[a], empty.data(), size_t(cap) * 8, cudaMemcpyHostToDevice));
+  d.ndist = reinterpret_cast<int32_t*>(take(16));
+  d.counts = reinterpret_cast<int32_t*>(take(16));
+  d.cell = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
+  d.rdup = reinterpret_cast<uint8_t*>(take(size_t(n)));
+  if (size_t(cur - base) > bytes) {
+    set_error("ingest scratch layout overflow");
+    return RAPP_E_ARG;
   }
-  if ((rc = alloc((void**)&d.lat, n * 8))) return rc;
-  RAPP_CUDA(cudaMemcpy((void*)d.lat, lat, n * 8, cudaMemcpyHostToDevice));
-  if ((rc = alloc((void**)&d.ndist, 4 * 4))) return rc;
-  RAPP_CUDA(cudaMemset(d.ndist, 0, 16));
-  if ((rc = alloc((void**)&d.counts, 4 * 4))) return rc;
-  RAPP_CUDA(cudaMemset(d.counts, 0, 16));
-  if ((rc = alloc((void**)&d.cell, n * 8))) return rc;
-  if ((rc = alloc((void**)&d.rdup, n))) return rc;
+  k_ing_init<<<(unsigned)std::min<int64_t>((cap + 255) / 256, int64_t(ctx->sm_count) * 8), 256>>>(d, cap);
+  RAPP_LAUNCHED();
+  int rc;
+  auto alloc = [&](void** p, size_t b) -> int {
+    RAPP_CUDA(cudaMalloc(p, b ? b : 8));
+    ing->allocs.push_back(*p);
+    return RAPP_OK;
+  };
   const int threads = 256;
   const unsigned rows_blocks =
       (unsigned)std::min<int64_t>((n + threads - 1) / threads, int64_t(ctx->sm_count) * 8);
@@ -373,10 +398,14 @@ int rapp_ingest_create(rapp_ctx* ctx, int64_t n, const int64_t* batch, const int
   const int32_t kmax = std::max(nd[0], std::max(nd[1], nd[2]));
   k_ing_rank<<<dim3((unsigned)std::max(1, (kmax + threads - 1) / threads), 3), threads>>>(d);
   RAPP_LAUNCHED();
-  if ((rc = alloc((void**)&d.first, cells * 8))) return rc;
-  RAPP_CUDA(cudaMemset(d.first, 0xFF, cells * 8));
-  if ((rc = alloc((void**)&d.grid, cells * 8))) return rc;
-  if ((rc = alloc((void**)&d.cflags, cells))) return rc;
+  {  // per-cell arrays in one allocation
+    char* cb = nullptr;
+    if ((rc = alloc((void**)&cb, size_t(cells) * 17 + 32))) return rc;
+    d.first = reinterpret_cast<unsigned long long*>(cb);
+    d.grid = reinterpret_cast<double*>(cb + size_t(cells) * 8);
+    d.cflags = reinterpret_cast<uint8_t*>(cb + size_t(cells) * 16);
+    RAPP_CUDA(cudaMemsetAsync(d.first, 0xFF, size_t(cells) * 8));
+  }
   k_ing_scatter<<<rows_blocks, threads>>>(d);
   RAPP_LAUNCHED();
   k_ing_fill<<<rows_blocks, threads>>>(d);
