@@ -242,6 +242,22 @@ int rapp_tick_read_parts(rapp_tick *t, int64_t *part_off, int32_t *part_sm,
                          int32_t *part_alloc, int32_t *part_npods, int64_t cap);
 int rapp_tick_counter(rapp_tick *t, int64_t *pod_counter);
 
+/* ---- run metrics finalize (SimulationEngine._finalize, hs/sim.py:586-621) ------------
+ * Functions in sorted-id order.  counts[f] = {arrived, rejected, unfinished, completed};
+ * latencies of f = latencies[lat_off[f] .. lat_off[f+1]) (any order); cost intervals of f =
+ * intervals[iv_off[f] .. iv_off[f+1]) rows {start_ms, end_ms (<0: open), sm, quota} in the
+ * reference's list order.  Outputs: violation curve [F][n_mult] over the SLO multipliers
+ * (baseline * m), nearest-rank percentiles [F][n_pct] for pct_q (NaN without latencies),
+ * cost [F] (compute_cost, sim.py:160-175, open intervals priced to end_ms) and cost per
+ * 1k completed requests [F].  n_mult <= 64, n_pct <= 8.  Host buffers. */
+int rapp_metrics_finalize(rapp_ctx *ctx, int64_t n_fns, const double *baseline_ms,
+                          const int64_t *counts, const int64_t *lat_off,
+                          const double *latencies, const int64_t *iv_off,
+                          const double *intervals, double price_per_gpu_hour, double end_ms,
+                          int32_t n_mult, const double *multipliers, int32_t n_pct,
+                          const int32_t *pct_q, double *curve_out, double *pct_out,
+                          double *cost_out, double *cost_per_1k_out);
+
 /* ---- measurement probes (bench.py; not on the product path) --------------------------
  * Non-FMA FP64 instruction rate of `device` (independent __dadd_rn / __dmul_rn chains on
  * every SM): the denominator of the lattice search's FP64 roofline. */

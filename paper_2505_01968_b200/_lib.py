@@ -74,6 +74,10 @@ SIGNATURES = [
                                              c_vp, c_vp]),
     ("rapp_mec_plan_timing", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("rapp_mec_plan_kernel_time", ctypes.c_int, [c_vp, c_dp, c_i64p]),
+    ("rapp_metrics_finalize", ctypes.c_int, [c_vp, ctypes.c_int64, c_dp, c_i64p, c_i64p, c_dp,
+                                             c_i64p, c_dp, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_int32, c_dp, ctypes.c_int32, c_i32p, c_dp,
+                                             c_dp, c_dp, c_dp]),
     ("rapp_probe_fp64", ctypes.c_int, [ctypes.c_int, c_dp, c_dp]),
     ("rapp_tick_create", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_i64p,
                                         ctypes.c_int64, c_i64p, c_i32p, c_i32p, ctypes.c_int64,

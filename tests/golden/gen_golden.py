@@ -480,8 +480,87 @@ def gen_ingest(hs):
     dump("ingest.json", out)
 
 
+# -- run metrics finalize --------------------------------------------------------------
+
+
+def _finalize_record(eng, sim_end, out):
+    def ivd(iv):
+        return [iv.function_id, iv.sm_percent, iv.quota_percent, hx(iv.start_ms), hx(iv.end_ms)]
+    return {
+        "functions": {f: hx(eng.functions[f].baseline_latency_ms) for f in eng.functions},
+        "counts": {f: [c.arrived, c.completed, c.rejected] for f, c in eng._counts.items()},
+        "latencies": {f: [hx(x) for x in v] for f, v in eng._latencies.items()},
+        "intervals": [ivd(iv) for iv in eng._intervals],
+        "price": hx(eng.cfg.price_per_gpu_hour), "sim_end": hx(sim_end),
+        "out": {"violation_curve": {f: [hx(x) for x in v] for f, v in out.violation_curve.items()},
+                "percentiles": {f: {k: hx(x) for k, x in v.items()}
+                                for f, v in out.percentiles.items()},
+                "cost": {f: hx(x) for f, x in out.cost.items()},
+                "cost_per_1k": {f: hx(x) for f, x in out.cost_per_1k.items()}}}
+
+
+def gen_metrics(hs):
+    """_finalize inputs/outputs captured from real reference simulations (the demo config,
+    three policies) plus synthetic engine states covering the edge cases."""
+    import tempfile
+    import types
+    from hybridscale import cli
+    from hybridscale.sim import FunctionCounts, PodCostInterval, SimConfig, SimulationEngine
+    records = []
+    orig = SimulationEngine._finalize
+
+    def capture(self, sim_end):
+        out = orig(self, sim_end)
+        records.append(_finalize_record(self, sim_end, out))
+        return out
+    SimulationEngine._finalize = capture
+    try:
+        demo = os.path.join(REF_PKG, "configs", "demo.yaml")
+        assert cli.main(["run", "--config", demo, "--out", tempfile.mkdtemp()]) == 0
+    finally:
+        SimulationEngine._finalize = orig
+    rng = random.Random(777)
+    for case in range(6):
+        nf = [3, 1, 5, 2, 4, 8][case]
+        fids = [f"fn-{rng.randrange(1000):03d}" for _ in range(nf)]
+        fids = list(dict.fromkeys(fids))
+        eng = types.SimpleNamespace()
+        eng.functions = {f: types.SimpleNamespace(baseline_latency_ms=rng.choice(
+            [20.0, 35.5, 12.25, 100.0, 7.0])) for f in fids}
+        eng._counts, eng._latencies, eng._intervals = {}, {}, []
+        for f in fids:
+            n = rng.choice([0, 1, 2, 3, 17, 100, 2500])
+            base = eng.functions[f].baseline_latency_ms
+            lat = [rng.choice([base * rng.choice([0.5, 1.0, 1.25, 2.0, 9.75, 10.0]),
+                               rng.uniform(0, 12 * base), float(rng.randrange(1, 400))])
+                   for _ in range(n)]
+            rejected = rng.randrange(0, 5)
+            unfinished = rng.randrange(0, 3)
+            arrived = n + rejected + unfinished if rng.random() > 0.1 or n else 0
+            eng._counts[f] = FunctionCounts(arrived=arrived, completed=n,
+                                            rejected=rejected if arrived else 0)
+            eng._latencies[f] = lat
+            for k in range(rng.randrange(0, 6)):
+                st = rng.uniform(0, 50000)
+                end = -1.0 if rng.random() < 0.3 else st + rng.choice([0.0, rng.uniform(0, 9e4)])
+                if rng.random() < 0.1:
+                    end = st - 5.0  # negative duration clamps to 0
+                eng._intervals.append(PodCostInterval(f, f"pod-{k}", "gpu-000",
+                                                      rng.randrange(1, 101),
+                                                      rng.randrange(1, 101), st, end))
+        eng._intervals.append(PodCostInterval("not-managed", "pod-x", "gpu-001", 50, 50, 0.0, 10.0))
+        rng.shuffle(eng._intervals)
+        eng.cfg = SimConfig(price_per_gpu_hour=rng.choice([2.48, 0.0, 3.1]))
+        eng._timeline = []
+        sim_end = rng.uniform(60000, 200000)
+        out = SimulationEngine._finalize(eng, sim_end)
+        records.append(_finalize_record(eng, sim_end, out))
+    dump("metrics.json", records)
+
+
 GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick,
-              "policy": gen_policy, "ingest": gen_ingest}
+              "policy": gen_policy, "ingest": gen_ingest,
+              "metrics": gen_metrics}
 
 
 def main(argv):
