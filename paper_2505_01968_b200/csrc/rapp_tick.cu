@@ -130,6 +130,7 @@ struct World {
   int32_t* row_kd;               // [F][kMaxPods] index of q0 inside the row
   double* rows;                  // [F][kMaxPods][kRow] throughput at q0 + k*delta
   int32_t* bref;                 // batch of sorted[0]
+  int32_t* bref_ok;              // bref inside the table's batch range (hs/perf.py:88-91)
   // speculative vertical walk against tick-start headroom (phase A), per sorted pod:
   int32_t* spec_avail;           // [F][kMaxPods] avail the walk assumed (-1: not walked)
   int32_t* spec_k;               // [F][kMaxPods] steps taken
@@ -395,6 +396,7 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
       cls = kUp;
       w.gap0[f] = __dsub_rn(R, up_thr);
       w.bref[f] = w.p_b[srt[0]];
+      w.bref_ok[f] = batch_ok(w, f, w.p_b[srt[0]]) ? 1 : 0;
     } else {
       const double mr = w.fn_min_rps[f];
       const double r_min = mr != mr ? w.r_min : mr;
@@ -537,17 +539,64 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
 // phase A2: throughput(batch_ref, sm, q) for sm, q in 1..100 of every scale-up function
 // ---------------------------------------------------------------------------------------
 // Only the quota multiples of delta are tabulated (the covering-quota scan reads those);
-// c_max at an off-step q_max is evaluated on demand by the commit warp.
-__global__ void k_tick_grid(World w) {
+// c_max at an off-step q_max is evaluated on demand by the commit warp.  The batch bracket
+// is fixed per function and the sm / quota brackets are shared by a whole row / column, so
+// they are located once into shared memory (same locate, same doubles) and every entry is
+// then 8 independent corner loads and the reference's 7 lerps + 2 divisions.
+__global__ void __launch_bounds__(256) k_tick_grid(World w) {
   const int f = blockIdx.x;
   if (w.policy != 0 || w.cls[f] != kUp) return;
   const int b = w.bref[f];
   if (!batch_ok(w, f, b)) return;  // phase B raises if the value is ever needed
+  __shared__ int2 s_j[100], s_k[100];
+  __shared__ double s_ts[100], s_tq[100];
+  __shared__ int s_i0, s_i1;
+  __shared__ double s_tb;
+  const TableDesc td = w.tds[w.fn_table[f]];
+  const double* seg = w.pool + td.off;
+  const double* ba = seg + td.ob;
+  const double* sa = seg + td.os;
+  const double* qa = seg + td.oq;
+  const double* v = seg + td.ov;
   const int d = w.delta, nq = 100 / d;
+  for (int i = threadIdx.x; i < 100; i += blockDim.x) {
+    int lo, hi;
+    double t;
+    locate(sa, td.ns, double(i + 1), lo, hi, t);
+    s_j[i] = make_int2(lo, hi);
+    s_ts[i] = t;
+    if (i < nq) {
+      locate(qa, td.nq, double((i + 1) * d), lo, hi, t);
+      s_k[i] = make_int2(lo, hi);
+      s_tq[i] = t;
+    }
+  }
+  if (threadIdx.x == 0) {
+    int lo, hi;
+    double t;
+    locate(ba, td.nb, double(b), lo, hi, t);
+    s_i0 = lo;
+    s_i1 = hi;
+    s_tb = t;
+  }
+  __syncthreads();
+  const int64_t plane = int64_t(td.ns) * td.nq;
+  const double* v0 = v + s_i0 * plane;
+  const double* v1 = v + s_i1 * plane;
+  const double tb = s_tb, bb = double(b);
   for (int i = threadIdx.x; i < 100 * nq; i += blockDim.x) {
-    const int sm = i / nq + 1, q = (i % nq + 1) * d;
-    w.tgrid[(int64_t(f) * 100 + (sm - 1)) * 100 + (q - 1)] =
-        thr_at(w, f, double(b), double(sm), double(q));
+    const int si = i / nq, qi = i - si * nq;
+    const int2 j = s_j[si], k = s_k[qi];
+    const double ts = s_ts[si], tq = s_tq[qi];
+    const int o00 = j.x * td.nq + k.x, o01 = j.x * td.nq + k.y;
+    const int o10 = j.y * td.nq + k.x, o11 = j.y * td.nq + k.y;
+    // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch
+    const double c00 = lerp_rn(v0[o00], v0[o01], tq);
+    const double c01 = lerp_rn(v0[o10], v0[o11], tq);
+    const double c10 = lerp_rn(v1[o00], v1[o01], tq);
+    const double c11 = lerp_rn(v1[o10], v1[o11], tq);
+    const double lat = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
+    w.tgrid[(int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1] = throughput(bb, lat);
   }
 }
 
@@ -562,10 +611,19 @@ struct Commit {
   uint64_t* sp;
   uint8_t* ovf;
   int ps;
-  int* nact;  // shared-memory action counter
+  int* nact;             // shared-memory action counter
+  int* serr;             // shared: an error was raised (checked between functions)
+  int* snpods;           // shared copy of *w.n_pods for the whole commit
+  long long* scounter;   // shared copy of *w.counter
 
   __device__ uint64_t* parts(int g) const {
     return ovf[g] ? w.g_parts + int64_t(g) * kPartCap : sp + int64_t(g) * ps;
+  }
+
+  // lane-0 code: record the first error (global, for the host) and stop the commit
+  __device__ void fail0(int code, int f) const {
+    set_err(w, code, f);
+    *serr = 1;
   }
 
   // before appending entry n to GPU g: move a full shared-memory list to global memory
@@ -594,15 +652,13 @@ struct Commit {
     __syncwarp();
   }
 
-  // change_quota (allocator.py:111-125) + occupancy bookkeeping
-  __device__ void change_quota(int p, int new_q) const {
-    const int g = w.p_gpu[p];
-    const int pos = find_part(g, w.p_puid[p]);
+  // change_quota (allocator.py:111-125) + occupancy bookkeeping, partition position known
+  __device__ void change_quota_at(int p, int g, int pos, int s, int old_q, int new_q) const {
     const uint64_t e = parts(g)[pos];
-    const int delta = new_q - w.p_q[p];
+    const int delta = new_q - old_q;
     set_entry(g, pos, part_pack(part_sm(e), part_alloc(e) + delta, part_npods(e), part_uid(e)));
     if (lane == 0) {
-      w.g_hgo[g] += w.p_s[p] * delta;
+      w.g_hgo[g] += s * delta;
       w.p_q[p] = new_q;
     }
     __syncwarp();
@@ -610,10 +666,9 @@ struct Commit {
 
   // place_pod (allocator.py:85-108): join the first same-sm partition with headroom, else
   // append a new partition
-  __device__ void place(int p, int g) const {
+  __device__ void place(int p, int g, int s, int q) const {
     uint64_t* P = parts(g);
     const int n = w.g_nparts[g];
-    const int s = w.p_s[p], q = w.p_q[p];
     int pos = 1 << 30;
     for (int i = lane; i < n; i += 32)
       if (part_sm(P[i]) == s && 100 - part_alloc(P[i]) >= q) pos = min(pos, i);
@@ -622,7 +677,7 @@ struct Commit {
     if (lane == 0) {
       if (pos == (1 << 30)) {
         if (n >= kPartCap || w.g_freesm[g] < s) {
-          set_err(w, RAPP_E_PLACEMENT, -1);
+          fail0(RAPP_E_PLACEMENT, -1);
         } else {
           make_room(g, n);
           P = parts(g);
@@ -645,9 +700,8 @@ struct Commit {
   }
 
   // release_pod (allocator.py:128-139): an emptied partition leaves the list (list.remove)
-  __device__ void release(int p) const {
-    const int g = w.p_gpu[p];
-    const int pos = find_part(g, w.p_puid[p]);
+  __device__ void release(int p, int f, int g, uint32_t uid, int s, int q) const {
+    const int pos = find_part(g, uid);
     __syncwarp();
     if (lane == 0) {
       uint64_t* P = parts(g);
@@ -659,21 +713,23 @@ struct Commit {
         w.g_nparts[g] = n - 1;
         w.g_freesm[g] += part_sm(e);
       } else {
-        P[pos] = part_pack(part_sm(e), part_alloc(e) - w.p_q[p], np, part_uid(e));
+        P[pos] = part_pack(part_sm(e), part_alloc(e) - q, np, part_uid(e));
       }
       w.g_npods[g] -= 1;
-      w.g_hgo[g] -= w.p_s[p] * w.p_q[p];
+      w.g_hgo[g] -= s * q;
       w.p_state[p] = kDead;
-      // drop from its function's pod list
-      const int f = w.p_fn[p];
-      if (f >= 0) {
-        int* L = w.fn_pods + f * kMaxPods;
-        const int n2 = w.fn_npods[f];
-        for (int i = 0; i < n2; ++i)
-          if (L[i] == p) {
-            L[i] = L[n2 - 1];
-            break;
-          }
+    }
+    // drop from its function's pod list (swap with the last entry)
+    if (f >= 0) {
+      int* L = w.fn_pods + f * kMaxPods;
+      const int n2 = w.fn_npods[f];
+      int at = 1 << 30;
+      for (int i = lane; i < n2; i += 32)
+        if (L[i] == p) at = min(at, i);
+      for (int o = 16; o > 0; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
+      __syncwarp();
+      if (lane == 0) {
+        if (at < n2) L[at] = L[n2 - 1];
         w.fn_npods[f] = n2 - 1;
       }
     }
@@ -688,35 +744,47 @@ struct Commit {
     __syncwarp();
   }
 
-  // new COLD_STARTING pod pod-%06d (sim.py:337-340, 505-516)
-  __device__ int new_pod(int f, int b, int s, int q, double now) const {
+  // new COLD_STARTING pod pod-%06d (sim.py:337-340, 505-516).  The 32 id bytes are built by
+  // the 32 lanes (byte k by lane k) and packed big-endian with warp OR-reductions.
+  // npods: the function's pod count (kept by the caller across its new pods).
+  __device__ int new_pod(int f, int b, int s, int q, double now, int& npods) const {
+    const long long c = *scounter;
+    int nd = 1;
+    long long top = 1;  // 10^(nd-1)
+    while (top <= c / 10) {
+      top *= 10;
+      ++nd;
+    }
+    const int width = nd > 6 ? nd : 6;
+    const int k = lane;
+    uint32_t ch = 0;
+    if (k < 4) {
+      ch = k == 0 ? 'p' : k == 1 ? 'o' : k == 2 ? 'd' : '-';
+    } else if (k - 4 < width) {
+      const int j = k - 4;           // digit j from the left of the zero-padded number
+      const int from_right = width - 1 - j;
+      long long pw = 1;
+      for (int i = 0; i < from_right; ++i) pw *= 10;
+      ch = uint32_t('0' + (from_right >= 19 ? 0 : (c / pw) % 10));
+    }
+    const uint32_t shift = 8u * uint32_t(3 - (k & 3));
+    const uint32_t part = ch << shift;  // byte k inside its 32-bit quarter-word
+    uint32_t word32[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      word32[i] = __reduce_or_sync(0xffffffffu, (k >> 2) == i ? part : 0u);
     int p = 0;
     if (lane == 0) {
-      p = (*w.n_pods)++;
-      if (p >= w.pod_cap || w.fn_npods[f] >= kMaxPods) {
-        set_err(w, RAPP_E_ARG, f);
+      p = (*snpods)++;
+      if (p >= w.pod_cap || npods >= kMaxPods) {
+        fail0(RAPP_E_ARG, f);
         p = -1;
       } else {
-        const int64_t c = (*w.counter)++;
-        char buf[32] = {0};
-        const char* pre = "pod-";
-        int len = 0;
-        for (; pre[len]; ++len) buf[len] = pre[len];
-        char dig[24];
-        int nd = 0;
-        int64_t v = c;
-        do {
-          dig[nd++] = char('0' + v % 10);
-          v /= 10;
-        } while (v > 0);
-        for (int k = nd; k < 6; ++k) buf[len++] = '0';
-        while (nd > 0) buf[len++] = dig[--nd];
+        *scounter = c + 1;
         PodId id;
-        for (int i = 0; i < 4; ++i) {
-          uint64_t x = 0;
-          for (int k = 0; k < 8; ++k) x = (x << 8) | uint8_t(buf[i * 8 + k]);
-          id.w[i] = x;
-        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          id.w[i] = (uint64_t(word32[2 * i]) << 32) | uint64_t(word32[2 * i + 1]);
         w.p_id[p] = id;
         w.p_fn[p] = f;
         w.p_b[p] = b;
@@ -724,10 +792,12 @@ struct Commit {
         w.p_q[p] = q;
         w.p_state[p] = kCold;
         w.p_ready[p] = __dadd_rn(now, w.cold_start);
-        w.fn_pods[f * kMaxPods + w.fn_npods[f]++] = p;
+        w.fn_pods[f * kMaxPods + npods] = p;
+        w.fn_npods[f] = npods + 1;
       }
     }
     p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= 0) ++npods;
     return p;
   }
 
@@ -798,37 +868,44 @@ struct Commit {
   }
 
   // most_efficient_config(target) via the key-sorted prefix-max index: the first lattice
-  // point (in (s*q, s, q, b) order) with prefix max >= min(target, max rps)
+  // point (in (s*q, s, q, b) order) with prefix max >= min(target, max rps).  Each round
+  // probes 1024 evenly spaced entries of the candidate range (32 independent loads per
+  // lane, one memory round trip) and keeps the one bucket that holds the answer, so a
+  // 291,200-point full-grid lattice takes two rounds.
   __device__ void mec(int f, double target, int& b, int& s, int& q) const {
     const double* pm = w.pmax + w.fn_lat_off[f];
     const int64_t L = w.fn_lat_len[f];
     const double top = pm[L - 1];
     const double t = target <= top ? target : top;  // target > top -> max-rps fallback
-    // 32-ary search for the first index with pm[i] >= t (pm non-decreasing, pm[L-1] >= t):
-    // invariant: the answer lies in [lo, hi]; probes past hi count as ">= t"
+    // invariant: the answer lies in [lo, hi] (pm non-decreasing, pm[hi] >= t)
     int64_t lo = 0, hi = L - 1;
-    while (hi - lo > 31) {
-      const int64_t step = (hi - lo + 31) / 32;
-      const int64_t probe = lo + step * lane;
-      const bool ge = probe > hi || pm[probe] >= t;
-      const unsigned mask = __ballot_sync(0xffffffffu, ge);
-      if (mask == 0) {
-        lo = lo + step * 31 + 1;
-      } else {
-        const int first = __ffs(mask) - 1;
-        if (first == 0) {
-          hi = lo;
-        } else {
-          const int64_t ph = lo + step * first;
-          lo = lo + step * (first - 1) + 1;
-          hi = ph < hi ? ph : hi;
-        }
+    while (true) {
+      const int64_t len = hi - lo + 1;
+      const int64_t step = (len + 1023) / 1024;  // probes lo + step*j, j < 1024
+      bool ge[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int64_t pos = lo + step * (int64_t(lane) * 32 + u);
+        ge[u] = pos > hi || pm[pos] >= t;
       }
+      int first = 32;  // first probe of this lane that is >= t
+#pragma unroll
+      for (int u = 31; u >= 0; --u)
+        if (ge[u]) first = u;
+      const unsigned mask = __ballot_sync(0xffffffffu, first < 32);
+      const int l0 = __ffs(mask) - 1;  // lane of the first >= probe (pm[hi] >= t: exists)
+      const int u0 = __shfl_sync(0xffffffffu, first, l0);
+      const int64_t jfirst = int64_t(l0) * 32 + u0;
+      if (jfirst == 0) break;  // pm[lo] >= t: the answer is lo
+      if (step == 1) {
+        lo = lo + jfirst;
+        break;
+      }
+      const int64_t ph = lo + step * jfirst;
+      hi = ph < hi ? ph : hi;
+      if (jfirst > 0) lo = lo + step * (jfirst - 1) + 1;
     }
-    const int64_t probe = lo + lane;
-    const bool ge = probe > hi || pm[probe] >= t;
-    const unsigned mask = __ballot_sync(0xffffffffu, ge);
-    const int64_t idx = lo + (__ffs(mask) - 1);
+    const int64_t idx = lo;
     const int nb = w.fn_nb[f];
     const int pair = w.pairs[w.fn_pairs_off[f] + int(idx / nb)];
     const TableDesc td = w.tds[w.fn_table[f]];
@@ -837,34 +914,49 @@ struct Commit {
     q = pair & 0xFFFF;
   }
 
-  // Function header + first sorted pod, prefetched for 32 functions at once by the commit
-  // loop (nothing here can change before the function's own turn in the tick).
+  // Function header + its first pod (scale-up: sorted[0]; scale-down: the first staged
+  // action's pod), prefetched for 32 functions at once by the commit loop: nothing here can
+  // change before the function's own turn in the tick.
   struct Pre {
     double gap0, sg0;
-    int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref;
+    int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods;
+    int nd, dkind, dquota, didle;
     uint32_t uid0;
   };
 
   __device__ Pre prefetch(int f) const {
     Pre r{};
     r.p0 = -1;
-    if (f < w.F && w.cls[f] == kUp && w.policy == 0) {
+    if (f >= w.F) return r;
+    const int cls = w.cls[f];
+    if (cls == kUp && w.policy == 0) {
       r.gap0 = w.gap0[f];
       r.m = w.nsorted[f];
       r.bref = w.bref[f];
+      r.brefok = w.bref_ok[f];
+      r.npods = w.fn_npods[f];
       r.sav0 = w.spec_avail[f * kMaxPods];
       r.sk0 = w.spec_k[f * kMaxPods];
       r.sg0 = w.spec_gain[f * kMaxPods];
       r.p0 = r.m > 0 ? w.sorted[f * kMaxPods] : -1;
-      if (r.p0 >= 0) {
-        const int p = r.p0;
-        r.st0 = w.p_state[p];
-        r.gpu0 = w.p_gpu[p];
-        r.uid0 = w.p_puid[p];
-        r.q0 = w.p_q[p];
-        r.b0 = w.p_b[p];
-        r.s0 = w.p_s[p];
+    } else if (cls == kDown) {
+      r.nd = w.ndown[f];
+      if (r.nd > 0) {
+        const DownAct a = w.down[f * kMaxPods];
+        r.dkind = a.kind;
+        r.dquota = a.quota;
+        r.p0 = a.pod;
       }
+    }
+    if (r.p0 >= 0) {
+      const int p = r.p0;
+      r.st0 = w.p_state[p];
+      r.gpu0 = w.p_gpu[p];
+      r.uid0 = w.p_puid[p];
+      r.q0 = w.p_q[p];
+      r.b0 = w.p_b[p];
+      r.s0 = w.p_s[p];
+      if (cls == kDown) r.didle = w.p_idle[p];
     }
     return r;
   }
@@ -883,6 +975,12 @@ struct Commit {
     r.sav0 = __shfl_sync(0xffffffffu, x.sav0, src);
     r.sk0 = __shfl_sync(0xffffffffu, x.sk0, src);
     r.bref = __shfl_sync(0xffffffffu, x.bref, src);
+    r.brefok = __shfl_sync(0xffffffffu, x.brefok, src);
+    r.npods = __shfl_sync(0xffffffffu, x.npods, src);
+    r.nd = __shfl_sync(0xffffffffu, x.nd, src);
+    r.dkind = __shfl_sync(0xffffffffu, x.dkind, src);
+    r.dquota = __shfl_sync(0xffffffffu, x.dquota, src);
+    r.didle = __shfl_sync(0xffffffffu, x.didle, src);
     r.uid0 = __shfl_sync(0xffffffffu, x.uid0, src);
     return r;
   }
@@ -891,6 +989,7 @@ struct Commit {
     const int d = w.delta;
     double gap = pre.gap0;
     const int m = pre.m;
+    int npods = pre.npods;
     const int* srt = w.sorted + f * kMaxPods;
     const double* rows = w.rows + int64_t(f) * kMaxPods * kRow;
     // vertical first, largest sm first (autoscaler.py:115-133)
@@ -931,8 +1030,9 @@ struct Commit {
       }
       if (kstar > 0) {
         const int nq = q0 + kstar * d;
-        change_quota(p, nq);
-        emit(f, kVUp, j == 0 ? pre.b0 : w.p_b[p], j == 0 ? pre.s0 : w.p_s[p], nq, p, g, 0);
+        const int s = j == 0 ? pre.s0 : w.p_s[p];
+        change_quota_at(p, g, pos, s, q0, nq);
+        emit(f, kVUp, j == 0 ? pre.b0 : w.p_b[p], s, nq, p, g, 0);
         gap = __dsub_rn(gap, gain);
       }
     }
@@ -944,14 +1044,27 @@ struct Commit {
         int sm, qmax;
         best_slot(g, sm, qmax);
         if (sm > 0 && qmax > 0) {
-          if (!batch_ok(w, f, bref)) {
-            if (lane == 0) set_err(w, RAPP_E_VALUE, f);
+          if (!pre.brefok) {
+            if (lane == 0) fail0(RAPP_E_VALUE, f);
+            __syncwarp();
             return;
           }
           const double* T = w.tgrid + (int64_t(f) * 100 + (sm - 1)) * 100;
+          // every throughput the branch may read, in one round of independent loads:
+          // lanes hold the quota steps (u*32 + lane + 1)*d <= qmax, u < 4 (d >= 1)
+          double tv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int qq = (u * 32 + lane + 1) * d;
+            tv[u] = qq <= qmax ? T[qq - 1] : 0.0;
+          }
           double cmax;
           if (qmax % d == 0) {
-            cmax = T[qmax - 1];
+            const int kq = qmax / d - 1;  // the step index of qmax
+            cmax = __shfl_sync(0xffffffffu, tv[0], kq & 31);
+            if (kq >= 32) cmax = __shfl_sync(0xffffffffu, tv[1], kq & 31);
+            if (kq >= 64) cmax = __shfl_sync(0xffffffffu, tv[2], kq & 31);
+            if (kq >= 96) cmax = __shfl_sync(0xffffffffu, tv[3], kq & 31);
           } else {  // max_quota_capability at an off-step quota (autoscaler.py:144)
             cmax = lane == 0 ? thr_at(w, f, double(bref), double(sm), double(qmax)) : 0.0;
             cmax = __shfl_sync(0xffffffffu, cmax, 0);
@@ -960,20 +1073,23 @@ struct Commit {
             // _covering_quota (autoscaler.py:168-175): first multiple of d <= qmax with
             // throughput >= gap, else qmax
             int quota = qmax;
-            for (int base = 0; base * d < qmax; base += 32) {
-              const int qq = (base + lane + 1) * d;
-              const bool hit = qq <= qmax && T[qq - 1] >= gap;
-              const unsigned mask = __ballot_sync(0xffffffffu, hit);
+            double tq = cmax;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int qq = (u * 32 + lane + 1) * d;
+              const unsigned mask = __ballot_sync(0xffffffffu, qq <= qmax && tv[u] >= gap);
               if (mask) {
-                quota = (base + __ffs(mask)) * d;
+                const int l = __ffs(mask) - 1;
+                quota = (u * 32 + l + 1) * d;
+                tq = __shfl_sync(0xffffffffu, tv[u], l);
                 break;
               }
             }
-            const int p = new_pod(f, bref, sm, quota, now);
+            const int p = new_pod(f, bref, sm, quota, now, npods);
             if (p < 0) return;
-            place(p, g);
+            place(p, g, sm, quota);
             emit(f, kHUp, bref, sm, quota, p, g, 0);
-            gap = __dsub_rn(gap, quota % d == 0 ? T[quota - 1] : cmax);  // quota == qmax
+            gap = __dsub_rn(gap, tq);  // == T[quota] on a step, cmax at the off-step qmax
           }
         }
       }
@@ -984,9 +1100,9 @@ struct Commit {
       if (g >= 0) {
         int b, s, q;
         mec(f, gap, b, s, q);
-        const int p = new_pod(f, b, s, q, now);
+        const int p = new_pod(f, b, s, q, now, npods);
         if (p < 0) return;
-        place(p, g);
+        place(p, g, s, q);
         emit(f, kHUp, b, s, q, p, g, 0);
       }
     }
@@ -1031,32 +1147,52 @@ struct Commit {
   __device__ void replica_up(int f, double now) const {
     const int* shape = w.fn_shape + 3 * f;
     const int want = w.wanted[f];
+    int npods = w.fn_npods[f];
     for (int i = 0; i < want; ++i) {
       const int g = pick_gpu(shape[1], shape[2]);
       if (g < 0) break;  // cluster saturated for this shape
-      const int p = new_pod(f, shape[0], shape[1], shape[2], now);
+      const int p = new_pod(f, shape[0], shape[1], shape[2], now, npods);
       if (p < 0) return;
-      place(p, g);
+      place(p, g, shape[1], shape[2]);
       emit(f, kHUp, shape[0], shape[1], shape[2], p, g, 0);
     }
   }
 
-  __device__ void scale_down(int f, double now) const {
-    const int na = w.ndown[f];
+  __device__ void scale_down(int f, double now, const Pre& pre) const {
+    const int na = pre.nd;
     const DownAct* acts = w.down + f * kMaxPods;
     for (int i = 0; i < na; ++i) {
-      const DownAct a = acts[i];
-      const int p = a.pod;
-      const int g = w.p_gpu[p];
-      if (a.kind == kVDown) {
-        change_quota(p, a.quota);
-        emit(f, kVDown, w.p_b[p], w.p_s[p], a.quota, p, g, 0);
+      int kind, p, quota, g, b, s, q, idle;
+      uint32_t uid;
+      if (i == 0) {
+        kind = pre.dkind;
+        p = pre.p0;
+        quota = pre.dquota;
+        g = pre.gpu0;
+        uid = pre.uid0;
+        b = pre.b0;
+        s = pre.s0;
+        q = pre.q0;
+        idle = pre.didle;
       } else {
-        const int b = w.p_b[p], s = w.p_s[p];
-        const bool idle = w.p_idle[p] != 0;
+        const DownAct a = acts[i];
+        kind = a.kind;
+        p = a.pod;
+        quota = a.quota;
+        g = w.p_gpu[p];
+        uid = w.p_puid[p];
+        b = w.p_b[p];
+        s = w.p_s[p];
+        q = w.p_q[p];
+        idle = w.p_idle[p];
+      }
+      if (kind == kVDown) {
+        change_quota_at(p, g, find_part(g, uid), s, q, quota);
+        emit(f, kVDown, b, s, quota, p, g, 0);
+      } else {
         if (lane == 0) w.p_state[p] = kDraining;
         __syncwarp();
-        if (idle) release(p);
+        if (idle) release(p, f, g, uid, s, q);
         emit(f, kHDown, b, s, 0, p, g, idle ? 1 : 0);
       }
     }
@@ -1102,8 +1238,16 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
     __syncwarp();
   }
   __syncwarp();
-  Commit c{v, lane, sp, ovf, ps, &s_nact};
-  bool stop = false;
+  __shared__ int s_err, s_npods;
+  __shared__ long long s_counter;
+  if (lane == 0) {
+    s_err = *(volatile int32_t*)w.err != 0;  // phase A errors stop the commit at once
+    s_npods = *w.n_pods;
+    s_counter = (long long)*w.counter;
+  }
+  __syncwarp();
+  Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter};
+  bool stop = s_err != 0;
   for (int base = 0; base < w.F && !stop; base += 32) {
     const int mine = base + lane < w.F ? w.cls[base + lane] : kNone;
     const Commit::Pre pre = c.prefetch(base + lane);
@@ -1118,13 +1262,18 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
         else
           c.replica_up(base + i, now);
       } else {
-        c.scale_down(base + i, now);
+        c.scale_down(base + i, now, Commit::bcast(pre, i));
       }
-      if (*(volatile int32_t*)w.err) {
+      __syncwarp();
+      if (s_err) {
         stop = true;
         break;
       }
     }
+  }
+  if (lane == 0) {
+    *w.n_pods = s_npods;
+    *w.counter = s_counter;
   }
   __syncwarp();
   if (lane == 0) *w.n_actions = s_nact;
@@ -1510,6 +1659,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.row_kd, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.rows, FP * kMaxPods * kRow))) return rc;
   if ((rc = dev_alloc(t.get(), &w.bref, FP))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.bref_ok, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_avail, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_k, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_gain, FP * kMaxPods))) return rc;

@@ -18,10 +18,11 @@ from paper_2505_01968_b200.autoscaler import ScalerConfig  # noqa: E402
 from paper_2505_01968_b200.tick import TickEngine  # noqa: E402
 
 
-def main(nticks=30, nfn=1000, ngpu=400):
-    fns, tables, cluster, caps = bench.make_config4_world(nfn, ngpu, seed=0, device=0)
+def main(nticks=30, nfn=1000, ngpu=400, full_grid=False):
+    fns, tables, cluster, caps = bench.make_config4_world(nfn, ngpu, seed=0, device=0,
+                                                          full_grid=full_grid)
     cluster2 = copy.deepcopy(cluster)
-    cfg = ScalerConfig(delta_iq=10)
+    cfg = ScalerConfig(delta_iq=1 if full_grid else 10)
     kw = dict(scaler_interval_ms=2000.0, cold_start_ms=5000.0, pod_counter=len(cluster.pods),
               device=0)
     eng = TickEngine(fns, tables, cluster, cfg, **kw)
@@ -50,4 +51,4 @@ def main(nticks=30, nfn=1000, ngpu=400):
 
 
 if __name__ == "__main__":
-    main()
+    main(nticks=int(os.environ.get("TICKS", "30")), full_grid="--full-grid" in sys.argv)
