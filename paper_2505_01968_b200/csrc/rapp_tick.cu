@@ -639,11 +639,10 @@ struct Commit {
   __device__ int find_part(int g, uint32_t uid) const {
     const uint64_t* P = parts(g);
     const int n = w.g_nparts[g];
-    int pos = 1 << 30;
+    unsigned pos = 1u << 30;
     for (int i = lane; i < n; i += 32)
-      if (part_uid(P[i]) == uid) pos = min(pos, i);
-    for (int o = 16; o > 0; o >>= 1) pos = min(pos, __shfl_xor_sync(0xffffffffu, pos, o));
-    return pos;
+      if (part_uid(P[i]) == uid) pos = min(pos, unsigned(i));
+    return int(__reduce_min_sync(0xffffffffu, pos));
   }
 
   __device__ void set_entry(int g, int pos, uint64_t e) const {
@@ -669,11 +668,10 @@ struct Commit {
   __device__ void place(int p, int g, int s, int q) const {
     uint64_t* P = parts(g);
     const int n = w.g_nparts[g];
-    int pos = 1 << 30;
+    unsigned upos = 1u << 30;
     for (int i = lane; i < n; i += 32)
-      if (part_sm(P[i]) == s && 100 - part_alloc(P[i]) >= q) pos = min(pos, i);
-    for (int o = 16; o > 0; o >>= 1) pos = min(pos, __shfl_xor_sync(0xffffffffu, pos, o));
-    __syncwarp();
+      if (part_sm(P[i]) == s && 100 - part_alloc(P[i]) >= q) upos = min(upos, unsigned(i));
+    const int pos = int(__reduce_min_sync(0xffffffffu, upos));
     if (lane == 0) {
       if (pos == (1 << 30)) {
         if (n >= kPartCap || w.g_freesm[g] < s) {
@@ -723,11 +721,10 @@ struct Commit {
     if (f >= 0) {
       int* L = w.fn_pods + f * kMaxPods;
       const int n2 = w.fn_npods[f];
-      int at = 1 << 30;
+      unsigned uat = 1u << 30;
       for (int i = lane; i < n2; i += 32)
-        if (L[i] == p) at = min(at, i);
-      for (int o = 16; o > 0; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
-      __syncwarp();
+        if (L[i] == p) uat = min(uat, unsigned(i));
+      const int at = int(__reduce_min_sync(0xffffffffu, uat));
       if (lane == 0) {
         if (at < n2) L[at] = L[n2 - 1];
         w.fn_npods[f] = n2 - 1;
@@ -804,6 +801,15 @@ struct Commit {
   // lowest (occupancy, rank) among used GPUs (autoscaler.py:139-141); occupancy compares
   // as the integer sum(sm*quota): /10000.0 is monotone and injective on 0..10000
   __device__ int argmin_used() const {
+    // occupancy <= 100*100 per GPU, so (occupancy, rank) packs into 32 bits for up to 2^18
+    // GPUs: one scan and one warp min-reduction
+    if (w.G <= (1 << 18)) {
+      unsigned best = ~0u;
+      for (int g = lane; g < w.G; g += 32)
+        if (w.g_npods[g] > 0) best = min(best, (unsigned(w.g_hgo[g]) << 18) | unsigned(g));
+      best = __reduce_min_sync(0xffffffffu, best);
+      return best == ~0u ? -1 : int(best & ((1u << 18) - 1));
+    }
     long long best = LLONG_MAX;
     for (int g = lane; g < w.G; g += 32)
       if (w.g_npods[g] > 0) {
@@ -818,11 +824,14 @@ struct Commit {
   }
 
   __device__ int first_free() const {
-    int best = 1 << 30;
+    unsigned best = 1u << 30;
     for (int g = lane; g < w.G; g += 32)
-      if (w.g_npods[g] == 0) best = min(best, g);
-    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-    return best == (1 << 30) ? -1 : best;
+      if (w.g_npods[g] == 0) {
+        best = unsigned(g);
+        break;  // g ascends within a lane
+      }
+    best = __reduce_min_sync(0xffffffffu, best);
+    return best == (1u << 30) ? -1 : int(best);
   }
 
   // max_avail_quota_and_sm (allocator.py:26-52): max of (sm*hr, sm, join=1) over
@@ -831,19 +840,18 @@ struct Commit {
     const uint64_t* P = parts(g);
     const int n = w.g_nparts[g];
     // key: prod (15 bits) | sm (8) | (255 - pos) (8): max key = max (prod, sm), first pos
-    long long best = -1;
+    // (prod <= 10^4 -> the key fits 31 bits: one redux instead of a shuffle tree)
+    unsigned ukey = 0;
     for (int i = lane; i < n; i += 32) {
       const int hr = 100 - part_alloc(P[i]);
       if (hr > 0) {
-        const long long k = ((long long)(part_sm(P[i]) * hr) << 16) |
-                            ((long long)part_sm(P[i]) << 8) | (255 - i);
-        best = k > best ? k : best;
+        const unsigned k = (unsigned(part_sm(P[i]) * hr) << 16) |
+                           (unsigned(part_sm(P[i])) << 8) | unsigned(255 - i);
+        ukey = k > ukey ? k : ukey;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const long long x = __shfl_xor_sync(0xffffffffu, best, o);
-      best = x > best ? x : best;
-    }
+    ukey = __reduce_max_sync(0xffffffffu, ukey);
+    const long long best = ukey == 0 ? -1 : (long long)ukey;
     sm = 0;
     q = 0;
     long long bprod = -1, bsm = -1, bjoin = -1;
@@ -920,7 +928,7 @@ struct Commit {
   struct Pre {
     double gap0, sg0;
     int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods;
-    int nd, dkind, dquota, didle;
+    int nd, dkind, dquota, didle, stamp;
     uint32_t uid0;
   };
 
@@ -941,6 +949,7 @@ struct Commit {
       r.p0 = r.m > 0 ? w.sorted[f * kMaxPods] : -1;
     } else if (cls == kDown) {
       r.nd = w.ndown[f];
+      r.stamp = w.stamp[f];
       if (r.nd > 0) {
         const DownAct a = w.down[f * kMaxPods];
         r.dkind = a.kind;
@@ -981,6 +990,7 @@ struct Commit {
     r.dkind = __shfl_sync(0xffffffffu, x.dkind, src);
     r.dquota = __shfl_sync(0xffffffffu, x.dquota, src);
     r.didle = __shfl_sync(0xffffffffu, x.didle, src);
+    r.stamp = __shfl_sync(0xffffffffu, x.stamp, src);
     r.uid0 = __shfl_sync(0xffffffffu, x.uid0, src);
     return r;
   }
@@ -1012,21 +1022,34 @@ struct Commit {
         spec_ok = false;  // later pods start from a different gap: walk them here
         const int kd = w.row_kd[f * kMaxPods + j];
         const double* row = rows + j * kRow + kd;  // row[k] = thr at q0 + k*d
+        // k* = first k >= 0 with q0+(k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0.
+        // k <= (100 - q0) / d < 128: every row value the walk may read is loaded in one
+        // round (lane l holds k = l, l+32, l+64, l+96), then 4 ballots find k*.
         const double cur = row[0];
-        // k* = first k >= 0 with q0+(k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0
-        for (int base = 0; kstar < 0; base += 32) {
-          const int k = base + lane;
+        double rk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = u * 32 + lane;
+          rk[u] = k > 0 && q0 + k * d <= avail ? row[k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = u * 32 + lane;
           bool stop;
           if (q0 + (k + 1) * d > avail) {
             stop = true;
           } else {
-            const double gk = k == 0 ? 0.0 : __dsub_rn(row[k], cur);
+            const double gk = k == 0 ? 0.0 : __dsub_rn(rk[u], cur);
             stop = !(__dsub_rn(gap, gk) > 0.0);
           }
           const unsigned mask = __ballot_sync(0xffffffffu, stop);
-          if (mask) kstar = base + __ffs(mask) - 1;
+          if (mask && kstar < 0) {
+            const int l = __ffs(mask) - 1;
+            kstar = u * 32 + l;
+            const double rs = __shfl_sync(0xffffffffu, rk[u], l);
+            if (kstar > 0) gain = __dsub_rn(rs, cur);
+          }
         }
-        if (kstar > 0) gain = __dsub_rn(row[kstar], cur);
       }
       if (kstar > 0) {
         const int nq = q0 + kstar * d;
@@ -1196,7 +1219,7 @@ struct Commit {
         emit(f, kHDown, b, s, 0, p, g, idle ? 1 : 0);
       }
     }
-    if (lane == 0 && w.stamp[f]) w.last_down[f] = now;
+    if (lane == 0 && pre.stamp) w.last_down[f] = now;
     __syncwarp();
   }
 };

@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
-TICKS=12 timeout 600 python tools/tick_profile.py > gpurun_out/tick_profile.log 2>&1
-TICKS=12 timeout 600 python tools/tick_profile.py --full-grid > gpurun_out/tick_profile_full.log 2>&1
-cat gpurun_out/tick_profile.log gpurun_out/tick_profile_full.log
+for r in 1 2; do
+for v in build_variants/prev.so paper_2505_01968_b200/librapp_b200.so; do
+echo "== $v"; RAPP_LIB=$v TICKS=8 timeout 600 python tools/tick_profile.py --full-grid 2>&1 | awk '{print $6}' | tr '\n' ' '; echo
+done; done
