@@ -242,6 +242,26 @@ int rapp_tick_read_parts(rapp_tick *t, int64_t *part_off, int32_t *part_sm,
                          int32_t *part_alloc, int32_t *part_npods, int64_t cap);
 int rapp_tick_counter(rapp_tick *t, int64_t *pod_counter);
 
+/* ---- learned RaPP predictor (§8(f) row 4, PerfModel protocol hs/perf.py:23-31) -------
+ * No reference counterpart exists (the paper's GNN/MLP predictor is out of the reference's
+ * scope), so this path has no parity target: it is checked against a PyTorch
+ * fp32 forward of the same BF16-rounded weights.  Model: x = [graph features (40) |
+ * 16 config features of (batch, sm%, quota%) | 0 pad] (64) -> relu(W1 x + b1) (128) ->
+ * relu(W2 . + b2) (128) -> exp(w3 . + b3) = latency ms.  Weights are fp32 row-major
+ * (W1 [128][64], W2 [128][128]) and are held as BF16; graph_features is [n_models][40]. */
+typedef struct rapp_mlp rapp_mlp;
+int rapp_mlp_create(rapp_ctx *ctx, int32_t n_models, const float *graph_features,
+                    const float *w1, const float *b1, const float *w2, const float *b2,
+                    const float *w3, float b3, rapp_mlp **out);
+int rapp_mlp_destroy(rapp_mlp *mlp);
+/* d_coords (n,3) float64 rows of one model -> d_out (n) float64 latency; tcgen05 GEMMs. */
+int rapp_mlp_predict_dev(rapp_mlp *mlp, int32_t model, const double *d_coords, int64_t n,
+                         double *d_out, void *stream);
+/* Diagnostics: same, and the first tile's raw FP32 accumulators (before bias) of both
+ * layers into d_acc[2][128][128]. */
+int rapp_mlp_debug_dev(rapp_mlp *mlp, int32_t model, const double *d_coords, int64_t n,
+                       double *d_out, float *d_acc, void *stream);
+
 /* ---- run metrics finalize (SimulationEngine._finalize, hs/sim.py:586-621) ------------
  * Functions in sorted-id order.  counts[f] = {arrived, rejected, unfinished, completed};
  * latencies of f = latencies[lat_off[f] .. lat_off[f+1]) (any order); cost intervals of f =

@@ -78,6 +78,13 @@ SIGNATURES = [
                                              c_i64p, c_dp, ctypes.c_double, ctypes.c_double,
                                              ctypes.c_int32, c_dp, ctypes.c_int32, c_i32p, c_dp,
                                              c_dp, c_dp, c_dp]),
+    ("rapp_mlp_create", ctypes.c_int, [c_vp, ctypes.c_int32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                       ctypes.c_float, ctypes.POINTER(c_vp)]),
+    ("rapp_mlp_destroy", ctypes.c_int, [c_vp]),
+    ("rapp_mlp_predict_dev", ctypes.c_int, [c_vp, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp,
+                                            c_vp]),
+    ("rapp_mlp_debug_dev", ctypes.c_int, [c_vp, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp,
+                                          c_vp, c_vp]),
     ("rapp_probe_fp64", ctypes.c_int, [ctypes.c_int, c_dp, c_dp]),
     ("rapp_tick_create", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_i64p,
                                         ctypes.c_int64, c_i64p, c_i32p, c_i32p, ctypes.c_int64,

@@ -1,0 +1,418 @@
+// Learned RaPP predictor (§8(f) row 4; parity unpinned — the reference ships no learned
+// model): a fused feature-assembly + 3-layer MLP forward on the 5th-generation
+// tensor cores.
+//
+//   x   = [graph features of the model (kGraph) | config features of (b, s%, q%) | 0 pad]  (64)
+//   h1  = relu(x  · W1ᵀ + b1)      (128)   tcgen05.mma kind::f16, BF16 in, FP32 acc in TMEM
+//   h2  = relu(h1 · W2ᵀ + b2)      (128)   same (h1 rounded to BF16 as the A operand)
+//   lat = exp(min(h2 · w3 + b3, 80))       CUDA cores, FP32, in the layer-2 epilogue
+//
+// One CTA of 4 warps processes 128-row tiles (persistent, 2 CTAs per SM so one CTA's
+// epilogue overlaps the other's MMAs).  Per tile: every thread assembles its row's
+// features straight into the SWIZZLE_128B K-major smem image of the A operand; thread 0
+// issues 4 (layer 1) / 8 (layer 2) tcgen05.mma of M=128, N=128, K=16 into two TMEM
+// accumulators (256 columns) and commits each layer to an mbarrier; the epilogue reads the
+// accumulator row of each thread (tcgen05.ld 32x32b: warp w owns TMEM lanes 32w..32w+31),
+// applies bias + ReLU, and writes the BF16 activations back as the next layer's swizzled
+// A operand.  The weights are uploaded once as pre-swizzled BF16 images and bulk-copied
+// into shared memory per CTA.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "rapp_internal.h"
+
+namespace rapp {
+
+constexpr int kMlpK0 = 64;      // input features (padded)
+constexpr int kMlpH = 128;      // hidden width
+constexpr int kMlpGraph = 40;   // graph-feature slots
+constexpr int kMlpCfg = 16;     // config features
+constexpr int kMlpTile = 128;   // rows per tile (UMMA M)
+constexpr int kMlpThreads = 128;
+// shared memory image (offsets from a 1024-byte aligned base)
+constexpr uint32_t kOffW1 = 0;                  // [128 n][64 k]  bf16, SW128   16 KB
+constexpr uint32_t kOffW2 = 16384;              // 2 panels [128 n][64 k]       32 KB
+constexpr uint32_t kOffX = 49152;               // [128 m][64 k]                16 KB
+constexpr uint32_t kOffH = 65536;               // 2 panels [128 m][64 k]       32 KB
+constexpr uint32_t kOffVec = 98304;             // b1, b2, w3 (fp32), graph features
+constexpr uint32_t kVecFloats = 3 * kMlpH + kMlpGraph + 8;
+constexpr uint32_t kMlpSmem = kOffVec + kVecFloats * 4 + 1024;  // + alignment slack
+constexpr uint32_t kWeightBytes = 16384 + 32768;
+
+// byte offset of element (r, k) inside a K-major SWIZZLE_128B panel of 64 bf16 columns:
+// 8-row x 128-byte atoms stacked along r; 16-byte chunk c of row r stored at c ^ (r % 8)
+__host__ __device__ inline uint32_t sw128_offset(uint32_t r, uint32_t k) {
+  return (r >> 3) * 1024u + (r & 7u) * 128u + ((((k * 2u) >> 4) ^ (r & 7u)) << 4) +
+         ((k * 2u) & 15u);
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B (8-row group stride),
+// LBO field 1 (unused for swizzled K-major), version 1 (sm100), base offset 0
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M = 128, N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kMlpH >> 3) << 17) |
+                            (uint32_t(kMlpTile >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void mlp_bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mlp_bar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(sbar), "r"(parity)
+        : "memory");
+  }
+}
+
+// 32 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // a -> low half (lower address)
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// The 16 per-configuration features of (batch, sm%, quota%), all O(1): scaled coordinates,
+// their reciprocals (the latency surface is ~ 1/s and 1/q), logs and products.  Coordinates
+// are clamped to the profiled box (batch 1..512, sm/quota 1..100%) the way the grid model
+// clamps sm and quota to its axes.
+__device__ __forceinline__ void config_features(double bd, double sd, double qd, float* f) {
+  const float b = fminf(fmaxf(float(bd), 1.0f), 512.0f);
+  const float s = fminf(fmaxf(float(sd), 1.0f), 100.0f);
+  const float q = fminf(fmaxf(float(qd), 1.0f), 100.0f);
+  f[0] = b * (1.0f / 32.0f);
+  f[1] = s * 0.01f;
+  f[2] = q * 0.01f;
+  f[3] = 1.0f / b;
+  f[4] = 1.0f / s;
+  f[5] = 1.0f / q;
+  f[6] = __log2f(b) * 0.2f;
+  f[7] = __log2f(s) * 0.15f;
+  f[8] = __log2f(q) * 0.15f;
+  f[9] = s * q * 1e-4f;
+  f[10] = 1.0f / (s * q);
+  f[11] = b / s * (1.0f / 32.0f);
+  f[12] = b / q * (1.0f / 32.0f);
+  f[13] = b / (s * q);
+  f[14] = sqrtf(b) * 0.2f;
+  f[15] = 1.0f;
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(sdst), "l"(src), "r"(bytes), "r"(sbar) : "memory");
+}
+
+struct MlpParams {
+  const uint8_t* wimg;   // pre-swizzled bf16 W1 | W2 images (kWeightBytes)
+  const float* vecs;     // b1[128] b2[128] w3[128]
+  float b3;
+  const float* graph;    // [n_models][kMlpGraph]
+  float* dbg;            // diagnostics: tile 0's raw accumulators (acc1 | acc2), or null
+};
+
+// coords: (n, 3) float64 rows (batch, sm%, quota%) of one model; out: latency (ms) float64
+__global__ void __launch_bounds__(kMlpThreads, 2)
+    k_mlp_stream(MlpParams P, int model, const double* __restrict__ coords, int64_t n,
+                 double* __restrict__ out) {
+  extern __shared__ uint8_t mlp_smem_raw[];
+  __shared__ uint64_t bar_w, bar1, bar2;
+  __shared__ uint32_t s_tmem;
+  const uint32_t raw = (uint32_t)__cvta_generic_to_shared(mlp_smem_raw);
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  uint8_t* base = mlp_smem_raw + (sbase - raw);
+  float* vec = reinterpret_cast<float*>(base + kOffVec);
+  const int t = threadIdx.x, warp = t >> 5;
+
+  if (t == 0) {
+    mlp_bar_init(&bar_w, 1);
+    mlp_bar_init(&bar1, 1);
+    mlp_bar_init(&bar2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: two 128-column fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(&s_tmem)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = t; i < 3 * kMlpH; i += blockDim.x) vec[i] = P.vecs[i];
+  for (int i = t; i < kMlpGraph; i += blockDim.x)
+    vec[3 * kMlpH + i] = P.graph[int64_t(model) * kMlpGraph + i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  if (t == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&bar_w)), "r"(kWeightBytes) : "memory");
+    bulk_g2s(sbase + kOffW1, P.wimg, kWeightBytes, &bar_w);
+  }
+  mlp_bar_wait(&bar_w, 0);
+
+  const float* b1 = vec;
+  const float* b2 = vec + kMlpH;
+  const float* w3 = vec + 2 * kMlpH;
+  const float* gf = vec + 3 * kMlpH;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;  // this warp's TMEM lane quadrant
+  const int64_t tiles = (n + kMlpTile - 1) / kMlpTile;
+  uint32_t it = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int64_t row = tile * kMlpTile + t;
+    // ---- feature assembly: row t of the A operand (64 bf16 = 8 swizzled chunks) ----
+    {
+      float f[kMlpK0];
+#pragma unroll
+      for (int i = 0; i < kMlpGraph; ++i) f[i] = gf[i];
+      double cb = 1.0, cs = 100.0, cq = 100.0;
+      if (row < n) {
+        cb = coords[3 * row];
+        cs = coords[3 * row + 1];
+        cq = coords[3 * row + 2];
+      }
+      config_features(cb, cs, cq, f + kMlpGraph);
+#pragma unroll
+      for (int i = kMlpGraph + kMlpCfg; i < kMlpK0; ++i) f[i] = 0.0f;
+      uint8_t* X = base + kOffX;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 v;
+        v.x = pack_bf16(f[8 * c + 0], f[8 * c + 1]);
+        v.y = pack_bf16(f[8 * c + 2], f[8 * c + 3]);
+        v.z = pack_bf16(f[8 * c + 4], f[8 * c + 5]);
+        v.w = pack_bf16(f[8 * c + 6], f[8 * c + 7]);
+        *reinterpret_cast<uint4*>(X + sw128_offset(t, 8 * c)) = v;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    // ---- layer 1: acc1 = X · W1ᵀ  (K = 64: 4 MMAs of K = 16) ----
+    if (t == 0) {
+#pragma unroll
+      for (int k = 0; k < kMlpK0 / 16; ++k)
+        umma_bf16(tmem, umma_desc(sbase + kOffX + 32 * k), umma_desc(sbase + kOffW1 + 32 * k),
+                  k > 0);
+      umma_commit(&bar1);
+    }
+    mlp_bar_wait(&bar1, it & 1);
+    tc_fence_after();
+    // ---- epilogue 1: h1 = relu(acc1 + b1) -> bf16 A operand of layer 2 ----
+    {
+      uint8_t* Hs = base + kOffH;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float v[32];
+        tmem_ld32(tmem + lane_base + 32 * cc, v);
+        if (P.dbg != nullptr && tile == 0)
+          for (int e = 0; e < 32; ++e) P.dbg[t * kMlpH + 32 * cc + e] = v[e];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
+          const int col = 32 * cc + 8 * g;
+          float h[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) h[e] = fmaxf(v[8 * g + e] + b1[col + e], 0.0f);
+          uint4 u;
+          u.x = pack_bf16(h[0], h[1]);
+          u.y = pack_bf16(h[2], h[3]);
+          u.z = pack_bf16(h[4], h[5]);
+          u.w = pack_bf16(h[6], h[7]);
+          const int panel = col >> 6;
+          *reinterpret_cast<uint4*>(Hs + panel * 16384 + sw128_offset(t, col & 63)) = u;
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    // ---- layer 2: acc2 = H · W2ᵀ  (K = 128: 2 panels x 4 MMAs) ----
+    if (t == 0) {
+#pragma unroll
+      for (int k = 0; k < kMlpH / 16; ++k) {
+        const uint32_t pa = sbase + kOffH + (k >> 2) * 16384 + 32 * (k & 3);
+        const uint32_t pb = sbase + kOffW2 + (k >> 2) * 16384 + 32 * (k & 3);
+        umma_bf16(tmem + kMlpH, umma_desc(pa), umma_desc(pb), k > 0);
+      }
+      umma_commit(&bar2);
+    }
+    mlp_bar_wait(&bar2, it & 1);
+    tc_fence_after();
+    // ---- epilogue 2: lat = exp(relu(acc2 + b2) · w3 + b3) ----
+    {
+      float acc = 0.0f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float v[32];
+        tmem_ld32(tmem + lane_base + kMlpH + 32 * cc, v);
+        if (P.dbg != nullptr && tile == 0)
+          for (int e = 0; e < 32; ++e) P.dbg[kMlpTile * kMlpH + t * kMlpH + 32 * cc + e] = v[e];
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          acc = fmaf(fmaxf(v[e] + b2[32 * cc + e], 0.0f), w3[32 * cc + e], acc);
+      }
+      if (row < n) out[row] = double(__expf(fminf(acc + P.b3, 80.0f)));
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+}  // namespace rapp
+
+using namespace rapp;
+
+struct rapp_mlp {
+  rapp_ctx* ctx = nullptr;
+  int n_models = 0;
+  uint8_t* d_wimg = nullptr;
+  float* d_vecs = nullptr;
+  float* d_graph = nullptr;
+  float b3 = 0.0f;
+};
+
+static uint16_t host_bf16(float x) {  // round to nearest even (finite inputs)
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  const uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7FFFu + lsb;
+  return uint16_t(u >> 16);
+}
+
+extern "C" {
+
+int rapp_mlp_create(rapp_ctx* ctx, int32_t n_models, const float* graph_features,
+                    const float* w1, const float* b1, const float* w2, const float* b2,
+                    const float* w3, float b3, rapp_mlp** out) {
+  if (!ctx || !out || n_models < 1 || !graph_features || !w1 || !b1 || !w2 || !b2 || !w3) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  std::unique_ptr<rapp_mlp> m(new rapp_mlp());
+  m->ctx = ctx;
+  m->n_models = n_models;
+  m->b3 = b3;
+  // pre-swizzled BF16 images: W1 [128 n][64 k], W2 [128 n][128 k] as two 64-column panels
+  std::vector<uint8_t> img(kWeightBytes, 0);
+  for (int nrow = 0; nrow < kMlpH; ++nrow)
+    for (int k = 0; k < kMlpK0; ++k) {
+      const uint16_t h = host_bf16(w1[nrow * kMlpK0 + k]);
+      std::memcpy(img.data() + sw128_offset(nrow, k), &h, 2);
+    }
+  for (int nrow = 0; nrow < kMlpH; ++nrow)
+    for (int k = 0; k < kMlpH; ++k) {
+      const uint16_t h = host_bf16(w2[nrow * kMlpH + k]);
+      std::memcpy(img.data() + 16384 + (k >> 6) * 16384 + sw128_offset(nrow, k & 63), &h, 2);
+    }
+  std::vector<float> vecs(3 * kMlpH);
+  std::memcpy(vecs.data(), b1, kMlpH * 4);
+  std::memcpy(vecs.data() + kMlpH, b2, kMlpH * 4);
+  std::memcpy(vecs.data() + 2 * kMlpH, w3, kMlpH * 4);
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  RAPP_CUDA(cudaMalloc(&m->d_wimg, kWeightBytes));
+  RAPP_CUDA(cudaMalloc(&m->d_vecs, vecs.size() * 4));
+  RAPP_CUDA(cudaMalloc(&m->d_graph, size_t(n_models) * kMlpGraph * 4));
+  RAPP_CUDA(cudaMemcpy(m->d_wimg, img.data(), kWeightBytes, cudaMemcpyHostToDevice));
+  RAPP_CUDA(cudaMemcpy(m->d_vecs, vecs.data(), vecs.size() * 4, cudaMemcpyHostToDevice));
+  RAPP_CUDA(cudaMemcpy(m->d_graph, graph_features, size_t(n_models) * kMlpGraph * 4,
+                       cudaMemcpyHostToDevice));
+  *out = m.release();
+  return RAPP_OK;
+}
+
+int rapp_mlp_destroy(rapp_mlp* m) {
+  if (!m) return RAPP_OK;
+  cudaSetDevice(m->ctx->device);
+  cudaDeviceSynchronize();
+  cudaFree(m->d_wimg);
+  cudaFree(m->d_vecs);
+  cudaFree(m->d_graph);
+  delete m;
+  return RAPP_OK;
+}
+
+static int mlp_launch(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
+                      double* d_out, float* d_dbg, void* stream) {
+  if (!m || model < 0 || model >= m->n_models || n < 0 || (n > 0 && (!d_coords || !d_out))) {
+    set_error("bad mlp handle, model id or buffers");
+    return RAPP_E_ARG;
+  }
+  if (n == 0) return RAPP_OK;
+  RAPP_CUDA(cudaSetDevice(m->ctx->device));
+  RAPP_CUDA(cudaFuncSetAttribute(k_mlp_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kMlpSmem));
+  const int64_t tiles = (n + kMlpTile - 1) / kMlpTile;
+  const int64_t blocks = std::min<int64_t>(tiles, int64_t(m->ctx->sm_count) * 2);
+  MlpParams P{m->d_wimg, m->d_vecs, m->b3, m->d_graph, d_dbg};
+  k_mlp_stream<<<(unsigned)blocks, kMlpThreads, kMlpSmem, (cudaStream_t)stream>>>(
+      P, model, d_coords, n, d_out);
+  RAPP_LAUNCHED();
+  return RAPP_OK;
+}
+
+int rapp_mlp_predict_dev(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
+                         double* d_out, void* stream) {
+  return mlp_launch(m, model, d_coords, n, d_out, nullptr, stream);
+}
+
+int rapp_mlp_debug_dev(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
+                       double* d_out, float* d_acc, void* stream) {
+  return mlp_launch(m, model, d_coords, n, d_out, d_acc, stream);
+}
+
+}  // extern "C"
