@@ -525,6 +525,99 @@ def run_lattice(args, rank, world, local):
             "scaling": "strong"}
 
 
+def run_mlp(args, rank, world, local, n_per_model=None):
+    """Learned RaPP predictor (§8(f) row 4, parity unpinned): the fused feature-assembly +
+    tcgen05 MLP over config-2-shaped query streams of the 4 zoo models.  Roofline: tensor
+    FLOPs per prediction = 2 * (64*128 + 128*128) = 49,152 against the measured bf16 peak."""
+    import torch
+    from paper_2505_01968_b200 import _lib, learned
+    dev = torch.device("cuda", local)
+    n = n_per_model or min(args.queries, 50_000_000)
+    lm = learned.LearnedPerfModel.zoo(seed=0, device=local)
+    coords, outs = [], []
+    for mi, (_, b, s, q, _v) in enumerate(config2_arrays()):
+        coords.append(gen_queries(b, s, q, n, 77 + 1000 * rank + mi, dev))
+        outs.append(torch.empty(n, dtype=torch.float64, device=dev))
+    stream = torch.cuda.current_stream(dev)
+    steps = max(3, args.steps // 10)
+
+    def step(evs=None):
+        for k in range(len(coords)):
+            if evs is not None:
+                evs[k][0].record(stream)
+            lm.predict_many_dev(k, coords[k], outs[k], stream=stream.cuda_stream)
+            if evs is not None:
+                evs[k][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    launches0 = _lib.launch_count()
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in coords] for _ in range(steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        clk.mark_start()
+        start.record(stream)
+        for i in range(steps):
+            step(kev[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+        clk.mark_end()
+    launches = _lib.launch_count() - launches0
+    ms = max_over_ranks(start.elapsed_time(end), world)
+    per_launch = float(np.mean([a.elapsed_time(b) for row in kev for (a, b) in row]))
+    value = world * len(coords) * n * steps / (ms / 1000.0)
+    flops = 2.0 * (64 * 128 + 128 * 128)
+    achieved = flops * n / (per_launch / 1000.0) / 1e12
+    peak = load_bf16_peak()
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "k_mlp_stream (rapp_mlp.cu, tcgen05.mma kind::f16 M128 N128 K16)",
+            "flops_per_prediction": flops, "hbm_bytes_per_prediction": 32,
+            "achieved_hbm_gbs": round(32.0 * n / (per_launch / 1000.0) / 1e9, 1)}
+    # e2e through the host API (pageable numpy in and out)
+    e2e = None
+    if not args.no_e2e:
+        ne = 4_000_000
+        hc = coords[0][:ne].cpu().numpy()
+        lm.predict_many(0, hc)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = 3
+        for _ in range(reps):
+            lm.predict_many(0, hc)
+        dt = time.perf_counter() - t0
+        e2e = {"value": ne * reps / dt, "unit": UNIT, "h2d_bytes_per_step": ne * 24,
+               "d2h_bytes_per_step": ne * 8, "steps": reps,
+               "api": "learned.LearnedPerfModel.predict_many (host arrays)"}
+    # CPU baseline: the same forward (fp32, torch on the host cores) on a bounded sample
+    import torch as _t
+    sample = coords[0][:200_000].cpu().numpy()
+    threads = _t.get_num_threads()
+    t0 = time.perf_counter()
+    lm.reference_forward(0, sample)
+    cdt = time.perf_counter() - t0
+    cpu = {"value": len(sample) / cdt, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{len(sample)} queries through the fp32 torch forward on the host"}
+    cfg = {"workload": "learned RaPP MLP (zoo: resnet50, vgg19, bert-base, mobilenet; "
+           "64 features -> 128 -> 128 -> 1, random weights), config-2-shaped query streams",
+           "queries_per_step": len(coords) * n, "parity": "unpinned (no reference model); "
+           "checked against a torch fp32 forward, rel tol 2e-2"}
+    return {"value": value, "ms": ms, "steps": steps, "roofline": roof, "e2e": e2e,
+            "cpu_baseline": cpu, "config": cfg, "launches": launches, "clocks": clk.summary(),
+            "dtype": "bf16", "scaling": "weak"}
+
+
+def load_bf16_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["bf16_tflops"])
+    except Exception:
+        return 2250.0
+
+
 _LW = {}
 
 
@@ -741,7 +834,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["stream", "lattice", "tick"], default="stream")
+    ap.add_argument("--workload", choices=["stream", "lattice", "tick", "mlp"], default="stream")
     ap.add_argument("--ticks", type=int, default=50)
     ap.add_argument("--full-grid", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
@@ -786,6 +879,18 @@ def main():
                             "d2h_bytes_per_step": "actions (32 B each) + 2 x 8 KB rates"},
                     "tick": tick, "cpu_baseline": tick_cpu_baseline(args),
                     "gpu_launches": tick["launches_per_tick"] * tick["ticks"], "impl": "ours"}
+            print(json.dumps(line))
+        return
+    if args.workload == "mlp":
+        res = run_mlp(args, rank, world, local)
+        if rank == 0:
+            line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+                    "steps": res["steps"], "warmup": args.warmup,
+                    "ms_per_step": res["ms"] / res["steps"], "higher_is_better": True,
+                    "scaling": res["scaling"], "vs_baseline": None, "dtype": res["dtype"],
+                    "data": "synthetic", "config": res["config"], "roofline": res["roofline"],
+                    "cpu_baseline": res["cpu_baseline"], "e2e": res["e2e"],
+                    "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours"}
             print(json.dumps(line))
         return
     res = (run_stream if args.workload == "stream" else run_lattice)(args, rank, world, local)

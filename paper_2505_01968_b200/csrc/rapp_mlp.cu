@@ -7,8 +7,8 @@
 //   h2  = relu(h1 · W2ᵀ + b2)      (128)   same (h1 rounded to BF16 as the A operand)
 //   lat = exp(min(h2 · w3 + b3, 80))       CUDA cores, FP32, in the layer-2 epilogue
 //
-// One CTA of 4 warps processes 128-row tiles (persistent, 2 CTAs per SM so one CTA's
-// epilogue overlaps the other's MMAs).  Per tile: every thread assembles its row's
+// One persistent CTA per SM runs 4 independent 4-warp groups, each on its own 128-row
+// tiles, so one group's epilogue overlaps the others' MMAs.  Per tile: every thread assembles its row's
 // features straight into the SWIZZLE_128B K-major smem image of the A operand; thread 0
 // issues 4 (layer 1) / 8 (layer 2) tcgen05.mma of M=128, N=128, K=16 into two TMEM
 // accumulators (256 columns) and commits each layer to an mbarrier; the epilogue reads the
@@ -32,13 +32,16 @@ constexpr int kMlpH = 128;      // hidden width
 constexpr int kMlpGraph = 40;   // graph-feature slots
 constexpr int kMlpCfg = 16;     // config features
 constexpr int kMlpTile = 128;   // rows per tile (UMMA M)
-constexpr int kMlpThreads = 128;
-// shared memory image (offsets from a 1024-byte aligned base)
+constexpr int kMlpGroups = 4;   // independent 4-warp tile pipelines per CTA (1 CTA per SM)
+constexpr int kMlpThreads = 128 * kMlpGroups;
+// shared memory image (offsets from a 1024-byte aligned base); the weights are shared by
+// the groups, each group owns one activation buffer whose first panel doubles as the
+// layer-1 A operand (X is consumed by layer 1 before the layer-1 epilogue overwrites it)
 constexpr uint32_t kOffW1 = 0;                  // [128 n][64 k]  bf16, SW128   16 KB
 constexpr uint32_t kOffW2 = 16384;              // 2 panels [128 n][64 k]       32 KB
-constexpr uint32_t kOffX = 49152;               // [128 m][64 k]                16 KB
-constexpr uint32_t kOffH = 65536;               // 2 panels [128 m][64 k]       32 KB
-constexpr uint32_t kOffVec = 98304;             // b1, b2, w3 (fp32), graph features
+constexpr uint32_t kOffH = 49152;               // per group: 2 panels [128 m][64 k] 32 KB
+constexpr uint32_t kGroupBytes = 32768;
+constexpr uint32_t kOffVec = kOffH + kMlpGroups * kGroupBytes;  // b1, b2, w3, graph
 constexpr uint32_t kVecFloats = 3 * kMlpH + kMlpGraph + 8;
 constexpr uint32_t kMlpSmem = kOffVec + kVecFloats * 4 + 1024;  // + alignment slack
 constexpr uint32_t kWeightBytes = 16384 + 32768;
@@ -162,38 +165,48 @@ struct MlpParams {
   float* dbg;            // diagnostics: tile 0's raw accumulators (acc1 | acc2), or null
 };
 
-// coords: (n, 3) float64 rows (batch, sm%, quota%) of one model; out: latency (ms) float64
-__global__ void __launch_bounds__(kMlpThreads, 2)
+__device__ __forceinline__ void group_sync(int group) {
+  asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(128) : "memory");
+}
+
+// coords: (n, 3) float64 rows (batch, sm%, quota%) of one model; out: latency (ms) float64.
+// One CTA per SM, kMlpGroups groups of 4 warps; group g takes tiles blockIdx.x*G + g + k*G*grid
+// and owns TMEM columns [128g, 128g+128) (both layers' accumulators: layer 1's is fully
+// read before layer 2's MMA is issued).
+__global__ void __launch_bounds__(kMlpThreads, 1)
     k_mlp_stream(MlpParams P, int model, const double* __restrict__ coords, int64_t n,
                  double* __restrict__ out) {
   extern __shared__ uint8_t mlp_smem_raw[];
-  __shared__ uint64_t bar_w, bar1, bar2;
+  __shared__ uint64_t bar_w, bar1[kMlpGroups], bar2[kMlpGroups];
   __shared__ uint32_t s_tmem;
   const uint32_t raw = (uint32_t)__cvta_generic_to_shared(mlp_smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   uint8_t* base = mlp_smem_raw + (sbase - raw);
   float* vec = reinterpret_cast<float*>(base + kOffVec);
-  const int t = threadIdx.x, warp = t >> 5;
+  const int warp = threadIdx.x >> 5, group = warp >> 2;
+  const int t = threadIdx.x & 127;  // row of the tile = TMEM lane
 
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     mlp_bar_init(&bar_w, 1);
-    mlp_bar_init(&bar1, 1);
-    mlp_bar_init(&bar2, 1);
+    for (int g = 0; g < kMlpGroups; ++g) {
+      mlp_bar_init(&bar1[g], 1);
+      mlp_bar_init(&bar2[g], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {  // TMEM: two 128-column fp32 accumulators
+  if (warp == 0) {  // TMEM: one 128-column fp32 accumulator per group
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(&s_tmem)), "r"(256));
+                 ::"r"((uint32_t)__cvta_generic_to_shared(&s_tmem)), "r"(128 * kMlpGroups));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = t; i < 3 * kMlpH; i += blockDim.x) vec[i] = P.vecs[i];
-  for (int i = t; i < kMlpGraph; i += blockDim.x)
+  for (int i = threadIdx.x; i < 3 * kMlpH; i += blockDim.x) vec[i] = P.vecs[i];
+  for (int i = threadIdx.x; i < kMlpGraph; i += blockDim.x)
     vec[3 * kMlpH + i] = P.graph[int64_t(model) * kMlpGraph + i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = s_tmem;
-  if (t == 0) {
+  const uint32_t tmem = s_tmem + 128u * group;
+  if (threadIdx.x == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
         (uint32_t)__cvta_generic_to_shared(&bar_w)), "r"(kWeightBytes) : "memory");
     bulk_g2s(sbase + kOffW1, P.wimg, kWeightBytes, &bar_w);
@@ -204,26 +217,42 @@ __global__ void __launch_bounds__(kMlpThreads, 2)
   const float* b2 = vec + kMlpH;
   const float* w3 = vec + 2 * kMlpH;
   const float* gf = vec + 3 * kMlpH;
-  const uint32_t lane_base = uint32_t(warp * 32) << 16;  // this warp's TMEM lane quadrant
+  const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;  // this warp's TMEM lanes
+  uint8_t* Hs = base + kOffH + group * kGroupBytes;
+  const uint32_t sH = sbase + kOffH + group * kGroupBytes;
+  const bool issuer = t == 0;
   const int64_t tiles = (n + kMlpTile - 1) / kMlpTile;
+  const int64_t stride = int64_t(gridDim.x) * kMlpGroups;
+  int64_t tile = int64_t(blockIdx.x) * kMlpGroups + group;
+  // coordinates of the current tile's row, loaded one tile ahead
+  double cb = 1.0, cs = 100.0, cq = 100.0;
+  if (tile < tiles && tile * kMlpTile + t < n) {
+    const int64_t r = tile * kMlpTile + t;
+    cb = coords[3 * r];
+    cs = coords[3 * r + 1];
+    cq = coords[3 * r + 2];
+  }
   uint32_t it = 0;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+  for (; tile < tiles; tile += stride, ++it) {
     const int64_t row = tile * kMlpTile + t;
+    // prefetch the next tile's coordinates (consumed one iteration later)
+    double nb = 1.0, ns = 100.0, nq = 100.0;
+    {
+      const int64_t nr = (tile + stride) * kMlpTile + t;
+      if (tile + stride < tiles && nr < n) {
+        nb = coords[3 * nr];
+        ns = coords[3 * nr + 1];
+        nq = coords[3 * nr + 2];
+      }
+    }
     // ---- feature assembly: row t of the A operand (64 bf16 = 8 swizzled chunks) ----
     {
       float f[kMlpK0];
 #pragma unroll
       for (int i = 0; i < kMlpGraph; ++i) f[i] = gf[i];
-      double cb = 1.0, cs = 100.0, cq = 100.0;
-      if (row < n) {
-        cb = coords[3 * row];
-        cs = coords[3 * row + 1];
-        cq = coords[3 * row + 2];
-      }
       config_features(cb, cs, cq, f + kMlpGraph);
 #pragma unroll
       for (int i = kMlpGraph + kMlpCfg; i < kMlpK0; ++i) f[i] = 0.0f;
-      uint8_t* X = base + kOffX;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint4 v;
@@ -231,71 +260,65 @@ __global__ void __launch_bounds__(kMlpThreads, 2)
         v.y = pack_bf16(f[8 * c + 2], f[8 * c + 3]);
         v.z = pack_bf16(f[8 * c + 4], f[8 * c + 5]);
         v.w = pack_bf16(f[8 * c + 6], f[8 * c + 7]);
-        *reinterpret_cast<uint4*>(X + sw128_offset(t, 8 * c)) = v;
+        *reinterpret_cast<uint4*>(Hs + sw128_offset(t, 8 * c)) = v;  // X = panel 0
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
     tc_fence_before();
-    __syncthreads();
+    group_sync(group);
     tc_fence_after();
-    // ---- layer 1: acc1 = X · W1ᵀ  (K = 64: 4 MMAs of K = 16) ----
-    if (t == 0) {
+    // ---- layer 1: acc = X · W1ᵀ  (K = 64: 4 MMAs of K = 16) ----
+    if (issuer) {
 #pragma unroll
       for (int k = 0; k < kMlpK0 / 16; ++k)
-        umma_bf16(tmem, umma_desc(sbase + kOffX + 32 * k), umma_desc(sbase + kOffW1 + 32 * k),
-                  k > 0);
-      umma_commit(&bar1);
+        umma_bf16(tmem, umma_desc(sH + 32 * k), umma_desc(sbase + kOffW1 + 32 * k), k > 0);
+      umma_commit(&bar1[group]);
     }
-    mlp_bar_wait(&bar1, it & 1);
+    mlp_bar_wait(&bar1[group], it & 1);
     tc_fence_after();
-    // ---- epilogue 1: h1 = relu(acc1 + b1) -> bf16 A operand of layer 2 ----
-    {
-      uint8_t* Hs = base + kOffH;
+    // ---- epilogue 1: h1 = relu(acc + b1) -> bf16 A operand of layer 2 ----
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        float v[32];
-        tmem_ld32(tmem + lane_base + 32 * cc, v);
-        if (P.dbg != nullptr && tile == 0)
-          for (int e = 0; e < 32; ++e) P.dbg[t * kMlpH + 32 * cc + e] = v[e];
+    for (int cc = 0; cc < 4; ++cc) {
+      float v[32];
+      tmem_ld32(tmem + lane_base + 32 * cc, v);
+      if (P.dbg != nullptr && tile == 0)
+        for (int e = 0; e < 32; ++e) P.dbg[t * kMlpH + 32 * cc + e] = v[e];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
-          const int col = 32 * cc + 8 * g;
-          float h[8];
+      for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
+        const int col = 32 * cc + 8 * g;
+        float h[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) h[e] = fmaxf(v[8 * g + e] + b1[col + e], 0.0f);
-          uint4 u;
-          u.x = pack_bf16(h[0], h[1]);
-          u.y = pack_bf16(h[2], h[3]);
-          u.z = pack_bf16(h[4], h[5]);
-          u.w = pack_bf16(h[6], h[7]);
-          const int panel = col >> 6;
-          *reinterpret_cast<uint4*>(Hs + panel * 16384 + sw128_offset(t, col & 63)) = u;
-        }
+        for (int e = 0; e < 8; ++e) h[e] = fmaxf(v[8 * g + e] + b1[col + e], 0.0f);
+        uint4 u;
+        u.x = pack_bf16(h[0], h[1]);
+        u.y = pack_bf16(h[2], h[3]);
+        u.z = pack_bf16(h[4], h[5]);
+        u.w = pack_bf16(h[6], h[7]);
+        *reinterpret_cast<uint4*>(Hs + (col >> 6) * 16384 + sw128_offset(t, col & 63)) = u;
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
-    __syncthreads();
+    group_sync(group);
     tc_fence_after();
-    // ---- layer 2: acc2 = H · W2ᵀ  (K = 128: 2 panels x 4 MMAs) ----
-    if (t == 0) {
+    // ---- layer 2: acc = H · W2ᵀ  (K = 128: 2 panels x 4 MMAs) ----
+    if (issuer) {
 #pragma unroll
       for (int k = 0; k < kMlpH / 16; ++k) {
-        const uint32_t pa = sbase + kOffH + (k >> 2) * 16384 + 32 * (k & 3);
-        const uint32_t pb = sbase + kOffW2 + (k >> 2) * 16384 + 32 * (k & 3);
-        umma_bf16(tmem + kMlpH, umma_desc(pa), umma_desc(pb), k > 0);
+        const uint32_t off = (k >> 2) * 16384 + 32 * (k & 3);
+        umma_bf16(tmem, umma_desc(sH + off), umma_desc(sbase + kOffW2 + off), k > 0);
       }
-      umma_commit(&bar2);
+      umma_commit(&bar2[group]);
     }
-    mlp_bar_wait(&bar2, it & 1);
+    mlp_bar_wait(&bar2[group], it & 1);
     tc_fence_after();
-    // ---- epilogue 2: lat = exp(relu(acc2 + b2) · w3 + b3) ----
+    // ---- epilogue 2: lat = exp(min(relu(acc + b2) · w3 + b3, 80)) ----
     {
       float acc = 0.0f;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         float v[32];
-        tmem_ld32(tmem + lane_base + kMlpH + 32 * cc, v);
+        tmem_ld32(tmem + lane_base + 32 * cc, v);
         if (P.dbg != nullptr && tile == 0)
           for (int e = 0; e < 32; ++e) P.dbg[kMlpTile * kMlpH + t * kMlpH + 32 * cc + e] = v[e];
 #pragma unroll
@@ -305,12 +328,16 @@ __global__ void __launch_bounds__(kMlpThreads, 2)
       if (row < n) out[row] = double(__expf(fminf(acc + P.b3, 80.0f)));
     }
     tc_fence_before();
-    __syncthreads();
+    group_sync(group);
     tc_fence_after();
+    cb = nb;
+    cs = ns;
+    cq = nq;
   }
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem),
+                 "r"(128 * kMlpGroups));
 }
 
 }  // namespace rapp
@@ -397,7 +424,8 @@ static int mlp_launch(rapp_mlp* m, int32_t model, const double* d_coords, int64_
   RAPP_CUDA(cudaFuncSetAttribute(k_mlp_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kMlpSmem));
   const int64_t tiles = (n + kMlpTile - 1) / kMlpTile;
-  const int64_t blocks = std::min<int64_t>(tiles, int64_t(m->ctx->sm_count) * 2);
+  const int64_t blocks = std::min<int64_t>((tiles + kMlpGroups - 1) / kMlpGroups,
+                                           int64_t(m->ctx->sm_count));
   MlpParams P{m->d_wimg, m->d_vecs, m->b3, m->d_graph, d_dbg};
   k_mlp_stream<<<(unsigned)blocks, kMlpThreads, kMlpSmem, (cudaStream_t)stream>>>(
       P, model, d_coords, n, d_out);
