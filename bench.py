@@ -923,6 +923,12 @@ def main():
                                     "roofline": lat["roofline"], "e2e": lat["e2e"],
                                     "config": lat["config"],
                                     "cpu_baseline": lattice_cpu_baseline()}
+        margs = argparse.Namespace(**{**vars(args), "steps": 30, "queries": 25_000_000})
+        mlp = run_mlp(margs, rank, world, local)
+        extra["learned_mlp"] = {"value": mlp["value"], "unit": UNIT,
+                                "ms_per_step": mlp["ms"] / mlp["steps"],
+                                "roofline": mlp["roofline"], "e2e": mlp["e2e"],
+                                "cpu_baseline": mlp["cpu_baseline"], "config": mlp["config"]}
         line["extra"] = extra
     print(json.dumps(line))
     if world > 1:
