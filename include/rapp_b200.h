@@ -226,6 +226,10 @@ int rapp_tick_run(rapp_tick *t, double now_ms, const int64_t *arrivals, const ui
                   const double *predicted_in, rapp_action *actions, int64_t max_actions,
                   int64_t *n_actions, double *observed_out, double *predicted_out);
 
+/* Host events between ticks: pods the simulator released (a DRAINING pod whose last
+ * request completed, hs/sim.py:424-438), applied in order before the next tick. */
+int rapp_tick_release(rapp_tick *t, const int64_t *pods, int64_t n);
+
 /* Same with device buffers and no host synchronisation (for timing / graphs). */
 int rapp_tick_run_dev(rapp_tick *t, double now_ms, const int64_t *d_arrivals,
                       const uint8_t *d_idle, void *stream);

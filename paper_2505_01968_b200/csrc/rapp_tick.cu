@@ -1316,6 +1316,26 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
   }
 }
 
+// Releases reported by the host between ticks (a DRAINING pod whose last request finished:
+// hs/sim.py:424-438 -> _release_pod -> allocator.release_pod, hs/allocator.py:128-139), in
+// the order given.  One warp; partition lists are read from global memory.
+__global__ void __launch_bounds__(32) k_tick_release(World w, const int32_t* __restrict__ list,
+                                                     int n) {
+  extern __shared__ uint8_t rel_ovf[];
+  __shared__ int s_nact, s_err, s_npods;
+  __shared__ long long s_counter;
+  const int lane = threadIdx.x & 31;
+  for (int g = lane; g < w.G; g += 32) rel_ovf[g] = 1;  // every list lives in global memory
+  if (lane == 0) s_err = 0;
+  __syncwarp();
+  Commit c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter};
+  for (int i = 0; i < n; ++i) {
+    const int p = list[i];
+    if (w.p_state[p] == kDead) continue;
+    c.release(p, w.p_fn[p], w.p_gpu[p], w.p_puid[p], w.p_s[p], w.p_q[p]);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // prefix-max index for the fresh-GPU search (built once; tables are immutable)
 // ---------------------------------------------------------------------------------------
@@ -1746,6 +1766,42 @@ static int tick_error(rapp_tick* t) {
     default: set_error("function %d: pod capacity exceeded", e[1]); break;
   }
   return e[0];
+}
+
+int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
+  if (!t || n < 0 || (n > 0 && !pods)) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  if (n == 0) return RAPP_OK;
+  RAPP_CUDA(cudaSetDevice(t->ctx->device));
+  int64_t known = t->h_npods;
+  if (known < 0) {
+    int32_t v = 0;
+    RAPP_CUDA(cudaMemcpy(&v, t->w.n_pods, sizeof v, cudaMemcpyDeviceToHost));
+    known = t->h_npods = v;
+  }
+  std::vector<int32_t> list((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (pods[i] < 0 || pods[i] >= known) {
+      set_error("release: pod index %lld out of range", (long long)pods[i]);
+      return RAPP_E_ARG;
+    }
+    list[(size_t)i] = (int32_t)pods[i];
+  }
+  int32_t* d = nullptr;
+  RAPP_CUDA(cudaMalloc(&d, (size_t)n * 4));
+  cudaError_t e = cudaMemcpyAsync(d, list.data(), (size_t)n * 4, cudaMemcpyHostToDevice,
+                                  t->stream);
+  if (e == cudaSuccess) {
+    k_tick_release<<<1, 32, (size_t)std::max(1, t->w.G), t->stream>>>(t->w, d, (int)n);
+    e = cudaGetLastError();
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(t->stream);
+  cudaFree(d);
+  RAPP_CUDA(e);
+  return RAPP_OK;
 }
 
 int rapp_tick_run_dev(rapp_tick* t, double now_ms, const int64_t* d_arrivals,

@@ -235,6 +235,26 @@ class TickEngine:
         if h is not None and _lib._lib is not None:
             _lib._lib.rapp_tick_destroy(h)
 
+    # -- host events between ticks ---------------------------------------------------------
+
+    def release(self, pod_ids, *, apply_to_host: bool = False) -> None:
+        """Pods the simulator released since the last tick (DRAINING pods whose last request
+        completed, hs/sim.py:424-438), in release order."""
+        ids = list(pod_ids)
+        if not ids:
+            return
+        index = {pid: i for i, pid in enumerate(self.pod_ids)}
+        try:
+            idx = np.array([index[pid] for pid in ids], dtype=np.int64)
+        except KeyError as exc:
+            raise InvariantViolation(f"release of unknown pod {exc.args[0]!r}") from None
+        _lib.check(_lib.load().rapp_tick_release(self._h, _lib.i64ptr(idx), len(idx)),
+                   "release")
+        if apply_to_host:
+            for pid in ids:
+                if pid in self.cluster.pods:
+                    allocator.release_pod(self.cluster, pid)
+
     # -- one tick -----------------------------------------------------------------------
 
     def tick(self, now_ms: float, arrivals, idle=None, *, predicted=None,

@@ -558,9 +558,136 @@ def gen_metrics(hs):
     dump("metrics.json", records)
 
 
+# -- trace replay: real simulator runs, captured at every scaler tick ------------------------
+
+
+def _replay_capture(hs, eng, name):
+    """Runs the engine, recording per tick what a batched _handle_scaler needs: arrivals,
+    idle pods, pods released by completions since the last tick, and the outcome."""
+    from hybridscale.sim import SimulationEngine
+    rec = {"name": name, "ticks": []}
+    state = {"in_tick": False, "released": [], "first": True}
+    orig_release = eng._release_pod
+    orig_handle = eng._handle_scaler
+    recorded = []
+    orig_decide = eng.policy.decide
+
+    def spy_decide(function, cl, rate):
+        acts = orig_decide(function, cl, rate)
+        recorded.extend(acts)
+        return acts
+
+    def spy_release(pod_id, now):
+        if not state["in_tick"]:
+            state["released"].append(pod_id)
+        return orig_release(pod_id, now)
+
+    def spy_handle(now):
+        if state["first"]:
+            state["first"] = False
+            rec["initial"] = cluster_dict(eng.cluster)
+            rec["pod_counter0"] = eng._pod_counter
+            state["released"].clear()
+        fids = sorted(eng.functions)
+        arrivals = [eng._tick_arrivals[f] for f in fids]
+        idle = sorted(pid for pid, rt in eng._runtimes.items() if rt.idle())
+        ready = sorted([pid, hx(rt.pod.ready_at_ms)] for pid, rt in eng._runtimes.items()
+                       if rt.pod.state.value == "cold_starting")
+        released = list(state["released"])
+        state["released"].clear()
+        recorded.clear()
+        n_before = eng._pod_counter
+        state["in_tick"] = True
+        orig_handle(now)
+        state["in_tick"] = False
+        tl = eng._timeline[-len(fids):]
+        rec["ticks"].append({
+            "now": hx(now), "arrivals": arrivals, "idle": idle, "released": released,
+            "cold": ready, "actions": action_list(recorded),
+            "new_pods": [f"pod-{i:06d}" for i in range(n_before, eng._pod_counter)],
+            "observed": [hx(p.observed_rps) for p in tl],
+            "predicted": [hx(p.predicted_rps) for p in tl]})
+
+    eng._release_pod = spy_release
+    eng._handle_scaler = spy_handle
+    eng.policy.decide = spy_decide
+    eng.run()
+    rec["trailing_released"] = list(state["released"])  # completions after the last tick
+    rec["final"] = cluster_dict(eng.cluster)
+    return rec
+
+
+def gen_replay(hs):
+    """Config-3-style trace replays through the reference simulator: the demo experiment
+    (2 functions, step-burst trace, all three policies) and a 100-function burst replay on
+    64 GPUs (hybrid).  Tables, functions and configs are stored with the captures."""
+    from hybridscale import (FunctionSpec, PerfTable, PodConfig, ScalerConfig, SimConfig,
+                             build_cluster, load_table)
+    from hybridscale.sim import SimulationEngine
+    from hybridscale.trace import merge_traces, synth_trace
+    runs = []
+    # 1) the demo experiment (pkg/configs/demo.yaml) built through the reference's own API
+    tables = {n: load_table(os.path.join(REF_PKG, "tables", n + ".csv"))
+              for n in ("resnet50", "bert-small")}
+    fdefs = [("resnet50", 20.0, [1, 2, 4, 8], PodConfig(8, 75, 20, 1)),
+             ("bert-small", 29.0, [1, 2, 4], PodConfig(4, 75, 20, 1))]
+    trace = merge_traces([
+        synth_trace("step", {"low": 20, "high": 200, "period_ms": 60000}, 42,
+                    function_id="resnet50", horizon_ms=240000.0),
+        synth_trace("step", {"low": 10, "high": 60, "period_ms": 60000}, 43,
+                    function_id="bert-small", horizon_ms=240000.0)])
+    kal = {"A": 1.0, "Q": 25.0, "H": 1.0, "D": 4.0, "P0": 1.0}
+    for policy in ("hybrid", "horizontal-only", "exclusive-gpu"):
+        fns = [FunctionSpec(function_id=f, baseline_latency_ms=bl, perf_table_ref=f,
+                            min_rps=1.0, allowed_batches=ab, initial=ini)
+               for f, bl, ab, ini in fdefs]
+        cluster = build_cluster(4, functions=fns, total_sm_units=80)
+        cfg = ScalerConfig(alpha=0.65, beta=0.45, delta_iq=10, cooldown_ms=30000.0, r_min=1.0)
+        simcfg = SimConfig(window_ms=100.0, scaler_interval_ms=1000.0, cold_start_ms=5000.0,
+                           queue_capacity=1000, seed=42)
+        eng = SimulationEngine(trace, fns, tables, cluster, cfg, simcfg, policy, kal)
+        rec = _replay_capture(hs, eng, f"demo-{policy}")
+        rec.update({"policy": policy, "functions": [fn_dict(f) for f in fns],
+                    "tables": {n: table_dict(t) for n, t in tables.items()},
+                    "alpha": hx(0.65), "beta": hx(0.45), "delta": 10,
+                    "cooldown_ms": hx(30000.0), "r_min": hx(1.0), "interval_ms": hx(1000.0),
+                    "cold_start_ms": hx(5000.0), "kalman": {k: hx(v) for k, v in kal.items()}})
+        runs.append(rec)
+    # 2) 100 functions, burst traces, 64 GPUs (BASELINE config 3), hybrid
+    rng = random.Random(3)
+    fns, tables, traces = [], {}, []
+    bs, ss, qs = [1, 2, 4, 8, 16, 32], list(range(10, 101, 10)), list(range(10, 101, 10))
+    for i in range(100):
+        fid = f"fn-{i:03d}"
+        fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
+        lat = np.array([[[(fixed + per * b) * (floor + (1.0 - floor) * (100.0 / s)) * (100.0 / q)
+                          for q in qs] for s in ss] for b in bs])
+        tables[fid] = PerfTable(fid, bs, ss, qs, lat)
+        fns.append(FunctionSpec(function_id=fid, baseline_latency_ms=20.0, perf_table_ref=fid,
+                                min_rps=1.0, allowed_batches=[1, 2, 4, 8],
+                                initial=PodConfig(4, rng.choice([20, 30, 40]), 20, 1)))
+        traces.append(synth_trace("burst", {"base": rng.uniform(2, 20),
+                                            "spike": rng.uniform(40, 120), "spike_prob": 0.2},
+                                  1000 + i, function_id=fid, horizon_ms=30000.0))
+    trace = merge_traces(traces)
+    cluster = build_cluster(64, functions=fns)
+    cfg = ScalerConfig(alpha=0.65, beta=0.45, delta_iq=10, cooldown_ms=5000.0, r_min=1.0)
+    simcfg = SimConfig(scaler_interval_ms=1000.0, cold_start_ms=2000.0, queue_capacity=1000,
+                       seed=7, max_drain_ms=5000.0)
+    eng = SimulationEngine(trace, fns, tables, cluster, cfg, simcfg, "hybrid", kal)
+    rec = _replay_capture(hs, eng, "burst-100")
+    rec.update({"policy": "hybrid", "functions": [fn_dict(f) for f in fns],
+                "tables": {n: table_dict(t) for n, t in tables.items()},
+                "alpha": hx(0.65), "beta": hx(0.45), "delta": 10, "cooldown_ms": hx(5000.0),
+                "r_min": hx(1.0), "interval_ms": hx(1000.0), "cold_start_ms": hx(2000.0),
+                "kalman": {k: hx(v) for k, v in kal.items()}})
+    runs.append(rec)
+    dump("replay.json", {"runs": runs})
+
+
 GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick,
               "policy": gen_policy, "ingest": gen_ingest,
-              "metrics": gen_metrics}
+              "metrics": gen_metrics, "replay": gen_replay}
 
 
 def main(argv):

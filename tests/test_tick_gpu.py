@@ -270,3 +270,43 @@ def test_replica_ticks_vs_oracle_at_scale(policy):
         assert got == [list(a) for a in acts], f"tick {k}"
         total += len(acts)
     assert total > 50
+
+
+def test_trace_replay_matches_reference_simulator():
+    """Every scaler tick of real reference simulations (the demo experiment under all three
+    policies, 240 ticks each, and a 100-function burst replay on 64 GPUs): the device tick
+    fed the simulator's arrivals, idle pods and between-tick releases makes the same
+    decisions, creates the same pod ids and reports the same rates (0 ulp)."""
+    from paper_2505_01968_b200 import PerfTable
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    g = load_golden("replay.json")
+    for run in g["runs"]:
+        fns = [function_from(f) for f in run["functions"]]
+        tables = {}
+        for name, t in run["tables"].items():
+            b, s, q, v = golden_table_arrays(t)
+            tables[name] = PerfTable(t["function_id"], t["batches"], t["sms"], t["quotas"], v)
+        cluster = cluster_from(run["initial"])
+        cfg = ScalerConfig(alpha=fx(run["alpha"]), beta=fx(run["beta"]), delta_iq=run["delta"],
+                           cooldown_ms=fx(run["cooldown_ms"]), r_min=fx(run["r_min"]))
+        eng = TickEngine(fns, tables, cluster, cfg,
+                         kalman_params={k: fx(v) for k, v in run["kalman"].items()},
+                         scaler_interval_ms=fx(run["interval_ms"]),
+                         cold_start_ms=fx(run["cold_start_ms"]),
+                         pod_counter=run["pod_counter0"], policy=run["policy"])
+        fids = sorted(f["id"] for f in run["functions"])
+        for k, t in enumerate(run["ticks"]):
+            eng.release(t["released"], apply_to_host=True)
+            res = eng.tick(fx(t["now"]), t["arrivals"], idle=set(t["idle"]),
+                           apply_to_host=True)
+            assert _acts(res.actions) == [list(a) for a in t["actions"]], (run["name"], k)
+            assert [a for a, x in zip(res.pod_ids, res.actions)
+                    if x.kind.value == "horizontal_up"] == t["new_pods"], (run["name"], k)
+            assert [res.observed[f] for f in fids] == [fx(x) for x in t["observed"]]
+            assert [res.predicted[f] for f in fids] == [fx(x) for x in t["predicted"]]
+            cluster.validate()
+        eng.release(run["trailing_released"], apply_to_host=True)
+        assert cluster_to(cluster) == golden_cluster_to(run["final"]), run["name"]
+        dev = eng.device_cluster_dict()
+        assert dev["pods"] == sorted(cluster_to(cluster)["pods"], key=str), run["name"]
