@@ -732,6 +732,59 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False, nfn=1000, ng
             "e2e_api": "TickEngine.tick (rapp_tick_run: H2D arrivals+idle, D2H actions+rates)"}
 
 
+def run_replay(args, local, name="burst-100", reps=3):
+    """Config 3: the 100-function burst trace replay captured from the reference simulator
+    (tests/golden/replay.json): every scaler tick through the public host API —
+    TickEngine.release (the simulator's between-tick releases) + TickEngine.tick (H2D
+    arrivals and idle flags, kernels, D2H actions and rates) — timed end to end per tick.
+    Decisions are checked against the capture on every tick."""
+    import torch
+    from paper_2505_01968_b200 import PerfTable
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from golden_io import cluster_from, function_from, fx
+    with open(os.path.join(ROOT, "tests", "golden", "replay.json")) as fh:
+        run = next(r for r in json.load(fh)["runs"] if r["name"] == name)
+    fns = [function_from(f) for f in run["functions"]]
+    tables = {}
+    for tn, t in run["tables"].items():
+        b, s_, q = (np.asarray(t[k], dtype=np.float64) for k in ("batches", "sms", "quotas"))
+        v = np.array([float.fromhex(x) for x in t["latency_ms"]]).reshape(len(b), len(s_), len(q))
+        tables[tn] = PerfTable(t["function_id"], t["batches"], t["sms"], t["quotas"], v,
+                               device=local)
+    cfg = ScalerConfig(alpha=fx(run["alpha"]), beta=fx(run["beta"]), delta_iq=run["delta"],
+                       cooldown_ms=fx(run["cooldown_ms"]), r_min=fx(run["r_min"]))
+    times = []
+    for rep in range(reps):
+        eng = TickEngine(fns, tables, cluster_from(run["initial"]), cfg,
+                         kalman_params={k: fx(v) for k, v in run["kalman"].items()},
+                         scaler_interval_ms=fx(run["interval_ms"]),
+                         cold_start_ms=fx(run["cold_start_ms"]),
+                         pod_counter=run["pod_counter0"], policy=run["policy"], device=local)
+        for t in run["ticks"]:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng.release(t["released"])
+            res = eng.tick(fx(t["now"]), t["arrivals"], idle=set(t["idle"]))
+            dt = time.perf_counter() - t0
+            if rep > 0:  # the first pass warms up
+                times.append(dt * 1e6)
+            got = [[a.function_id, a.kind.value, a.batch, a.sm_percent, a.quota_percent,
+                    a.pod_id, a.gpu_id] for a in res.actions]
+            if got != [list(a) for a in t["actions"]]:
+                raise RuntimeError("replay decisions differ from the reference capture")
+    acts = sum(len(t["actions"]) for t in run["ticks"])
+    return {"functions": len(fns), "gpus_simulated": len(run["initial"]["gpus"]),
+            "ticks": len(run["ticks"]), "actions": acts, "passes_timed": reps - 1,
+            "e2e_us_median": float(np.median(times)), "e2e_us_max": float(np.max(times)),
+            "decisions": "identical to the reference simulator on every tick",
+            "reference_us_per_tick": 90100.0,
+            "reference_note": "reference _handle_scaler on a 100-function replay, measured in "
+                              "the build container (SURVEY.md §8(d) config 3)",
+            "api": "TickEngine.release + TickEngine.tick (host arrays, idle pod ids)"}
+
+
 def tick_cpu_baseline(args, nticks=2):
     """The scaler oracle (pure-Python restatement of the reference tick, oracle/) on one
     host core for the same config-4 world: seconds per tick.  The reference itself spends
@@ -914,7 +967,8 @@ def main():
     if world == 1 and args.workload == "stream" and not args.no_extra:
         # the second half of the metric ("scaling decisions/tick latency") and config 5
         extra = {"tick_config4": run_tick(args, local, ticks=20),
-                 "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64)}
+                 "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64),
+                 "replay_config3": run_replay(args, local)}
         extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
         largs = argparse.Namespace(**{**vars(args), "steps": 50, "functions": 3125})
         lat = run_lattice(largs, rank, world, local)

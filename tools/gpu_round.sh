@@ -1,1 +1,2 @@
-timeout 600 python -m pytest tests/test_tick_gpu.py -x -q -k "replay or golden" 2>&1 | tail -30
+timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
+tail -c 3000 gpurun_out/bench_default.log
