@@ -603,6 +603,40 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
 // ---------------------------------------------------------------------------------------
 // phase B: sequential commit (one warp)
 // ---------------------------------------------------------------------------------------
+// mbarrier + bulk-copy helpers for the commit's row staging
+__device__ __forceinline__ void tk_bar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tk_bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tk_bulk(void* dst, const void* src, uint32_t bytes,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+      "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void tk_bar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(sbar), "r"(parity)
+        : "memory");
+  }
+}
+
+// the first pod's quota row of a function, staged for the commit (102 doubles = 816 B,
+// the 101-entry row plus 8 bytes of the next row so the bulk size is a multiple of 16)
+constexpr int kRowStage = 102;
+
 struct Commit {
   const World& w;
   int lane;
@@ -927,7 +961,7 @@ struct Commit {
   // change before the function's own turn in the tick.
   struct Pre {
     double gap0, sg0;
-    int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods;
+    int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods, kd0;
     int nd, dkind, dquota, didle, stamp;
     uint32_t uid0;
   };
@@ -946,6 +980,7 @@ struct Commit {
       r.sav0 = w.spec_avail[f * kMaxPods];
       r.sk0 = w.spec_k[f * kMaxPods];
       r.sg0 = w.spec_gain[f * kMaxPods];
+      r.kd0 = w.row_kd[f * kMaxPods];
       r.p0 = r.m > 0 ? w.sorted[f * kMaxPods] : -1;
     } else if (cls == kDown) {
       r.nd = w.ndown[f];
@@ -986,6 +1021,7 @@ struct Commit {
     r.bref = __shfl_sync(0xffffffffu, x.bref, src);
     r.brefok = __shfl_sync(0xffffffffu, x.brefok, src);
     r.npods = __shfl_sync(0xffffffffu, x.npods, src);
+    r.kd0 = __shfl_sync(0xffffffffu, x.kd0, src);
     r.nd = __shfl_sync(0xffffffffu, x.nd, src);
     r.dkind = __shfl_sync(0xffffffffu, x.dkind, src);
     r.dquota = __shfl_sync(0xffffffffu, x.dquota, src);
@@ -995,7 +1031,8 @@ struct Commit {
     return r;
   }
 
-  __device__ void scale_up(int f, double now, const Pre& pre) const {
+  // srow0: the function's first-pod quota row staged in shared memory (see k_tick_commit)
+  __device__ void scale_up(int f, double now, const Pre& pre, const double* srow0) const {
     const int d = w.delta;
     double gap = pre.gap0;
     const int m = pre.m;
@@ -1020,8 +1057,9 @@ struct Commit {
         gain = j == 0 ? pre.sg0 : w.spec_gain[f * kMaxPods + j];
       } else {
         spec_ok = false;  // later pods start from a different gap: walk them here
-        const int kd = w.row_kd[f * kMaxPods + j];
-        const double* row = rows + j * kRow + kd;  // row[k] = thr at q0 + k*d
+        const int kd = j == 0 ? pre.kd0 : w.row_kd[f * kMaxPods + j];
+        // row[k] = thr at q0 + k*d
+        const double* row = j == 0 ? srow0 + kd : rows + j * kRow + kd;
         // k* = first k >= 0 with q0+(k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0.
         // k <= (100 - q0) / d < 128: every row value the walk may read is loaded in one
         // round (lane l holds k = l, l+32, l+64, l+96), then 4 ballots find k*.
@@ -1229,7 +1267,11 @@ struct Commit {
 // used-GPU argmin and the first-free scan then read shared memory only.  Function classes
 // are fetched 32 at a time and only active functions are visited, in sorted order.
 __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int smem_g, int ps) {
-  extern __shared__ __align__(16) int32_t sg[];
+  // dynamic shared layout: [row staging 2 x 32 x kRowStage doubles][5*G summaries]
+  //                        [partition cache G*ps uint64 (8-aligned)][ovf G bytes]
+  extern __shared__ __align__(16) int32_t smem_dyn[];
+  double* s_rows = reinterpret_cast<double*>(smem_dyn);
+  int32_t* sg = smem_dyn + 2 * 32 * kRowStage * 2;
   __shared__ int s_nact;
   const int lane = threadIdx.x & 31;
   World v = w;
@@ -1271,9 +1313,40 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
   __syncwarp();
   Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter};
   bool stop = s_err != 0;
-  for (int base = 0; base < w.F && !stop; base += 32) {
-    const int mine = base + lane < w.F ? w.cls[base + lane] : kNone;
+  // First-pod quota rows of the scale-up functions of a batch of 32 are bulk-copied into
+  // shared memory one batch ahead (double buffer), so a vertical walk that has to be
+  // redone (its partition's headroom changed since phase A) reads shared memory.
+  __shared__ uint64_t s_rbar[2];
+  if (lane == 0) {
+    tk_bar_init(&s_rbar[0]);
+    tk_bar_init(&s_rbar[1]);
+  }
+  __syncwarp();
+  auto stage = [&](int b0, int cls_lane, int buf) {
+    const bool want = w.policy == 0 && cls_lane == kUp;
+    const unsigned wm = __ballot_sync(0xffffffffu, want);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs earlier reads
+    if (lane == 0) tk_bar_expect(&s_rbar[buf], uint32_t(__popc(wm)) * kRowStage * 8u);
+    __syncwarp();
+    if (want)
+      tk_bulk(s_rows + (buf * 32 + lane) * kRowStage, w.rows + int64_t(b0 + lane) * kMaxPods * kRow,
+              kRowStage * 8u, &s_rbar[buf]);
+  };
+  int cls_cur = lane < w.F ? w.cls[lane] : kNone;
+  int cls_nxt = 32 + lane < w.F ? w.cls[32 + lane] : kNone;
+  if (!stop) stage(0, cls_cur, 0);
+  int staged = 1;  // batches whose copies were issued
+  int j = 0;
+  for (int base = 0; base < w.F && !stop; base += 32, ++j) {
+    const int mine = cls_cur;
     const Commit::Pre pre = c.prefetch(base + lane);
+    if (base + 32 < w.F) {
+      stage(base + 32, cls_nxt, (j + 1) & 1);
+      ++staged;
+    }
+    cls_cur = cls_nxt;
+    cls_nxt = base + 64 + lane < w.F ? w.cls[base + 64 + lane] : kNone;
+    tk_bar_wait(&s_rbar[j & 1], (j >> 1) & 1);
     unsigned act = __ballot_sync(0xffffffffu, mine != kNone);
     while (act) {
       const int i = __ffs(act) - 1;
@@ -1281,7 +1354,7 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
       const int cls = __shfl_sync(0xffffffffu, mine, i);
       if (cls == kUp) {
         if (w.policy == 0)
-          c.scale_up(base + i, now, Commit::bcast(pre, i));
+          c.scale_up(base + i, now, Commit::bcast(pre, i), s_rows + ((j & 1) * 32 + i) * kRowStage);
         else
           c.replica_up(base + i, now);
       } else {
@@ -1294,6 +1367,8 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
       }
     }
   }
+  // no bulk copy may still be in flight into shared memory when the CTA exits
+  for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
   if (lane == 0) {
     *w.n_pods = s_npods;
     *w.counter = s_counter;
@@ -1460,13 +1535,14 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     RAPP_LAUNCHED();
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
-    const size_t budget = 200 * 1024;
+    const size_t budget = 160 * 1024;  // + the row staging below
     const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
     const int smem_g = gbytes + size_t(w.G) <= budget ? 1 : 0;
     int ps = 0;
     if (smem_g)
       ps = (int)std::min<size_t>(12, (budget - gbytes - size_t(w.G)) / (8 * std::max(1, w.G)));
-    const size_t bytes = gbytes + size_t(w.G) * ps * 8 + size_t(w.G) + 16;
+    const size_t bytes = size_t(2 * 32 * kRowStage) * 8 + gbytes + size_t(w.G) * ps * 8 +
+                         size_t(w.G) + 16;
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
     k_tick_commit<<<1, 32, bytes, st>>>(w, now, smem_g, ps);
