@@ -780,12 +780,8 @@ struct Commit {
   // npods: the function's pod count (kept by the caller across its new pods).
   __device__ int new_pod(int f, int b, int s, int q, double now, int& npods) const {
     const long long c = *scounter;
-    int nd = 1;
-    long long top = 1;  // 10^(nd-1)
-    while (top <= c / 10) {
-      top *= 10;
-      ++nd;
-    }
+    int nd = 1;  // decimal digits of c
+    for (unsigned long long v = (unsigned long long)c / 10ull; v; v /= 10ull) ++nd;
     const int width = nd > 6 ? nd : 6;
     const int k = lane;
     uint32_t ch = 0;
@@ -794,9 +790,18 @@ struct Commit {
     } else if (k - 4 < width) {
       const int j = k - 4;           // digit j from the left of the zero-padded number
       const int from_right = width - 1 - j;
-      long long pw = 1;
-      for (int i = 0; i < from_right; ++i) pw *= 10;
-      ch = uint32_t('0' + (from_right >= 19 ? 0 : (c / pw) % 10));
+      // divisions by the constant 10 only (multiply-high), 32-bit when the counter fits
+      uint32_t digit;
+      if (c < (1ll << 32)) {
+        uint32_t v = uint32_t(c);
+        for (int i = 0; i < from_right && v; ++i) v /= 10u;
+        digit = v % 10u;
+      } else {
+        unsigned long long v = (unsigned long long)c;
+        for (int i = 0; i < from_right && v; ++i) v /= 10ull;
+        digit = uint32_t(v % 10ull);
+      }
+      ch = uint32_t('0') + digit;
     }
     const uint32_t shift = 8u * uint32_t(3 - (k & 3));
     const uint32_t part = ch << shift;  // byte k inside its 32-bit quarter-word
