@@ -286,9 +286,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
 #pragma unroll
       for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
         const int col = 32 * cc + 8 * g;
+        const float4 ba = *reinterpret_cast<const float4*>(b1 + col);      // broadcast
+        const float4 bb = *reinterpret_cast<const float4*>(b1 + col + 4);  // LDS.128
+        const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
         float h[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) h[e] = fmaxf(v[8 * g + e] + b1[col + e], 0.0f);
+        for (int e = 0; e < 8; ++e) h[e] = fmaxf(v[8 * g + e] + bv[e], 0.0f);
         uint4 u;
         u.x = pack_bf16(h[0], h[1]);
         u.y = pack_bf16(h[2], h[3]);
@@ -322,8 +325,14 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
         if (P.dbg != nullptr && tile == 0)
           for (int e = 0; e < 32; ++e) P.dbg[kMlpTile * kMlpH + t * kMlpH + 32 * cc + e] = v[e];
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          acc = fmaf(fmaxf(v[e] + b2[32 * cc + e], 0.0f), w3[32 * cc + e], acc);
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 bq = *reinterpret_cast<const float4*>(b2 + 32 * cc + 4 * e4);
+          const float4 wq = *reinterpret_cast<const float4*>(w3 + 32 * cc + 4 * e4);
+          acc = fmaf(fmaxf(v[4 * e4 + 0] + bq.x, 0.0f), wq.x, acc);
+          acc = fmaf(fmaxf(v[4 * e4 + 1] + bq.y, 0.0f), wq.y, acc);
+          acc = fmaf(fmaxf(v[4 * e4 + 2] + bq.z, 0.0f), wq.z, acc);
+          acc = fmaf(fmaxf(v[4 * e4 + 3] + bq.w, 0.0f), wq.w, acc);
+        }
       }
       if (row < n) out[row] = double(__expf(fminf(acc + P.b3, 80.0f)));
     }

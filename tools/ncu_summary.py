@@ -29,6 +29,9 @@ KEYS = {
     "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum": "dfma_thread_inst",
     "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum": "dadd_thread_inst",
     "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul_thread_inst",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct",
+    "sm__ops_path_tensor_src_bf16_dst_fp32.sum.pct_of_peak_sustained_elapsed": "tensor_bf16_ops_pct",
+    "smsp__sass_inst_executed_op_utcmma.sum": "utcmma_inst",
 }
 UNITS = {"dram__bytes_read.sum": 1, "dram__bytes_write.sum": 1}
 
