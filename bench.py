@@ -600,13 +600,32 @@ def run_mlp(args, rank, world, local, n_per_model=None):
     cdt = time.perf_counter() - t0
     cpu = {"value": len(sample) / cdt, "unit": UNIT, "cores": threads, "kind": "port",
            "sample": f"{len(sample)} queries through the fp32 torch forward on the host"}
+    # the fused search over the learned predictions (feasibility + packed-key argmin in
+    # the layer-2 epilogue): config-5-shaped lattices, 32 batches x 100 sm x 100 quota
+    nfs = 625
+    bl = torch.arange(1, 33, dtype=torch.float64, device=dev)
+    sl = torch.arange(1, 101, dtype=torch.float64, device=dev)
+    mof = torch.arange(nfs, dtype=torch.int32, device=dev) % len(lm.names)
+    tg = torch.full((nfs,), 2000.0, dtype=torch.float64, device=dev)
+    lm.search_dev(mof, tg, bl, sl, 1)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(3):
+        lm.search_dev(mof, tg, bl, sl, 1, stream=stream.cuda_stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    search = {"points_per_s": nfs * 32 * 100 * 100 * 3 / (s0.elapsed_time(s1) / 1000.0),
+              "functions": nfs, "lattice": "32 batches x 100 sm x 100 quota",
+              "ms_per_search": s0.elapsed_time(s1) / 3,
+              "api": "LearnedPerfModel.search_dev (rapp_mlp_search_dev)"}
     cfg = {"workload": "learned RaPP MLP (zoo: resnet50, vgg19, bert-base, mobilenet; "
            "64 features -> 128 -> 128 -> 1, random weights), config-2-shaped query streams",
            "queries_per_step": len(coords) * n, "parity": "unpinned (no reference model); "
            "checked against a torch fp32 forward, rel tol 2e-2"}
     return {"value": value, "ms": ms, "steps": steps, "roofline": roof, "e2e": e2e,
             "cpu_baseline": cpu, "config": cfg, "launches": launches, "clocks": clk.summary(),
-            "dtype": "bf16", "scaling": "weak"}
+            "dtype": "bf16", "scaling": "weak", "search": search}
 
 
 def load_bf16_peak():
@@ -943,7 +962,8 @@ def main():
                     "scaling": res["scaling"], "vs_baseline": None, "dtype": res["dtype"],
                     "data": "synthetic", "config": res["config"], "roofline": res["roofline"],
                     "cpu_baseline": res["cpu_baseline"], "e2e": res["e2e"],
-                    "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours"}
+                    "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours",
+                    "search": res["search"]}
             print(json.dumps(line))
         return
     res = (run_stream if args.workload == "stream" else run_lattice)(args, rank, world, local)
@@ -982,7 +1002,8 @@ def main():
         extra["learned_mlp"] = {"value": mlp["value"], "unit": UNIT,
                                 "ms_per_step": mlp["ms"] / mlp["steps"],
                                 "roofline": mlp["roofline"], "e2e": mlp["e2e"],
-                                "cpu_baseline": mlp["cpu_baseline"], "config": mlp["config"]}
+                                "cpu_baseline": mlp["cpu_baseline"], "config": mlp["config"],
+                                "search": mlp["search"]}
         line["extra"] = extra
     print(json.dumps(line))
     if world > 1:

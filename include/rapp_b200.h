@@ -261,6 +261,16 @@ int rapp_mlp_destroy(rapp_mlp *mlp);
 /* d_coords (n,3) float64 rows of one model -> d_out (n) float64 latency; tcgen05 GEMMs. */
 int rapp_mlp_predict_dev(rapp_mlp *mlp, int32_t model, const double *d_coords, int64_t n,
                          double *d_out, void *stream);
+/* most_efficient_config over the learned predictions (hs/perf.py:104-145 semantics): for
+ * function f (model d_model_of_fn[f]) the lattice batches x sms x range(step, 101, step);
+ * rps = b / (latency / 1000.0) in FP64; d_keys[f] = the packed min (s*q, s_idx, q, b_idx) key
+ * over rps >= d_targets[f], else over rps == max rps (the reference's fallback order);
+ * key bits: cost << 32 | s_idx << 20 | q << 12 | b_idx.  d_scratch: 2 * n_fn uint64.
+ * sms must be integral in [0, 2^24); both axes sorted, at most 4096 values. */
+int rapp_mlp_search_dev(rapp_mlp *mlp, int64_t n_fn, const int32_t *d_model_of_fn,
+                        const double *d_targets, int32_t n_batches, const double *d_batches,
+                        int32_t n_sms, const double *d_sms, int32_t quota_step,
+                        uint64_t *d_keys, uint64_t *d_scratch, void *stream);
 /* Diagnostics: same, and the first tile's raw FP32 accumulators (before bias) of both
  * layers into d_acc[2][128][128]. */
 int rapp_mlp_debug_dev(rapp_mlp *mlp, int32_t model, const double *d_coords, int64_t n,

@@ -83,6 +83,9 @@ SIGNATURES = [
     ("rapp_mlp_destroy", ctypes.c_int, [c_vp]),
     ("rapp_mlp_predict_dev", ctypes.c_int, [c_vp, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp,
                                             c_vp]),
+    ("rapp_mlp_search_dev", ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, c_vp, ctypes.c_int32,
+                                           c_vp, ctypes.c_int32, c_vp, ctypes.c_int32, c_vp,
+                                           c_vp, c_vp]),
     ("rapp_mlp_debug_dev", ctypes.c_int, [c_vp, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp,
                                           c_vp, c_vp]),
     ("rapp_probe_fp64", ctypes.c_int, [ctypes.c_int, c_dp, c_dp]),

@@ -42,7 +42,8 @@ constexpr uint32_t kOffW2 = 16384;              // 2 panels [128 n][64 k]       
 constexpr uint32_t kOffH = 49152;               // per group: 2 panels [128 m][64 k] 32 KB
 constexpr uint32_t kGroupBytes = 32768;
 constexpr uint32_t kOffVec = kOffH + kMlpGroups * kGroupBytes;  // b1, b2, w3, graph
-constexpr uint32_t kVecFloats = 3 * kMlpH + kMlpGraph + 8;
+constexpr int kMlpMaxModels = 16;
+constexpr uint32_t kVecFloats = 3 * kMlpH + kMlpGraph * kMlpMaxModels;
 constexpr uint32_t kMlpSmem = kOffVec + kVecFloats * 4 + 1024;  // + alignment slack
 constexpr uint32_t kWeightBytes = 16384 + 32768;
 
@@ -163,6 +164,33 @@ struct MlpParams {
   float b3;
   const float* graph;    // [n_models][kMlpGraph]
   float* dbg;            // diagnostics: tile 0's raw accumulators (acc1 | acc2), or null
+  int n_models;
+};
+
+// What the rows of the tiles are (template MODE of k_mlp):
+//   kStream   rows of `coords` (one model), latency written to `out`
+//   kSearch   lattice points B x S x range(step, 101, step) of function f (its own model);
+//             per function: min packed key (s*q, s_idx, q, b_idx) over rps >= target, and
+//             the max rps (bit pattern, positive doubles order as integers)
+//   kFallback the same over rps >= max rps, for the functions flagged in `fallback` only
+enum : int { kStream = 0, kSearch = 1, kFallback = 2 };
+
+struct MlpWork {
+  // stream
+  int model;
+  const double* coords;
+  int64_t n;
+  double* out;
+  // search
+  int64_t n_fn, tiles_per_fn, points;
+  const int32_t* model_of_fn;
+  const double* targets;          // kSearch: target rps; kFallback: unused
+  const double* batches;          // sorted lattice batches (doubles)
+  const double* sms;              // sorted lattice sm values
+  int32_t nB, nS, nQ, step;
+  unsigned long long* keys;       // [n_fn] meet keys (init ~0)
+  unsigned long long* maxr;       // [n_fn] max rps bits (init 0)
+  const int32_t* fallback;        // [n_fn] 1: no feasible point after kSearch
 };
 
 __device__ __forceinline__ void group_sync(int group) {
@@ -173,9 +201,10 @@ __device__ __forceinline__ void group_sync(int group) {
 // One CTA per SM, kMlpGroups groups of 4 warps; group g takes tiles blockIdx.x*G + g + k*G*grid
 // and owns TMEM columns [128g, 128g+128) (both layers' accumulators: layer 1's is fully
 // read before layer 2's MMA is issued).
-__global__ void __launch_bounds__(kMlpThreads, 1)
-    k_mlp_stream(MlpParams P, int model, const double* __restrict__ coords, int64_t n,
-                 double* __restrict__ out) {
+template <int MODE>
+__global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) {
+  const double* __restrict__ coords = W.coords;
+  const int64_t n = MODE == kStream ? W.n : W.n_fn * W.tiles_per_fn * kMlpTile;
   extern __shared__ uint8_t mlp_smem_raw[];
   __shared__ uint64_t bar_w, bar1[kMlpGroups], bar2[kMlpGroups];
   __shared__ uint32_t s_tmem;
@@ -200,8 +229,15 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   for (int i = threadIdx.x; i < 3 * kMlpH; i += blockDim.x) vec[i] = P.vecs[i];
-  for (int i = threadIdx.x; i < kMlpGraph; i += blockDim.x)
-    vec[3 * kMlpH + i] = P.graph[int64_t(model) * kMlpGraph + i];
+  // graph features: the stream's model, or every model (search rows pick their function's)
+  float* sgraph = vec + 3 * kMlpH;
+  if (MODE == kStream) {
+    for (int i = threadIdx.x; i < kMlpGraph; i += blockDim.x)
+      sgraph[i] = P.graph[int64_t(W.model) * kMlpGraph + i];
+  } else {
+    for (int i = threadIdx.x; i < P.n_models * kMlpGraph; i += blockDim.x)
+      sgraph[i] = P.graph[i];
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -216,7 +252,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   const float* b1 = vec;
   const float* b2 = vec + kMlpH;
   const float* w3 = vec + 2 * kMlpH;
-  const float* gf = vec + 3 * kMlpH;
+
   const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;  // this warp's TMEM lanes
   uint8_t* Hs = base + kOffH + group * kGroupBytes;
   const uint32_t sH = sbase + kOffH + group * kGroupBytes;
@@ -224,26 +260,44 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   const int64_t tiles = (n + kMlpTile - 1) / kMlpTile;
   const int64_t stride = int64_t(gridDim.x) * kMlpGroups;
   int64_t tile = int64_t(blockIdx.x) * kMlpGroups + group;
-  // coordinates of the current tile's row, loaded one tile ahead
+  // stream: coordinates of the current tile's row, loaded one tile ahead
   double cb = 1.0, cs = 100.0, cq = 100.0;
-  if (tile < tiles && tile * kMlpTile + t < n) {
+  if (MODE == kStream && tile < tiles && tile * kMlpTile + t < n) {
     const int64_t r = tile * kMlpTile + t;
     cb = coords[3 * r];
     cs = coords[3 * r + 1];
     cq = coords[3 * r + 2];
   }
   uint32_t it = 0;
-  for (; tile < tiles; tile += stride, ++it) {
-    const int64_t row = tile * kMlpTile + t;
-    // prefetch the next tile's coordinates (consumed one iteration later)
+  for (; tile < tiles; tile += stride) {
+    int64_t row = tile * kMlpTile + t;
+    const float* gf = sgraph;
+    int64_t fn = 0;
+    bool valid = row < n;
+    int32_t bi = 0, si = 0, qv = 0;
     double nb = 1.0, ns = 100.0, nq = 100.0;
-    {
+    if (MODE == kStream) {
+      // prefetch the next tile's coordinates (consumed one iteration later)
       const int64_t nr = (tile + stride) * kMlpTile + t;
       if (tile + stride < tiles && nr < n) {
         nb = coords[3 * nr];
         ns = coords[3 * nr + 1];
         nq = coords[3 * nr + 2];
       }
+    } else {
+      fn = tile / W.tiles_per_fn;
+      if (MODE == kFallback && W.fallback[fn] == 0) continue;  // uniform over the group
+      const int64_t pi = (tile - fn * W.tiles_per_fn) * kMlpTile + t;
+      valid = pi < W.points;
+      const int64_t pc = valid ? pi : 0;
+      bi = int32_t(pc % W.nB);
+      const int64_t rest = pc / W.nB;
+      qv = int32_t(rest % W.nQ + 1) * W.step;
+      si = int32_t(rest / W.nQ);
+      cb = W.batches[bi];
+      cs = W.sms[si];
+      cq = double(qv);
+      gf = sgraph + W.model_of_fn[fn] * kMlpGraph;
     }
     // ---- feature assembly: row t of the A operand (64 bf16 = 8 swizzled chunks) ----
     {
@@ -334,11 +388,39 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
           acc = fmaf(fmaxf(v[4 * e4 + 3] + bq.w, 0.0f), wq.w, acc);
         }
       }
-      if (row < n) out[row] = double(__expf(fminf(acc + P.b3, 80.0f)));
+      const double lat = double(__expf(fminf(acc + P.b3, 80.0f)));
+      if (MODE == kStream) {
+        if (row < n) W.out[row] = lat;
+      } else {
+        // throughput = batch / (latency / 1000.0) (hs/perf.py:95-98), feasibility and the
+        // packed lexicographic key of most_efficient_config (hs/perf.py:123-138)
+        const double rps = __ddiv_rn(cb, __ddiv_rn(lat, 1000.0));
+        const double tgt = MODE == kSearch ? W.targets[fn]
+                                           : __longlong_as_double((long long)W.maxr[fn]);
+        const bool ok = valid && rps >= tgt;
+        const uint64_t sv = uint64_t(cs);
+        unsigned long long key = ok ? ((sv * uint64_t(qv)) << 32) | (uint64_t(si) << 20) |
+                                          (uint64_t(qv) << 12) | uint64_t(bi)
+                                    : ~0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long x = __shfl_xor_sync(0xffffffffu, key, o);
+          key = x < key ? x : key;
+        }
+        if ((threadIdx.x & 31) == 0 && key != ~0ull) atomicMin(W.keys + fn, key);
+        if (MODE == kSearch) {
+          unsigned long long rb = valid && rps > 0.0 ? (unsigned long long)__double_as_longlong(rps) : 0ull;
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, rb, o);
+            rb = x > rb ? x : rb;
+          }
+          if ((threadIdx.x & 31) == 0 && rb) atomicMax(W.maxr + fn, rb);
+        }
+      }
     }
     tc_fence_before();
     group_sync(group);
     tc_fence_after();
+    ++it;
     cb = nb;
     cs = ns;
     cq = nq;
@@ -375,8 +457,9 @@ extern "C" {
 int rapp_mlp_create(rapp_ctx* ctx, int32_t n_models, const float* graph_features,
                     const float* w1, const float* b1, const float* w2, const float* b2,
                     const float* w3, float b3, rapp_mlp** out) {
-  if (!ctx || !out || n_models < 1 || !graph_features || !w1 || !b1 || !w2 || !b2 || !w3) {
-    set_error("null argument");
+  if (!ctx || !out || n_models < 1 || n_models > kMlpMaxModels || !graph_features || !w1 ||
+      !b1 || !w2 || !b2 || !w3) {
+    set_error("null argument or more than %d models", kMlpMaxModels);
     return RAPP_E_ARG;
   }
   std::unique_ptr<rapp_mlp> m(new rapp_mlp());
@@ -422,6 +505,23 @@ int rapp_mlp_destroy(rapp_mlp* m) {
   return RAPP_OK;
 }
 
+}  // extern "C"
+
+namespace rapp {
+
+template <int MODE>
+static int mlp_run(rapp_mlp* m, const MlpWork& W, int64_t rows, float* d_dbg, void* stream) {
+  RAPP_CUDA(cudaFuncSetAttribute(k_mlp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kMlpSmem));
+  const int64_t tiles = (rows + kMlpTile - 1) / kMlpTile;
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>((tiles + kMlpGroups - 1) / kMlpGroups, int64_t(m->ctx->sm_count)));
+  MlpParams P{m->d_wimg, m->d_vecs, m->b3, m->d_graph, d_dbg, m->n_models};
+  k_mlp<MODE><<<(unsigned)blocks, kMlpThreads, kMlpSmem, (cudaStream_t)stream>>>(P, W);
+  RAPP_LAUNCHED();
+  return RAPP_OK;
+}
+
 static int mlp_launch(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
                       double* d_out, float* d_dbg, void* stream) {
   if (!m || model < 0 || model >= m->n_models || n < 0 || (n > 0 && (!d_coords || !d_out))) {
@@ -430,17 +530,33 @@ static int mlp_launch(rapp_mlp* m, int32_t model, const double* d_coords, int64_
   }
   if (n == 0) return RAPP_OK;
   RAPP_CUDA(cudaSetDevice(m->ctx->device));
-  RAPP_CUDA(cudaFuncSetAttribute(k_mlp_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kMlpSmem));
-  const int64_t tiles = (n + kMlpTile - 1) / kMlpTile;
-  const int64_t blocks = std::min<int64_t>((tiles + kMlpGroups - 1) / kMlpGroups,
-                                           int64_t(m->ctx->sm_count));
-  MlpParams P{m->d_wimg, m->d_vecs, m->b3, m->d_graph, d_dbg};
-  k_mlp_stream<<<(unsigned)blocks, kMlpThreads, kMlpSmem, (cudaStream_t)stream>>>(
-      P, model, d_coords, n, d_out);
-  RAPP_LAUNCHED();
-  return RAPP_OK;
+  MlpWork W{};
+  W.model = model;
+  W.coords = d_coords;
+  W.n = n;
+  W.out = d_out;
+  return mlp_run<kStream>(m, W, n, d_dbg, stream);
 }
+
+__global__ void k_mlp_search_prepare(int64_t n_fn, unsigned long long* keys,
+                                     unsigned long long* maxr) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n_fn;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    keys[f] = ~0ull;
+    maxr[f] = 0ull;
+  }
+}
+
+__global__ void k_mlp_search_flags(int64_t n_fn, const unsigned long long* keys,
+                                   int32_t* fallback) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n_fn;
+       f += int64_t(gridDim.x) * blockDim.x)
+    fallback[f] = keys[f] == ~0ull ? 1 : 0;
+}
+
+}  // namespace rapp (host helpers)
+
+extern "C" {
 
 int rapp_mlp_predict_dev(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
                          double* d_out, void* stream) {
@@ -450,6 +566,53 @@ int rapp_mlp_predict_dev(rapp_mlp* m, int32_t model, const double* d_coords, int
 int rapp_mlp_debug_dev(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
                        double* d_out, float* d_acc, void* stream) {
   return mlp_launch(m, model, d_coords, n, d_out, d_acc, stream);
+}
+
+int rapp_mlp_search_dev(rapp_mlp* m, int64_t n_fn, const int32_t* d_model_of_fn,
+                        const double* d_targets, int32_t n_batches, const double* d_batches,
+                        int32_t n_sms, const double* d_sms, int32_t quota_step,
+                        uint64_t* d_keys, uint64_t* d_scratch, void* stream) {
+  if (!m || n_fn < 0 || (n_fn > 0 && (!d_model_of_fn || !d_targets || !d_batches || !d_sms ||
+                                      !d_keys || !d_scratch))) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  if (quota_step < 1 || quota_step > 100) {
+    set_error("quota_step must be in [1, 100]");  // hs/perf.py:116-117
+    return RAPP_E_VALUE;
+  }
+  if (n_batches < 1 || n_batches > 4096 || n_sms < 1 || n_sms > 4096) {
+    set_error("lattice axes must hold 1..4096 values");
+    return RAPP_E_ARG;
+  }
+  if (n_fn == 0) return RAPP_OK;
+  RAPP_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  MlpWork W{};
+  W.n_fn = n_fn;
+  W.nB = n_batches;
+  W.nS = n_sms;
+  W.nQ = 100 / quota_step;
+  W.step = quota_step;
+  W.points = int64_t(W.nB) * W.nS * W.nQ;
+  W.tiles_per_fn = (W.points + kMlpTile - 1) / kMlpTile;
+  W.model_of_fn = d_model_of_fn;
+  W.targets = d_targets;
+  W.batches = d_batches;
+  W.sms = d_sms;
+  W.keys = reinterpret_cast<unsigned long long*>(d_keys);
+  W.maxr = reinterpret_cast<unsigned long long*>(d_scratch);
+  int32_t* fb = reinterpret_cast<int32_t*>(d_scratch + n_fn);  // scratch: 2*n_fn u64
+  W.fallback = fb;
+  const unsigned hb = (unsigned)std::min<int64_t>((n_fn + 255) / 256, 1024);
+  k_mlp_search_prepare<<<hb, 256, 0, st>>>(n_fn, W.keys, W.maxr);
+  RAPP_LAUNCHED();
+  const int64_t rows = n_fn * W.tiles_per_fn * kMlpTile;
+  int rc = mlp_run<kSearch>(m, W, rows, nullptr, stream);
+  if (rc) return rc;
+  k_mlp_search_flags<<<hb, 256, 0, st>>>(n_fn, W.keys, fb);
+  RAPP_LAUNCHED();
+  return mlp_run<kFallback>(m, W, rows, nullptr, stream);
 }
 
 }  // extern "C"

@@ -256,6 +256,46 @@ class LearnedPerfModel:
         self.predict_many_dev(model, c, out)
         return out.cpu().numpy()
 
+    def search_dev(self, model_of_fn, targets, batches, sms, quota_step: int = 10, *,
+                   stream=None):
+        """most_efficient_config over the learned predictions for many functions at once
+        (hs/perf.py:104-145 semantics on this model's rps): CUDA tensors model_of_fn (int32),
+        targets (float64), batches / sms (float64, sorted) -> packed keys (uint64 as int64)."""
+        import torch
+        dev = targets.device
+        n = int(targets.shape[0])
+        if not 1 <= quota_step <= 100:
+            raise ValueError("quota_step must be in [1, 100]")
+        keys = torch.empty(n, dtype=torch.int64, device=dev)
+        scratch = torch.empty(2 * n, dtype=torch.int64, device=dev)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.load().rapp_mlp_search_dev(
+            self._h, n, model_of_fn.data_ptr(), targets.data_ptr(), int(batches.shape[0]),
+            batches.data_ptr(), int(sms.shape[0]), sms.data_ptr(), int(quota_step),
+            keys.data_ptr(), scratch.data_ptr(), stream), "search")
+        return keys
+
+    def search(self, model_of_fn, targets, batches=(1, 2, 4, 8, 16, 32),
+               sms=tuple(range(1, 101)), quota_step: int = 10) -> list[tuple[int, int, int]]:
+        """Host API: one (b, s, q) per function."""
+        import torch
+        t = np.ascontiguousarray(targets, dtype=np.float64)
+        if np.any(t <= 0):
+            raise ValueError("target_rps must be positive")
+        idx = [self.names.index(m) if isinstance(m, str) else int(m) for m in model_of_fn]
+        dev = torch.device("cuda", self.ctx.device)
+        bl = sorted({int(b) for b in batches})
+        sl = sorted({int(s) for s in sms})
+        keys = self.search_dev(torch.tensor(idx, dtype=torch.int32, device=dev),
+                               torch.from_numpy(t).to(dev),
+                               torch.tensor(bl, dtype=torch.float64, device=dev),
+                               torch.tensor(sl, dtype=torch.float64, device=dev), quota_step)
+        out = []
+        for k in keys.cpu().numpy().view(np.uint64).tolist():
+            out.append((bl[k & 0xFFF], sl[(k >> 20) & 0xFFF], (k >> 12) & 0xFF))
+        return out
+
     def for_model(self, name: str) -> "_ModelView":
         return _ModelView(self, self.names.index(name))
 
@@ -289,3 +329,13 @@ class _ModelView:
 
     def throughput(self, batch: float, sm_percent: float, quota_percent: float) -> float:
         return batch / (self.predict_latency(batch, sm_percent, quota_percent) / 1000.0)
+
+    def most_efficient_config(self, target_rps: float, *, quota_step: int = 10,
+                              batches=None, sms=tuple(range(1, 101))):
+        """hs/perf.py:104-145 over this model's predictions (lattice batches x sms x quota
+        steps; batches default to 1..32 powers of two)."""
+        if target_rps <= 0:
+            raise ValueError("target_rps must be positive")
+        return self.lm.search([self.index], [target_rps],
+                              batches=batches or (1, 2, 4, 8, 16, 32), sms=sms,
+                              quota_step=quota_step)[0]

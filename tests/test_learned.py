@@ -60,3 +60,41 @@ def test_mlp_large_stream_and_perfmodel_view():
     view = lm.for_model("bert-base")
     lat = view.predict_latency(8, 50, 50)
     assert lat > 0 and view.throughput(8, 50, 50) == pytest.approx(8 / (lat / 1000.0))
+
+
+def _host_search(lm, model, target, bl, sl, step):
+    """most_efficient_config (hs/perf.py:104-145) over the kernel's own predictions."""
+    qs = list(range(step, 101, step))
+    pts = np.array([(b, s, q) for s in sl for q in qs for b in bl], dtype=np.float64)
+    lat = lm.predict_many(model, pts)
+    rps = pts[:, 0] / (lat / 1000.0)
+    best_meet, best_all = None, None
+    for (b, s, q), r in zip(pts.astype(int).tolist(), rps.tolist()):
+        ka = (-r, s * q, s, q, b)
+        if best_all is None or ka < best_all:
+            best_all = ka
+        if r >= target:
+            km = (s * q, s, q, b)
+            if best_meet is None or km < best_meet:
+                best_meet = km
+    if best_meet is not None:
+        return best_meet[3], best_meet[1], best_meet[2]
+    return best_all[4], best_all[2], best_all[3]
+
+
+@pytest.mark.gpu
+def test_learned_search_matches_host_search_over_the_same_predictions():
+    lm = learned.LearnedPerfModel.zoo(seed=2)
+    bl, sl = [1, 2, 4, 8, 16, 32], list(range(5, 101, 5))
+    rng = np.random.default_rng(9)
+    models, targets = [], []
+    for i in range(24):
+        m = i % 4
+        view = lm.for_model(lm.names[m])
+        peak = view.throughput(32, 100, 100)
+        targets.append(float(peak * rng.choice([1e-3, 0.05, 0.3, 0.7, 0.99, 5.0])))
+        models.append(m)
+    for step in (10, 25):
+        got = lm.search(models, targets, batches=bl, sms=sl, quota_step=step)
+        for m, t, g in zip(models, targets, got):
+            assert g == _host_search(lm, m, t, bl, sl, step), (m, t, step)

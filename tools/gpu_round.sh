@@ -1,2 +1,1 @@
-timeout 300 python -m pytest tests/test_learned.py -x -q 2>&1 | tail -2
-timeout 600 python bench.py --workload mlp --steps 30 2>&1 | tail -1 | cut -c 1-900
+timeout 600 python bench.py --workload mlp --steps 30 > gpurun_out/bench_mlp.log 2>&1; tail -c 600 gpurun_out/bench_mlp.log
