@@ -1,1 +1,1 @@
-timeout 600 python bench.py --workload mlp --steps 30 > gpurun_out/bench_mlp.log 2>&1; tail -c 600 gpurun_out/bench_mlp.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
