@@ -383,13 +383,14 @@ def run_stream(args, rank, world, local):
             "scaling": "weak", "avg_launch_ms": avg_launch_ms}
 
 
-def load_traffic(n):
-    """DRAM bytes per launch for the stream kernel from the committed ncu capture."""
+def load_traffic(n, kernel="k_interp_stream", field="dram_bytes_per_prediction"):
+    """DRAM bytes per launch of a kernel from the committed ncu capture (per-unit figure x
+    the units one launch processes)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            per_pred = float(json.load(fh)["k_interp_stream"]["dram_bytes_per_prediction"])
-        return round(per_pred * n)
+            per_unit = float(json.load(fh)[kernel][field])
+        return round(per_unit * n)
     except Exception:
         return None
 
@@ -480,7 +481,8 @@ def run_lattice(args, rank, world, local):
     achieved = my_points * ops_pt / kern_s / 1e12
     peak = fp64_peak(local) / 1e12
     roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(peak, 3),
-            "unit": "Tops/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "unit": "Tops/s", "frac": round(achieved / peak, 4),
+            "traffic": load_traffic(my_points, "k_mec_lattice", "dram_bytes_per_point"),
             "kernel": "k_mec_lattice<meet> (rapp_search.cu)",
             "peak_source": "measured: rapp_probe_fp64 (independent __dadd_rn/__dmul_rn chains "
                            "on every SM, min of the two rates)",
@@ -572,7 +574,7 @@ def run_mlp(args, rank, world, local, n_per_model=None):
     achieved = flops * n / (per_launch / 1000.0) / 1e12
     peak = load_bf16_peak()
     roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": load_traffic(n, "k_mlp_stream"),
             "kernel": "k_mlp_stream (rapp_mlp.cu, tcgen05.mma kind::f16 M128 N128 K16)",
             "flops_per_prediction": flops, "hbm_bytes_per_prediction": 32,
             "achieved_hbm_gbs": round(32.0 * n / (per_launch / 1000.0) / 1e9, 1)}
