@@ -30,7 +30,13 @@
 #include "rapp_device.cuh"
 #include "rapp_internal.h"
 
+#ifndef RAPP_K3_UNROLL
+#define RAPP_K3_UNROLL 4
+#endif
+
 namespace rapp {
+
+constexpr int kK3Unroll = RAPP_K3_UNROLL;  // unroll of the per-batch-entry loop
 
 struct FnDesc {
   int32_t table;
@@ -224,6 +230,30 @@ __global__ void __launch_bounds__(kSearchThreads)
       return c;
     };
     int found = 1 << 30;  // first feasible batch entry (entries ascend with b)
+    if (!MINLAT && pos_table) {
+      // finite positive grid (checked at upload): every interpolated latency is > 0, so
+      // `rps >= target` is exactly `lat <= threshold` — no division on this path.  One flat
+      // pass over the batch entries; at a segment boundary (uniform across the CTA) the
+      // segment's row values are produced and c1 - c0 is formed once, so each entry costs
+      // the reference's final batch lerp c0 + (c1 - c0) * tb, a compare and a select.
+      int sg = 0;
+      int4 S = sSeg[0];
+      double c0 = row(S.x);
+      double d = __dsub_rn(S.y == S.x ? c0 : row(S.y), c0);
+      int end = S.w;
+#pragma unroll (kK3Unroll)
+      for (int bi = 0; bi < nB; ++bi) {
+        if (bi == end) {
+          S = sSeg[++sg];
+          c0 = row(S.x);
+          d = __dsub_rn(S.y == S.x ? c0 : row(S.y), c0);
+          end = S.w;
+        }
+        const double2 tt = sTT[bi];
+        const double lat = __dadd_rn(c0, __dmul_rn(d, tt.x));
+        found = lat <= tt.y && bi < found ? bi : found;
+      }
+    } else
     for (int sg = 0; sg < nseg; ++sg) {
       const int4 S = sSeg[sg];
       const double c0 = row(S.x);
