@@ -128,7 +128,8 @@ static bool strictly_ascending(const double* a, int64_t n) {
 }
 
 int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b,
-              const double* s, const double* q, const double* v, bool scratch, int32_t* id) {
+              const double* s, const double* q, const double* v, bool scratch, int32_t* id,
+              int32_t reuse_slot, int64_t reuse_cap, int64_t* total_out) {
   if (nb < 1 || ns < 1 || nq < 1) {
     set_error("empty table");  // hs/perf.py:86-87 "empty table"
     return RAPP_E_TABLE;
@@ -179,7 +180,11 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
 
   RAPP_CUDA(cudaSetDevice(ctx->device));
   int32_t slot;
-  if (scratch && ctx->scratch_table >= 0 && ctx->scratch_cap >= total) {
+  if (total_out) *total_out = total;
+  if (reuse_slot >= 0 && reuse_cap >= total) {
+    slot = reuse_slot;  // an evicted stateless table's segment, rewritten in place
+    td.off = ctx->tables[slot].off;
+  } else if (scratch && ctx->scratch_table >= 0 && ctx->scratch_cap >= total) {
     slot = ctx->scratch_table;  // reuse the scratch segment in place
     td.off = ctx->tables[slot].off;
   } else {
@@ -481,12 +486,74 @@ int rapp_locate(const double* axis, int64_t n, double x, int64_t* lo, int64_t* h
   return RAPP_OK;
 }
 
+// Tables given to the stateless entry points are kept (up to kStatelessCache distinct ones,
+// LRU) and matched by exact content, so a caller that passes the same table every call
+// pays the upload and the fast-path build once.  The reference kernel accepts any
+// ascending axes without validation; so does this entry point (_grid_cy.pyx contract).
+constexpr size_t kStatelessCache = 8;
+
 static int stateless_table(rapp_ctx* ctx, const double* b_axis, int64_t nb, const double* s_axis,
                            int64_t ns, const double* q_axis, int64_t nq, const double* values,
                            int32_t* id) {
-  // The reference kernel accepts any ascending axes without validation; so does this
-  // entry point (no strictness check), matching _grid_cy.pyx's raw-buffer contract.
-  return table_put(ctx, nb, ns, nq, b_axis, s_axis, q_axis, values, true, id);
+  if (nb < 1 || ns < 1 || nq < 1 || nb * ns * nq > (int64_t(1) << 27))
+    return table_put(ctx, nb, ns, nq, b_axis, s_axis, q_axis, values, true, id);
+  const size_t nv = size_t(nb * ns * nq);
+  std::vector<double> key;
+  key.reserve(3 + size_t(nb + ns + nq) + nv);
+  key.push_back(double(nb));
+  key.push_back(double(ns));
+  key.push_back(double(nq));
+  key.insert(key.end(), b_axis, b_axis + nb);
+  key.insert(key.end(), s_axis, s_axis + ns);
+  key.insert(key.end(), q_axis, q_axis + nq);
+  key.insert(key.end(), values, values + nv);
+  uint64_t h = 0x9E3779B97F4A7C15ull;
+  for (double d : key) {
+    uint64_t w;
+    memcpy(&w, &d, 8);
+    h = (h ^ w) * 0xff51afd7ed558ccdull;
+    h ^= h >> 29;
+  }
+  const uint64_t now = ++ctx->stateless_clock;
+  for (auto& e : ctx->stateless)
+    if (e.hash == h && e.key.size() == key.size() &&
+        memcmp(e.key.data(), key.data(), key.size() * 8) == 0) {
+      e.used = now;
+      *id = e.id;
+      return RAPP_OK;
+    }
+  rapp_ctx::StatelessTable* victim = nullptr;
+  if (ctx->stateless.size() >= kStatelessCache) {
+    victim = &ctx->stateless[0];
+    for (auto& e : ctx->stateless)
+      if (e.used < victim->used) victim = &e;
+  }
+  int64_t total = 0;
+  int rc = table_put(ctx, nb, ns, nq, b_axis, s_axis, q_axis, values, false, id,
+                     victim ? victim->id : -1, victim ? victim->cap : 0, &total);
+  if (rc) return rc;
+  if (victim && *id == victim->id) {  // rewritten in place
+    victim->key.swap(key);
+    victim->hash = h;
+    victim->used = now;
+    return RAPP_OK;
+  }
+  if (victim) {  // did not fit the victim's segment: a new slot replaces it
+    victim->key.swap(key);
+    victim->hash = h;
+    victim->id = *id;
+    victim->cap = total;
+    victim->used = now;
+    return RAPP_OK;
+  }
+  rapp_ctx::StatelessTable e;
+  e.key.swap(key);
+  e.hash = h;
+  e.id = *id;
+  e.cap = total;
+  e.used = now;
+  ctx->stateless.push_back(std::move(e));
+  return RAPP_OK;
 }
 
 int rapp_interp3(const double* b_axis, int64_t nb, const double* s_axis, int64_t ns,

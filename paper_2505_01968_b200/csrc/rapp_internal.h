@@ -88,6 +88,18 @@ struct rapp_ctx {
   bool fast_attr_set = false;
   bool force_literal = false;  // RAPP_FORCE_LITERAL=1: always use the literal K2 kernel
   rapp::HostPipe pipe;
+  // stateless entry points (rapp_interp3_many & co. take raw axes + values per call): the
+  // last few distinct tables stay resident, matched by exact content, so repeated calls on
+  // the same table skip the upload and the fast-path build
+  struct StatelessTable {
+    std::vector<double> key;  // nb, ns, nq, axes, values (exact comparison)
+    uint64_t hash = 0;
+    int32_t id = -1;
+    int64_t cap = 0;         // doubles reserved in the pool for this slot
+    uint64_t used = 0;       // LRU stamp
+  };
+  std::vector<StatelessTable> stateless;
+  uint64_t stateless_clock = 0;
   double* d_small = nullptr;  // 64 doubles of scratch for scalar calls
 };
 
@@ -95,7 +107,8 @@ namespace rapp {
 // Appends a table to the pool (or overwrites the scratch slot when scratch == true).
 int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b,
               const double* s, const double* q, const double* v, bool scratch,
-              int32_t* id);
+              int32_t* id, int32_t reuse_slot = -1, int64_t reuse_cap = 0,
+              int64_t* total_out = nullptr);
 // The per-device default context used by the stateless entry points.
 int default_ctx(rapp_ctx** out);
 int ensure_pipe(rapp_ctx* ctx, int64_t rows);
