@@ -1489,6 +1489,14 @@ struct rapp_tick {
   uint8_t* d_idle = nullptr;
   double* d_pred_in = nullptr;
   int32_t* h_count = nullptr;  // pinned: n_actions, err, err_fn
+  // pinned staging for the host API: inputs [arrivals F x i64 | predicted F x f64 | idle
+  // pod_cap bytes], outputs [actions 1024 | observed F | predicted F], so every copy of a
+  // tick is asynchronous and the tick synchronises once
+  uint8_t* h_in = nullptr;
+  uint8_t* h_out = nullptr;
+  int32_t* d_rel = nullptr;   // between-tick release list (grown on demand)
+  int32_t* h_rel = nullptr;   // pinned staging for it
+  int64_t rel_cap = 0;
   int64_t h_npods = 0;         // pods created so far (host copy of w.n_pods)
 };
 
@@ -1799,6 +1807,8 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &t->d_idle, (size_t)cap))) return rc;
   if ((rc = dev_alloc(t.get(), &t->d_pred_in, FP))) return rc;
   RAPP_CUDA(cudaMallocHost(&t->h_count, 4 * sizeof(int32_t)));
+  RAPP_CUDA(cudaMallocHost(&t->h_in, FP * 16 + (size_t)cap + 64));
+  RAPP_CUDA(cudaMallocHost(&t->h_out, 1024 * sizeof(rapp_action) + FP * 16 + 64));
   t->h_npods = n_pods;
   // build the fresh-GPU search index
   for (int f0 = 0; f0 < F; f0 += 32768) {
@@ -1819,6 +1829,10 @@ int rapp_tick_destroy(rapp_tick* t) {
   cudaStreamSynchronize(t->stream);
   for (void* p : t->allocs) cudaFree(p);
   if (t->h_count) cudaFreeHost(t->h_count);
+  if (t->h_in) cudaFreeHost(t->h_in);
+  if (t->d_rel) cudaFree(t->d_rel);
+  if (t->h_rel) cudaFreeHost(t->h_rel);
+  if (t->h_out) cudaFreeHost(t->h_out);
   cudaStreamDestroy(t->stream);
   delete t;
   return RAPP_OK;
@@ -1862,26 +1876,27 @@ int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
     RAPP_CUDA(cudaMemcpy(&v, t->w.n_pods, sizeof v, cudaMemcpyDeviceToHost));
     known = t->h_npods = v;
   }
-  std::vector<int32_t> list((size_t)n);
+  if (n > t->rel_cap) {  // grow the persistent release buffers
+    RAPP_CUDA(cudaStreamSynchronize(t->stream));
+    if (t->d_rel) RAPP_CUDA(cudaFree(t->d_rel));
+    if (t->h_rel) RAPP_CUDA(cudaFreeHost(t->h_rel));
+    t->rel_cap = std::max<int64_t>(n, 1024);
+    RAPP_CUDA(cudaMalloc(&t->d_rel, (size_t)t->rel_cap * 4));
+    RAPP_CUDA(cudaMallocHost(&t->h_rel, (size_t)t->rel_cap * 4));
+  }
   for (int64_t i = 0; i < n; ++i) {
     if (pods[i] < 0 || pods[i] >= known) {
       set_error("release: pod index %lld out of range", (long long)pods[i]);
       return RAPP_E_ARG;
     }
-    list[(size_t)i] = (int32_t)pods[i];
   }
-  int32_t* d = nullptr;
-  RAPP_CUDA(cudaMalloc(&d, (size_t)n * 4));
-  cudaError_t e = cudaMemcpyAsync(d, list.data(), (size_t)n * 4, cudaMemcpyHostToDevice,
-                                  t->stream);
-  if (e == cudaSuccess) {
-    k_tick_release<<<1, 32, (size_t)std::max(1, t->w.G), t->stream>>>(t->w, d, (int)n);
-    e = cudaGetLastError();
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(t->stream);
-  cudaFree(d);
-  RAPP_CUDA(e);
+  RAPP_CUDA(cudaStreamSynchronize(t->stream));  // the staging buffer is free again
+  for (int64_t i = 0; i < n; ++i) t->h_rel[i] = (int32_t)pods[i];
+  RAPP_CUDA(cudaMemcpyAsync(t->d_rel, t->h_rel, (size_t)n * 4, cudaMemcpyHostToDevice,
+                            t->stream));
+  // stream-ordered before the next tick; no host synchronisation needed here
+  k_tick_release<<<1, 32, (size_t)std::max(1, t->w.G), t->stream>>>(t->w, t->d_rel, (int)n);
+  RAPP_LAUNCHED();
   return RAPP_OK;
 }
 
@@ -1928,23 +1943,38 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
     t->h_npods = v;
   }
   const int64_t np = t->h_npods;  // tracked on the host: no round trip before the launch
-  if (F) RAPP_CUDA(cudaMemcpyAsync(t->d_arrivals, arrivals, F * 8, cudaMemcpyHostToDevice, st));
-  if (idle && np) RAPP_CUDA(cudaMemcpyAsync(t->d_idle, idle, (size_t)np, cudaMemcpyHostToDevice, st));
+  // inputs through pinned staging (asynchronous copies)
+  int64_t* s_arr = reinterpret_cast<int64_t*>(t->h_in);
+  double* s_pred = reinterpret_cast<double*>(t->h_in + F * 8);
+  uint8_t* s_idle = t->h_in + F * 16;
+  if (F) {
+    memcpy(s_arr, arrivals, F * 8);
+    RAPP_CUDA(cudaMemcpyAsync(t->d_arrivals, s_arr, F * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (idle && np) {
+    memcpy(s_idle, idle, (size_t)np);
+    RAPP_CUDA(cudaMemcpyAsync(t->d_idle, s_idle, (size_t)np, cudaMemcpyHostToDevice, st));
+  }
   if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
-  if (predicted_in && F)
-    RAPP_CUDA(cudaMemcpyAsync(t->d_pred_in, predicted_in, F * 8, cudaMemcpyHostToDevice, st));
+  if (predicted_in && F) {
+    memcpy(s_pred, predicted_in, F * 8);
+    RAPP_CUDA(cudaMemcpyAsync(t->d_pred_in, s_pred, F * 8, cudaMemcpyHostToDevice, st));
+  }
   int rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr, st);
   if (rc) return rc;
   // one synchronisation for the usual case: count, status, rates and the first actions
   RAPP_CUDA(cudaMemcpyAsync(t->h_count, w.n_actions, 4, cudaMemcpyDeviceToHost, st));
   RAPP_CUDA(cudaMemcpyAsync(t->h_count + 1, w.err, 4, cudaMemcpyDeviceToHost, st));
   RAPP_CUDA(cudaMemcpyAsync(t->h_count + 2, w.err_fn, 4, cudaMemcpyDeviceToHost, st));
+  rapp_action* s_act = reinterpret_cast<rapp_action*>(t->h_out);
+  double* s_obs = reinterpret_cast<double*>(t->h_out + 1024 * sizeof(rapp_action));
+  double* s_prd = s_obs + F;
   const int64_t spec = actions ? std::min<int64_t>(max_actions, 1024) : 0;
   if (spec > 0)
-    RAPP_CUDA(cudaMemcpyAsync(actions, w.actions, (size_t)spec * sizeof(rapp_action),
+    RAPP_CUDA(cudaMemcpyAsync(s_act, w.actions, (size_t)spec * sizeof(rapp_action),
                               cudaMemcpyDeviceToHost, st));
-  if (observed_out && F) RAPP_CUDA(cudaMemcpyAsync(observed_out, w.obs, F * 8, cudaMemcpyDeviceToHost, st));
-  if (predicted_out && F) RAPP_CUDA(cudaMemcpyAsync(predicted_out, w.pred, F * 8, cudaMemcpyDeviceToHost, st));
+  if (observed_out && F) RAPP_CUDA(cudaMemcpyAsync(s_obs, w.obs, F * 8, cudaMemcpyDeviceToHost, st));
+  if (predicted_out && F) RAPP_CUDA(cudaMemcpyAsync(s_prd, w.pred, F * 8, cudaMemcpyDeviceToHost, st));
   RAPP_CUDA(cudaStreamSynchronize(st));
   if (t->h_count[1] != RAPP_OK) {
     if ((rc = tick_error(t))) return rc;
@@ -1955,6 +1985,9 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
     set_error("action buffer too small (%lld > %lld)", (long long)n, (long long)max_actions);
     return RAPP_E_ARG;
   }
+  if (observed_out && F) memcpy(observed_out, s_obs, F * 8);
+  if (predicted_out && F) memcpy(predicted_out, s_prd, F * 8);
+  if (actions) memcpy(actions, s_act, (size_t)std::min<int64_t>(n, spec) * sizeof(rapp_action));
   if (actions && n > spec) {
     RAPP_CUDA(cudaMemcpyAsync(actions + spec, w.actions + spec,
                               (size_t)(n - spec) * sizeof(rapp_action), cudaMemcpyDeviceToHost,
