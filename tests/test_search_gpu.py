@@ -116,3 +116,25 @@ def test_config5_shaped_functions_vs_oracle():
     for t, target, g in zip(tables[:3], targets[:3], got[:3]):
         assert g == or_most_efficient_config(t._b_axis, t._s_axis, t._q_axis, t.latency_ms,
                                              target, 1, allowed)
+
+
+def test_config5_full_size_sampled_and_repeatable():
+    """BASELINE config 5 at full size: 3,125 functions x 32 x 100 x 100 = 10^9 lattice
+    points in one pass.  Two runs give identical decisions (order-independent packed-key
+    reduction), and a sample of 24 functions equals the C oracle (hs/perf.py:104-145)."""
+    import bench
+    from paper_2505_01968_b200 import PerfTableSet
+    tables = bench.make_config5_tables(3125, seed=0, device=0)
+    allowed = list(range(1, 33))
+    ts = PerfTableSet([(t, allowed) for t in tables], quota_step=1)
+    assert ts.points == 3125 * 32 * 100 * 100
+    rng = np.random.default_rng(17)
+    scale = rng.choice([0.001, 0.3, 0.5, 0.9, 1.5], 3125)  # 1.5 x max: the fallback branch
+    targets = [float(s * bench.max_lattice_rps(t)) for s, t in zip(scale, tables)]
+    first = ts.search(targets)
+    assert ts.search(targets) == first
+    for f in rng.choice(3125, 24, replace=False).tolist():
+        t = tables[f]
+        want = or_most_efficient_config(t._b_axis, t._s_axis, t._q_axis, t.latency_ms,
+                                        targets[f], 1, allowed)
+        assert first[f] == want, f

@@ -1,11 +1,1 @@
-timeout 900 python -m pytest tests/test_tick_gpu.py -x -q 2>&1 | tail -2
-timeout 600 python -c "
-import sys, argparse; sys.path.insert(0,'.')
-import bench
-a = argparse.Namespace(ticks=20, steps=20)
-print(bench.run_replay(a, 0))
-t = bench.run_tick(a, 0, ticks=20)
-print(t['device_us_median'], t['e2e_us_median'])
-t = bench.run_tick(a, 0, ticks=20, nfn=100, ngpu=64)
-print(t['device_us_median'], t['e2e_us_median'])
-"
+timeout 900 python -m pytest tests/test_search_gpu.py -x -q 2>&1 | tail -3
