@@ -249,10 +249,12 @@ int rapp_tick_counter(rapp_tick *t, int64_t *pod_counter);
 /* ---- learned RaPP predictor (§8(f) row 4, PerfModel protocol hs/perf.py:23-31) -------
  * No reference counterpart exists (the paper's GNN/MLP predictor is out of the reference's
  * scope), so this path has no parity target: it is checked against a PyTorch
- * fp32 forward of the same BF16-rounded weights.  Model: x = [graph features (40) |
- * 16 config features of (batch, sm%, quota%) | 0 pad] (64) -> relu(W1 x + b1) (128) ->
- * relu(W2 . + b2) (128) -> exp(w3 . + b3) = latency ms.  Weights are fp32 row-major
- * (W1 [128][64], W2 [128][128]) and are held as BF16; graph_features is [n_models][40]. */
+ * fp32 forward of the same BF16 operands.  Model: x = [graph features (40) | 16 config
+ * features of (batch, sm%, quota%), the last the constant 1 | 0 pad] (64) -> relu(W1 x + b1)
+ * (127 units + a constant unit) -> relu(W2 . + b2) (127 + 1) -> exp(min(w3 . + b3, 80)) =
+ * latency ms.  The biases ride on the constant feature / units (b1 replaces W1 column 55,
+ * b2 W2 column 127, b3 w3[127]), so all three layers are BF16 tensor-core GEMMs.  Weights
+ * are fp32 row-major (W1 [128][64], W2 [128][128], w3 [128]); graph_features [n][40]. */
 typedef struct rapp_mlp rapp_mlp;
 int rapp_mlp_create(rapp_ctx *ctx, int32_t n_models, const float *graph_features,
                     const float *w1, const float *b1, const float *w2, const float *b2,

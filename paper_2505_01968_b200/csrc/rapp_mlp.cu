@@ -2,20 +2,23 @@
 // model): a fused feature-assembly + 3-layer MLP forward on the 5th-generation
 // tensor cores.
 //
-//   x   = [graph features of the model (kGraph) | config features of (b, s%, q%) | 0 pad]  (64)
-//   h1  = relu(x  · W1ᵀ + b1)      (128)   tcgen05.mma kind::f16, BF16 in, FP32 acc in TMEM
-//   h2  = relu(h1 · W2ᵀ + b2)      (128)   same (h1 rounded to BF16 as the A operand)
-//   lat = exp(min(h2 · w3 + b3, 80))       CUDA cores, FP32, in the layer-2 epilogue
+//   x   = [graph features of the model (40) | config features of (b, s%, q%) (16, the last
+//          one the constant 1) | 0 pad]                                          (64)
+//   h1  = relu(W1 x)        127 units + a constant-1 unit                         (128)
+//   h2  = relu(W2 h1)       127 units + a constant-1 unit                         (128)
+//   lat = exp(min(w3 . h2, 80))
+// Biases ride on the constant units (column 55 of W1, column 127 of W2 and w3), so every
+// layer is one GEMM: tcgen05.mma kind::f16, BF16 operands (weights, x, h1, h2), FP32
+// accumulators in TMEM; layer 3 is an N=16 MMA of which column 0 is used.
 //
 // One persistent CTA per SM runs 4 independent 4-warp groups, each on its own 128-row
-// tiles, so one group's epilogue overlaps the others' MMAs.  Per tile: every thread assembles its row's
-// features straight into the SWIZZLE_128B K-major smem image of the A operand; thread 0
-// issues 4 (layer 1) / 8 (layer 2) tcgen05.mma of M=128, N=128, K=16 into two TMEM
-// accumulators (256 columns) and commits each layer to an mbarrier; the epilogue reads the
-// accumulator row of each thread (tcgen05.ld 32x32b: warp w owns TMEM lanes 32w..32w+31),
-// applies bias + ReLU, and writes the BF16 activations back as the next layer's swizzled
-// A operand.  The weights are uploaded once as pre-swizzled BF16 images and bulk-copied
-// into shared memory per CTA.
+// tiles, so one group's epilogue overlaps the others' MMAs.  Per tile: every thread writes
+// its row's features straight into the SWIZZLE_128B K-major smem image of the A operand
+// (the model's graph part is a pre-packed BF16 copy); thread 0 of the group issues the
+// layer's MMAs into the group's 128 TMEM columns and commits them to an mbarrier; the
+// epilogue reads the thread's TMEM lane (tcgen05.ld 32x32b: warp w owns lanes 32(w%4)..),
+// converts with cvt.rn.relu.bf16x2 and writes the next layer's swizzled A operand.  The
+// weights are uploaded once as pre-swizzled BF16 images and bulk-copied into shared memory.
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -39,13 +42,17 @@ constexpr int kMlpThreads = 128 * kMlpGroups;
 // layer-1 A operand (X is consumed by layer 1 before the layer-1 epilogue overwrites it)
 constexpr uint32_t kOffW1 = 0;                  // [128 n][64 k]  bf16, SW128   16 KB
 constexpr uint32_t kOffW2 = 16384;              // 2 panels [128 n][64 k]       32 KB
-constexpr uint32_t kOffH = 49152;               // per group: 2 panels [128 m][64 k] 32 KB
+constexpr uint32_t kOffW3 = 49152;              // 2 panels [16 n][64 k]         4 KB
+constexpr uint32_t kW3Panel = 2048;
+constexpr uint32_t kOffH = 53248;               // per group: 2 panels [128 m][64 k] 32 KB
 constexpr uint32_t kGroupBytes = 32768;
-constexpr uint32_t kOffVec = kOffH + kMlpGroups * kGroupBytes;  // b1, b2, w3, graph
+constexpr uint32_t kOffVec = kOffH + kMlpGroups * kGroupBytes;  // packed graph features
 constexpr int kMlpMaxModels = 16;
-constexpr uint32_t kVecFloats = 3 * kMlpH + kMlpGraph * kMlpMaxModels;
-constexpr uint32_t kMlpSmem = kOffVec + kVecFloats * 4 + 1024;  // + alignment slack
-constexpr uint32_t kWeightBytes = 16384 + 32768;
+constexpr uint32_t kGraphChunks = 5;            // 40 bf16 = 5 x 16-byte chunks per model
+constexpr uint32_t kMlpSmem = kOffVec + kMlpMaxModels * kGraphChunks * 16 + 1024;
+constexpr uint32_t kWeightBytes = 16384 + 32768 + 4096;
+constexpr int kConstCol = kMlpGraph + kMlpCfg - 1;  // feature 55 == 1.0 (carries layer 1's bias)
+constexpr int kConstUnit = kMlpH - 1;               // hidden unit 127 == 1.0
 
 // byte offset of element (r, k) inside a K-major SWIZZLE_128B panel of 64 bf16 columns:
 // 8-row x 128-byte atoms stacked along r; 16-byte chunk c of row r stored at c ^ (r % 8)
@@ -61,16 +68,33 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
-// instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M = 128, N = 128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kMlpH >> 3) << 17) |
-                            (uint32_t(kMlpTile >> 4) << 24);
+// instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M = 128, N = n
+constexpr uint32_t idesc_n(uint32_t n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | (uint32_t(kMlpTile >> 4) << 24);
+}
+constexpr uint32_t kIdesc = idesc_n(kMlpH);
+constexpr uint32_t kIdesc16 = idesc_n(16);
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
-                                          uint32_t accumulate) {
+                                          uint32_t accumulate, uint32_t idesc = kIdesc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-      ::"r"(tmem_d), "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// relu and round two fp32 values to a packed bf16x2 word (lo -> lower address)
+__device__ __forceinline__ uint32_t relu_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(r);
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -159,10 +183,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* src, uint32_
 }
 
 struct MlpParams {
-  const uint8_t* wimg;   // pre-swizzled bf16 W1 | W2 images (kWeightBytes)
-  const float* vecs;     // b1[128] b2[128] w3[128]
-  float b3;
-  const float* graph;    // [n_models][kMlpGraph]
+  const uint8_t* wimg;   // pre-swizzled bf16 W1 | W2 | W3 images (kWeightBytes)
+  const uint4* gpack;    // [n_models][5] graph features, packed bf16 (16-byte chunks)
   float* dbg;            // diagnostics: tile 0's raw accumulators (acc1 | acc2), or null
   int n_models;
 };
@@ -193,6 +215,29 @@ struct MlpWork {
   const int32_t* fallback;        // [n_fn] 1: no feasible point after kSearch
 };
 
+// TMEM accumulator row (128 fp32 columns) -> relu -> bf16 -> this row of the next layer's
+// SWIZZLE_128B K-major A operand (two 64-column panels); dbg: optional raw copy
+__device__ __forceinline__ void epilogue_relu_bf16(uint32_t taddr, uint8_t* Hs, int t,
+                                                   float* dbg) {
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    float v[32];
+    tmem_ld32(taddr + 32 * cc, v);
+    if (dbg != nullptr)
+      for (int e = 0; e < 32; ++e) dbg[t * kMlpH + 32 * cc + e] = v[e];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
+      const int col = 32 * cc + 8 * g;
+      uint4 u;
+      u.x = relu_bf16x2(v[8 * g + 0], v[8 * g + 1]);
+      u.y = relu_bf16x2(v[8 * g + 2], v[8 * g + 3]);
+      u.z = relu_bf16x2(v[8 * g + 4], v[8 * g + 5]);
+      u.w = relu_bf16x2(v[8 * g + 6], v[8 * g + 7]);
+      *reinterpret_cast<uint4*>(Hs + (col >> 6) * 16384 + sw128_offset(t, col & 63)) = u;
+    }
+  }
+}
+
 __device__ __forceinline__ void group_sync(int group) {
   asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(128) : "memory");
 }
@@ -206,12 +251,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
   const double* __restrict__ coords = W.coords;
   const int64_t n = MODE == kStream ? W.n : W.n_fn * W.tiles_per_fn * kMlpTile;
   extern __shared__ uint8_t mlp_smem_raw[];
-  __shared__ uint64_t bar_w, bar1[kMlpGroups], bar2[kMlpGroups];
+  __shared__ uint64_t bar_w, bar1[kMlpGroups], bar2[kMlpGroups], bar3[kMlpGroups];
   __shared__ uint32_t s_tmem;
   const uint32_t raw = (uint32_t)__cvta_generic_to_shared(mlp_smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   uint8_t* base = mlp_smem_raw + (sbase - raw);
-  float* vec = reinterpret_cast<float*>(base + kOffVec);
+  uint4* sgraph = reinterpret_cast<uint4*>(base + kOffVec);
   const int warp = threadIdx.x >> 5, group = warp >> 2;
   const int t = threadIdx.x & 127;  // row of the tile = TMEM lane
 
@@ -220,6 +265,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
     for (int g = 0; g < kMlpGroups; ++g) {
       mlp_bar_init(&bar1[g], 1);
       mlp_bar_init(&bar2[g], 1);
+      mlp_bar_init(&bar3[g], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -228,15 +274,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
                  ::"r"((uint32_t)__cvta_generic_to_shared(&s_tmem)), "r"(128 * kMlpGroups));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = threadIdx.x; i < 3 * kMlpH; i += blockDim.x) vec[i] = P.vecs[i];
-  // graph features: the stream's model, or every model (search rows pick their function's)
-  float* sgraph = vec + 3 * kMlpH;
+  // packed graph features: the stream's model, or every model (search rows pick theirs)
   if (MODE == kStream) {
-    for (int i = threadIdx.x; i < kMlpGraph; i += blockDim.x)
-      sgraph[i] = P.graph[int64_t(W.model) * kMlpGraph + i];
+    for (int i = threadIdx.x; i < int(kGraphChunks); i += blockDim.x)
+      sgraph[i] = P.gpack[int64_t(W.model) * kGraphChunks + i];
   } else {
-    for (int i = threadIdx.x; i < P.n_models * kMlpGraph; i += blockDim.x)
-      sgraph[i] = P.graph[i];
+    for (int i = threadIdx.x; i < P.n_models * int(kGraphChunks); i += blockDim.x)
+      sgraph[i] = P.gpack[i];
   }
   tc_fence_before();
   __syncthreads();
@@ -249,9 +293,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
   }
   mlp_bar_wait(&bar_w, 0);
 
-  const float* b1 = vec;
-  const float* b2 = vec + kMlpH;
-  const float* w3 = vec + 2 * kMlpH;
 
   const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;  // this warp's TMEM lanes
   uint8_t* Hs = base + kOffH + group * kGroupBytes;
@@ -271,7 +312,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
   uint32_t it = 0;
   for (; tile < tiles; tile += stride) {
     int64_t row = tile * kMlpTile + t;
-    const float* gf = sgraph;
+    const uint4* gf = sgraph;
     int64_t fn = 0;
     bool valid = row < n;
     int32_t bi = 0, si = 0, qv = 0;
@@ -297,25 +338,25 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
       cb = W.batches[bi];
       cs = W.sms[si];
       cq = double(qv);
-      gf = sgraph + W.model_of_fn[fn] * kMlpGraph;
+      gf = sgraph + W.model_of_fn[fn] * kGraphChunks;
     }
     // ---- feature assembly: row t of the A operand (64 bf16 = 8 swizzled chunks) ----
     {
-      float f[kMlpK0];
 #pragma unroll
-      for (int i = 0; i < kMlpGraph; ++i) f[i] = gf[i];
-      config_features(cb, cs, cq, f + kMlpGraph);
+      for (int c = 0; c < int(kGraphChunks); ++c)  // graph part: pre-packed copy
+        *reinterpret_cast<uint4*>(Hs + sw128_offset(t, 8 * c)) = gf[c];
+      float f[kMlpCfg];
+      config_features(cb, cs, cq, f);
 #pragma unroll
-      for (int i = kMlpGraph + kMlpCfg; i < kMlpK0; ++i) f[i] = 0.0f;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint4 v;
         v.x = pack_bf16(f[8 * c + 0], f[8 * c + 1]);
         v.y = pack_bf16(f[8 * c + 2], f[8 * c + 3]);
         v.z = pack_bf16(f[8 * c + 4], f[8 * c + 5]);
         v.w = pack_bf16(f[8 * c + 6], f[8 * c + 7]);
-        *reinterpret_cast<uint4*>(Hs + sw128_offset(t, 8 * c)) = v;  // X = panel 0
+        *reinterpret_cast<uint4*>(Hs + sw128_offset(t, kMlpGraph + 8 * c)) = v;
       }
+      *reinterpret_cast<uint4*>(Hs + sw128_offset(t, 56)) = make_uint4(0, 0, 0, 0);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
     tc_fence_before();
@@ -330,30 +371,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
     }
     mlp_bar_wait(&bar1[group], it & 1);
     tc_fence_after();
-    // ---- epilogue 1: h1 = relu(acc + b1) -> bf16 A operand of layer 2 ----
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      float v[32];
-      tmem_ld32(tmem + lane_base + 32 * cc, v);
-      if (P.dbg != nullptr && tile == 0)
-        for (int e = 0; e < 32; ++e) P.dbg[t * kMlpH + 32 * cc + e] = v[e];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
-        const int col = 32 * cc + 8 * g;
-        const float4 ba = *reinterpret_cast<const float4*>(b1 + col);      // broadcast
-        const float4 bb = *reinterpret_cast<const float4*>(b1 + col + 4);  // LDS.128
-        const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
-        float h[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) h[e] = fmaxf(v[8 * g + e] + bv[e], 0.0f);
-        uint4 u;
-        u.x = pack_bf16(h[0], h[1]);
-        u.y = pack_bf16(h[2], h[3]);
-        u.z = pack_bf16(h[4], h[5]);
-        u.w = pack_bf16(h[6], h[7]);
-        *reinterpret_cast<uint4*>(Hs + (col >> 6) * 16384 + sw128_offset(t, col & 63)) = u;
-      }
-    }
+    // ---- epilogue 1: h1 = relu(acc) -> bf16 A operand of layer 2 (bias: constant column) ----
+    epilogue_relu_bf16(tmem + lane_base, Hs, t, P.dbg != nullptr && tile == 0 ? P.dbg : nullptr);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     group_sync(group);
@@ -369,26 +388,29 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
     }
     mlp_bar_wait(&bar2[group], it & 1);
     tc_fence_after();
-    // ---- epilogue 2: lat = exp(min(relu(acc + b2) · w3 + b3, 80)) ----
-    {
-      float acc = 0.0f;
+    // ---- epilogue 2: h2 = relu(acc) -> bf16 A operand of layer 3 ----
+    epilogue_relu_bf16(tmem + lane_base, Hs, t,
+                       P.dbg != nullptr && tile == 0 ? P.dbg + kMlpTile * kMlpH : nullptr);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    group_sync(group);
+    tc_fence_after();
+    // ---- layer 3: acc[:, 0..15] = H2 · W3ᵀ (N = 16, column 0 = w3 . h2 incl. bias) ----
+    if (issuer) {
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        float v[32];
-        tmem_ld32(tmem + lane_base + 32 * cc, v);
-        if (P.dbg != nullptr && tile == 0)
-          for (int e = 0; e < 32; ++e) P.dbg[kMlpTile * kMlpH + t * kMlpH + 32 * cc + e] = v[e];
-#pragma unroll
-        for (int e4 = 0; e4 < 8; ++e4) {
-          const float4 bq = *reinterpret_cast<const float4*>(b2 + 32 * cc + 4 * e4);
-          const float4 wq = *reinterpret_cast<const float4*>(w3 + 32 * cc + 4 * e4);
-          acc = fmaf(fmaxf(v[4 * e4 + 0] + bq.x, 0.0f), wq.x, acc);
-          acc = fmaf(fmaxf(v[4 * e4 + 1] + bq.y, 0.0f), wq.y, acc);
-          acc = fmaf(fmaxf(v[4 * e4 + 2] + bq.z, 0.0f), wq.z, acc);
-          acc = fmaf(fmaxf(v[4 * e4 + 3] + bq.w, 0.0f), wq.w, acc);
-        }
+      for (int k = 0; k < kMlpH / 16; ++k) {
+        const uint32_t off = (k >> 2) * 16384 + 32 * (k & 3);
+        const uint32_t offw = (k >> 2) * kW3Panel + 32 * (k & 3);
+        umma_bf16(tmem, umma_desc(sH + off), umma_desc(sbase + kOffW3 + offw), k > 0,
+                  kIdesc16);
       }
-      const double lat = double(__expf(fminf(acc + P.b3, 80.0f)));
+      umma_commit(&bar3[group]);
+    }
+    mlp_bar_wait(&bar3[group], it & 1);
+    tc_fence_after();
+    {
+      const float acc = tmem_ld1(tmem + lane_base);
+      const double lat = double(__expf(fminf(acc, 80.0f)));
       if (MODE == kStream) {
         if (row < n) W.out[row] = lat;
       } else {
@@ -439,9 +461,7 @@ struct rapp_mlp {
   rapp_ctx* ctx = nullptr;
   int n_models = 0;
   uint8_t* d_wimg = nullptr;
-  float* d_vecs = nullptr;
-  float* d_graph = nullptr;
-  float b3 = 0.0f;
+  uint4* d_gpack = nullptr;
 };
 
 static uint16_t host_bf16(float x) {  // round to nearest even (finite inputs)
@@ -465,31 +485,46 @@ int rapp_mlp_create(rapp_ctx* ctx, int32_t n_models, const float* graph_features
   std::unique_ptr<rapp_mlp> m(new rapp_mlp());
   m->ctx = ctx;
   m->n_models = n_models;
-  m->b3 = b3;
-  // pre-swizzled BF16 images: W1 [128 n][64 k], W2 [128 n][128 k] as two 64-column panels
+  // effective weights: biases on the constant feature / unit, the constant units fed 1.0
+  std::vector<float> e1(size_t(kMlpH) * kMlpK0), e2(size_t(kMlpH) * kMlpH), e3(16 * kMlpH, 0.f);
+  for (int n = 0; n < kMlpH; ++n) {
+    for (int k = 0; k < kMlpK0; ++k) e1[n * kMlpK0 + k] = w1[n * kMlpK0 + k];
+    e1[n * kMlpK0 + kConstCol] = b1[n];
+    for (int k = 0; k < kMlpH; ++k) e2[n * kMlpH + k] = w2[n * kMlpH + k];
+    e2[n * kMlpH + kConstUnit] = b2[n];
+  }
+  for (int k = 0; k < kMlpK0; ++k) e1[kConstUnit * kMlpK0 + k] = k == kConstCol ? 1.f : 0.f;
+  for (int k = 0; k < kMlpH; ++k) e2[kConstUnit * kMlpH + k] = k == kConstUnit ? 1.f : 0.f;
+  for (int k = 0; k < kMlpH; ++k) e3[k] = w3[k];
+  e3[kConstUnit] = b3;
+  // pre-swizzled BF16 images: W1 [128 n][64 k]; W2 [128 n][128 k] and W3 [16 n][128 k] as
+  // two 64-column panels each
   std::vector<uint8_t> img(kWeightBytes, 0);
-  for (int nrow = 0; nrow < kMlpH; ++nrow)
+  for (int n = 0; n < kMlpH; ++n)
     for (int k = 0; k < kMlpK0; ++k) {
-      const uint16_t h = host_bf16(w1[nrow * kMlpK0 + k]);
-      std::memcpy(img.data() + sw128_offset(nrow, k), &h, 2);
+      const uint16_t h = host_bf16(e1[n * kMlpK0 + k]);
+      std::memcpy(img.data() + kOffW1 + sw128_offset(n, k), &h, 2);
     }
-  for (int nrow = 0; nrow < kMlpH; ++nrow)
+  for (int n = 0; n < kMlpH; ++n)
     for (int k = 0; k < kMlpH; ++k) {
-      const uint16_t h = host_bf16(w2[nrow * kMlpH + k]);
-      std::memcpy(img.data() + 16384 + (k >> 6) * 16384 + sw128_offset(nrow, k & 63), &h, 2);
+      const uint16_t h = host_bf16(e2[n * kMlpH + k]);
+      std::memcpy(img.data() + kOffW2 + (k >> 6) * 16384 + sw128_offset(n, k & 63), &h, 2);
     }
-  std::vector<float> vecs(3 * kMlpH);
-  std::memcpy(vecs.data(), b1, kMlpH * 4);
-  std::memcpy(vecs.data() + kMlpH, b2, kMlpH * 4);
-  std::memcpy(vecs.data() + 2 * kMlpH, w3, kMlpH * 4);
+  for (int n = 0; n < 16; ++n)
+    for (int k = 0; k < kMlpH; ++k) {
+      const uint16_t h = host_bf16(e3[n * kMlpH + k]);
+      std::memcpy(img.data() + kOffW3 + (k >> 6) * kW3Panel + sw128_offset(n, k & 63), &h, 2);
+    }
+  // graph features packed as BF16, 8 per 16-byte chunk
+  std::vector<uint16_t> gp(size_t(n_models) * kGraphChunks * 8, 0);
+  for (int mi = 0; mi < n_models; ++mi)
+    for (int i = 0; i < kMlpGraph; ++i)
+      gp[size_t(mi) * kGraphChunks * 8 + i] = host_bf16(graph_features[mi * kMlpGraph + i]);
   RAPP_CUDA(cudaSetDevice(ctx->device));
   RAPP_CUDA(cudaMalloc(&m->d_wimg, kWeightBytes));
-  RAPP_CUDA(cudaMalloc(&m->d_vecs, vecs.size() * 4));
-  RAPP_CUDA(cudaMalloc(&m->d_graph, size_t(n_models) * kMlpGraph * 4));
+  RAPP_CUDA(cudaMalloc(&m->d_gpack, gp.size() * 2));
   RAPP_CUDA(cudaMemcpy(m->d_wimg, img.data(), kWeightBytes, cudaMemcpyHostToDevice));
-  RAPP_CUDA(cudaMemcpy(m->d_vecs, vecs.data(), vecs.size() * 4, cudaMemcpyHostToDevice));
-  RAPP_CUDA(cudaMemcpy(m->d_graph, graph_features, size_t(n_models) * kMlpGraph * 4,
-                       cudaMemcpyHostToDevice));
+  RAPP_CUDA(cudaMemcpy(m->d_gpack, gp.data(), gp.size() * 2, cudaMemcpyHostToDevice));
   *out = m.release();
   return RAPP_OK;
 }
@@ -499,8 +534,7 @@ int rapp_mlp_destroy(rapp_mlp* m) {
   cudaSetDevice(m->ctx->device);
   cudaDeviceSynchronize();
   cudaFree(m->d_wimg);
-  cudaFree(m->d_vecs);
-  cudaFree(m->d_graph);
+  cudaFree(m->d_gpack);
   delete m;
   return RAPP_OK;
 }
@@ -516,7 +550,7 @@ static int mlp_run(rapp_mlp* m, const MlpWork& W, int64_t rows, float* d_dbg, vo
   const int64_t tiles = (rows + kMlpTile - 1) / kMlpTile;
   const int64_t blocks = std::max<int64_t>(
       1, std::min<int64_t>((tiles + kMlpGroups - 1) / kMlpGroups, int64_t(m->ctx->sm_count)));
-  MlpParams P{m->d_wimg, m->d_vecs, m->b3, m->d_graph, d_dbg, m->n_models};
+  MlpParams P{m->d_wimg, m->d_gpack, d_dbg, m->n_models};
   k_mlp<MODE><<<(unsigned)blocks, kMlpThreads, kMlpSmem, (cudaStream_t)stream>>>(P, W);
   RAPP_LAUNCHED();
   return RAPP_OK;

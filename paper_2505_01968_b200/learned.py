@@ -15,7 +15,9 @@ against a PyTorch fp32 forward of the same BF16 weights.
   feature row is written straight into the swizzled shared-memory A operand and the two
   hidden layers are `tcgen05.mma` GEMMs with TMEM accumulators.
 * Weights are random (seeded) — there is no trained model to load; the architecture, not
-  the accuracy, is what this component provides.
+  the accuracy, is what this component provides.  The biases ride on a constant input
+  feature and a constant hidden unit (127 real units + 1 per hidden layer), so all three
+  layers are tensor-core GEMMs with BF16 operands (`effective_weights`).
 """
 
 from __future__ import annotations
@@ -300,19 +302,35 @@ class LearnedPerfModel:
         return _ModelView(self, self.names.index(name))
 
     # -- the fp32 reference forward (test infrastructure for the parity-unpinned path) --
+    def effective_weights(self):
+        """The weights the kernel multiplies (rapp_mlp_create): biases on the constant
+        feature (55) / constant hidden unit (127), the constant units fed 1.0."""
+        w = self.weights
+        c_in, c_h = N_GRAPH + N_CFG - 1, HIDDEN - 1
+        e1 = w.w1.astype(np.float32).copy()
+        e1[:, c_in] = w.b1
+        e1[c_h, :] = 0.0
+        e1[c_h, c_in] = 1.0
+        e2 = w.w2.astype(np.float32).copy()
+        e2[:, c_h] = w.b2
+        e2[c_h, :] = 0.0
+        e2[c_h, c_h] = 1.0
+        e3 = w.w3.astype(np.float32).copy()
+        e3[c_h] = w.b3
+        return e1, e2, e3
+
     def reference_forward(self, model: int, coords: np.ndarray) -> np.ndarray:
+        """fp32 forward of the same BF16 operands (x, weights, h1, h2 rounded to BF16)."""
         import torch
         bf = torch.bfloat16
-        w = self.weights
+        e1, e2, e3 = (torch.from_numpy(a).to(bf).float() for a in self.effective_weights())
         x = np.zeros((len(coords), K0), dtype=np.float32)
         x[:, :N_GRAPH] = self.graph[model]
         x[:, N_GRAPH:N_GRAPH + N_CFG] = config_features_ref(coords)
         X = torch.from_numpy(x).to(bf).float()
-        W1 = torch.from_numpy(w.w1).to(bf).float()
-        W2 = torch.from_numpy(w.w2).to(bf).float()
-        h1 = torch.relu(X @ W1.T + torch.from_numpy(w.b1)).to(bf).float()
-        h2 = torch.relu(h1 @ W2.T + torch.from_numpy(w.b2))
-        y = h2 @ torch.from_numpy(w.w3) + w.b3
+        h1 = torch.relu(X @ e1.T).to(bf).float()
+        h2 = torch.relu(h1 @ e2.T).to(bf).float()
+        y = h2 @ e3
         return torch.exp(torch.clamp(y, max=80.0)).double().numpy()
 
 

@@ -25,8 +25,8 @@ x = np.zeros((n, 64), dtype=np.float32)
 x[:, :40] = lm.graph[0]
 x[:, 40:56] = learned.config_features_ref(c)
 X = torch.from_numpy(x).to(bf).float()
-W1 = torch.from_numpy(w.w1).to(bf).float()
-ref1 = (X @ W1.T).numpy()
+e1, e2, e3 = (torch.from_numpy(a).to(bf).float() for a in lm.effective_weights())
+ref1 = (X @ e1.T).numpy()
 print("acc1 vs ref1: max abs diff", np.abs(a[0] - ref1).max(), "ref scale", np.abs(ref1).max())
 print("acc1[0,:8]", a[0, 0, :8])
 print("ref1[0,:8]", ref1[0, :8])
@@ -35,8 +35,8 @@ print("ref1[9,:8]", ref1[9, :8])
 # does acc1 match a row/col permutation?
 for name, cand in (("transpose", ref1.T),):
     print(name, np.abs(a[0] - cand).max())
-h1 = torch.relu(torch.from_numpy(ref1) + torch.from_numpy(w.b1)).to(bf).float()
-ref2 = (h1 @ torch.from_numpy(w.w2).to(bf).float().T).numpy()
+h1 = torch.relu(torch.from_numpy(ref1)).to(bf).float()
+ref2 = (h1 @ e2.T).numpy()
 print("acc2 vs ref2: max abs diff", np.abs(a[1] - ref2).max(), "ref scale", np.abs(ref2).max())
 print("out[:8]", out[:8].cpu().numpy())
 print("ref[:8]", lm.reference_forward(0, c)[:8])
