@@ -28,6 +28,11 @@
 
 #include "rapp_internal.h"
 
+#ifndef RAPP_MLP_L3_MMA
+#define RAPP_MLP_L3_MMA 0  // 0: layer-3 dot product on the CUDA cores (faster: N=16 MMAs cost
+                           //    nearly as much tensor-pipe time as N=128 ones); 1: N=16 MMA
+#endif
+
 namespace rapp {
 
 constexpr int kMlpK0 = 64;      // input features (padded)
@@ -49,7 +54,7 @@ constexpr uint32_t kGroupBytes = 32768;
 constexpr uint32_t kOffVec = kOffH + kMlpGroups * kGroupBytes;  // packed graph features
 constexpr int kMlpMaxModels = 16;
 constexpr uint32_t kGraphChunks = 5;            // 40 bf16 = 5 x 16-byte chunks per model
-constexpr uint32_t kMlpSmem = kOffVec + kMlpMaxModels * kGraphChunks * 16 + 1024;
+constexpr uint32_t kMlpSmem = kOffVec + kMlpMaxModels * kGraphChunks * 16 + kMlpH * 4 + 1024;
 constexpr uint32_t kWeightBytes = 16384 + 32768 + 4096;
 constexpr int kConstCol = kMlpGraph + kMlpCfg - 1;  // feature 55 == 1.0 (carries layer 1's bias)
 constexpr int kConstUnit = kMlpH - 1;               // hidden unit 127 == 1.0
@@ -183,6 +188,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* src, uint32_
 }
 
 struct MlpParams {
+  const float* w3f;      // layer-3 weights incl. bias, BF16-rounded, as fp32 [128]
   const uint8_t* wimg;   // pre-swizzled bf16 W1 | W2 | W3 images (kWeightBytes)
   const uint4* gpack;    // [n_models][5] graph features, packed bf16 (16-byte chunks)
   float* dbg;            // diagnostics: tile 0's raw accumulators (acc1 | acc2), or null
@@ -281,6 +287,10 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
   } else {
     for (int i = threadIdx.x; i < P.n_models * int(kGraphChunks); i += blockDim.x)
       sgraph[i] = P.gpack[i];
+  }
+  {  // layer-3 weights as fp32 after the graph features (CUDA-core layer 3 variant)
+    float* w3s = reinterpret_cast<float*>(sgraph + kMlpMaxModels * kGraphChunks);
+    for (int i = threadIdx.x; i < kMlpH; i += blockDim.x) w3s[i] = P.w3f[i];
   }
   tc_fence_before();
   __syncthreads();
@@ -388,6 +398,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
     }
     mlp_bar_wait(&bar2[group], it & 1);
     tc_fence_after();
+#if RAPP_MLP_L3_MMA
     // ---- epilogue 2: h2 = relu(acc) -> bf16 A operand of layer 3 ----
     epilogue_relu_bf16(tmem + lane_base, Hs, t,
                        P.dbg != nullptr && tile == 0 ? P.dbg + kMlpTile * kMlpH : nullptr);
@@ -410,6 +421,23 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
     tc_fence_after();
     {
       const float acc = tmem_ld1(tmem + lane_base);
+#else
+    // ---- epilogue 2 + layer 3 on the CUDA cores: h2 = bf16(relu(acc)), acc3 = w3 . h2 ----
+    {
+      float acc = 0.0f;
+      const float* w3f = reinterpret_cast<const float*>(sgraph + kMlpMaxModels * kGraphChunks);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float v[32];
+        tmem_ld32(tmem + lane_base + 32 * cc, v);
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const uint32_t h = relu_bf16x2(v[e], v[e + 1]);
+          acc = fmaf(__uint_as_float(h << 16), w3f[32 * cc + e], acc);
+          acc = fmaf(__uint_as_float(h & 0xFFFF0000u), w3f[32 * cc + e + 1], acc);
+        }
+      }
+#endif
       const double lat = double(__expf(fminf(acc, 80.0f)));
       if (MODE == kStream) {
         if (row < n) W.out[row] = lat;
@@ -462,6 +490,7 @@ struct rapp_mlp {
   int n_models = 0;
   uint8_t* d_wimg = nullptr;
   uint4* d_gpack = nullptr;
+  float* d_w3f = nullptr;
 };
 
 static uint16_t host_bf16(float x) {  // round to nearest even (finite inputs)
@@ -525,6 +554,13 @@ int rapp_mlp_create(rapp_ctx* ctx, int32_t n_models, const float* graph_features
   RAPP_CUDA(cudaMalloc(&m->d_gpack, gp.size() * 2));
   RAPP_CUDA(cudaMemcpy(m->d_wimg, img.data(), kWeightBytes, cudaMemcpyHostToDevice));
   RAPP_CUDA(cudaMemcpy(m->d_gpack, gp.data(), gp.size() * 2, cudaMemcpyHostToDevice));
+  std::vector<float> w3f(kMlpH);
+  for (int k = 0; k < kMlpH; ++k) {
+    const uint32_t u = uint32_t(host_bf16(e3[k])) << 16;
+    std::memcpy(&w3f[k], &u, 4);
+  }
+  RAPP_CUDA(cudaMalloc(&m->d_w3f, kMlpH * 4));
+  RAPP_CUDA(cudaMemcpy(m->d_w3f, w3f.data(), kMlpH * 4, cudaMemcpyHostToDevice));
   *out = m.release();
   return RAPP_OK;
 }
@@ -535,6 +571,7 @@ int rapp_mlp_destroy(rapp_mlp* m) {
   cudaDeviceSynchronize();
   cudaFree(m->d_wimg);
   cudaFree(m->d_gpack);
+  cudaFree(m->d_w3f);
   delete m;
   return RAPP_OK;
 }
@@ -550,7 +587,7 @@ static int mlp_run(rapp_mlp* m, const MlpWork& W, int64_t rows, float* d_dbg, vo
   const int64_t tiles = (rows + kMlpTile - 1) / kMlpTile;
   const int64_t blocks = std::max<int64_t>(
       1, std::min<int64_t>((tiles + kMlpGroups - 1) / kMlpGroups, int64_t(m->ctx->sm_count)));
-  MlpParams P{m->d_wimg, m->d_gpack, d_dbg, m->n_models};
+  MlpParams P{m->d_w3f, m->d_wimg, m->d_gpack, d_dbg, m->n_models};
   k_mlp<MODE><<<(unsigned)blocks, kMlpThreads, kMlpSmem, (cudaStream_t)stream>>>(P, W);
   RAPP_LAUNCHED();
   return RAPP_OK;
