@@ -7,9 +7,10 @@
 //   h1  = relu(W1 x)        127 units + a constant-1 unit                         (128)
 //   h2  = relu(W2 h1)       127 units + a constant-1 unit                         (128)
 //   lat = exp(min(w3 . h2, 80))
-// Biases ride on the constant units (column 55 of W1, column 127 of W2 and w3), so every
-// layer is one GEMM: tcgen05.mma kind::f16, BF16 operands (weights, x, h1, h2), FP32
-// accumulators in TMEM; layer 3 is an N=16 MMA of which column 0 is used.
+// Biases ride on the constant units (column 55 of W1, column 127 of W2 and w3), so each
+// hidden layer is one GEMM: tcgen05.mma kind::f16, BF16 operands (weights, x, h1), FP32
+// accumulators in TMEM; the output dot product over the BF16 h2 runs on the CUDA cores in
+// the layer-2 epilogue (RAPP_MLP_L3_MMA=1 runs it as an N=16 MMA instead).
 //
 // One persistent CTA per SM runs 4 independent 4-warp groups, each on its own 128-row
 // tiles, so one group's epilogue overlaps the others' MMAs.  Per tile: every thread writes
