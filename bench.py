@@ -723,12 +723,16 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False, nfn=1000, ng
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(total)]
     launches0 = _lib.launch_count()
-    for k in range(total):
-        evs[k][0].record(stream)
-        _lib.check(lib.rapp_tick_run_dev(eng._h, interval_ms * (k + 1), d_arr[k].data_ptr(),
-                                         d_idle.data_ptr(), stream.cuda_stream))
-        evs[k][1].record(stream)
-        torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        clk.mark_start()
+        for k in range(total):
+            evs[k][0].record(stream)
+            _lib.check(lib.rapp_tick_run_dev(eng._h, interval_ms * (k + 1),
+                                             d_arr[k].data_ptr(), d_idle.data_ptr(),
+                                             stream.cuda_stream))
+            evs[k][1].record(stream)
+            torch.cuda.synchronize()
+        clk.mark_end()
     launches = (_lib.launch_count() - launches0) // total
     dev_us = [evs[k][0].elapsed_time(evs[k][1]) * 1000.0 for k in range(warmup, total)]
     # end-to-end through the public host API (each tick: H2D inputs, kernels, D2H results)
@@ -750,7 +754,7 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False, nfn=1000, ng
             "device_us_median": float(np.median(dev_us)), "device_us_max": float(np.max(dev_us)),
             "e2e_us_median": float(np.median(e2e_us)), "e2e_us_max": float(np.max(e2e_us)),
             "actions_per_tick_mean": float(np.mean(acts)), "launches_per_tick": int(launches),
-            "world_build_s": round(build_s, 3),
+            "world_build_s": round(build_s, 3), "clocks": clk.summary(),
             "e2e_api": "TickEngine.tick (rapp_tick_run: H2D arrivals+idle, D2H actions+rates)"}
 
 
@@ -953,7 +957,8 @@ def main():
                             "h2d_bytes_per_step": 1000 * 8 + 1000,
                             "d2h_bytes_per_step": "actions (32 B each) + 2 x 8 KB rates"},
                     "tick": tick, "cpu_baseline": tick_cpu_baseline(args),
-                    "gpu_launches": tick["launches_per_tick"] * tick["ticks"], "impl": "ours"}
+                    "gpu_launches": tick["launches_per_tick"] * tick["ticks"],
+                    "clocks": tick["clocks"], "impl": "ours"}
             print(json.dumps(line))
         return
     if args.workload == "mlp":
