@@ -1869,6 +1869,7 @@ int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
     return RAPP_E_ARG;
   }
   if (n == 0) return RAPP_OK;
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
   RAPP_CUDA(cudaSetDevice(t->ctx->device));
   int64_t known = t->h_npods;
   if (known < 0) {

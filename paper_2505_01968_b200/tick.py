@@ -237,13 +237,22 @@ class TickEngine:
 
     # -- host events between ticks ---------------------------------------------------------
 
+    def _pod_index(self) -> dict:
+        """pod id -> device pod index, extended incrementally as ticks create pods."""
+        idx = getattr(self, "_index", None)
+        if idx is None:
+            idx = self._index = {}
+        for i in range(len(idx), len(self.pod_ids)):
+            idx[self.pod_ids[i]] = i
+        return idx
+
     def release(self, pod_ids, *, apply_to_host: bool = False) -> None:
         """Pods the simulator released since the last tick (DRAINING pods whose last request
         completed, hs/sim.py:424-438), in release order."""
         ids = list(pod_ids)
         if not ids:
             return
-        index = {pid: i for i, pid in enumerate(self.pod_ids)}
+        index = self._pod_index()
         try:
             idx = np.array([index[pid] for pid in ids], dtype=np.int64)
         except KeyError as exc:
