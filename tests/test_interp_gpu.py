@@ -263,3 +263,31 @@ def test_config2_stream_large_vs_oracle():
         c = bench.gen_queries(b, s, q, 6_000_000, 77 + mi, dev)
         got = t.predict_latency_many(c).cpu().numpy()
         assert same_bits(got, or_interp3_many(b, s, q, v, c.cpu().numpy())), name
+
+
+def test_stateless_table_cache_alternating_tables(kern):
+    """The stateless entry points keep the last 8 distinct tables resident (exact content
+    match): 12 tables of different shapes, called in an interleaved order with evictions,
+    in-place segment reuse and tables that differ in one value only, stay bit-exact."""
+    rng = np.random.default_rng(21)
+    tables = []
+    for i in range(12):
+        nb, ns, nq = (3 + i % 4, 5 + (i * 7) % 11, 4 + (i * 5) % 9)
+        b = np.cumsum(rng.uniform(0.5, 3.0, nb))
+        s = np.cumsum(rng.uniform(1.0, 9.0, ns))
+        q = np.cumsum(rng.uniform(1.0, 9.0, nq))
+        v = rng.uniform(1.0, 100.0, (nb, ns, nq))
+        tables.append((b, s, q, v))
+    b0, s0, q0, v0 = tables[0]
+    v1 = v0.copy()
+    v1[1, 2, 3] = np.nextafter(v1[1, 2, 3], np.inf)  # one ulp apart: a different table
+    tables.append((b0, s0, q0, v1))
+    order = [0, 1, 2, 3, 0, 12, 4, 5, 6, 7, 8, 9, 0, 10, 11, 12, 3, 1, 0, 12]
+    for k in order:
+        b, s, q, v = tables[k]
+        c = np.column_stack([rng.uniform(b[0] - 1, b[-1] + 1, 3000),
+                             rng.uniform(s[0] - 1, s[-1] + 1, 3000),
+                             rng.uniform(q[0] - 1, q[-1] + 1, 3000)])
+        out = np.empty(len(c))
+        kern.interp3_many(b, s, q, v, c, out)
+        assert same_bits(out, or_interp3_many(b, s, q, v, c)), k
