@@ -582,18 +582,20 @@ def run_mlp(args, rank, world, local, n_per_model=None):
     # e2e through the host API (pageable numpy in and out)
     e2e = None
     if not args.no_e2e:
-        ne = 4_000_000
-        hc = coords[0][:ne].cpu().numpy()
-        lm.predict_many(0, hc)
+        ne = 25_000_000
+        hc = coords[0][:ne].cpu().pin_memory()
+        ho = torch.empty(ne, dtype=torch.float64).pin_memory()
+        lm.predict_many(0, hc.numpy(), ho.numpy())
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = 3
         for _ in range(reps):
-            lm.predict_many(0, hc)
+            lm.predict_many(0, hc.numpy(), ho.numpy())
         dt = time.perf_counter() - t0
         e2e = {"value": ne * reps / dt, "unit": UNIT, "h2d_bytes_per_step": ne * 24,
                "d2h_bytes_per_step": ne * 8, "steps": reps,
-               "api": "learned.LearnedPerfModel.predict_many (host arrays)"}
+               "api": "learned.LearnedPerfModel.predict_many (C ABI rapp_mlp_predict_host, "
+                      "pinned host buffers)"}
     # CPU baseline: the same forward (fp32, torch on the host cores) on a bounded sample
     import torch as _t
     sample = coords[0][:200_000].cpu().numpy()

@@ -263,6 +263,9 @@ int rapp_mlp_destroy(rapp_mlp *mlp);
 /* d_coords (n,3) float64 rows of one model -> d_out (n) float64 latency; tcgen05 GEMMs. */
 int rapp_mlp_predict_dev(rapp_mlp *mlp, int32_t model, const double *d_coords, int64_t n,
                          double *d_out, void *stream);
+/* Same over host buffers through the chunked copy-in / kernel / copy-out pipeline. */
+int rapp_mlp_predict_host(rapp_mlp *mlp, int32_t model, const double *coords, int64_t n,
+                          double *out);
 /* most_efficient_config over the learned predictions (hs/perf.py:104-145 semantics): for
  * function f (model d_model_of_fn[f]) the lattice batches x sms x range(step, 101, step);
  * rps = b / (latency / 1000.0) in FP64; d_keys[f] = the packed min (s*q, s_idx, q, b_idx) key

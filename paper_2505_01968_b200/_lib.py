@@ -83,6 +83,8 @@ SIGNATURES = [
     ("rapp_mlp_destroy", ctypes.c_int, [c_vp]),
     ("rapp_mlp_predict_dev", ctypes.c_int, [c_vp, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp,
                                             c_vp]),
+    ("rapp_mlp_predict_host", ctypes.c_int, [c_vp, ctypes.c_int32, c_dp, ctypes.c_int64,
+                                             c_dp]),
     ("rapp_mlp_search_dev", ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, c_vp, ctypes.c_int32,
                                            c_vp, ctypes.c_int32, c_vp, ctypes.c_int32, c_vp,
                                            c_vp, c_vp]),

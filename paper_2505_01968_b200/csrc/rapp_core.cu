@@ -4,6 +4,7 @@
 // Reference: hs/_kernels/_grid_cy.pyx (paths relative to /root/reference/pkg/src/hybridscale).
 #include <cstdarg>
 #include <cstring>
+#include <functional>
 #include <memory>
 
 #include "rapp_device.cuh"
@@ -270,8 +271,10 @@ static bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-static int interp_host(rapp_ctx* ctx, int32_t table_id, const double* coords, int64_t n,
-                       double* out) {
+// Chunked host pipeline: copy-in / device step / copy-out of successive chunks overlap on
+// kDepth streams; `launch(d_in, rows, d_out, stream)` runs the device step of one chunk.
+int pipe_run(rapp_ctx* ctx, const double* coords, int64_t n, double* out,
+             const std::function<int(const double*, int64_t, double*, cudaStream_t)>& launch) {
   if (n <= 0) return RAPP_OK;
   constexpr int64_t kChunk = int64_t(1) << 21;  // rows per stage (48 MiB in, 16 MiB out)
   const int64_t chunk = n < kChunk ? n : kChunk;
@@ -305,7 +308,7 @@ static int interp_host(rapp_ctx* ctx, int32_t table_id, const double* coords, in
       src = p.h_in[k];
     }
     RAPP_CUDA(cudaMemcpyAsync(p.d_in[k], src, (size_t)rn * 24, cudaMemcpyHostToDevice, st));
-    if ((rc = launch_interp(ctx, table_id, p.d_in[k], rn, p.d_out[k], nullptr, st))) return rc;
+    if ((rc = launch(p.d_in[k], rn, p.d_out[k], st))) return rc;
     double* dst = pin_out ? out + r0 : p.h_out[k];
     RAPP_CUDA(cudaMemcpyAsync(dst, p.d_out[k], (size_t)rn * 8, cudaMemcpyDeviceToHost, st));
     RAPP_CUDA(cudaEventRecord(p.done[k], st));
@@ -314,6 +317,14 @@ static int interp_host(rapp_ctx* ctx, int32_t table_id, const double* coords, in
   for (int k = 0; k < HostPipe::kDepth; ++k)
     if ((rc = drain(k))) return rc;
   return RAPP_OK;
+}
+
+static int interp_host(rapp_ctx* ctx, int32_t table_id, const double* coords, int64_t n,
+                       double* out) {
+  return pipe_run(ctx, coords, n, out,
+                  [&](const double* d_in, int64_t rows, double* d_out, cudaStream_t st) {
+                    return launch_interp(ctx, table_id, d_in, rows, d_out, nullptr, st);
+                  });
 }
 
 static std::mutex g_default_mu;

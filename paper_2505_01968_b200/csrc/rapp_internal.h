@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -112,6 +113,9 @@ int table_put(rapp_ctx* ctx, int64_t nb, int64_t ns, int64_t nq, const double* b
 // The per-device default context used by the stateless entry points.
 int default_ctx(rapp_ctx** out);
 int ensure_pipe(rapp_ctx* ctx, int64_t rows);
+// chunked, stream-overlapped host->device->host pipeline over (n,3) coords -> (n) out
+int pipe_run(rapp_ctx* ctx, const double* coords, int64_t n, double* out,
+             const std::function<int(const double*, int64_t, double*, cudaStream_t)>& launch);
 // fast-path extras layout (doubles, see rapp_stream.cu):
 //   [params 3 x 8][lut_b|lut_s|lut_q int32 x kLut each][iv_b|iv_s|iv_q (2n each)][pad][cells]
 struct FastLayout {

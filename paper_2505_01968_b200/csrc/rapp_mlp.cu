@@ -635,6 +635,20 @@ int rapp_mlp_predict_dev(rapp_mlp* m, int32_t model, const double* d_coords, int
   return mlp_launch(m, model, d_coords, n, d_out, nullptr, stream);
 }
 
+int rapp_mlp_predict_host(rapp_mlp* m, int32_t model, const double* coords, int64_t n,
+                          double* out) {
+  if (!m || model < 0 || model >= m->n_models || n < 0 || (n > 0 && (!coords || !out))) {
+    set_error("bad mlp handle, model id or buffers");
+    return RAPP_E_ARG;
+  }
+  std::lock_guard<std::mutex> lk(m->ctx->mu);
+  RAPP_CUDA(cudaSetDevice(m->ctx->device));
+  return pipe_run(m->ctx, coords, n, out,
+                  [&](const double* d_in, int64_t rows, double* d_out, cudaStream_t st) {
+                    return mlp_launch(m, model, d_in, rows, d_out, nullptr, st);
+                  });
+}
+
 int rapp_mlp_debug_dev(rapp_mlp* m, int32_t model, const double* d_coords, int64_t n,
                        double* d_out, float* d_acc, void* stream) {
   return mlp_launch(m, model, d_coords, n, d_out, d_acc, stream);

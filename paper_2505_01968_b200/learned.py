@@ -250,13 +250,15 @@ class LearnedPerfModel:
                                                     stream), "predict")
         return out
 
-    def predict_many(self, model: int, coords: np.ndarray) -> np.ndarray:
-        import torch
-        dev = torch.device("cuda", self.ctx.device)
-        c = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.float64)).to(dev)
-        out = torch.empty(c.shape[0], dtype=torch.float64, device=dev)
-        self.predict_many_dev(model, c, out)
-        return out.cpu().numpy()
+    def predict_many(self, model: int, coords: np.ndarray, out=None) -> np.ndarray:
+        """Host API: (n, 3) float64 -> (n) latency ms through the chunked, stream-overlapped
+        copy-in / kernel / copy-out pipeline (page-locked buffers are DMA'd directly)."""
+        c = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 3)
+        if out is None:
+            out = np.empty(c.shape[0], dtype=np.float64)
+        _lib.check(_lib.load().rapp_mlp_predict_host(self._h, int(model), _lib.dptr(c),
+                                                     c.shape[0], _lib.dptr(out)), "predict")
+        return out
 
     def search_dev(self, model_of_fn, targets, batches, sms, quota_step: int = 10, *,
                    stream=None):
