@@ -997,6 +997,7 @@ def main():
     if world == 1 and args.workload == "stream" and not args.no_extra:
         # the second half of the metric ("scaling decisions/tick latency") and config 5
         extra = {"tick_config4": run_tick(args, local, ticks=20),
+                 "tick_config4_full_grid": run_tick(args, local, ticks=10, full_grid=True),
                  "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64),
                  "replay_config3": run_replay(args, local)}
         extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
