@@ -1,11 +1,4 @@
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_mlp -s 1 -c 1 -o gpurun_out/prof_mlp_r01e python -c "
-import sys; sys.path.insert(0,'.')
-import torch
-from paper_2505_01968_b200 import learned
-lm = learned.LearnedPerfModel.zoo()
-n = 20_000_000
-c = torch.rand((n,3), dtype=torch.float64, device='cuda') * torch.tensor([31.,99.,99.], dtype=torch.float64, device='cuda') + 1
-o = torch.empty(n, dtype=torch.float64, device='cuda')
-for _ in range(2): lm.predict_many_dev(0, c, o)
-torch.cuda.synchronize()
-" > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_tick_gpu.py -x -q 2>&1 | tail -2
+echo "== full"; TICKS=8 timeout 300 python tools/tick_profile.py --full-grid 2>&1 | awk '{print $6}' | tr '\n' ' '; echo
+echo "== cfg4"; TICKS=8 timeout 300 python tools/tick_profile.py 2>&1 | awk '{print $6}' | tr '\n' ' '; echo
+TICKS=2 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_tick -c 20 --csv --log-file gpurun_out/ncu_tick_side.csv python tools/tick_profile.py > gpurun_out/ncu_tick_side.log 2>&1; echo "ncu rc=$?"; tail -3 gpurun_out/ncu_tick_side.log
