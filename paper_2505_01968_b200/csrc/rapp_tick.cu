@@ -590,13 +590,15 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
     const double ts = s_ts[si], tq = s_tq[qi];
     const int o00 = j.x * td.nq + k.x, o01 = j.x * td.nq + k.y;
     const int o10 = j.y * td.nq + k.x, o11 = j.y * td.nq + k.y;
-    // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch
-    const double c00 = lerp_rn(v0[o00], v0[o01], tq);
-    const double c01 = lerp_rn(v0[o10], v0[o11], tq);
-    const double c10 = lerp_rn(v1[o00], v1[o01], tq);
-    const double c11 = lerp_rn(v1[o10], v1[o11], tq);
+    // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch.  The
+    // table reads and the grid writes are streaming (evict-first) so this pass does not
+    // push the commit's working set (phase A outputs, cluster state) out of L2.
+    const double c00 = lerp_rn(__ldcs(v0 + o00), __ldcs(v0 + o01), tq);
+    const double c01 = lerp_rn(__ldcs(v0 + o10), __ldcs(v0 + o11), tq);
+    const double c10 = lerp_rn(__ldcs(v1 + o00), __ldcs(v1 + o01), tq);
+    const double c11 = lerp_rn(__ldcs(v1 + o10), __ldcs(v1 + o11), tq);
     const double lat = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
-    w.tgrid[(int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1] = throughput(bb, lat);
+    __stcs(w.tgrid + (int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1, throughput(bb, lat));
   }
 }
 
