@@ -161,6 +161,22 @@ __device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
   return !(x < ba[0] || x > ba[td.nb - 1]);  // hs/perf.py:88-91
 }
 
+#ifdef RAPP_TICK_PROF
+// diagnostics build only: cycles of the commit's parts, summed over ticks (lane 0)
+__device__ unsigned long long g_tick_prof[8];
+__shared__ unsigned long long s_tprof[8];  // per-launch accumulators, flushed at the end
+#define TPROF_T0() long long _tp0 = clock64()
+#define TPROF_ACC(i)                                                   \
+  do {                                                                 \
+    const long long _tp1 = clock64();                                  \
+    if ((threadIdx.x & 31) == 0) s_tprof[i] += (unsigned long long)(_tp1 - _tp0); \
+    _tp0 = _tp1;                                                       \
+  } while (0)
+#else
+#define TPROF_T0() (void)0
+#define TPROF_ACC(i) (void)0
+#endif
+
 __device__ void set_err(const World& w, int code, int f) {
   if (atomicCAS(w.err, 0, code) == 0) *w.err_fn = f;
 }
@@ -973,7 +989,9 @@ struct Commit {
     uint32_t uid0;
   };
 
-  __device__ Pre prefetch(int f) const {
+  __device__ Pre prefetch(int f) const { return prefetch_of(w, f); }
+
+  __device__ static Pre prefetch_of(const World& w, int f) {
     Pre r{};
     r.p0 = -1;
     if (f >= w.F) return r;
@@ -1040,6 +1058,7 @@ struct Commit {
 
   // srow0: the function's first-pod quota row staged in shared memory (see k_tick_commit)
   __device__ void scale_up(int f, double now, const Pre& pre, const double* srow0) const {
+    TPROF_T0();
     const int d = w.delta;
     double gap = pre.gap0;
     const int m = pre.m;
@@ -1056,6 +1075,7 @@ struct Commit {
       const int pos = find_part(g, j == 0 ? pre.uid0 : w.p_puid[p]);
       const int q0 = j == 0 ? pre.q0 : w.p_q[p];
       const int avail = q0 + (100 - part_alloc(parts(g)[pos]));
+      TPROF_ACC(5);  // headroom lookup
       int kstar = -1;
       double gain = 0.0;
       const int sav = j == 0 ? pre.sav0 : w.spec_avail[f * kMaxPods + j];
@@ -1096,6 +1116,7 @@ struct Commit {
           }
         }
       }
+      TPROF_ACC(1);  // spec check / re-walk
       if (kstar > 0) {
         const int nq = q0 + kstar * d;
         const int s = j == 0 ? pre.s0 : w.p_s[p];
@@ -1103,7 +1124,9 @@ struct Commit {
         emit(f, kVUp, j == 0 ? pre.b0 : w.p_b[p], s, nq, p, g, 0);
         gap = __dsub_rn(gap, gain);
       }
+      TPROF_ACC(7);  // change_quota + emit
     }
+    TPROF_ACC(1);
     const int bref = pre.bref;
     // one pod on the used GPU with the lowest occupancy (autoscaler.py:137-152)
     if (gap > 0.0) {
@@ -1162,6 +1185,7 @@ struct Commit {
         }
       }
     }
+    TPROF_ACC(2);  // used-GPU branch
     // one pod on a fresh GPU at the most cost-efficient configuration (autoscaler.py:155-165)
     if (gap > 0.0) {
       const int g = first_free();
@@ -1174,6 +1198,7 @@ struct Commit {
         emit(f, kHUp, b, s, q, p, g, 0);
       }
     }
+    TPROF_ACC(3);  // fresh-GPU branch
   }
 
   // check_placement (allocator.py:63-82) == nullptr: a joinable same-sm partition with
@@ -1227,6 +1252,7 @@ struct Commit {
   }
 
   __device__ void scale_down(int f, double now, const Pre& pre) const {
+    TPROF_T0();
     const int na = pre.nd;
     const DownAct* acts = w.down + f * kMaxPods;
     for (int i = 0; i < na; ++i) {
@@ -1266,6 +1292,7 @@ struct Commit {
     }
     if (lane == 0 && pre.stamp) w.last_down[f] = now;
     __syncwarp();
+    TPROF_ACC(4);
   }
 };
 
@@ -1273,7 +1300,9 @@ struct Commit {
 // next partition uid) live in shared memory for the whole tick when they fit: the
 // used-GPU argmin and the first-free scan then read shared memory only.  Function classes
 // are fetched 32 at a time and only active functions are visited, in sorted order.
-__global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int smem_g, int ps) {
+constexpr int kPreDepth = 4;  // batches of function headers the helper warp runs ahead
+
+__global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int smem_g, int ps) {
   // dynamic shared layout: [row staging 2 x 32 x kRowStage doubles][5*G summaries]
   //                        [partition cache G*ps uint64 (8-aligned)][ovf G bytes]
   extern __shared__ __align__(16) int32_t smem_dyn[];
@@ -1281,6 +1310,37 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
   int32_t* sg = smem_dyn + 2 * 32 * kRowStage * 2;
   __shared__ int s_nact;
   const int lane = threadIdx.x & 31;
+  // Warp 1 is a helper: it reads the headers of the next kPreDepth batches of 32 functions
+  // (each function's own phase-A outputs and first pod — nothing an earlier function of the
+  // tick can change) into a shared ring while warp 0 commits, so warp 0 never waits on
+  // those dependent global loads.
+  __shared__ Commit::Pre s_pre[kPreDepth][32];
+  __shared__ int s_pcls[kPreDepth][32];
+  __shared__ volatile int s_ready[kPreDepth];
+  __shared__ volatile int s_done, s_stop;
+  if (threadIdx.x < kPreDepth) s_ready[threadIdx.x] = -1;
+  if (threadIdx.x == 0) {
+    s_done = -1;
+    s_stop = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    for (int b = 0, base = 0; base < w.F; ++b, base += 32) {
+      const int slot = b % kPreDepth;
+      while (s_done < b - kPreDepth) {  // the slot is free once batch b - depth is done
+        if (s_stop) return;
+        __nanosleep(32);
+      }
+      if (s_stop) return;
+      const int f = base + lane;
+      s_pcls[slot][lane] = f < w.F ? w.cls[f] : kNone;
+      s_pre[slot][lane] = Commit::prefetch_of(w, f);
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) s_ready[slot] = b;
+    }
+    return;
+  }
   World v = w;
   const int G = w.G;
   // shared layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)][ovf G bytes]
@@ -1320,6 +1380,10 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
   __syncwarp();
   Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter};
   bool stop = s_err != 0;
+#ifdef RAPP_TICK_PROF
+  if (lane < 8) s_tprof[lane] = 0;
+  __syncwarp();
+#endif
   // First-pod quota rows of the scale-up functions of a batch of 32 are bulk-copied into
   // shared memory one batch ahead (double buffer), so a vertical walk that has to be
   // redone (its partition's headroom changed since phase A) reads shared memory.
@@ -1339,33 +1403,38 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
       tk_bulk(s_rows + (buf * 32 + lane) * kRowStage, w.rows + int64_t(b0 + lane) * kMaxPods * kRow,
               kRowStage * 8u, &s_rbar[buf]);
   };
-  int cls_cur = lane < w.F ? w.cls[lane] : kNone;
   int cls_nxt = 32 + lane < w.F ? w.cls[32 + lane] : kNone;
-  if (!stop) stage(0, cls_cur, 0);
+  if (!stop) stage(0, lane < w.F ? w.cls[lane] : kNone, 0);
   int staged = 1;  // batches whose copies were issued
   int j = 0;
+  TPROF_T0();
   for (int base = 0; base < w.F && !stop; base += 32, ++j) {
-    const int mine = cls_cur;
-    const Commit::Pre pre = c.prefetch(base + lane);
+    TPROF_ACC(6);  // (the functions of the previous batch, accounted separately)
+    const int slot = j % kPreDepth;
+    while (s_ready[slot] != j) {
+    }
+    __threadfence_block();
+    const int mine = s_pcls[slot][lane];
     if (base + 32 < w.F) {
       stage(base + 32, cls_nxt, (j + 1) & 1);
       ++staged;
     }
-    cls_cur = cls_nxt;
     cls_nxt = base + 64 + lane < w.F ? w.cls[base + 64 + lane] : kNone;
     tk_bar_wait(&s_rbar[j & 1], (j >> 1) & 1);
+    TPROF_ACC(0);  // waits for the header ring and the staged rows
     unsigned act = __ballot_sync(0xffffffffu, mine != kNone);
     while (act) {
       const int i = __ffs(act) - 1;
       act &= act - 1;
       const int cls = __shfl_sync(0xffffffffu, mine, i);
+      const Commit::Pre& pre = s_pre[slot][i];
       if (cls == kUp) {
         if (w.policy == 0)
-          c.scale_up(base + i, now, Commit::bcast(pre, i), s_rows + ((j & 1) * 32 + i) * kRowStage);
+          c.scale_up(base + i, now, pre, s_rows + ((j & 1) * 32 + i) * kRowStage);
         else
           c.replica_up(base + i, now);
       } else {
-        c.scale_down(base + i, now, Commit::bcast(pre, i));
+        c.scale_down(base + i, now, pre);
       }
       __syncwarp();
       if (s_err) {
@@ -1373,9 +1442,16 @@ __global__ void __launch_bounds__(32) k_tick_commit(World w, double now, int sme
         break;
       }
     }
+    __syncwarp();
+    if (lane == 0) s_done = j;
   }
+  if (lane == 0) s_stop = 1;  // release the helper if the commit stopped early
   // no bulk copy may still be in flight into shared memory when the CTA exits
   for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
+#ifdef RAPP_TICK_PROF
+  __syncwarp();
+  if (lane < 8) g_tick_prof[lane] += s_tprof[lane];
+#endif
   if (lane == 0) {
     *w.n_pods = s_npods;
     *w.counter = s_counter;
@@ -1550,7 +1626,7 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     RAPP_LAUNCHED();
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
-    const size_t budget = 160 * 1024;  // + the row staging below
+    const size_t budget = 150 * 1024;  // + the row staging below and ~12 KB static
     const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
     const int smem_g = gbytes + size_t(w.G) <= budget ? 1 : 0;
     int ps = 0;
@@ -1560,7 +1636,7 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
                          size_t(w.G) + 16;
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
-    k_tick_commit<<<1, 32, bytes, st>>>(w, now, smem_g, ps);
+    k_tick_commit<<<1, 64, bytes, st>>>(w, now, smem_g, ps);
     RAPP_LAUNCHED();
   }
   return RAPP_OK;
@@ -2131,5 +2207,17 @@ int rapp_tick_counter(rapp_tick* t, int64_t* c) {
   RAPP_CUDA(cudaMemcpy(c, t->w.counter, 8, cudaMemcpyDeviceToHost));
   return RAPP_OK;
 }
+
+#ifdef RAPP_TICK_PROF
+int rapp_tick_prof_read(uint64_t* out8, int reset) {
+  RAPP_CUDA(cudaDeviceSynchronize());
+  RAPP_CUDA(cudaMemcpyFromSymbol(out8, g_tick_prof, 64));
+  if (reset) {
+    uint64_t z[8] = {};
+    RAPP_CUDA(cudaMemcpyToSymbol(g_tick_prof, z, 64));
+  }
+  return RAPP_OK;
+}
+#endif
 
 }  // extern "C"
