@@ -118,6 +118,9 @@ struct World {
   int32_t* p_state;
   double* p_ready;
   PodId* p_id;
+  int64_t* p_ctr;                // pod-%06d counter of a pod the commit created whose id is
+                                 // not formatted yet (-1: formatted) — formatted off the
+                                 // commit's critical path (next prologue / before reads)
   const uint8_t* p_idle;         // per tick input
   int64_t* counter;              // next pod-%06d counter
   // phase A / A2 outputs
@@ -163,8 +166,8 @@ __device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
 
 #ifdef RAPP_TICK_PROF
 // diagnostics build only: cycles of the commit's parts, summed over ticks (lane 0)
-__device__ unsigned long long g_tick_prof[8];
-__shared__ unsigned long long s_tprof[8];  // per-launch accumulators, flushed at the end
+__device__ unsigned long long g_tick_prof[16];
+__shared__ unsigned long long s_tprof[16];  // per-launch accumulators, flushed at the end
 #define TPROF_T0() long long _tp0 = clock64()
 #define TPROF_ACC(i)                                                   \
   do {                                                                 \
@@ -185,10 +188,46 @@ __device__ void set_err(const World& w, int code, int f) {
 // prologue: cold starts that ended at or before `now` (ready events precede the scaler
 // event at equal timestamps, sim.py:40-44), output reset
 // ---------------------------------------------------------------------------------------
-__global__ void k_tick_prologue(World w, double now) {
+// "pod-%06d" (sim.py:337-340), big-endian packed so integer order is byte-string order
+__device__ __forceinline__ PodId format_pod_id(long long c) {
+  char buf[32] = {'p', 'o', 'd', '-'};
+  int nd = 1;
+  for (unsigned long long v = (unsigned long long)c / 10ull; v; v /= 10ull) ++nd;
+  const int width = nd > 6 ? nd : 6;
+  unsigned long long v = (unsigned long long)c;
+  for (int i = width - 1; i >= 0; --i) {
+    buf[4 + i] = char('0' + v % 10ull);
+    v /= 10ull;
+  }
+  PodId id;
+  for (int i = 0; i < 4; ++i) {
+    uint64_t x = 0;
+    for (int k = 0; k < 8; ++k) x = (x << 8) | uint8_t(buf[i * 8 + k]);
+    id.w[i] = x;
+  }
+  return id;
+}
+
+__device__ __forceinline__ void format_pending(const World& w, int p) {
+  const long long c = w.p_ctr[p];
+  if (c >= 0) {
+    w.p_id[p] = format_pod_id(c);
+    w.p_ctr[p] = -1;
+  }
+}
+
+__global__ void k_tick_format_ids(World w) {
   const int n = *w.n_pods;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    format_pending(w, p);
+}
+
+__global__ void k_tick_prologue(World w, double now) {
+  const int n = *w.n_pods;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    format_pending(w, p);
     if (w.p_state[p] == kCold && w.p_ready[p] <= now) w.p_state[p] = kRunning;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *w.n_actions = 0;
     *w.err = 0;
@@ -667,6 +706,14 @@ struct Commit {
   int* serr;             // shared: an error was raised (checked between functions)
   int* snpods;           // shared copy of *w.n_pods for the whole commit
   long long* scounter;   // shared copy of *w.counter
+  uint32_t* skey;        // shared argmin keys per GPU: npods > 0 ? occupancy << 18 | rank : ~0
+                         // (null: scan the summaries)
+
+  // lane-0 code: refresh GPU g's argmin key after its pod count / occupancy changed
+  __device__ void rekey0(int g) const {
+    if (skey != nullptr)
+      skey[g] = w.g_npods[g] > 0 ? (uint32_t(w.g_hgo[g]) << 18) | uint32_t(g) : ~0u;
+  }
 
   __device__ uint64_t* parts(int g) const {
     return ovf[g] ? w.g_parts + int64_t(g) * kPartCap : sp + int64_t(g) * ps;
@@ -710,6 +757,7 @@ struct Commit {
     set_entry(g, pos, part_pack(part_sm(e), part_alloc(e) + delta, part_npods(e), part_uid(e)));
     if (lane == 0) {
       w.g_hgo[g] += s * delta;
+      rekey0(g);
       w.p_q[p] = new_q;
     }
     __syncwarp();
@@ -745,6 +793,7 @@ struct Commit {
       w.p_gpu[p] = g;
       w.g_npods[g] += 1;
       w.g_hgo[g] += s * q;
+      rekey0(g);
     }
     __syncwarp();
   }
@@ -767,6 +816,7 @@ struct Commit {
       }
       w.g_npods[g] -= 1;
       w.g_hgo[g] -= s * q;
+      rekey0(g);
       w.p_state[p] = kDead;
     }
     // drop from its function's pod list (swap with the last entry)
@@ -793,40 +843,10 @@ struct Commit {
     __syncwarp();
   }
 
-  // new COLD_STARTING pod pod-%06d (sim.py:337-340, 505-516).  The 32 id bytes are built by
-  // the 32 lanes (byte k by lane k) and packed big-endian with warp OR-reductions.
+  // new COLD_STARTING pod pod-%06d (sim.py:337-340, 505-516); nothing in this tick reads the
+  // new pod's id string, so only its counter value is recorded here.
   // npods: the function's pod count (kept by the caller across its new pods).
   __device__ int new_pod(int f, int b, int s, int q, double now, int& npods) const {
-    const long long c = *scounter;
-    int nd = 1;  // decimal digits of c
-    for (unsigned long long v = (unsigned long long)c / 10ull; v; v /= 10ull) ++nd;
-    const int width = nd > 6 ? nd : 6;
-    const int k = lane;
-    uint32_t ch = 0;
-    if (k < 4) {
-      ch = k == 0 ? 'p' : k == 1 ? 'o' : k == 2 ? 'd' : '-';
-    } else if (k - 4 < width) {
-      const int j = k - 4;           // digit j from the left of the zero-padded number
-      const int from_right = width - 1 - j;
-      // divisions by the constant 10 only (multiply-high), 32-bit when the counter fits
-      uint32_t digit;
-      if (c < (1ll << 32)) {
-        uint32_t v = uint32_t(c);
-        for (int i = 0; i < from_right && v; ++i) v /= 10u;
-        digit = v % 10u;
-      } else {
-        unsigned long long v = (unsigned long long)c;
-        for (int i = 0; i < from_right && v; ++i) v /= 10ull;
-        digit = uint32_t(v % 10ull);
-      }
-      ch = uint32_t('0') + digit;
-    }
-    const uint32_t shift = 8u * uint32_t(3 - (k & 3));
-    const uint32_t part = ch << shift;  // byte k inside its 32-bit quarter-word
-    uint32_t word32[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      word32[i] = __reduce_or_sync(0xffffffffu, (k >> 2) == i ? part : 0u);
     int p = 0;
     if (lane == 0) {
       p = (*snpods)++;
@@ -834,12 +854,8 @@ struct Commit {
         fail0(RAPP_E_ARG, f);
         p = -1;
       } else {
-        *scounter = c + 1;
-        PodId id;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          id.w[i] = (uint64_t(word32[2 * i]) << 32) | uint64_t(word32[2 * i + 1]);
-        w.p_id[p] = id;
+        const long long c = (*scounter)++;
+        w.p_ctr[p] = c;  // the id string is formatted later (format_pending)
         w.p_fn[p] = f;
         w.p_b[p] = b;
         w.p_s[p] = s;
@@ -860,6 +876,12 @@ struct Commit {
   __device__ int argmin_used() const {
     // occupancy <= 100*100 per GPU, so (occupancy, rank) packs into 32 bits for up to 2^18
     // GPUs: one scan and one warp min-reduction
+    if (skey != nullptr) {  // maintained keys: one shared-memory word per GPU
+      unsigned best = ~0u;
+      for (int g = lane; g < w.G; g += 32) best = min(best, skey[g]);
+      best = __reduce_min_sync(0xffffffffu, best);
+      return best == ~0u ? -1 : int(best & ((1u << 18) - 1));
+    }
     if (w.G <= (1 << 18)) {
       unsigned best = ~0u;
       for (int g = lane; g < w.G; g += 32)
@@ -1131,9 +1153,11 @@ struct Commit {
     // one pod on the used GPU with the lowest occupancy (autoscaler.py:137-152)
     if (gap > 0.0) {
       const int g = argmin_used();
+      TPROF_ACC(8);
       if (g >= 0) {
         int sm, qmax;
         best_slot(g, sm, qmax);
+        TPROF_ACC(9);
         if (sm > 0 && qmax > 0) {
           if (!pre.brefok) {
             if (lane == 0) fail0(RAPP_E_VALUE, f);
@@ -1176,10 +1200,14 @@ struct Commit {
                 break;
               }
             }
+            TPROF_ACC(10);  // T loads + covering quota
             const int p = new_pod(f, bref, sm, quota, now, npods);
+            TPROF_ACC(11);  // new_pod
             if (p < 0) return;
             place(p, g, sm, quota);
+            TPROF_ACC(12);  // place
             emit(f, kHUp, bref, sm, quota, p, g, 0);
+            TPROF_ACC(13);  // emit
             gap = __dsub_rn(gap, tq);  // == T[quota] on a step, cmax at the off-step qmax
           }
         }
@@ -1346,6 +1374,8 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   // shared layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)][ovf G bytes]
   uint64_t* sp = reinterpret_cast<uint64_t*>(sg + ((5 * G + 1) & ~1));
   uint8_t* ovf = reinterpret_cast<uint8_t*>(sp + int64_t(G) * ps);
+  uint32_t* skey = (smem_g && G <= (1 << 18))
+                       ? reinterpret_cast<uint32_t*>(ovf + ((G + 3) & ~3)) : nullptr;
   if (lane == 0) s_nact = 0;
   for (int g = lane; g < G; g += 32) {
     const int n = w.g_nparts[g];
@@ -1367,6 +1397,9 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
     v.g_nparts = sg + 2 * G;
     v.g_freesm = sg + 3 * G;
     v.g_nextuid = reinterpret_cast<uint32_t*>(sg + 4 * G);
+    if (skey != nullptr)
+      for (int g = lane; g < G; g += 32)
+        skey[g] = sg[g] > 0 ? (uint32_t(sg[G + g]) << 18) | uint32_t(g) : ~0u;
     __syncwarp();
   }
   __syncwarp();
@@ -1378,10 +1411,10 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
     s_counter = (long long)*w.counter;
   }
   __syncwarp();
-  Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter};
+  Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter, skey};
   bool stop = s_err != 0;
 #ifdef RAPP_TICK_PROF
-  if (lane < 8) s_tprof[lane] = 0;
+  if (lane < 16) s_tprof[lane] = 0;
   __syncwarp();
 #endif
   // First-pod quota rows of the scale-up functions of a batch of 32 are bulk-copied into
@@ -1450,7 +1483,7 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
 #ifdef RAPP_TICK_PROF
   __syncwarp();
-  if (lane < 8) g_tick_prof[lane] += s_tprof[lane];
+  if (lane < 16) g_tick_prof[lane] += s_tprof[lane];
 #endif
   if (lane == 0) {
     *w.n_pods = s_npods;
@@ -1486,7 +1519,7 @@ __global__ void __launch_bounds__(32) k_tick_release(World w, const int32_t* __r
   for (int g = lane; g < w.G; g += 32) rel_ovf[g] = 1;  // every list lives in global memory
   if (lane == 0) s_err = 0;
   __syncwarp();
-  Commit c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter};
+  Commit c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter, nullptr};
   for (int i = 0; i < n; ++i) {
     const int p = list[i];
     if (w.p_state[p] == kDead) continue;
@@ -1633,7 +1666,7 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     if (smem_g)
       ps = (int)std::min<size_t>(12, (budget - gbytes - size_t(w.G)) / (8 * std::max(1, w.G)));
     const size_t bytes = size_t(2 * 32 * kRowStage) * 8 + gbytes + size_t(w.G) * ps * 8 +
-                         size_t(w.G) + 16;
+                         size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16;  // + argmin keys
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
     k_tick_commit<<<1, 64, bytes, st>>>(w, now, smem_g, ps);
@@ -1846,6 +1879,8 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   UP(w.p_state, p_state)
   UP(w.p_ready, p_ready)
   UP(w.p_id, p_id)
+  if ((rc = dev_alloc(t.get(), &w.p_ctr, (size_t)cap))) return rc;
+  RAPP_CUDA(cudaMemset(w.p_ctr, 0xFF, (size_t)cap * sizeof(int64_t)));  // -1: nothing pending
   UP(w.fn_npods, fn_npods)
   UP(w.fn_pods, fn_pods)
 #undef UP
@@ -2094,6 +2129,11 @@ int rapp_tick_read_pods(rapp_tick* t, rapp_pod_desc* out, int64_t cap, int64_t* 
   RAPP_CUDA(cudaMemcpy(&np, w.n_pods, 4, cudaMemcpyDeviceToHost));
   *n = np;
   if (!out) return RAPP_OK;
+  if (np > 0) {  // ids of pods created by the last tick are formatted lazily
+    k_tick_format_ids<<<std::max(1, std::min(1024, (np + 255) / 256)), 256, 0, t->stream>>>(w);
+    RAPP_LAUNCHED();
+    RAPP_CUDA(cudaStreamSynchronize(t->stream));
+  }
   if (np > cap) {
     set_error("pod buffer too small");
     return RAPP_E_ARG;
@@ -2211,10 +2251,10 @@ int rapp_tick_counter(rapp_tick* t, int64_t* c) {
 #ifdef RAPP_TICK_PROF
 int rapp_tick_prof_read(uint64_t* out8, int reset) {
   RAPP_CUDA(cudaDeviceSynchronize());
-  RAPP_CUDA(cudaMemcpyFromSymbol(out8, g_tick_prof, 64));
+  RAPP_CUDA(cudaMemcpyFromSymbol(out8, g_tick_prof, 128));
   if (reset) {
-    uint64_t z[8] = {};
-    RAPP_CUDA(cudaMemcpyToSymbol(g_tick_prof, z, 64));
+    uint64_t z[16] = {};
+    RAPP_CUDA(cudaMemcpyToSymbol(g_tick_prof, z, 128));
   }
   return RAPP_OK;
 }

@@ -1,4 +1,5 @@
 timeout 900 python -m pytest tests/test_tick_gpu.py -x -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 RAPP_LIB=build_variants/prof.so timeout 600 python tools/tick_commit_breakdown.py --full-grid 2>&1 | tail -12 | head -4
 for v in build_variants/prev.so paper_2505_01968_b200/librapp_b200.so; do
 echo "== $v full"; RAPP_LIB=$v TICKS=8 timeout 600 python tools/tick_profile.py --full-grid 2>&1 | awk '{print $6}' | tr '\n' ' '; echo

@@ -16,8 +16,10 @@ from paper_2505_01968_b200 import _lib  # noqa: E402
 from paper_2505_01968_b200.autoscaler import ScalerConfig  # noqa: E402
 from paper_2505_01968_b200.tick import TickEngine  # noqa: E402
 
-NAMES = ["batch prefetch+stage", "vertical spec/walk", "used-GPU branch", "fresh-GPU branch",
-         "scale-down", "vertical headroom", "functions (wall)", "vertical change+emit"]
+NAMES = ["batch wait", "vertical spec/walk", "used-GPU rest", "fresh-GPU branch",
+         "scale-down", "vertical headroom", "functions (wall)", "vertical change+emit",
+         "hu argmin", "hu best_slot", "hu T+covering", "hu new_pod", "hu place", "hu emit",
+         "-", "-"]
 
 
 def main(full_grid, nticks=6):
@@ -32,7 +34,7 @@ def main(full_grid, nticks=6):
     lib = _lib.load()
     rd = lib.rapp_tick_prof_read
     rd.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    buf = np.zeros(8, dtype=np.uint64)
+    buf = np.zeros(16, dtype=np.uint64)
     rd(buf.ctypes.data, 1)
     rng = random.Random(0)
     order = sorted(fns, key=lambda f: f.function_id)
@@ -47,7 +49,7 @@ def main(full_grid, nticks=6):
         mix = collections.Counter(str(x.kind).split(".")[-1] for x in res.actions)
         us = buf.astype(np.float64) / 1.9e3
         print(f"tick {k} actions {len(res.actions)} {dict(mix)}")
-        print("   " + ", ".join(f"{NAMES[i]} {us[i]:.0f}us" for i in range(8) if NAMES[i] != "-"))
+        print("   " + ", ".join(f"{NAMES[i]} {us[i]:.0f}us" for i in range(16) if NAMES[i] != "-"))
 
 
 if __name__ == "__main__":
