@@ -744,6 +744,12 @@ struct Commit {
     return int(__reduce_min_sync(0xffffffffu, pos));
   }
 
+  // find_part with a position hint (checked by one load of the hinted entry)
+  __device__ int find_part_hint(int g, uint32_t uid, int hint) const {
+    if (hint >= 0 && hint < w.g_nparts[g] && part_uid(parts(g)[hint]) == uid) return hint;
+    return find_part(g, uid);
+  }
+
   __device__ void set_entry(int g, int pos, uint64_t e) const {
     __syncwarp();
     if (lane == 0) parts(g)[pos] = e;
@@ -1008,6 +1014,7 @@ struct Commit {
     double gap0, sg0;
     int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods, kd0;
     int nd, dkind, dquota, didle, stamp;
+    int pos0;  // hint: position of the first pod's partition at tick start (-1: none)
     uint32_t uid0;
   };
 
@@ -1048,6 +1055,16 @@ struct Commit {
       r.b0 = w.p_b[p];
       r.s0 = w.p_s[p];
       if (cls == kDown) r.didle = w.p_idle[p];
+      // partitions keep their order except for removals, so the tick-start position is
+      // almost always still right; the committer validates it with one load
+      const uint64_t* P = w.g_parts + int64_t(r.gpu0) * kPartCap;
+      const int n = w.g_nparts[r.gpu0];
+      r.pos0 = -1;
+      for (int i = 0; i < n; ++i)
+        if (part_uid(P[i]) == r.uid0) {
+          r.pos0 = i;
+          break;
+        }
     }
     return r;
   }
@@ -1094,7 +1111,7 @@ struct Commit {
       const int p = j == 0 ? pre.p0 : srt[j];
       if ((j == 0 ? pre.st0 : w.p_state[p]) != kRunning) continue;
       const int g = j == 0 ? pre.gpu0 : w.p_gpu[p];
-      const int pos = find_part(g, j == 0 ? pre.uid0 : w.p_puid[p]);
+      const int pos = j == 0 ? find_part_hint(g, pre.uid0, pre.pos0) : find_part(g, w.p_puid[p]);
       const int q0 = j == 0 ? pre.q0 : w.p_q[p];
       const int avail = q0 + (100 - part_alloc(parts(g)[pos]));
       TPROF_ACC(5);  // headroom lookup
@@ -1309,7 +1326,8 @@ struct Commit {
         idle = w.p_idle[p];
       }
       if (kind == kVDown) {
-        change_quota_at(p, g, find_part(g, uid), s, q, quota);
+        change_quota_at(p, g, i == 0 ? find_part_hint(g, uid, pre.pos0) : find_part(g, uid), s, q,
+                        quota);
         emit(f, kVDown, b, s, quota, p, g, 0);
       } else {
         if (lane == 0) w.p_state[p] = kDraining;
