@@ -639,6 +639,7 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
   const double* v0 = v + s_i0 * plane;
   const double* v1 = v + s_i1 * plane;
   const double tb = s_tb, bb = double(b);
+  const bool fast = td.fast != 0;  // finite positive values (checked at upload)
   for (int i = threadIdx.x; i < 100 * nq; i += blockDim.x) {
     const int si = i / nq, qi = i - si * nq;
     const int2 j = s_j[si], k = s_k[qi];
@@ -647,12 +648,26 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
     const int o10 = j.y * td.nq + k.x, o11 = j.y * td.nq + k.y;
     // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch.  The
     // table reads and the grid writes are streaming (evict-first) so this pass does not
-    // push the commit's working set (phase A outputs, cluster state) out of L2.
-    const double c00 = lerp_rn(__ldcs(v0 + o00), __ldcs(v0 + o01), tq);
-    const double c01 = lerp_rn(__ldcs(v0 + o10), __ldcs(v0 + o11), tq);
-    const double c10 = lerp_rn(__ldcs(v1 + o00), __ldcs(v1 + o01), tq);
-    const double c11 = lerp_rn(__ldcs(v1 + o10), __ldcs(v1 + o11), tq);
-    const double lat = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
+    // push the commit's working set (phase A outputs, cluster state) out of L2.  On a node
+    // bracket (lo == hi, t == 0) of a finite table lerp(v, v, 0) == v exactly, so those
+    // lerps and their second loads are skipped (every quota step of a 1..100% table, and
+    // every sm on the table's own grid, is a node).
+    double lat;
+    if (fast && k.x == k.y) {
+      const double a00 = __ldcs(v0 + o00), a10 = __ldcs(v1 + o00);
+      if (j.x == j.y) {
+        lat = lerp_rn(a00, a10, tb);
+      } else {
+        const double a01 = __ldcs(v0 + o10), a11 = __ldcs(v1 + o10);
+        lat = lerp_rn(lerp_rn(a00, a01, ts), lerp_rn(a10, a11, ts), tb);
+      }
+    } else {
+      const double c00 = lerp_rn(__ldcs(v0 + o00), __ldcs(v0 + o01), tq);
+      const double c01 = lerp_rn(__ldcs(v0 + o10), __ldcs(v0 + o11), tq);
+      const double c10 = lerp_rn(__ldcs(v1 + o00), __ldcs(v1 + o01), tq);
+      const double c11 = lerp_rn(__ldcs(v1 + o10), __ldcs(v1 + o11), tq);
+      lat = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
+    }
     __stcs(w.tgrid + (int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1, throughput(bb, lat));
   }
 }

@@ -1,3 +1,5 @@
-timeout 600 python bench.py --workload tick > gpurun_out/bench_tick.log 2>&1
-timeout 900 python bench.py --workload tick --full-grid --ticks 20 > gpurun_out/bench_tick_full.log 2>&1
-for f in bench_tick bench_tick_full; do tail -1 gpurun_out/$f.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); t=d['tick']; print(t['grid'], t['device_us_median'], t['device_us_max'], t['e2e_us_median'], d['clocks'])"; done
+timeout 900 python -m pytest tests/test_tick_gpu.py -x -q 2>&1 | tail -2
+for v in build_variants/prev.so paper_2505_01968_b200/librapp_b200.so; do
+echo "== $v full"; RAPP_LIB=$v TICKS=8 timeout 600 python tools/tick_profile.py --full-grid 2>&1 | awk '{print $6}' | tr '\n' ' '; echo
+echo "== $v cfg4"; RAPP_LIB=$v TICKS=8 timeout 600 python tools/tick_profile.py 2>&1 | awk '{print $6}' | tr '\n' ' '; echo
+done
