@@ -760,6 +760,64 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False, nfn=1000, ng
             "e2e_api": "TickEngine.tick (rapp_tick_run: H2D arrivals+idle, D2H actions+rates)"}
 
 
+def run_config1(args, local, reps=20):
+    """BASELINE config 1 (the reference's CPU-runnable case): the ResNet-50 table queried
+    over b = 1..32 x sm = 10..100 x quota = 1..100 (291,200 points, latency + rps) and
+    most_efficient_config for 64 log-spaced targets at quota steps 1 and 10 — device time
+    per sweep / per batched search, next to the reference's compiled kernel on one core."""
+    import torch
+    from paper_2505_01968_b200 import PerfTable, PerfTableSet
+    s = list(range(10, 101, 10))
+    q = list(range(10, 101, 10))
+    lat = surface(*MODELS["resnet50"], BATCHES, s, q)
+    t = PerfTable("resnet50", BATCHES, s, q, lat, device=local)
+    b3, s3, q3 = np.meshgrid(np.arange(1, 33.0), np.arange(10, 101.0), np.arange(1, 101.0),
+                             indexing="ij")
+    c = np.ascontiguousarray(np.column_stack([b3.ravel(), s3.ravel(), q3.ravel()]))
+    dev = torch.device("cuda", local)
+    dc = torch.from_numpy(c).to(dev)
+    out = torch.empty(len(c), dtype=torch.float64, device=dev)
+    rps = torch.empty_like(out)
+    st = torch.cuda.current_stream(dev)
+    t.predict_latency_many(dc, out, rps, stream=st.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        t.predict_latency_many(dc, out, rps, stream=st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    sweep_us = e0.elapsed_time(e1) * 1000.0 / reps
+    peak = t.throughput(32, 100, 100)
+    targets = torch.tensor(np.geomspace(0.001, 2.0 * peak, 64), dtype=torch.float64,
+                           device=dev)
+    search_us = {}
+    for step in (1, 10):
+        ts = PerfTableSet([(t, None)] * 64, quota_step=step)
+        o = torch.empty((64, 3), dtype=torch.int32, device=dev)
+        ts.search_dev(targets, o)
+        e0.record(st)
+        for _ in range(reps):
+            ts.search_dev(targets, o, stream=st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        search_us[f"quota_step_{step}"] = e0.elapsed_time(e1) * 1000.0 / reps
+    ref = None
+    try:
+        from oracle.binding import load_reference_kernel
+        k = load_reference_kernel()
+        if k is not None:
+            o2 = np.empty(len(c))
+            t0 = time.perf_counter()
+            k.interp3_many(t._b_axis, t._s_axis, t._q_axis, t.latency_ms, c, o2)
+            ref = {"sweep_us": (time.perf_counter() - t0) * 1e6, "cores": 1,
+                   "kind": "reference", "what": "the reference's compiled interp3_many"}
+    except Exception:  # noqa: BLE001 — the baseline is optional on a box without oracle/_ref
+        ref = None
+    return {"points": len(c), "sweep_us_device": sweep_us,
+            "sweep_predictions_per_s": len(c) / (sweep_us * 1e-6),
+            "search_64_targets_us_device": search_us, "cpu_baseline": ref}
+
+
 def run_replay(args, local, name="burst-100", reps=3):
     """Config 3: the 100-function burst trace replay captured from the reference simulator
     (tests/golden/replay.json): every scaler tick through the public host API —
@@ -999,7 +1057,8 @@ def main():
         extra = {"tick_config4": run_tick(args, local, ticks=20),
                  "tick_config4_full_grid": run_tick(args, local, ticks=10, full_grid=True),
                  "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64),
-                 "replay_config3": run_replay(args, local)}
+                 "replay_config3": run_replay(args, local),
+                 "config1": run_config1(args, local)}
         extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
         largs = argparse.Namespace(**{**vars(args), "steps": 50, "functions": 3125})
         lat = run_lattice(largs, rank, world, local)
