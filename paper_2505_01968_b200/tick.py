@@ -103,12 +103,13 @@ class TickResult:
         """Reference-shaped actions (horizontal_up carries pod_id None)."""
         if self._actions is None:
             e = self._engine
+            fids, gids, mk = e.fids, e.gids, ScalingAction._trusted
+            hup = ActionKind.HORIZONTAL_UP
             out = []
             for a, pid in zip(self.raw.tolist(), self.pod_ids):
                 kind = KINDS[a[1]]
-                out.append(ScalingAction(e.fids[a[0]], kind, a[2], a[3], a[4],
-                                         None if kind is ActionKind.HORIZONTAL_UP else pid,
-                                         e.gids[a[6]]))
+                out.append(mk(fids[a[0]], kind, a[2], a[3], a[4],
+                              None if kind is hup else pid, gids[a[6]]))
             self._actions = out
         return self._actions
 
