@@ -43,19 +43,38 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
           defines: tuple[str, ...] = ()) -> str:
-    """Builds the library; `out`/`defines` make tuning variants (e.g. RAPP_STREAM_ILP=1)."""
+    """Builds the library; `out`/`defines` make tuning variants (e.g. RAPP_STREAM_ILP=1).
+    Translation units compile in parallel (no device code crosses files), then link."""
+    import concurrent.futures
+    import tempfile
     target = out or LIB
     if out is None and not force and not _stale():
         return LIB
     tmp = target + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", tmp, *sources(),
-           "-lcudart"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building librapp_b200.so")
+    flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines]]
+    with tempfile.TemporaryDirectory() as objdir:
+        def compile_one(src):
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            res = subprocess.run([NVCC, *flags, "-c", "-o", obj, src], capture_output=True,
+                                 text=True)
+            return src, obj, res
+        srcs = sources()
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+            results = list(ex.map(compile_one, srcs))
+        log = ""
+        for src, _, res in results:
+            log += res.stdout + res.stderr
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
+        res = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                              "-o", tmp, *[obj for _, obj, _ in results], "-lcudart"],
+                             capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed linking librapp_b200.so")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(log)
     os.replace(tmp, target)
     return target
 
