@@ -1,8 +1,7 @@
-timeout 900 python -m pytest tests/test_tick_gpu.py -x -q 2>&1 | tail -2
-timeout 600 python -c "
-import sys, argparse; sys.path.insert(0,'.')
-import bench
-a = argparse.Namespace(ticks=20, steps=20)
-r = bench.run_replay(a, 0); print('replay', r['e2e_us_median'], r['e2e_us_max'])
-t = bench.run_tick(a, 0, ticks=20); print('cfg4', t['device_us_median'], t['e2e_us_median'])
-"
+timeout 600 python -m pytest tests/test_tick_gpu.py -q 2>&1 | tail -2
+for i in 1 2; do
+echo "== new full"; TICKS=40 timeout 300 python tools/tick_profile.py --full-grid 2>&1 | python tools/tick_summary.py
+echo "== prev full"; RAPP_LIB=build_variants/prev.so TICKS=40 timeout 300 python tools/tick_profile.py --full-grid 2>&1 | python tools/tick_summary.py
+done
+echo "== new cfg4"; TICKS=40 timeout 300 python tools/tick_profile.py 2>&1 | python tools/tick_summary.py
+echo "== prev cfg4"; RAPP_LIB=build_variants/prev.so TICKS=40 timeout 300 python tools/tick_profile.py 2>&1 | python tools/tick_summary.py
