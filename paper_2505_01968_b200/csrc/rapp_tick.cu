@@ -62,6 +62,21 @@ struct DownAct {
   int32_t kind, pod, quota, _pad;
 };
 
+// A function whose whole commit is known from phase A up to a validation ("straight-line"):
+// a scale-up whose speculative vertical walk closes the gap (no horizontal step), or a
+// scale-down of vertical steps only.  Steps are the walked pods / staged actions in order:
+// pod, GPU, tick-start partition position and uid, its sm / batch, quota before and after,
+// and (scale-up) the tick-start quota allocated on the partition the walk assumed.
+constexpr int kFastSteps = 2;
+struct FastStep {
+  int32_t p, g, pos, s, b, qold, qnew, alloc0;  // alloc0 < 0: nothing to validate
+  uint32_t uid;
+};
+struct FastRec {
+  int32_t n;  // 0: not straight-line
+  FastStep st[kFastSteps];
+};
+
 // partition entry: sm (8 bits) | alloc (8 bits) | npods (16 bits) | uid (32 bits)
 __host__ __device__ inline uint64_t part_pack(int sm, int alloc, int npods, uint32_t uid) {
   return uint64_t(uint32_t(sm) & 0xFF) | (uint64_t(uint32_t(alloc) & 0xFF) << 8) |
@@ -138,6 +153,7 @@ struct World {
   int32_t* spec_avail;           // [F][kMaxPods] avail the walk assumed (-1: not walked)
   int32_t* spec_k;               // [F][kMaxPods] steps taken
   double* spec_gain;             // [F][kMaxPods] gain of those steps
+  FastRec* fast;                 // [F] straight-line commits (n = 0: none)
   double* tgrid;                 // [F][100][100] throughput(bref, sm, q)
   int32_t* ndown;
   DownAct* down;                 // [F][kMaxPods]
@@ -480,6 +496,9 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
       // the gap left by pods 0..j-1 of this function, so phase B reuses it verbatim while
       // every headroom it observes equals the one assumed here.
       double gap = w.gap0[f];
+      FastRec fr;
+      fr.n = 0;
+      bool simple = true;
       for (int j = 0; j < m; ++j) {
         w.spec_avail[f * kMaxPods + j] = -1;
         if (!(gap > 0.0)) continue;
@@ -487,10 +506,11 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
         if (w.p_state[p] != kRunning) continue;
         const int g = w.p_gpu[p];
         const uint64_t* P = w.g_parts + int64_t(g) * kPartCap;
-        int alloc = 100;
+        int alloc = 100, pos = -1;
         for (int i = 0; i < w.g_nparts[g]; ++i)
           if (part_uid(P[i]) == w.p_puid[p]) {
             alloc = part_alloc(P[i]);
+            pos = i;
             break;
           }
         const int q0 = w.p_q[p];
@@ -506,7 +526,18 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
         w.spec_k[f * kMaxPods + j] = k;
         w.spec_gain[f * kMaxPods + j] = gain;
         if (k > 0) gap = __dsub_rn(gap, gain);
+        // a second walked pod on the same partition would see the first one's change
+        for (int t = 0; t < fr.n && t < kFastSteps; ++t)
+          if (fr.st[t].g == g && fr.st[t].uid == w.p_puid[p]) simple = false;
+        if (fr.n < kFastSteps && pos >= 0)
+          fr.st[fr.n] = FastStep{p, g, pos, w.p_s[p], w.p_b[p], q0, q0 + k * d, alloc,
+                                 w.p_puid[p]};
+        else
+          simple = false;
+        ++fr.n;
       }
+      w.fast[f].n = simple && !(gap > 0.0) ? fr.n : 0;
+      for (int t = 0; t < fr.n && t < kFastSteps; ++t) w.fast[f].st[t] = fr.st[t];
       w.cls[f] = kUp;
     }
     return;
@@ -586,6 +617,26 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
     }
     w.ndown[f] = na;
     w.stamp[f] = na > 0;
+    // vertical steps only: no decision reads shared state, the commit just applies them
+    bool simple = na > 0 && na <= kFastSteps;
+    for (int i = 0; i < na && simple; ++i) {
+      const DownAct a = out[i];
+      const int p = a.pod, g = w.p_gpu[p];
+      const uint64_t* P = w.g_parts + int64_t(g) * kPartCap;
+      int pos = -1;
+      for (int k = 0; k < w.g_nparts[g]; ++k)
+        if (part_uid(P[k]) == w.p_puid[p]) {
+          pos = k;
+          break;
+        }
+      if (a.kind != kVDown || pos < 0) {
+        simple = false;
+        break;
+      }
+      w.fast[f].st[i] = FastStep{p, g, pos, w.p_s[p], w.p_b[p], w.p_q[p], a.quota, -1,
+                                 w.p_puid[p]};
+    }
+    w.fast[f].n = simple ? na : 0;
     w.cls[f] = kDown;
   }
 }
@@ -708,6 +759,12 @@ __device__ __forceinline__ void tk_bar_wait(uint64_t* bar, uint32_t parity) {
 // the first pod's quota row of a function, staged for the commit (102 doubles = 816 B,
 // the 101-entry row plus 8 bytes of the next row so the bulk size is a multiple of 16)
 constexpr int kRowStage = 102;
+
+// conflict-mark slot of partition (g, pos) for fast_run (collisions only shorten runs)
+constexpr int kFastHash = 512;
+__device__ __forceinline__ int fast_hash(int g, int pos) {
+  return int((uint32_t(g) * 2654435761u + uint32_t(pos) * 40503u) >> 23) & (kFastHash - 1);
+}
 
 struct Commit {
   const World& w;
@@ -1311,6 +1368,90 @@ struct Commit {
     }
   }
 
+  // Commits a run of straight-line functions (FastRec) at once, one per lane.  `cand`: the
+  // active lanes from the next function up to (excluding) the first active function that is
+  // not straight-line, in sorted order.  Lane l joins the run when every partition it
+  // validates still has its tick-start allocation and is not written by a lower lane of the
+  // run — exactly the conditions under which the sequential commit would take phase A's
+  // walk verbatim — and every lane below it joined too.  Returns the lanes committed (their
+  // changes applied, actions emitted in function order); 0 leaves the first one to the
+  // sequential path.  htab: conflict marks (epoch << 5 | 31 - lane) by partition hash.
+  __device__ unsigned fast_run(int base, unsigned cand, const FastRec& r, int stamp,
+                               double now, uint32_t* htab, uint32_t epoch) const {
+    const bool in = (cand >> lane) & 1;
+    const int n = in ? r.n : 0;
+    bool ok = in;
+    uint64_t* P[kFastSteps];
+    bool wr[kFastSteps];
+#pragma unroll
+    for (int k = 0; k < kFastSteps; ++k) {
+      P[k] = nullptr;
+      wr[k] = false;
+      if (k < n) {
+        const FastStep& st = r.st[k];
+        uint64_t* L = parts(st.g);
+        if (st.pos < w.g_nparts[st.g] && part_uid(L[st.pos]) == st.uid) {
+          P[k] = L + st.pos;
+          if (st.alloc0 >= 0 && part_alloc(*P[k]) != st.alloc0) ok = false;
+          wr[k] = st.qnew != st.qold;
+        } else {
+          ok = false;
+        }
+      }
+    }
+    const uint32_t mark = (epoch << 5) | uint32_t(31 - lane);
+#pragma unroll
+    for (int k = 0; k < kFastSteps; ++k)
+      if (ok && wr[k]) atomicMax(htab + fast_hash(r.st[k].g, r.st[k].pos), mark);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kFastSteps; ++k)
+      if (ok && k < n && r.st[k].alloc0 >= 0) {
+        const uint32_t v = htab[fast_hash(r.st[k].g, r.st[k].pos)];
+        if ((v >> 5) == epoch && int(31 - (v & 31)) < lane) ok = false;
+      }
+    const unsigned bad = cand & ~__ballot_sync(0xffffffffu, ok);
+    const unsigned run = bad ? cand & ((1u << (__ffs(bad) - 1)) - 1) : cand;
+    if (run == 0) return 0;
+    const bool mine = (run >> lane) & 1;
+    int cnt = 0;
+    if (mine) {
+#pragma unroll
+      for (int k = 0; k < kFastSteps; ++k)
+        if (wr[k]) {
+          const FastStep& st = r.st[k];
+          const int delta = st.qnew - st.qold;
+          atomicAdd(reinterpret_cast<unsigned long long*>(P[k]),
+                    (unsigned long long)((long long)delta * 256));  // alloc field (bits 8..15)
+          atomicAdd(w.g_hgo + st.g, st.s * delta);
+          w.p_q[st.p] = st.qnew;
+          ++cnt;
+        }
+    }
+    __syncwarp();
+    const unsigned b1 = __ballot_sync(0xffffffffu, mine && cnt >= 1);
+    const unsigned b2 = __ballot_sync(0xffffffffu, mine && cnt >= 2);
+    const unsigned below = (1u << lane) - 1;
+    const int at0 = *nact;
+    if (mine) {
+      int at = at0 + __popc(b1 & below) + __popc(b2 & below);
+      const int f = base + lane;
+#pragma unroll
+      for (int k = 0; k < kFastSteps; ++k)
+        if (wr[k]) {
+          const FastStep& st = r.st[k];
+          rekey0(st.g);  // after every lane's occupancy update (syncwarp above)
+          w.actions[at++] = rapp_action{f, st.alloc0 >= 0 ? kVUp : kVDown, st.b, st.s,
+                                        st.qnew, st.p, st.g, 0};
+        }
+      if (stamp && r.st[0].alloc0 < 0) w.last_down[f] = now;
+    }
+    __syncwarp();
+    if (lane == 0) *nact = at0 + __popc(b1) + __popc(b2);
+    __syncwarp();
+    return run;
+  }
+
   __device__ void scale_down(int f, double now, const Pre& pre) const {
     TPROF_T0();
     const int na = pre.nd;
@@ -1377,6 +1518,9 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   // those dependent global loads.
   __shared__ Commit::Pre s_pre[kPreDepth][32];
   __shared__ int s_pcls[kPreDepth][32];
+  __shared__ FastRec s_fast[kPreDepth][32];
+  __shared__ uint32_t s_htab[kFastHash];
+  for (int i = threadIdx.x; i < kFastHash; i += blockDim.x) s_htab[i] = 0;
   __shared__ volatile int s_ready[kPreDepth];
   __shared__ volatile int s_done, s_stop;
   if (threadIdx.x < kPreDepth) s_ready[threadIdx.x] = -1;
@@ -1394,8 +1538,18 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
       }
       if (s_stop) return;
       const int f = base + lane;
-      s_pcls[slot][lane] = f < w.F ? w.cls[f] : kNone;
+      const int cf = f < w.F ? w.cls[f] : kNone;
+      s_pcls[slot][lane] = cf;
       s_pre[slot][lane] = Commit::prefetch_of(w, f);
+      {
+        FastRec& fr = s_fast[slot][lane];
+        fr.n = 0;
+        if (w.policy == 0 && cf != kNone) {
+          const int n = w.fast[f].n;
+          for (int k = 0; k < n; ++k) fr.st[k] = w.fast[f].st[k];
+          fr.n = n;
+        }
+      }
       __threadfence_block();
       __syncwarp();
       if (lane == 0) s_ready[slot] = b;
@@ -1473,6 +1627,7 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   if (!stop) stage(0, lane < w.F ? w.cls[lane] : kNone, 0);
   int staged = 1;  // batches whose copies were issued
   int j = 0;
+  uint32_t epoch = 0;  // fast_run conflict-mark epochs
   TPROF_T0();
   for (int base = 0; base < w.F && !stop; base += 32, ++j) {
     TPROF_ACC(6);  // (the functions of the previous batch, accounted separately)
@@ -1489,8 +1644,20 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
     tk_bar_wait(&s_rbar[j & 1], (j >> 1) & 1);
     TPROF_ACC(0);  // waits for the header ring and the staged rows
     unsigned act = __ballot_sync(0xffffffffu, mine != kNone);
+    const unsigned fastm = __ballot_sync(0xffffffffu, mine != kNone && s_fast[slot][lane].n > 0);
     while (act) {
       const int i = __ffs(act) - 1;
+      if ((fastm >> i) & 1) {
+        // straight-line functions from i up to the next one that is not
+        const unsigned slow = act & ~fastm;
+        const unsigned cand = act & fastm & (slow ? (1u << (__ffs(slow) - 1)) - 1 : ~0u);
+        const unsigned done = c.fast_run(base, cand, s_fast[slot][lane], s_pre[slot][lane].stamp,
+                                         now, s_htab, ++epoch);
+        if (done) {
+          act &= ~done;
+          continue;
+        }
+      }
       act &= act - 1;
       const int cls = __shfl_sync(0xffffffffu, mine, i);
       const Commit::Pre& pre = s_pre[slot][i];
@@ -1692,12 +1859,14 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     RAPP_LAUNCHED();
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
-    const size_t budget = 150 * 1024;  // + the row staging below and ~12 KB static
+    // 227 KB per CTA minus the row staging and ~25 KB of static shared memory
+    const size_t budget = 227 * 1024 - size_t(2 * 32 * kRowStage) * 8 - 26 * 1024;
     const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
-    const int smem_g = gbytes + size_t(w.G) <= budget ? 1 : 0;
+    const size_t fixed = gbytes + size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16;
+    const int smem_g = fixed <= budget ? 1 : 0;
     int ps = 0;
     if (smem_g)
-      ps = (int)std::min<size_t>(12, (budget - gbytes - size_t(w.G)) / (8 * std::max(1, w.G)));
+      ps = (int)std::min<size_t>(12, (budget - fixed) / (8 * std::max(1, w.G)));
     const size_t bytes = size_t(2 * 32 * kRowStage) * 8 + gbytes + size_t(w.G) * ps * 8 +
                          size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16;  // + argmin keys
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1941,6 +2110,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.spec_avail, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_k, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_gain, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.fast, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.tgrid, FP * 100 * 100))) return rc;
   if ((rc = dev_alloc(t.get(), &w.ndown, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.down, FP * kMaxPods))) return rc;
