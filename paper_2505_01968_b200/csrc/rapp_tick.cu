@@ -62,18 +62,23 @@ struct DownAct {
   int32_t kind, pod, quota, _pad;
 };
 
-// A function whose whole commit is known from phase A up to a validation ("straight-line"):
-// a scale-up whose speculative vertical walk closes the gap (no horizontal step), or a
-// scale-down of vertical steps only.  Steps are the walked pods / staged actions in order:
-// pod, GPU, tick-start partition position and uid, its sm / batch, quota before and after,
-// and (scale-up) the tick-start quota allocated on the partition the walk assumed.
+// A function whose commit is known from phase A up to a validation ("straight-line"): a
+// scale-up whose speculative vertical walk closes the gap (kFastUp) or leaves `gap` for the
+// horizontal branch (kFastTail: the walk is straight-line, the rest runs sequentially), or
+// a scale-down of vertical steps only (kFastDown).  Steps are the walked pods / staged
+// actions in order: pod, GPU, tick-start partition position and uid, its sm / batch, quota
+// before and after, and (scale-up) the tick-start quota allocated on the partition the walk
+// assumed.
 constexpr int kFastSteps = 2;
 struct FastStep {
   int32_t p, g, pos, s, b, qold, qnew, alloc0;  // alloc0 < 0: nothing to validate
   uint32_t uid;
 };
+enum : int { kFastNone = 0, kFastUp = 1, kFastTail = 2, kFastDown = 3 };
 struct FastRec {
-  int32_t n;  // 0: not straight-line
+  double gap;    // kFastTail: the gap the walk leaves
+  int32_t kind;  // kFast*
+  int32_t n;     // steps
   FastStep st[kFastSteps];
 };
 
@@ -182,8 +187,8 @@ __device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
 
 #ifdef RAPP_TICK_PROF
 // diagnostics build only: cycles of the commit's parts, summed over ticks (lane 0)
-__device__ unsigned long long g_tick_prof[16];
-__shared__ unsigned long long s_tprof[16];  // per-launch accumulators, flushed at the end
+__device__ unsigned long long g_tick_prof[32];
+__shared__ unsigned long long s_tprof[32];  // per-launch accumulators, flushed at the end
 #define TPROF_T0() long long _tp0 = clock64()
 #define TPROF_ACC(i)                                                   \
   do {                                                                 \
@@ -536,7 +541,9 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
           simple = false;
         ++fr.n;
       }
-      w.fast[f].n = simple && !(gap > 0.0) ? fr.n : 0;
+      w.fast[f].kind = !simple ? kFastNone : gap > 0.0 ? kFastTail : kFastUp;
+      w.fast[f].n = fr.n;
+      w.fast[f].gap = gap;
       for (int t = 0; t < fr.n && t < kFastSteps; ++t) w.fast[f].st[t] = fr.st[t];
       w.cls[f] = kUp;
     }
@@ -636,7 +643,8 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
       w.fast[f].st[i] = FastStep{p, g, pos, w.p_s[p], w.p_b[p], w.p_q[p], a.quota, -1,
                                  w.p_puid[p]};
     }
-    w.fast[f].n = simple ? na : 0;
+    w.fast[f].kind = simple ? kFastDown : kFastNone;
+    w.fast[f].n = na;
     w.cls[f] = kDown;
   }
 }
@@ -698,8 +706,8 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
     const int o00 = j.x * td.nq + k.x, o01 = j.x * td.nq + k.y;
     const int o10 = j.y * td.nq + k.x, o11 = j.y * td.nq + k.y;
     // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch.  The
-    // table reads and the grid writes are streaming (evict-first) so this pass does not
-    // push the commit's working set (phase A outputs, cluster state) out of L2.  On a node
+    // table reads are streaming (evict-first) so this pass does not push the commit's
+    // working set (phase A outputs, cluster state) out of L2.  On a node
     // bracket (lo == hi, t == 0) of a finite table lerp(v, v, 0) == v exactly, so those
     // lerps and their second loads are skipped (every quota step of a 1..100% table, and
     // every sm on the table's own grid, is a node).
@@ -719,7 +727,8 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
       const double c11 = lerp_rn(__ldcs(v1 + o10), __ldcs(v1 + o11), tq);
       lat = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
     }
-    __stcs(w.tgrid + (int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1, throughput(bb, lat));
+    // default-policy store: the commit's used-GPU branch reads these rows back from L2
+    w.tgrid[(int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1] = throughput(bb, lat);
   }
 }
 
@@ -759,6 +768,19 @@ __device__ __forceinline__ void tk_bar_wait(uint64_t* bar, uint32_t parity) {
 // the first pod's quota row of a function, staged for the commit (102 doubles = 816 B,
 // the 101-entry row plus 8 bytes of the next row so the bulk size is a multiple of 16)
 constexpr int kRowStage = 102;
+
+// loads through generic pointers known to address shared memory
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int lds_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
 
 // conflict-mark slot of partition (g, pos) for fast_run (collisions only shorten runs)
 constexpr int kFastHash = 512;
@@ -1238,6 +1260,13 @@ struct Commit {
       TPROF_ACC(7);  // change_quota + emit
     }
     TPROF_ACC(1);
+    scale_up_h(f, now, pre, gap, npods);
+  }
+
+  // the horizontal part of _scale_up (autoscaler.py:137-165) for the gap the walk left
+  __device__ void scale_up_h(int f, double now, const Pre& pre, double gap, int npods) const {
+    TPROF_T0();
+    const int d = w.delta;
     const int bref = pre.bref;
     // one pod on the used GPU with the lowest occupancy (autoscaler.py:137-152)
     if (gap > 0.0) {
@@ -1376,42 +1405,55 @@ struct Commit {
   // walk verbatim — and every lane below it joined too.  Returns the lanes committed (their
   // changes applied, actions emitted in function order); 0 leaves the first one to the
   // sequential path.  htab: conflict marks (epoch << 5 | 31 - lane) by partition hash.
+  // dead: the lanes whose own validation failed (their partitions changed since phase A;
+  // the sequential path redoes them).
   __device__ unsigned fast_run(int base, unsigned cand, const FastRec& r, int stamp,
-                               double now, uint32_t* htab, uint32_t epoch) const {
+                               double now, uint32_t* htab, uint32_t epoch,
+                               unsigned& dead) const {
     const bool in = (cand >> lane) & 1;
-    const int n = in ? r.n : 0;
+    // every field up front (independent shared loads, one latency)
+    const int n = r.n, kind = r.kind;
+    FastStep st[kFastSteps];
+#pragma unroll
+    for (int k = 0; k < kFastSteps; ++k) st[k] = r.st[k];
     bool ok = in;
-    uint64_t* P[kFastSteps];
+    uint32_t pa[kFastSteps];  // shared address of the entry's low word
     bool wr[kFastSteps];
 #pragma unroll
     for (int k = 0; k < kFastSteps; ++k) {
-      P[k] = nullptr;
-      wr[k] = false;
-      if (k < n) {
-        const FastStep& st = r.st[k];
-        uint64_t* L = parts(st.g);
-        if (st.pos < w.g_nparts[st.g] && part_uid(L[st.pos]) == st.uid) {
-          P[k] = L + st.pos;
-          if (st.alloc0 >= 0 && part_alloc(*P[k]) != st.alloc0) ok = false;
-          wr[k] = st.qnew != st.qold;
-        } else {
-          ok = false;
-        }
-      }
+      const bool have = in && k < n;
+      const int g = have ? st[k].g : 0;
+      const int pos = have && st[k].pos < ps ? st[k].pos : 0;
+      pa[k] = (uint32_t)__cvta_generic_to_shared(sp + int64_t(g) * ps + pos);
+      const uint64_t e = lds_u64(pa[k]);
+      const int np = lds_s32(w.g_nparts + g);
+      const int o = ovf[g];
+      // shared-memory lists only; the position and uid still those of phase A
+      const bool good = o == 0 && st[k].pos < np && st[k].pos < ps &&
+                        part_uid(e) == st[k].uid &&
+                        (st[k].alloc0 < 0 || part_alloc(e) == st[k].alloc0);
+      if (have && !good) ok = false;
+      wr[k] = have && st[k].qnew != st[k].qold;
     }
-    const uint32_t mark = (epoch << 5) | uint32_t(31 - lane);
+    dead = cand & ~__ballot_sync(0xffffffffu, ok);
+    if (cand & (cand - 1)) {  // more than one lane: conflicts with lower lanes' writes
+      const uint32_t mark = (epoch << 5) | uint32_t(31 - lane);
 #pragma unroll
-    for (int k = 0; k < kFastSteps; ++k)
-      if (ok && wr[k]) atomicMax(htab + fast_hash(r.st[k].g, r.st[k].pos), mark);
-    __syncwarp();
+      for (int k = 0; k < kFastSteps; ++k)
+        if (ok && wr[k]) atomicMax(htab + fast_hash(st[k].g, st[k].pos), mark);
+      __syncwarp();
 #pragma unroll
-    for (int k = 0; k < kFastSteps; ++k)
-      if (ok && k < n && r.st[k].alloc0 >= 0) {
-        const uint32_t v = htab[fast_hash(r.st[k].g, r.st[k].pos)];
-        if ((v >> 5) == epoch && int(31 - (v & 31)) < lane) ok = false;
-      }
+      for (int k = 0; k < kFastSteps; ++k)
+        if (ok && k < n && st[k].alloc0 >= 0) {
+          const uint32_t v = htab[fast_hash(st[k].g, st[k].pos)];
+          if ((v >> 5) == epoch && int(31 - (v & 31)) < lane) ok = false;
+        }
+    }
     const unsigned bad = cand & ~__ballot_sync(0xffffffffu, ok);
     const unsigned run = bad ? cand & ((1u << (__ffs(bad) - 1)) - 1) : cand;
+#ifdef RAPP_TICK_PROF
+    if (lane == 0) s_tprof[14] += __popc(run);
+#endif
     if (run == 0) return 0;
     const bool mine = (run >> lane) & 1;
     int cnt = 0;
@@ -1419,32 +1461,36 @@ struct Commit {
 #pragma unroll
       for (int k = 0; k < kFastSteps; ++k)
         if (wr[k]) {
-          const FastStep& st = r.st[k];
-          const int delta = st.qnew - st.qold;
-          atomicAdd(reinterpret_cast<unsigned long long*>(P[k]),
-                    (unsigned long long)((long long)delta * 256));  // alloc field (bits 8..15)
-          atomicAdd(w.g_hgo + st.g, st.s * delta);
-          w.p_q[st.p] = st.qnew;
+          const int delta = st[k].qnew - st[k].qold;
+          // shared-memory reductions: the alloc field (bits 8..15 of the entry's low word,
+          // 0..100 before and after, so nothing carries) and the GPU's occupancy
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(pa[k]), "r"(uint32_t(delta * 256))
+                       : "memory");
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(
+              (uint32_t)__cvta_generic_to_shared(w.g_hgo + st[k].g)), "r"(st[k].s * delta)
+                       : "memory");
+          w.p_q[st[k].p] = st[k].qnew;
           ++cnt;
         }
     }
-    __syncwarp();
     const unsigned b1 = __ballot_sync(0xffffffffu, mine && cnt >= 1);
     const unsigned b2 = __ballot_sync(0xffffffffu, mine && cnt >= 2);
-    const unsigned below = (1u << lane) - 1;
     const int at0 = *nact;
+    __syncwarp();  // every lane's reductions are done
     if (mine) {
-      int at = at0 + __popc(b1 & below) + __popc(b2 & below);
+      int at = at0 + __popc(b1 & ((1u << lane) - 1)) + __popc(b2 & ((1u << lane) - 1));
       const int f = base + lane;
 #pragma unroll
       for (int k = 0; k < kFastSteps; ++k)
         if (wr[k]) {
-          const FastStep& st = r.st[k];
-          rekey0(st.g);  // after every lane's occupancy update (syncwarp above)
-          w.actions[at++] = rapp_action{f, st.alloc0 >= 0 ? kVUp : kVDown, st.b, st.s,
-                                        st.qnew, st.p, st.g, 0};
+          const int g = st[k].g;
+          if (skey != nullptr)
+            skey[g] = lds_s32(w.g_npods + g) > 0
+                          ? (uint32_t(lds_s32(w.g_hgo + g)) << 18) | uint32_t(g) : ~0u;
+          w.actions[at++] = rapp_action{f, kind == kFastDown ? kVDown : kVUp, st[k].b, st[k].s,
+                                        st[k].qnew, st[k].p, g, 0};
         }
-      if (stamp && r.st[0].alloc0 < 0) w.last_down[f] = now;
+      if (stamp && kind == kFastDown) w.last_down[f] = now;
     }
     __syncwarp();
     if (lane == 0) *nact = at0 + __popc(b1) + __popc(b2);
@@ -1543,11 +1589,16 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
       s_pre[slot][lane] = Commit::prefetch_of(w, f);
       {
         FastRec& fr = s_fast[slot][lane];
-        fr.n = 0;
+        fr.kind = kFastNone;
         if (w.policy == 0 && cf != kNone) {
-          const int n = w.fast[f].n;
-          for (int k = 0; k < n; ++k) fr.st[k] = w.fast[f].st[k];
-          fr.n = n;
+          const int kind = w.fast[f].kind;
+          if (kind != kFastNone) {
+            const int n = w.fast[f].n;
+            for (int k = 0; k < n; ++k) fr.st[k] = w.fast[f].st[k];
+            fr.n = n;
+            fr.gap = w.fast[f].gap;
+          }
+          fr.kind = kind;
         }
       }
       __threadfence_block();
@@ -1601,7 +1652,7 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter, skey};
   bool stop = s_err != 0;
 #ifdef RAPP_TICK_PROF
-  if (lane < 16) s_tprof[lane] = 0;
+  s_tprof[lane] = 0;
   __syncwarp();
 #endif
   // First-pod quota rows of the scale-up functions of a batch of 32 are bulk-copied into
@@ -1644,17 +1695,49 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
     tk_bar_wait(&s_rbar[j & 1], (j >> 1) & 1);
     TPROF_ACC(0);  // waits for the header ring and the staged rows
     unsigned act = __ballot_sync(0xffffffffu, mine != kNone);
-    const unsigned fastm = __ballot_sync(0xffffffffu, mine != kNone && s_fast[slot][lane].n > 0);
+    // (straight-line commits update the shared-memory GPU summaries: smem_g only)
+    const int fk = mine != kNone && smem_g ? s_fast[slot][lane].kind : kFastNone;
+    unsigned fastm = __ballot_sync(0xffffffffu, fk == kFastUp || fk == kFastDown);
+    unsigned tailm = __ballot_sync(0xffffffffu, fk == kFastTail);
+#ifdef RAPP_TICK_PROF
+    if (lane == 0) s_tprof[15] += __popc(fastm | tailm);
+#endif
     while (act) {
       const int i = __ffs(act) - 1;
-      if ((fastm >> i) & 1) {
-        // straight-line functions from i up to the next one that is not
+      if (((fastm | tailm) >> i) & 1) {
+        // straight-line functions from i up to the next one that is not, plus that one
+        // when only its horizontal branch is not
         const unsigned slow = act & ~fastm;
-        const unsigned cand = act & fastm & (slow ? (1u << (__ffs(slow) - 1)) - 1 : ~0u);
+        const int s0 = slow ? __ffs(slow) - 1 : 32;
+        unsigned cand = act & fastm & (s0 < 32 ? (1u << s0) - 1 : ~0u);
+        if (s0 < 32 && ((tailm >> s0) & 1)) cand |= 1u << s0;
+        unsigned dead;
+#ifdef RAPP_TICK_PROF
+        const long long _fr0 = clock64();
+#endif
         const unsigned done = c.fast_run(base, cand, s_fast[slot][lane], s_pre[slot][lane].stamp,
-                                         now, s_htab, ++epoch);
+                                         now, s_htab, ++epoch, dead);
+        fastm &= ~dead;  // a changed partition stays changed: no second attempt
+        tailm &= ~dead;
+#ifdef RAPP_TICK_PROF
+        if (lane == 0) {
+          s_tprof[16] += clock64() - _fr0;
+          s_tprof[17] += 1;
+          s_tprof[19] += done != 0;
+        }
+#endif
         if (done) {
           act &= ~done;
+          const unsigned tl = done & tailm;  // the run's last lane, walk applied
+          if (tl) {
+            const int k = __ffs(tl) - 1;
+            c.scale_up_h(base + k, now, s_pre[slot][k], s_fast[slot][k].gap, s_pre[slot][k].npods);
+            __syncwarp();
+            if (s_err) {
+              stop = true;
+              break;
+            }
+          }
           continue;
         }
       }
@@ -1683,7 +1766,7 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
 #ifdef RAPP_TICK_PROF
   __syncwarp();
-  if (lane < 16) g_tick_prof[lane] += s_tprof[lane];
+  g_tick_prof[lane] += s_tprof[lane];
 #endif
   if (lane == 0) {
     *w.n_pods = s_npods;
@@ -1859,8 +1942,8 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     RAPP_LAUNCHED();
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
-    // 227 KB per CTA minus the row staging and ~25 KB of static shared memory
-    const size_t budget = 227 * 1024 - size_t(2 * 32 * kRowStage) * 8 - 26 * 1024;
+    // 227 KB per CTA minus the row staging and the static shared memory (~26 KB)
+    const size_t budget = 227 * 1024 - size_t(2 * 32 * kRowStage) * 8 - 28 * 1024;
     const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
     const size_t fixed = gbytes + size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16;
     const int smem_g = fixed <= budget ? 1 : 0;
@@ -2454,10 +2537,10 @@ int rapp_tick_counter(rapp_tick* t, int64_t* c) {
 #ifdef RAPP_TICK_PROF
 int rapp_tick_prof_read(uint64_t* out8, int reset) {
   RAPP_CUDA(cudaDeviceSynchronize());
-  RAPP_CUDA(cudaMemcpyFromSymbol(out8, g_tick_prof, 128));
+  RAPP_CUDA(cudaMemcpyFromSymbol(out8, g_tick_prof, 256));
   if (reset) {
-    uint64_t z[16] = {};
-    RAPP_CUDA(cudaMemcpyToSymbol(g_tick_prof, z, 128));
+    uint64_t z[32] = {};
+    RAPP_CUDA(cudaMemcpyToSymbol(g_tick_prof, z, 256));
   }
   return RAPP_OK;
 }

@@ -19,7 +19,8 @@ from paper_2505_01968_b200.tick import TickEngine  # noqa: E402
 NAMES = ["batch wait", "vertical spec/walk", "used-GPU rest", "fresh-GPU branch",
          "scale-down", "vertical headroom", "functions (wall)", "vertical change+emit",
          "hu argmin", "hu best_slot", "hu T+covering", "hu new_pod", "hu place", "hu emit",
-         "-", "-"]
+         "fast lanes", "fast candidates", "fast_run", "fast_run calls", "-", "runs committed"]
+COUNTS = (14, 15, 17, 19)
 
 
 def main(full_grid, nticks=6):
@@ -34,7 +35,7 @@ def main(full_grid, nticks=6):
     lib = _lib.load()
     rd = lib.rapp_tick_prof_read
     rd.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    buf = np.zeros(16, dtype=np.uint64)
+    buf = np.zeros(32, dtype=np.uint64)
     rd(buf.ctypes.data, 1)
     rng = random.Random(0)
     order = sorted(fns, key=lambda f: f.function_id)
@@ -48,8 +49,10 @@ def main(full_grid, nticks=6):
         eng2.tick(2000.0 * (k + 1), host)
         mix = collections.Counter(str(x.kind).split(".")[-1] for x in res.actions)
         us = buf.astype(np.float64) / 1.9e3
+        for i in COUNTS:
+            us[i] = buf[i]  # counts, not cycles
         print(f"tick {k} actions {len(res.actions)} {dict(mix)}")
-        print("   " + ", ".join(f"{NAMES[i]} {us[i]:.0f}us" for i in range(16) if NAMES[i] != "-"))
+        print("   " + ", ".join(f"{NAMES[i]} {us[i]:.0f}us" for i in range(len(NAMES)) if NAMES[i] != "-"))
 
 
 if __name__ == "__main__":
