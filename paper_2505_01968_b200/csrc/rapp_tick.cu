@@ -495,41 +495,58 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
             thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 + k * d));
     }
     __syncwarp();
-    if (lane == 0) {
+    {
       // Speculate the vertical walk (autoscaler.py:115-133) with the tick-start headroom
       // of each pod's partition.  The walk of pod j depends only on that headroom and on
       // the gap left by pods 0..j-1 of this function, so phase B reuses it verbatim while
-      // every headroom it observes equals the one assumed here.
+      // every headroom it observes equals the one assumed here.  Warp-wide: every lane
+      // holds the same gap; the partition lookup and the walk's stopping step are found
+      // lane-parallel.
       double gap = w.gap0[f];
       FastRec fr;
       fr.n = 0;
       bool simple = true;
       for (int j = 0; j < m; ++j) {
-        w.spec_avail[f * kMaxPods + j] = -1;
+        if (lane == 0) w.spec_avail[f * kMaxPods + j] = -1;
         if (!(gap > 0.0)) continue;
         const int p = srt[j];
         if (w.p_state[p] != kRunning) continue;
         const int g = w.p_gpu[p];
+        const uint32_t uid = w.p_puid[p];
         const uint64_t* P = w.g_parts + int64_t(g) * kPartCap;
-        int alloc = 100, pos = -1;
-        for (int i = 0; i < w.g_nparts[g]; ++i)
-          if (part_uid(P[i]) == w.p_puid[p]) {
-            alloc = part_alloc(P[i]);
-            pos = i;
-            break;
-          }
+        const int np = w.g_nparts[g];
+        unsigned upos = 1u << 30;
+        for (int i = lane; i < np; i += 32)
+          if (part_uid(P[i]) == uid) upos = min(upos, unsigned(i));
+        upos = __reduce_min_sync(0xffffffffu, upos);
+        const int pos = upos < unsigned(np) ? int(upos) : -1;
+        const int alloc = pos >= 0 ? part_alloc(P[pos]) : 100;
         const int q0 = w.p_q[p];
         const int avail = q0 + (100 - alloc);
-        const double* row = rows + j * kRow + w.row_kd[f * kMaxPods + j];
-        int k = 0;
+        const double* row = rows + j * kRow + (q0 - 1) / d;
+        // k = first step with q0 + (k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0
+        // (k <= (100 - q0) / d < 128: lanes hold k = lane + 32u)
+        const double cur = row[0];
+        int k = -1;
         double gain = 0.0;
-        while (q0 + (k + 1) * d <= avail && __dsub_rn(gap, gain) > 0.0) {
-          ++k;
-          gain = __dsub_rn(row[k], row[0]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = u * 32 + lane;
+          const bool in = kk > 0 && q0 + kk * d <= avail;
+          const double gk = in ? __dsub_rn(row[kk], cur) : 0.0;
+          const bool stop = q0 + (kk + 1) * d > avail || !(__dsub_rn(gap, gk) > 0.0);
+          const unsigned mask = __ballot_sync(0xffffffffu, stop);
+          if (mask && k < 0) {
+            const int l = __ffs(mask) - 1;
+            k = u * 32 + l;
+            gain = __shfl_sync(0xffffffffu, gk, l);
+          }
         }
-        w.spec_avail[f * kMaxPods + j] = avail;
-        w.spec_k[f * kMaxPods + j] = k;
-        w.spec_gain[f * kMaxPods + j] = gain;
+        if (lane == 0) {
+          w.spec_avail[f * kMaxPods + j] = avail;
+          w.spec_k[f * kMaxPods + j] = k;
+          w.spec_gain[f * kMaxPods + j] = gain;
+        }
         if (k > 0) gap = __dsub_rn(gap, gain);
         // a second walked pod on the same partition would see the first one's change
         for (int t = 0; t < fr.n && t < kFastSteps; ++t)
@@ -541,11 +558,13 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
           simple = false;
         ++fr.n;
       }
-      w.fast[f].kind = !simple ? kFastNone : gap > 0.0 ? kFastTail : kFastUp;
-      w.fast[f].n = fr.n;
-      w.fast[f].gap = gap;
-      for (int t = 0; t < fr.n && t < kFastSteps; ++t) w.fast[f].st[t] = fr.st[t];
-      w.cls[f] = kUp;
+      if (lane == 0) {
+        w.fast[f].kind = !simple ? kFastNone : gap > 0.0 ? kFastTail : kFastUp;
+        w.fast[f].n = fr.n;
+        w.fast[f].gap = gap;
+        for (int t = 0; t < fr.n && t < kFastSteps; ++t) w.fast[f].st[t] = fr.st[t];
+        w.cls[f] = kUp;
+      }
     }
     return;
   }
@@ -585,7 +604,10 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
           thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 - k * d));
   }
   __syncwarp();
-  if (lane == 0) {
+  cap = __shfl_sync(0xffffffffu, cap, 0);
+  {
+    // warp-wide: every lane holds the same excess; each pod's stopping step is found
+    // lane-parallel, the staged actions are written by lane 0
     double excess = __dsub_rn(cap, R);
     int alive = nr, na = 0;
     DownAct* out = w.down + f * kMaxPods;
@@ -598,30 +620,50 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
       const int q0 = w.p_q[p];
       const int kd = (q0 - 1) / d;
       const double cur = row[kd];
+      // q_k = max(q0 - k d, 0), shed_k = q_k == 0 ? cur : cur - row[kd - k]; the loop stops
+      // at the first k >= 1 with q_k == 0 or !(excess - shed_k > 0) (k <= ceil(q0/d) <= 100)
       int q = q0;
       double shed = 0.0;
-      while (q > 0 && __dsub_rn(excess, shed) > 0.0) {
-        q = q - d > 0 ? q - d : 0;
-        shed = q == 0 ? cur : __dsub_rn(cur, row[kd - (q0 - q) / d]);
+      if (__dsub_rn(excess, 0.0) > 0.0) {  // (the loop's first test, k = 0)
+        int ks = -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = u * 32 + lane + 1;
+          const int qk = q0 - kk * d > 0 ? q0 - kk * d : 0;
+          const double sk = qk == 0 ? cur : __dsub_rn(cur, row[kd - kk]);
+          const bool stop = qk == 0 || !(__dsub_rn(excess, sk) > 0.0);
+          const unsigned mask = __ballot_sync(0xffffffffu, stop);
+          if (mask && ks < 0) {
+            const int l = __ffs(mask) - 1;
+            ks = u * 32 + l + 1;
+            q = __shfl_sync(0xffffffffu, qk, l);
+            shed = __shfl_sync(0xffffffffu, sk, l);
+          }
+        }
       }
       if (q == 0) {
         if (alive <= 1) {
           const int floor_q = q0 - d * ((q0 - 1) / d);
           if (floor_q < q0) {
             shed = __dsub_rn(cur, row[kd - (q0 - floor_q) / d]);
-            out[na++] = DownAct{kVDown, p, floor_q, 0};
+            if (lane == 0) out[na] = DownAct{kVDown, p, floor_q, 0};
+            ++na;
             excess = __dsub_rn(excess, shed);
           }
           continue;
         }
         --alive;
-        out[na++] = DownAct{kHDown, p, 0, 0};
+        if (lane == 0) out[na] = DownAct{kHDown, p, 0, 0};
+        ++na;
         excess = __dsub_rn(excess, cur);
       } else if (q < q0) {
-        out[na++] = DownAct{kVDown, p, q, 0};
+        if (lane == 0) out[na] = DownAct{kVDown, p, q, 0};
+        ++na;
         excess = __dsub_rn(excess, shed);
       }
     }
+    __syncwarp();
+    if (lane != 0) return;
     w.ndown[f] = na;
     w.stamp[f] = na > 0;
     // vertical steps only: no decision reads shared state, the commit just applies them
