@@ -1019,8 +1019,18 @@ struct Commit {
     // occupancy <= 100*100 per GPU, so (occupancy, rank) packs into 32 bits for up to 2^18
     // GPUs: one scan and one warp min-reduction
     if (skey != nullptr) {  // maintained keys: one shared-memory word per GPU
+      // 8 independent loads per lane in flight (a plain strided loop waits on each)
       unsigned best = ~0u;
-      for (int g = lane; g < w.G; g += 32) best = min(best, skey[g]);
+      for (int g0 = 0; g0 < w.G; g0 += 256) {
+        unsigned k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int g = g0 + u * 32 + lane;
+          k[u] = g < w.G ? skey[g] : ~0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) best = min(best, k[u]);
+      }
       best = __reduce_min_sync(0xffffffffu, best);
       return best == ~0u ? -1 : int(best & ((1u << 18) - 1));
     }
