@@ -1662,7 +1662,8 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   World v = w;
   const int G = w.G;
   // shared layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)][ovf G bytes]
-  uint64_t* sp = reinterpret_cast<uint64_t*>(sg + ((5 * G + 1) & ~1));
+  // (no summaries region when they live in global memory)
+  uint64_t* sp = reinterpret_cast<uint64_t*>(sg + (smem_g ? ((5 * G + 1) & ~1) : 0));
   uint8_t* ovf = reinterpret_cast<uint8_t*>(sp + int64_t(G) * ps);
   uint32_t* skey = (smem_g && G <= (1 << 18))
                        ? reinterpret_cast<uint32_t*>(ovf + ((G + 3) & ~3)) : nullptr;
@@ -2002,8 +2003,9 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     int ps = 0;
     if (smem_g)
       ps = (int)std::min<size_t>(12, (budget - fixed) / (8 * std::max(1, w.G)));
-    const size_t bytes = size_t(2 * 32 * kRowStage) * 8 + gbytes + size_t(w.G) * ps * 8 +
-                         size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16;  // + argmin keys
+    const size_t bytes = smem_g ? size_t(2 * 32 * kRowStage) * 8 + gbytes + size_t(w.G) * ps * 8 +
+                                      size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16  // + keys
+                                : size_t(2 * 32 * kRowStage) * 8 + size_t(w.G) + 16;   // ovf only
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
     k_tick_commit<<<1, 64, bytes, st>>>(w, now, smem_g, ps);

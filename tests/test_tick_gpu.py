@@ -152,6 +152,19 @@ def test_random_worlds_vs_oracle(delta, ngpu, nfn):
                   cold_start_ms=1500.0)
 
 
+def test_many_gpus_global_summaries_vs_oracle():
+    """6,000 / 9,000 GPUs: the partition lists, then also the per-GPU summaries, no longer
+    fit the commit's shared-memory budget, so the commit runs on global memory (and without
+    straight-line runs); ids past gpu-999 also exercise string-ordered GPU ranks."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    for ngpu in (6000, 9000):  # summaries in shared memory without partition lists; neither
+        fns, tables, cluster, _ = bench.make_config4_world(48, ngpu, seed=11)
+        cfg = ScalerConfig(alpha=0.85, beta=0.4, delta_iq=10, cooldown_ms=1000.0, r_min=1.0)
+        _oracle_ticks(fns, tables, cluster, cfg, 4, seed=11, interval_ms=1000.0,
+                      cold_start_ms=1500.0)
+
+
 def test_full_grid_fresh_gpu_search_vs_oracle():
     """Full-grid tables (32x91x100, delta 1): the fresh-GPU most_efficient_config runs on a
     291,200-point lattice through the prefix-max index."""
