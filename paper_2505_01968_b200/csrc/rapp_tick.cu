@@ -898,8 +898,9 @@ struct Commit {
     const int delta = new_q - old_q;
     set_entry(g, pos, part_pack(part_sm(e), part_alloc(e) + delta, part_npods(e), part_uid(e)));
     if (lane == 0) {
-      w.g_hgo[g] += s * delta;
-      rekey0(g);
+      const int h1 = w.g_hgo[g] + s * delta;
+      w.g_hgo[g] = h1;
+      if (skey != nullptr) skey[g] = (uint32_t(h1) << 18) | uint32_t(g);  // the pod is resident
       w.p_q[p] = new_q;
     }
     __syncwarp();
@@ -936,6 +937,45 @@ struct Commit {
       w.g_npods[g] += 1;
       w.g_hgo[g] += s * q;
       rekey0(g);
+    }
+    __syncwarp();
+  }
+
+  // place() right after best_slot(g) (nothing changed g's list since): the lanes still hold
+  // the entries of a list of <= 32 partitions, so the join search is one ballot
+  __device__ void place_known(int p, int g, int s, int q, uint64_t e0, int n) const {
+    if (n > 32) {
+      place(p, g, s, q);
+      return;
+    }
+    const unsigned hit =
+        __ballot_sync(0xffffffffu, lane < n && part_sm(e0) == s && 100 - part_alloc(e0) >= q);
+    const int pos = hit ? __ffs(hit) - 1 : -1;
+    const uint64_t e = __shfl_sync(0xffffffffu, e0, pos < 0 ? 0 : pos);
+    if (lane == 0) {
+      uint64_t* P = parts(g);
+      if (pos < 0) {
+        if (n >= kPartCap || w.g_freesm[g] < s) {
+          fail0(RAPP_E_PLACEMENT, -1);
+        } else {
+          make_room(g, n);
+          P = parts(g);
+          const uint32_t uid = w.g_nextuid[g]++;
+          P[n] = part_pack(s, q, 1, uid);
+          w.g_nparts[g] = n + 1;
+          w.g_freesm[g] -= s;
+          w.p_puid[p] = uid;
+        }
+      } else {
+        P[pos] = part_pack(part_sm(e), part_alloc(e) + q, part_npods(e) + 1, part_uid(e));
+        w.p_puid[p] = part_uid(e);
+      }
+      w.p_gpu[p] = g;
+      const int np1 = w.g_npods[g] + 1;
+      const int h1 = w.g_hgo[g] + s * q;
+      w.g_npods[g] = np1;
+      w.g_hgo[g] = h1;
+      if (skey != nullptr) skey[g] = (uint32_t(h1) << 18) | uint32_t(g);
     }
     __syncwarp();
   }
@@ -1067,17 +1107,21 @@ struct Commit {
 
   // max_avail_quota_and_sm (allocator.py:26-52): max of (sm*hr, sm, join=1) over
   // partitions with headroom (first wins ties), then (free*100, free, 0) if strictly greater
-  __device__ void best_slot(int g, int& sm, int& q) const {
+  // e0 / n: this lane's entry of the list (lane < n) and the list length, for place_known
+  __device__ void best_slot(int g, int& sm, int& q, uint64_t& e0, int& n) const {
     const uint64_t* P = parts(g);
-    const int n = w.g_nparts[g];
+    n = w.g_nparts[g];
+    const int free_sm = w.g_freesm[g];
+    e0 = lane < n ? P[lane] : 0;
     // key: prod (15 bits) | sm (8) | (255 - pos) (8): max key = max (prod, sm), first pos
     // (prod <= 10^4 -> the key fits 31 bits: one redux instead of a shuffle tree)
     unsigned ukey = 0;
     for (int i = lane; i < n; i += 32) {
-      const int hr = 100 - part_alloc(P[i]);
+      const uint64_t e = i == lane ? e0 : P[i];
+      const int hr = 100 - part_alloc(e);
       if (hr > 0) {
-        const unsigned k = (unsigned(part_sm(P[i]) * hr) << 16) |
-                           (unsigned(part_sm(P[i])) << 8) | unsigned(255 - i);
+        const unsigned k = (unsigned(part_sm(e) * hr) << 16) | (unsigned(part_sm(e)) << 8) |
+                           unsigned(255 - i);
         ukey = k > ukey ? k : ukey;
       }
     }
@@ -1086,15 +1130,16 @@ struct Commit {
     sm = 0;
     q = 0;
     long long bprod = -1, bsm = -1, bjoin = -1;
-    if (best >= 0) {
-      const int pos = 255 - int(best & 0xFF);
-      sm = part_sm(P[pos]);
-      q = 100 - part_alloc(P[pos]);
+    if (best >= 0) {  // (sm, headroom) of the best partition: a lane still holds it
+      const int pos = 255 - int(ukey & 0xFF);
+      const uint64_t eb = __shfl_sync(0xffffffffu, e0, pos & 31);
+      const uint64_t e = pos < 32 ? eb : P[pos];
+      sm = part_sm(e);
+      q = 100 - part_alloc(e);
       bprod = (long long)sm * q;
       bsm = sm;
       bjoin = 1;
     }
-    const int free_sm = w.g_freesm[g];
     if (free_sm > 0) {
       const long long fp = (long long)free_sm * 100;
       const bool greater = best < 0 || fp > bprod || (fp == bprod && (free_sm > bsm ||
@@ -1325,8 +1370,9 @@ struct Commit {
       const int g = argmin_used();
       TPROF_ACC(8);
       if (g >= 0) {
-        int sm, qmax;
-        best_slot(g, sm, qmax);
+        int sm, qmax, nl;
+        uint64_t el;
+        best_slot(g, sm, qmax, el, nl);
         TPROF_ACC(9);
         if (sm > 0 && qmax > 0) {
           if (!pre.brefok) {
@@ -1374,7 +1420,7 @@ struct Commit {
             const int p = new_pod(f, bref, sm, quota, now, npods);
             TPROF_ACC(11);  // new_pod
             if (p < 0) return;
-            place(p, g, sm, quota);
+            place_known(p, g, sm, quota, el, nl);
             TPROF_ACC(12);  // place
             emit(f, kHUp, bref, sm, quota, p, g, 0);
             TPROF_ACC(13);  // emit
