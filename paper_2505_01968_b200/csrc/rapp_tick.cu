@@ -23,7 +23,11 @@
 //    that read shared state — partition headroom for the vertical walk, the lowest
 //    (occupancy, gpu id) used GPU, its best slot, the covering quota, the first free GPU
 //    and the fresh-GPU configuration search (prefix-max index, see below) — applying each
-//    action to the device cluster before the next function decides.
+//    action to the device cluster before the next function decides.  Consecutive
+//    functions whose commit phase A already knows up to a validation (FastRec: a vertical
+//    walk that closes the gap, or one followed by the horizontal branch, or vertical
+//    scale-down steps) are committed one per lane in a single step (Commit::fast_run),
+//    under exactly the conditions in which the sequential walk would repeat phase A's.
 //
 // Every floating-point expression is evaluated in the reference's order with individually
 // rounded operations (interp3 / throughput from rapp_device.cuh; explicit _rn intrinsics).
