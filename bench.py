@@ -402,24 +402,29 @@ def load_traffic(n, kernel="k_interp_stream", field="dram_bytes_per_prediction")
 
 def lattice_fp64_ops(table, batches, step):
     """FP64 operations K3 executes per lattice point of one function (algorithmic work of
-    the segment formulation, rapp_search.cu): per (s, q) pair 9 ops (three lerps of
-    sub/mul/add) for every distinct table row a batch segment brackets, 1 sub per segment,
-    and per point the final batch lerp (mul, add) plus the feasibility compare."""
-    from paper_2505_01968_b200.perf import PerfTable  # noqa: F401  (typing only)
+    the run formulation, rapp_search.cu): the lattice's sm values are table nodes, so a
+    row value is one quota lerp (sub/mul/add); batch entries are grouped in runs by their
+    lower row (node hits and clamps join the run at their row), each run needs its lower
+    row (3 ops), its upper row unless the run above produced it (3 ops) and one sub; every
+    point is the final batch lerp (mul, add) plus the feasibility compare."""
     ax = list(table._b_axis)
-    segs, rows = [], set()
+    last = len(ax) - 1
+    runs = []
     for b in batches:
         if b <= ax[0]:
-            br = (0, 0)
+            lo = 0
         elif b >= ax[-1]:
-            br = (len(ax) - 1, len(ax) - 1)
+            lo = last
         else:
             lo = max(i for i in range(len(ax)) if ax[i] <= b)
-            br = (lo, lo) if ax[lo] == b else (lo, lo + 1)
-        if not segs or segs[-1] != br:
-            segs.append(br)
-        rows.update(br)
-    per_pair = 9 * len(rows) + len(segs) + 3 * len(batches)
+        if not runs or runs[-1] != lo:
+            runs.append(lo)
+    per_pair, up = 3 * len(batches), -2
+    for lo in reversed(runs):
+        per_pair += 3
+        if lo != last:
+            per_pair += 1 + (0 if lo + 1 == up else 3)
+        up = lo
     return per_pair / len(batches)
 
 

@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(kSearchThreads)
   p += (p - smem) & 1;                           // 16-byte alignment for the vectors below
   double2* sTT = (double2*)p;      p += 2 * nB;  // (tb, threshold) per batch entry
   int4* sSeg = (int4*)p;           p += 2 * nB;  // runs of entries sharing a row bracket
-  __shared__ int s_nseg;
+  int4* sLo = (int4*)p;            p += 2 * nB;  // runs of entries sharing a lower row
+  __shared__ int s_nseg, s_nlo;
 
   // per-axis brackets, once per CTA (locate semantics, _grid_cy.pyx:9-33)
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -186,18 +187,35 @@ __global__ void __launch_bounds__(kSearchThreads)
   __syncthreads();
   // batch entries are sorted, so entries bracketed by the same table rows (i0, i1) are
   // consecutive: one segment per bracket, its two row values computed once per (s, q)
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int i = 0; i < nB; ++i) {
-      if (i == 0 || sI[i].x != sI[i - 1].x || sI[i].y != sI[i - 1].y)
-        sSeg[n++] = make_int4(sI[i].x, sI[i].y, i, i + 1);
-      else
-        sSeg[n - 1].w = i + 1;
+  // (warp 0: run heads by ballot, positions by popcount prefix)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int n = 0, m = 0;
+    for (int base = 0; base < nB; base += 32) {
+      const int i = base + lane;
+      const bool in = i < nB;
+      const int2 cur = in ? sI[i] : make_int2(0, 0);
+      const int2 prv = in && i > 0 ? sI[i - 1] : make_int2(-1, -1);
+      const bool hs = in && (cur.x != prv.x || cur.y != prv.y);
+      const bool hl = in && cur.x != prv.x;
+      const unsigned ms = __ballot_sync(0xffffffffu, hs), ml = __ballot_sync(0xffffffffu, hl);
+      const unsigned below = (1u << lane) - 1u;
+      if (hs) sSeg[n + __popc(ms & below)] = make_int4(cur.x, cur.y, i, 0);
+      if (hl) sLo[m + __popc(ml & below)] = make_int4(cur.x, i, 0, 0);
+      n += __popc(ms);
+      m += __popc(ml);
     }
-    s_nseg = n;
+    __syncwarp();
+    // run ends: the next run's start (or nB)
+    for (int k = lane; k < n; k += 32) sSeg[k].w = k + 1 < n ? sSeg[k + 1].z : nB;
+    for (int k = lane; k < m; k += 32) sLo[k].z = k + 1 < m ? sLo[k + 1].y : nB;
+    if (lane == 0) {
+      s_nseg = n;
+      s_nlo = m;
+    }
   }
   __syncthreads();
-  const int nseg = s_nseg;
+  const int nseg = s_nseg, nlo = s_nlo;
   const bool pos_table = td.fast != 0;  // fast-path tables are finite and positive
 
   const double target = targets[f];
@@ -207,13 +225,23 @@ __global__ void __launch_bounds__(kSearchThreads)
   unsigned long long best = kNoKey;
   const int64_t row_stride = int64_t(ns) * nq;
 
-  for (int pr = p0 + threadIdx.x; pr < p1; pr += blockDim.x) {
-    const int si = pr / nQ, qi = pr - si * nQ;
+  auto record = [&](int si, int qi, int found) {
+    if (found < (1 << 30)) {
+      const uint64_t s = uint64_t(sa[si]);
+      const uint64_t q = uint64_t((qi + 1) * step);
+      const unsigned long long k =
+          ((s * q) << 32) | (uint64_t(si) << 20) | (q << 12) | uint64_t(found);
+      best = k < best ? k : best;
+    }
+  };
+
+  // Any table, any pair: the reference's row values (two-entry cache, rows visited in
+  // ascending order) and the batch segments.  Returns the first feasible batch entry.
+  auto generic_pair = [&](int si, int qi) -> int {
     const int2 jj = sJ[si], kk = sK[qi];
     const double ts = sTs[si], tq = sTq[qi];
     const int o00 = jj.x * nq + kk.x, o01 = jj.x * nq + kk.y;
     const int o10 = jj.y * nq + kk.x, o11 = jj.y * nq + kk.y;
-    // two-entry cache of per-row (c0 / c1) values; rows are visited in ascending order
     int ra = -1, rb = -1;
     double ca = 0.0, cb = 0.0;
     auto row = [&](int i) -> double {
@@ -230,30 +258,6 @@ __global__ void __launch_bounds__(kSearchThreads)
       return c;
     };
     int found = 1 << 30;  // first feasible batch entry (entries ascend with b)
-    if (!MINLAT && pos_table) {
-      // finite positive grid (checked at upload): every interpolated latency is > 0, so
-      // `rps >= target` is exactly `lat <= threshold` — no division on this path.  One flat
-      // pass over the batch entries; at a segment boundary (uniform across the CTA) the
-      // segment's row values are produced and c1 - c0 is formed once, so each entry costs
-      // the reference's final batch lerp c0 + (c1 - c0) * tb, a compare and a select.
-      int sg = 0;
-      int4 S = sSeg[0];
-      double c0 = row(S.x);
-      double d = __dsub_rn(S.y == S.x ? c0 : row(S.y), c0);
-      int end = S.w;
-#pragma unroll (kK3Unroll)
-      for (int bi = 0; bi < nB; ++bi) {
-        if (bi == end) {
-          S = sSeg[++sg];
-          c0 = row(S.x);
-          d = __dsub_rn(S.y == S.x ? c0 : row(S.y), c0);
-          end = S.w;
-        }
-        const double2 tt = sTT[bi];
-        const double lat = __dadd_rn(c0, __dmul_rn(d, tt.x));
-        found = lat <= tt.y && bi < found ? bi : found;
-      }
-    } else
     for (int sg = 0; sg < nseg; ++sg) {
       const int4 S = sSeg[sg];
       const double c0 = row(S.x);
@@ -264,8 +268,7 @@ __global__ void __launch_bounds__(kSearchThreads)
           if (lat >= 0.0) atomicMin(&sMin[bi], (unsigned long long)__double_as_longlong(lat));
         }
       } else if (pos_table) {
-        // finite positive grid (checked at upload): every interpolated latency is > 0, so
-        // `rps >= target` is exactly `lat <= threshold` — no division on this path
+        // finite positive grid: `rps >= target` is exactly `lat <= threshold`
         for (int bi = S.z; bi < S.w; ++bi) {
           const double2 tt = sTT[bi];
           const double lat = lerp_rn(c0, c1, tt.x);  // the reference's final batch lerp
@@ -280,12 +283,79 @@ __global__ void __launch_bounds__(kSearchThreads)
         }
       }
     }
-    if (!MINLAT && found < (1 << 30)) {
-      const uint64_t s = uint64_t(sa[si]);
-      const uint64_t q = uint64_t((qi + 1) * step);
-      const unsigned long long k =
-          ((s * q) << 32) | (uint64_t(si) << 20) | (q << 12) | uint64_t(found);
-      best = k < best ? k : best;
+    return found;
+  };
+
+  const int bd = int(blockDim.x);
+  if (!MINLAT && pos_table) {
+    // Meet pass over a finite positive grid (checked at upload): every interpolated
+    // latency is > 0, so `rps >= target` is exactly `lat <= threshold` — no division.
+    // Exact shortcuts of the reference's arithmetic for such grids (x + (y - x) * 0 == x
+    // for finite positive x and finite y):
+    //  * the lattice's sm values are the table's own nodes (j0 == j1, ts == 0), so a row
+    //    value is its quota lerp c_j0 — the same double the reference's c0 = c_j0 +
+    //    (c_j1 - c_j0) * 0 yields;
+    //  * a node hit or clamp (lo == hi, tb == 0) gives row(lo), which is also
+    //    row(lo) + (row(lo + 1) - row(lo)) * 0, so it joins the run of entries with lower
+    //    row lo; entries with lo == last use d = 0.
+    // Runs and entries are walked in descending order (the last feasible entry seen is the
+    // first in lattice order); each run needs one new row value.  Two (s, q) pairs per
+    // thread share the run bookkeeping and every (tb, threshold) load.
+    const int last = nb - 1;
+    for (int pa = p0 + int(threadIdx.x); pa < p1; pa += 2 * bd) {
+      const int pb = pa + bd < p1 ? pa + bd : pa;  // a lone last pair is evaluated twice
+      const int sia = pa / nQ, qia = pa - sia * nQ;
+      const int sib = pb / nQ, qib = pb - sib * nQ;
+      const int2 ja = sJ[sia], jb = sJ[sib];
+      if (ja.x != ja.y || jb.x != jb.y) {  // not produced by a lattice over table sms
+        record(sia, qia, generic_pair(sia, qia));
+        record(sib, qib, generic_pair(sib, qib));
+        continue;
+      }
+      const int2 ka = sK[qia], kb = sK[qib];
+      const double tqa = sTq[qia], tqb = sTq[qib];
+      const double* __restrict__ a0 = v + (ja.x * nq + ka.x);
+      const double* __restrict__ a1 = v + (ja.x * nq + ka.y);
+      const double* __restrict__ b0 = v + (jb.x * nq + kb.x);
+      const double* __restrict__ b1 = v + (jb.x * nq + kb.y);
+      int up = -2, fa = 1 << 30, fb = 1 << 30;
+      double cua = 0.0, cub = 0.0;
+      for (int sg = nlo - 1; sg >= 0; --sg) {
+        const int4 S = sLo[sg];
+        const int64_t o = int64_t(S.x) * row_stride;
+        const double c0a = lerp_rn(a0[o], a1[o], tqa);
+        const double c0b = lerp_rn(b0[o], b1[o], tqb);
+        double da = 0.0, db = 0.0;
+        if (S.x != last) {
+          double c1a = cua, c1b = cub;
+          if (S.x + 1 != up) {
+            const int64_t o1 = o + row_stride;
+            c1a = lerp_rn(a0[o1], a1[o1], tqa);
+            c1b = lerp_rn(b0[o1], b1[o1], tqb);
+          }
+          da = __dsub_rn(c1a, c0a);
+          db = __dsub_rn(c1b, c0b);
+        }
+        up = S.x;
+        cua = c0a;
+        cub = c0b;
+#pragma unroll (kK3Unroll)
+        for (int bi = S.z - 1; bi >= S.y; --bi) {
+          const double2 tt = sTT[bi];
+          const double la = __dadd_rn(c0a, __dmul_rn(da, tt.x));
+          const double lb = __dadd_rn(c0b, __dmul_rn(db, tt.x));
+          fa = la <= tt.y ? bi : fa;
+          fb = lb <= tt.y ? bi : fb;
+        }
+      }
+      record(sia, qia, fa);
+      record(sib, qib, fb);
+    }
+  } else {
+    for (int pr = p0 + int(threadIdx.x); pr < p1; pr += bd) {
+      const int si = pr / nQ, qi = pr - si * nQ;
+      const int found = generic_pair(si, qi);
+      if (!MINLAT) record(si, qi, found);
     }
   }
 
@@ -484,7 +554,7 @@ int rapp_mec_plan_create(rapp_ctx* ctx, int64_t nfn, const int32_t* table_of_fn,
     }
   pl->total_b = (int64_t)blist.size();
   pl->smem_table = max_seg * 8 <= kSearchSmemTable;
-  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 10 * max_nB + 2;
+  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 12 * max_nB + 2;
   pl->smem_bytes = (size_t)((pl->smem_table ? max_seg : 0) + brk) * 8;
   if (pl->smem_bytes > 200 * 1024) {
     set_error("lattice search shared-memory footprint %zu bytes too large", pl->smem_bytes);
