@@ -26,6 +26,7 @@
 //    one atomicMin per CTA into the per-function slot.
 #include <cstring>
 #include <memory>
+#include <type_traits>
 
 #include "rapp_device.cuh"
 #include "rapp_internal.h"
@@ -37,6 +38,10 @@
 namespace rapp {
 
 constexpr int kK3Unroll = RAPP_K3_UNROLL;  // unroll of the per-batch-entry loop
+#ifndef RAPP_K3_PAIRS
+#define RAPP_K3_PAIRS 3
+#endif
+constexpr int kK3Pairs = RAPP_K3_PAIRS;  // (s, q) pairs per thread in the meet pass
 
 struct FnDesc {
   int32_t table;
@@ -299,58 +304,75 @@ __global__ void __launch_bounds__(kSearchThreads)
     //    row(lo) + (row(lo + 1) - row(lo)) * 0, so it joins the run of entries with lower
     //    row lo; entries with lo == last use d = 0.
     // Runs and entries are walked in descending order (the last feasible entry seen is the
-    // first in lattice order); each run needs one new row value.  Two (s, q) pairs per
+    // first in lattice order); each run needs one new row value.  kK3Pairs (s, q) pairs per
     // thread share the run bookkeeping and every (tb, threshold) load.
     const int last = nb - 1;
-    for (int pa = p0 + int(threadIdx.x); pa < p1; pa += 2 * bd) {
-      const int pb = pa + bd < p1 ? pa + bd : pa;  // a lone last pair is evaluated twice
-      const int sia = pa / nQ, qia = pa - sia * nQ;
-      const int sib = pb / nQ, qib = pb - sib * nQ;
-      const int2 ja = sJ[sia], jb = sJ[sib];
-      if (ja.x != ja.y || jb.x != jb.y) {  // not produced by a lattice over table sms
-        record(sia, qia, generic_pair(sia, qia));
-        record(sib, qib, generic_pair(sib, qib));
-        continue;
+    // pairs pa, pa + bd, ..., pa + (NP - 1) * bd (all < p1)
+    auto fast = [&](int pa, auto np_tag) {
+      constexpr int NP = decltype(np_tag)::value;
+      int si[NP], qi[NP];
+      bool node = true;
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        const int pu = pa + u * bd;
+        si[u] = pu / nQ;
+        qi[u] = pu - si[u] * nQ;
+        const int2 j = sJ[si[u]];
+        node = node && j.x == j.y;
       }
-      const int2 ka = sK[qia], kb = sK[qib];
-      const double tqa = sTq[qia], tqb = sTq[qib];
-      const double* __restrict__ a0 = v + (ja.x * nq + ka.x);
-      const double* __restrict__ a1 = v + (ja.x * nq + ka.y);
-      const double* __restrict__ b0 = v + (jb.x * nq + kb.x);
-      const double* __restrict__ b1 = v + (jb.x * nq + kb.y);
-      int up = -2, fa = 1 << 30, fb = 1 << 30;
-      double cua = 0.0, cub = 0.0;
+      if (!node) {  // not produced by a lattice over table sms
+#pragma unroll
+        for (int u = 0; u < NP; ++u) record(si[u], qi[u], generic_pair(si[u], qi[u]));
+        return;
+      }
+      const double* __restrict__ r0[NP];
+      const double* __restrict__ r1[NP];
+      double tq[NP], cu[NP], c0[NP], d[NP];
+      int fnd[NP];
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        const int js = sJ[si[u]].x;
+        const int2 k = sK[qi[u]];
+        r0[u] = v + (js * nq + k.x);
+        r1[u] = v + (js * nq + k.y);
+        tq[u] = sTq[qi[u]];
+        cu[u] = 0.0;
+        fnd[u] = 1 << 30;
+      }
+      int up = -2;
       for (int sg = nlo - 1; sg >= 0; --sg) {
         const int4 S = sLo[sg];
         const int64_t o = int64_t(S.x) * row_stride;
-        const double c0a = lerp_rn(a0[o], a1[o], tqa);
-        const double c0b = lerp_rn(b0[o], b1[o], tqb);
-        double da = 0.0, db = 0.0;
-        if (S.x != last) {
-          double c1a = cua, c1b = cub;
-          if (S.x + 1 != up) {
-            const int64_t o1 = o + row_stride;
-            c1a = lerp_rn(a0[o1], a1[o1], tqa);
-            c1b = lerp_rn(b0[o1], b1[o1], tqb);
+        const bool top = S.x == last, reuse = S.x + 1 == up;
+#pragma unroll
+        for (int u = 0; u < NP; ++u) {
+          c0[u] = lerp_rn(r0[u][o], r1[u][o], tq[u]);
+          d[u] = 0.0;
+          if (!top) {
+            const double c1 = reuse ? cu[u] : lerp_rn(r0[u][o + row_stride],
+                                                      r1[u][o + row_stride], tq[u]);
+            d[u] = __dsub_rn(c1, c0[u]);
           }
-          da = __dsub_rn(c1a, c0a);
-          db = __dsub_rn(c1b, c0b);
+          cu[u] = c0[u];
         }
         up = S.x;
-        cua = c0a;
-        cub = c0b;
 #pragma unroll (kK3Unroll)
         for (int bi = S.z - 1; bi >= S.y; --bi) {
           const double2 tt = sTT[bi];
-          const double la = __dadd_rn(c0a, __dmul_rn(da, tt.x));
-          const double lb = __dadd_rn(c0b, __dmul_rn(db, tt.x));
-          fa = la <= tt.y ? bi : fa;
-          fb = lb <= tt.y ? bi : fb;
+#pragma unroll
+          for (int u = 0; u < NP; ++u) {
+            const double lat = __dadd_rn(c0[u], __dmul_rn(d[u], tt.x));
+            fnd[u] = lat <= tt.y ? bi : fnd[u];
+          }
         }
       }
-      record(sia, qia, fa);
-      record(sib, qib, fb);
-    }
+#pragma unroll
+      for (int u = 0; u < NP; ++u) record(si[u], qi[u], fnd[u]);
+    };
+    int pa = p0 + int(threadIdx.x);
+    for (; pa + (kK3Pairs - 1) * bd < p1; pa += kK3Pairs * bd)
+      fast(pa, std::integral_constant<int, kK3Pairs>());
+    for (; pa < p1; pa += bd) fast(pa, std::integral_constant<int, 1>());
   } else {
     for (int pr = p0 + int(threadIdx.x); pr < p1; pr += bd) {
       const int si = pr / nQ, qi = pr - si * nQ;
