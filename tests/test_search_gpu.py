@@ -138,3 +138,45 @@ def test_config5_full_size_sampled_and_repeatable():
         want = or_most_efficient_config(t._b_axis, t._s_axis, t._q_axis, t.latency_ms,
                                         targets[f], 1, allowed)
         assert first[f] == want, f
+
+
+def _rough(rng, nb, ns, nq, fid):
+    """Random monotone grid (positive; latency non-decreasing in batch, non-increasing in sm
+    and quota, as the loader requires) whose batch growth is superlinear in places, so
+    feasibility is not monotone in b."""
+    from paper_2505_01968_b200 import PerfTable
+    bs = sorted(rng.sample(range(1, 33), nb))
+    ss = sorted(rng.sample(range(1, 101), ns))
+    qs = sorted(rng.sample(range(1, 101), nq))
+    gb = np.cumsum([rng.uniform(0.5, 8.0) * (rng.random() < 0.5 and 6.0 or 1.0)
+                    for _ in bs])
+    gs = np.cumsum([rng.uniform(0.1, 1.0) for _ in ss])[::-1]
+    gq = np.cumsum([rng.uniform(0.1, 1.0) for _ in qs])[::-1]
+    lat = gb[:, None, None] * gs[None, :, None] * gq[None, None, :] + rng.uniform(0.1, 2.0)
+    return PerfTable(fid, bs, ss, qs, lat)
+
+
+def test_sparse_batch_lists_and_rough_tables_vs_oracle():
+    """K3's run formulation: batch lists that skip table rows, hit only nodes, start or end
+    on the axis ends, single-row tables; pair counts that leave ragged per-thread tails."""
+    from paper_2505_01968_b200 import PerfTableSet
+    rng = random.Random(2024)
+    fns, targets = [], []
+    for i in range(80):
+        t = _rough(rng, rng.randint(1, 7), rng.randint(1, 37), rng.randint(1, 23), f"r{i}")
+        lo, hi = t.batches[0], t.batches[-1]
+        allowed = rng.choice([
+            None, [lo, hi], [hi], [lo], list(t.batches), sorted(rng.sample(range(1, 33), 5)),
+            list(range(lo, hi + 1, 3)), [b for b in range(1, 33) if b not in t.batches]])
+        if allowed is not None and not any(lo <= b <= hi for b in allowed):
+            allowed = None
+        peak = max(t.throughput(b, t.sms[-1], 100) for b in t.batches)
+        fns.append((t, allowed))
+        targets.append(rng.choice([0.05, 0.4, 0.7, 0.95, 1.0, 2.0]) * peak)
+    for step in (1, 7, 25):
+        ts = PerfTableSet(fns, quota_step=step)
+        got = ts.search(targets)
+        for (t, allowed), target, g in zip(fns, targets, got):
+            want = or_most_efficient_config(t._b_axis, t._s_axis, t._q_axis, t.latency_ms,
+                                            target, step, allowed)
+            assert g == want, (t.function_id, target, step, allowed)
