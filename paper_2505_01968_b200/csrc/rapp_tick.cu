@@ -182,6 +182,48 @@ __device__ __forceinline__ double thr_at(const World& w, int f, double b, double
   return throughput(b, lat);  // b / (lat / 1000.0), hs/perf.py:95-98
 }
 
+// thr_at along one quota row: the batch and sm brackets of (b, s) are located once, each
+// entry locates its quota and evaluates the same interp3 expression (same doubles).
+struct ThrRow {
+  const double* qa;
+  const double* v;
+  int nq;
+  int64_t r00, r01, r10, r11;
+  double tb, ts, b;
+};
+
+__device__ __forceinline__ ThrRow thr_row(const World& w, int f, double b, double s) {
+  const TableDesc td = w.tds[w.fn_table[f]];
+  const double* seg = w.pool + td.off;
+  ThrRow r;
+  int i0, i1, j0, j1;
+  locate(seg + td.ob, td.nb, b, i0, i1, r.tb);
+  locate(seg + td.os, td.ns, s, j0, j1, r.ts);
+  r.qa = seg + td.oq;
+  r.v = seg + td.ov;
+  r.nq = td.nq;
+  r.r00 = (int64_t(i0) * td.ns + j0) * td.nq;
+  r.r01 = (int64_t(i0) * td.ns + j1) * td.nq;
+  r.r10 = (int64_t(i1) * td.ns + j0) * td.nq;
+  r.r11 = (int64_t(i1) * td.ns + j1) * td.nq;
+  r.b = b;
+  return r;
+}
+
+__device__ __forceinline__ double thr_row_at(const ThrRow& r, double q) {
+  int k0, k1;
+  double tq;
+  locate(r.qa, r.nq, q, k0, k1, tq);
+  const double* v = r.v;
+  const double c00 = lerp_rn(v[r.r00 + k0], v[r.r00 + k1], tq);
+  const double c01 = lerp_rn(v[r.r01 + k0], v[r.r01 + k1], tq);
+  const double c10 = lerp_rn(v[r.r10 + k0], v[r.r10 + k1], tq);
+  const double c11 = lerp_rn(v[r.r11 + k0], v[r.r11 + k1], tq);
+  const double c0 = lerp_rn(c00, c01, r.ts);
+  const double c1 = lerp_rn(c10, c11, r.ts);
+  return throughput(r.b, lerp_rn(c0, c1, r.tb));  // b / (lat / 1000.0), hs/perf.py:95-98
+}
+
 __device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
   const TableDesc td = w.tds[w.fn_table[f]];
   const double* ba = w.pool + td.off + td.ob;
@@ -494,9 +536,9 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
       if (w.p_state[p] != kRunning) continue;
       const int q0 = w.p_q[p];
       const int kd = (q0 - 1) / d, ku = (100 - q0) / d;
+      const ThrRow tr = thr_row(w, f, double(w.p_b[p]), double(w.p_s[p]));
       for (int k = 1 + lane; k <= ku; k += 32)
-        rows[j * kRow + kd + k] =
-            thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 + k * d));
+        rows[j * kRow + kd + k] = thr_row_at(tr, double(q0 + k * d));
     }
     __syncwarp();
     {
@@ -603,9 +645,9 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
     while (srt[j] != p) ++j;
     const int q0 = w.p_q[p];
     const int kd = (q0 - 1) / d;
+    const ThrRow tr = thr_row(w, f, double(w.p_b[p]), double(w.p_s[p]));
     for (int k = 1 + lane; k <= kd; k += 32)
-      rows[j * kRow + kd - k] =
-          thr_at(w, f, double(w.p_b[p]), double(w.p_s[p]), double(q0 - k * d));
+      rows[j * kRow + kd - k] = thr_row_at(tr, double(q0 - k * d));
   }
   __syncwarp();
   cap = __shfl_sync(0xffffffffu, cap, 0);
@@ -745,36 +787,51 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
   const double* v1 = v + s_i1 * plane;
   const double tb = s_tb, bb = double(b);
   const bool fast = td.fast != 0;  // finite positive values (checked at upload)
-  for (int i = threadIdx.x; i < 100 * nq; i += blockDim.x) {
-    const int si = i / nq, qi = i - si * nq;
-    const int2 j = s_j[si], k = s_k[qi];
-    const double ts = s_ts[si], tq = s_tq[qi];
-    const int o00 = j.x * td.nq + k.x, o01 = j.x * td.nq + k.y;
-    const int o10 = j.y * td.nq + k.x, o11 = j.y * td.nq + k.y;
-    // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch.  The
-    // table reads are streaming (evict-first) so this pass does not push the commit's
-    // working set (phase A outputs, cluster state) out of L2.  On a node
-    // bracket (lo == hi, t == 0) of a finite table lerp(v, v, 0) == v exactly, so those
-    // lerps and their second loads are skipped (every quota step of a 1..100% table, and
-    // every sm on the table's own grid, is a node).
-    double lat;
-    if (fast && k.x == k.y) {
-      const double a00 = __ldcs(v0 + o00), a10 = __ldcs(v1 + o00);
-      if (j.x == j.y) {
-        lat = lerp_rn(a00, a10, tb);
+  // kGridU entries per thread per round: every table load of the round is issued before
+  // the first store (the stores could alias the loads as far as the compiler knows)
+  constexpr int kGridU = 4;
+  const int total = 100 * nq;
+  for (int i0 = threadIdx.x; i0 < total; i0 += kGridU * blockDim.x) {
+    double lat[kGridU];
+    int64_t out[kGridU];
+#pragma unroll
+    for (int u = 0; u < kGridU; ++u) {
+      const int i = i0 + u * int(blockDim.x);
+      out[u] = -1;
+      lat[u] = 0.0;
+      if (i >= total) continue;
+      const int si = i / nq, qi = i - si * nq;
+      out[u] = (int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1;
+      const int2 j = s_j[si], k = s_k[qi];
+      const double ts = s_ts[si], tq = s_tq[qi];
+      const int o00 = j.x * td.nq + k.x, o01 = j.x * td.nq + k.y;
+      const int o10 = j.y * td.nq + k.x, o11 = j.y * td.nq + k.y;
+      // interp3 (_grid_cy.pyx:45-51): c_ij = lerp along quota, then sm, then batch.  The
+      // table reads are streaming (evict-first) so this pass does not push the commit's
+      // working set (phase A outputs, cluster state) out of L2.  On a node
+      // bracket (lo == hi, t == 0) of a finite table lerp(v, v, 0) == v exactly, so those
+      // lerps and their second loads are skipped (every quota step of a 1..100% table, and
+      // every sm on the table's own grid, is a node).
+      if (fast && k.x == k.y) {
+        const double a00 = __ldcs(v0 + o00), a10 = __ldcs(v1 + o00);
+        if (j.x == j.y) {
+          lat[u] = lerp_rn(a00, a10, tb);
+        } else {
+          const double a01 = __ldcs(v0 + o10), a11 = __ldcs(v1 + o10);
+          lat[u] = lerp_rn(lerp_rn(a00, a01, ts), lerp_rn(a10, a11, ts), tb);
+        }
       } else {
-        const double a01 = __ldcs(v0 + o10), a11 = __ldcs(v1 + o10);
-        lat = lerp_rn(lerp_rn(a00, a01, ts), lerp_rn(a10, a11, ts), tb);
+        const double c00 = lerp_rn(__ldcs(v0 + o00), __ldcs(v0 + o01), tq);
+        const double c01 = lerp_rn(__ldcs(v0 + o10), __ldcs(v0 + o11), tq);
+        const double c10 = lerp_rn(__ldcs(v1 + o00), __ldcs(v1 + o01), tq);
+        const double c11 = lerp_rn(__ldcs(v1 + o10), __ldcs(v1 + o11), tq);
+        lat[u] = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
       }
-    } else {
-      const double c00 = lerp_rn(__ldcs(v0 + o00), __ldcs(v0 + o01), tq);
-      const double c01 = lerp_rn(__ldcs(v0 + o10), __ldcs(v0 + o11), tq);
-      const double c10 = lerp_rn(__ldcs(v1 + o00), __ldcs(v1 + o01), tq);
-      const double c11 = lerp_rn(__ldcs(v1 + o10), __ldcs(v1 + o11), tq);
-      lat = lerp_rn(lerp_rn(c00, c01, ts), lerp_rn(c10, c11, ts), tb);
     }
-    // default-policy store: the commit's used-GPU branch reads these rows back from L2
-    w.tgrid[(int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1] = throughput(bb, lat);
+    // default-policy stores: the commit's used-GPU branch reads these rows back from L2
+#pragma unroll
+    for (int u = 0; u < kGridU; ++u)
+      if (out[u] >= 0) w.tgrid[out[u]] = throughput(bb, lat[u]);
   }
 }
 
