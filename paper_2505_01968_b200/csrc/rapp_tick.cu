@@ -2033,6 +2033,8 @@ __global__ void k_index_scan(World w, int f0) {
 
 using namespace rapp;
 
+constexpr size_t kOutHead = 16;  // n_actions, err, err_fn, pad (int32 each)
+
 struct rapp_tick {
   rapp_ctx* ctx = nullptr;
   World w{};
@@ -2042,7 +2044,8 @@ struct rapp_tick {
   int64_t* d_arrivals = nullptr;
   uint8_t* d_idle = nullptr;
   double* d_pred_in = nullptr;
-  int32_t* h_count = nullptr;  // pinned: n_actions, err, err_fn
+  uint8_t* d_in = nullptr;     // input block (d_arrivals, d_pred_in, d_idle point into it)
+  uint8_t* d_out = nullptr;    // output block (w.n_actions ... w.actions point into it)
   // pinned staging for the host API: inputs [arrivals F x i64 | predicted F x f64 | idle
   // pod_cap bytes], outputs [actions 1024 | observed F | predicted F], so every copy of a
   // tick is asynchronous and the tick synchronises once
@@ -2340,8 +2343,20 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   w.pool = ctx->d_pool;
   // scratch / outputs
   const size_t FP = (size_t)std::max(F, 1);
-  if ((rc = dev_alloc(t.get(), &w.obs, FP))) return rc;
-  if ((rc = dev_alloc(t.get(), &w.pred, FP))) return rc;
+  // outputs a host call reads back, in one block so one copy returns them:
+  // [n_actions, err, err_fn, pad][observed F][predicted F][actions]
+  {
+    uint8_t* ob = nullptr;
+    const size_t out_bytes = kOutHead + FP * 16 + FP * (kMaxPods + 4) * sizeof(rapp_action);
+    if ((rc = dev_alloc(t.get(), &ob, out_bytes))) return rc;
+    t->d_out = ob;
+    w.n_actions = reinterpret_cast<int32_t*>(ob);
+    w.err = reinterpret_cast<int32_t*>(ob + 4);
+    w.err_fn = reinterpret_cast<int32_t*>(ob + 8);
+    w.obs = reinterpret_cast<double*>(ob + kOutHead);
+    w.pred = w.obs + FP;
+    w.actions = reinterpret_cast<rapp_action*>(ob + kOutHead + FP * 16);
+  }
   if ((rc = dev_alloc(t.get(), &w.cls, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.gap0, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.wanted, FP))) return rc;
@@ -2359,16 +2374,18 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.ndown, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.down, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.stamp, FP))) return rc;
-  if ((rc = dev_alloc(t.get(), &w.actions, FP * (kMaxPods + 4)))) return rc;
-  if ((rc = dev_alloc(t.get(), &w.n_actions, 1))) return rc;
-  if ((rc = dev_alloc(t.get(), &w.err, 1))) return rc;
-  if ((rc = dev_alloc(t.get(), &w.err_fn, 1))) return rc;
-  if ((rc = dev_alloc(t.get(), &t->d_arrivals, FP))) return rc;
-  if ((rc = dev_alloc(t.get(), &t->d_idle, (size_t)cap))) return rc;
-  if ((rc = dev_alloc(t.get(), &t->d_pred_in, FP))) return rc;
-  RAPP_CUDA(cudaMallocHost(&t->h_count, 4 * sizeof(int32_t)));
+  // inputs of a host call, in one block mirrored by the pinned staging (one copy):
+  // [arrivals F x i64][predicted F x f64][idle flags pod_cap bytes]
+  {
+    uint8_t* ib = nullptr;
+    if ((rc = dev_alloc(t.get(), &ib, FP * 16 + (size_t)cap))) return rc;
+    t->d_in = ib;
+    t->d_arrivals = reinterpret_cast<int64_t*>(ib);
+    t->d_pred_in = reinterpret_cast<double*>(ib + FP * 8);
+    t->d_idle = ib + FP * 16;
+  }
   RAPP_CUDA(cudaMallocHost(&t->h_in, FP * 16 + (size_t)cap + 64));
-  RAPP_CUDA(cudaMallocHost(&t->h_out, 1024 * sizeof(rapp_action) + FP * 16 + 64));
+  RAPP_CUDA(cudaMallocHost(&t->h_out, kOutHead + FP * 16 + 1024 * sizeof(rapp_action)));
   t->h_npods = n_pods;
   // build the fresh-GPU search index
   for (int f0 = 0; f0 < F; f0 += 32768) {
@@ -2388,7 +2405,6 @@ int rapp_tick_destroy(rapp_tick* t) {
   cudaSetDevice(t->ctx->device);
   cudaStreamSynchronize(t->stream);
   for (void* p : t->allocs) cudaFree(p);
-  if (t->h_count) cudaFreeHost(t->h_count);
   if (t->h_in) cudaFreeHost(t->h_in);
   if (t->d_rel) cudaFree(t->d_rel);
   if (t->h_rel) cudaFreeHost(t->h_rel);
@@ -2504,43 +2520,34 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
     t->h_npods = v;
   }
   const int64_t np = t->h_npods;  // tracked on the host: no round trip before the launch
-  // inputs through pinned staging (asynchronous copies)
+  // inputs through pinned staging in the device block's layout: one H2D copy
+  const size_t FP = std::max<size_t>(F, 1);
   int64_t* s_arr = reinterpret_cast<int64_t*>(t->h_in);
-  double* s_pred = reinterpret_cast<double*>(t->h_in + F * 8);
-  uint8_t* s_idle = t->h_in + F * 16;
-  if (F) {
-    memcpy(s_arr, arrivals, F * 8);
-    RAPP_CUDA(cudaMemcpyAsync(t->d_arrivals, s_arr, F * 8, cudaMemcpyHostToDevice, st));
-  }
-  if (idle && np) {
-    memcpy(s_idle, idle, (size_t)np);
-    RAPP_CUDA(cudaMemcpyAsync(t->d_idle, s_idle, (size_t)np, cudaMemcpyHostToDevice, st));
-  }
+  double* s_pred = reinterpret_cast<double*>(t->h_in + FP * 8);
+  uint8_t* s_idle = t->h_in + FP * 16;
+  if (F) memcpy(s_arr, arrivals, F * 8);
+  if (predicted_in && F) memcpy(s_pred, predicted_in, F * 8);
+  if (idle && np) memcpy(s_idle, idle, (size_t)np);
+  RAPP_CUDA(cudaMemcpyAsync(t->d_in, t->h_in, FP * 16 + (idle ? (size_t)np : 0),
+                            cudaMemcpyHostToDevice, st));
   if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
-  if (predicted_in && F) {
-    memcpy(s_pred, predicted_in, F * 8);
-    RAPP_CUDA(cudaMemcpyAsync(t->d_pred_in, s_pred, F * 8, cudaMemcpyHostToDevice, st));
-  }
   int rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr, st);
   if (rc) return rc;
-  // one synchronisation for the usual case: count, status, rates and the first actions
-  RAPP_CUDA(cudaMemcpyAsync(t->h_count, w.n_actions, 4, cudaMemcpyDeviceToHost, st));
-  RAPP_CUDA(cudaMemcpyAsync(t->h_count + 1, w.err, 4, cudaMemcpyDeviceToHost, st));
-  RAPP_CUDA(cudaMemcpyAsync(t->h_count + 2, w.err_fn, 4, cudaMemcpyDeviceToHost, st));
-  rapp_action* s_act = reinterpret_cast<rapp_action*>(t->h_out);
-  double* s_obs = reinterpret_cast<double*>(t->h_out + 1024 * sizeof(rapp_action));
-  double* s_prd = s_obs + F;
+  // one D2H copy and one synchronisation for the usual case: count, status, rates and the
+  // first actions (the output block's prefix)
   const int64_t spec = actions ? std::min<int64_t>(max_actions, 1024) : 0;
-  if (spec > 0)
-    RAPP_CUDA(cudaMemcpyAsync(s_act, w.actions, (size_t)spec * sizeof(rapp_action),
-                              cudaMemcpyDeviceToHost, st));
-  if (observed_out && F) RAPP_CUDA(cudaMemcpyAsync(s_obs, w.obs, F * 8, cudaMemcpyDeviceToHost, st));
-  if (predicted_out && F) RAPP_CUDA(cudaMemcpyAsync(s_prd, w.pred, F * 8, cudaMemcpyDeviceToHost, st));
+  RAPP_CUDA(cudaMemcpyAsync(t->h_out, t->d_out,
+                            kOutHead + FP * 16 + (size_t)spec * sizeof(rapp_action),
+                            cudaMemcpyDeviceToHost, st));
+  const int32_t* h_count = reinterpret_cast<const int32_t*>(t->h_out);
+  const double* s_obs = reinterpret_cast<const double*>(t->h_out + kOutHead);
+  const double* s_prd = s_obs + FP;
+  const rapp_action* s_act = reinterpret_cast<const rapp_action*>(t->h_out + kOutHead + FP * 16);
   RAPP_CUDA(cudaStreamSynchronize(st));
-  if (t->h_count[1] != RAPP_OK) {
+  if (h_count[1] != RAPP_OK) {
     if ((rc = tick_error(t))) return rc;
   }
-  const int64_t n = t->h_count[0];
+  const int64_t n = h_count[0];
   *n_actions = n;
   if (n > max_actions) {
     set_error("action buffer too small (%lld > %lld)", (long long)n, (long long)max_actions);
