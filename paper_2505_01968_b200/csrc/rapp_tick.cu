@@ -1707,9 +1707,18 @@ struct Commit {
 // next partition uid) live in shared memory for the whole tick when they fit: the
 // used-GPU argmin and the first-free scan then read shared memory only.  Function classes
 // are fetched 32 at a time and only active functions are visited, in sorted order.
-constexpr int kPreDepth = 4;  // batches of function headers the helper warp runs ahead
+#ifndef RAPP_TICK_HELPERS
+#define RAPP_TICK_HELPERS 2
+#endif
+#ifndef RAPP_TICK_PREDEPTH
+#define RAPP_TICK_PREDEPTH 4
+#endif
+constexpr int kHelpers = RAPP_TICK_HELPERS;     // helper warps filling the header ring
+constexpr int kPreDepth = RAPP_TICK_PREDEPTH;   // batches of function headers in the ring
+constexpr int kCommitThreads = 32 * (1 + kHelpers);
 
-__global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int smem_g, int ps) {
+__global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double now, int smem_g,
+                                                                int ps) {
   // dynamic shared layout: [row staging 2 x 32 x kRowStage doubles][5*G summaries]
   //                        [partition cache G*ps uint64 (8-aligned)][ovf G bytes]
   extern __shared__ __align__(16) int32_t smem_dyn[];
@@ -1717,10 +1726,11 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   int32_t* sg = smem_dyn + 2 * 32 * kRowStage * 2;
   __shared__ int s_nact;
   const int lane = threadIdx.x & 31;
-  // Warp 1 is a helper: it reads the headers of the next kPreDepth batches of 32 functions
-  // (each function's own phase-A outputs and first pod — nothing an earlier function of the
-  // tick can change) into a shared ring while warp 0 commits, so warp 0 never waits on
-  // those dependent global loads.
+  // Warps 1..kHelpers are helpers: they read the headers of the next kPreDepth batches of
+  // 32 functions (each function's own phase-A outputs and first pod — nothing an earlier
+  // function of the tick can change) into a shared ring while warp 0 commits, helper h
+  // taking batches h-1, h-1+kHelpers, ..., so warp 0 never waits on those dependent
+  // global loads.
   __shared__ Commit::Pre s_pre[kPreDepth][32];
   __shared__ int s_pcls[kPreDepth][32];
   __shared__ FastRec s_fast[kPreDepth][32];
@@ -1735,7 +1745,8 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   }
   __syncthreads();
   if (threadIdx.x >= 32) {
-    for (int b = 0, base = 0; base < w.F; ++b, base += 32) {
+    const int h = (threadIdx.x >> 5) - 1;
+    for (int b = h, base = 32 * h; base < w.F; b += kHelpers, base += 32 * kHelpers) {
       const int slot = b % kPreDepth;
       while (s_done < b - kPreDepth) {  // the slot is free once batch b - depth is done
         if (s_stop) return;
@@ -1766,6 +1777,9 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
     }
     return;
   }
+#ifdef RAPP_TICK_PROF
+  const long long _pro0 = clock64();
+#endif
   World v = w;
   const int G = w.G;
   // shared layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)][ovf G bytes]
@@ -1814,6 +1828,7 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
 #ifdef RAPP_TICK_PROF
   s_tprof[lane] = 0;
   __syncwarp();
+  if (lane == 0) s_tprof[20] = clock64() - _pro0;  // prologue: state into shared memory
 #endif
   // First-pod quota rows of the scale-up functions of a batch of 32 are bulk-copied into
   // shared memory one batch ahead (double buffer), so a vertical walk that has to be
@@ -1925,8 +1940,7 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
   // no bulk copy may still be in flight into shared memory when the CTA exits
   for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
 #ifdef RAPP_TICK_PROF
-  __syncwarp();
-  g_tick_prof[lane] += s_tprof[lane];
+  const long long _epi0 = clock64();
 #endif
   if (lane == 0) {
     *w.n_pods = s_npods;
@@ -1948,6 +1962,12 @@ __global__ void __launch_bounds__(64) k_tick_commit(World w, double now, int sme
       w.g_nextuid[g] = uint32_t(sg[4 * G + g]);
     }
   }
+#ifdef RAPP_TICK_PROF
+  __syncwarp();
+  if (lane == 0) s_tprof[21] = clock64() - _epi0;  // epilogue: state back to global memory
+  __syncwarp();
+  g_tick_prof[lane] += s_tprof[lane];
+#endif
 }
 
 // Releases reported by the host between ticks (a DRAINING pod whose last request finished:
@@ -2105,8 +2125,14 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     RAPP_LAUNCHED();
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
-    // 227 KB per CTA minus the row staging and the static shared memory (~26 KB)
-    const size_t budget = 227 * 1024 - size_t(2 * 32 * kRowStage) * 8 - 28 * 1024;
+    // 227 KB per CTA minus the row staging and the static shared memory
+    static size_t static_smem = 0;  // the kernel's static shared memory (header ring etc.)
+    if (static_smem == 0) {
+      cudaFuncAttributes fa{};
+      RAPP_CUDA(cudaFuncGetAttributes(&fa, k_tick_commit));
+      static_smem = fa.sharedSizeBytes + 1024;
+    }
+    const size_t budget = 227 * 1024 - size_t(2 * 32 * kRowStage) * 8 - static_smem;
     const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
     const size_t fixed = gbytes + size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16;
     const int smem_g = fixed <= budget ? 1 : 0;
@@ -2118,7 +2144,7 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
                                 : size_t(2 * 32 * kRowStage) * 8 + size_t(w.G) + 16;   // ovf only
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
-    k_tick_commit<<<1, 64, bytes, st>>>(w, now, smem_g, ps);
+    k_tick_commit<<<1, kCommitThreads, bytes, st>>>(w, now, smem_g, ps);
     RAPP_LAUNCHED();
   }
   return RAPP_OK;

@@ -19,7 +19,8 @@ from paper_2505_01968_b200.tick import TickEngine  # noqa: E402
 NAMES = ["batch wait", "vertical spec/walk", "used-GPU rest", "fresh-GPU branch",
          "scale-down", "vertical headroom", "functions (wall)", "vertical change+emit",
          "hu argmin", "hu best_slot", "hu T+covering", "hu new_pod", "hu place", "hu emit",
-         "fast lanes", "fast candidates", "fast_run", "fast_run calls", "-", "runs committed"]
+         "fast lanes", "fast candidates", "fast_run", "fast_run calls", "-", "runs committed",
+         "prologue", "epilogue"]
 COUNTS = (14, 15, 17, 19)
 
 
