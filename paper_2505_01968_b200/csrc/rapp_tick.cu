@@ -231,6 +231,24 @@ __device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
   return !(x < ba[0] || x > ba[td.nb - 1]);  // hs/perf.py:88-91
 }
 
+// Programmatic dependent launch between the tick's kernels: each kernel lets its
+// successor launch as soon as all of its CTAs are running (griddepcontrol.launch_dependents)
+// and waits for its predecessor's completion (griddepcontrol.wait) only before it reads
+// what the predecessor wrote, so launch latency and independent set-up overlap.
+#ifndef RAPP_TICK_PDL
+#define RAPP_TICK_PDL 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if RAPP_TICK_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if RAPP_TICK_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 #ifdef RAPP_TICK_PROF
 // diagnostics build only: cycles of the commit's parts, summed over ticks (lane 0)
 __device__ unsigned long long g_tick_prof[32];
@@ -290,6 +308,7 @@ __global__ void k_tick_format_ids(World w) {
 }
 
 __global__ void k_tick_prologue(World w, double now) {
+  pdl_trigger();
   const int n = *w.n_pods;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     format_pending(w, p);
@@ -417,6 +436,8 @@ __device__ void replica_phase_a(const World& w, int f, int lane, double R, doubl
 // ---------------------------------------------------------------------------------------
 __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ arrivals,
                                const double* __restrict__ pred_in) {
+  pdl_trigger();
+  pdl_wait();  // the prologue's pod-state promotions
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (f >= w.F) return;
@@ -746,6 +767,8 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
 // they are located once into shared memory (same locate, same doubles) and every entry is
 // then 8 independent corner loads and the reference's 7 lerps + 2 divisions.
 __global__ void __launch_bounds__(256) k_tick_grid(World w) {
+  pdl_trigger();
+  pdl_wait();  // phase A's classes and reference batches
   const int f = blockIdx.x;
   if (w.policy != 0 || w.cls[f] != kUp) return;
   const int b = w.bref[f];
@@ -1743,6 +1766,36 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
     s_done = -1;
     s_stop = 0;
   }
+#ifdef RAPP_TICK_PROF
+  const long long _pro0 = clock64();
+#endif
+  // The tick's cluster state into shared memory, by every warp (the helpers start their
+  // ring after it).  Layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)]
+  // [ovf G bytes][argmin keys] (no summaries region when they live in global memory).
+  const int G = w.G;
+  uint64_t* sp = reinterpret_cast<uint64_t*>(sg + (smem_g ? ((5 * G + 1) & ~1) : 0));
+  uint8_t* ovf = reinterpret_cast<uint8_t*>(sp + int64_t(G) * ps);
+  uint32_t* skey = (smem_g && G <= (1 << 18))
+                       ? reinterpret_cast<uint32_t*>(ovf + ((G + 3) & ~3)) : nullptr;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const int n = w.g_nparts[g];
+    const bool cached = n <= ps && ps > 0;
+    ovf[g] = cached ? 0 : 1;
+    if (cached)
+      for (int i = 0; i < n; ++i) sp[int64_t(g) * ps + i] = w.g_parts[int64_t(g) * kPartCap + i];
+    if (smem_g) {
+      const int np = w.g_npods[g], hgo = w.g_hgo[g];
+      sg[g] = np;
+      sg[G + g] = hgo;
+      sg[2 * G + g] = n;
+      sg[3 * G + g] = w.g_freesm[g];
+      sg[4 * G + g] = int32_t(w.g_nextuid[g]);
+      if (skey != nullptr) skey[g] = np > 0 ? (uint32_t(hgo) << 18) | uint32_t(g) : ~0u;
+    }
+  }
+  // (the cluster state above is written only by commits and releases, never by the tick's
+  // earlier kernels; everything below reads their outputs)
+  pdl_wait();
   __syncthreads();
   if (threadIdx.x >= 32) {
     const int h = (threadIdx.x >> 5) - 1;
@@ -1777,43 +1830,15 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
     }
     return;
   }
-#ifdef RAPP_TICK_PROF
-  const long long _pro0 = clock64();
-#endif
   World v = w;
-  const int G = w.G;
-  // shared layout: [5*G summaries][partition cache G*ps uint64 (8-aligned)][ovf G bytes]
-  // (no summaries region when they live in global memory)
-  uint64_t* sp = reinterpret_cast<uint64_t*>(sg + (smem_g ? ((5 * G + 1) & ~1) : 0));
-  uint8_t* ovf = reinterpret_cast<uint8_t*>(sp + int64_t(G) * ps);
-  uint32_t* skey = (smem_g && G <= (1 << 18))
-                       ? reinterpret_cast<uint32_t*>(ovf + ((G + 3) & ~3)) : nullptr;
-  if (lane == 0) s_nact = 0;
-  for (int g = lane; g < G; g += 32) {
-    const int n = w.g_nparts[g];
-    const bool cached = n <= ps && ps > 0;
-    ovf[g] = cached ? 0 : 1;
-    if (cached)
-      for (int i = 0; i < n; ++i) sp[int64_t(g) * ps + i] = w.g_parts[int64_t(g) * kPartCap + i];
-  }
   if (smem_g) {
-    for (int g = lane; g < G; g += 32) {
-      sg[g] = w.g_npods[g];
-      sg[G + g] = w.g_hgo[g];
-      sg[2 * G + g] = w.g_nparts[g];
-      sg[3 * G + g] = w.g_freesm[g];
-      sg[4 * G + g] = int32_t(w.g_nextuid[g]);
-    }
     v.g_npods = sg;
     v.g_hgo = sg + G;
     v.g_nparts = sg + 2 * G;
     v.g_freesm = sg + 3 * G;
     v.g_nextuid = reinterpret_cast<uint32_t*>(sg + 4 * G);
-    if (skey != nullptr)
-      for (int g = lane; g < G; g += 32)
-        skey[g] = sg[g] > 0 ? (uint32_t(sg[G + g]) << 18) | uint32_t(g) : ~0u;
-    __syncwarp();
   }
+  if (lane == 0) s_nact = 0;
   __syncwarp();
   __shared__ int s_err, s_npods;
   __shared__ long long s_counter;
@@ -2112,6 +2137,24 @@ static void unpack_id(const PodId& id, char* s) {
     for (int k = 0; k < 8; ++k) s[i * 8 + k] = char((id.w[i] >> (8 * (7 - k))) & 0xFF);
 }
 
+// launch with programmatic stream serialization (the kernel calls pdl_wait before it
+// reads its predecessor's outputs)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = RAPP_TICK_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uint8_t* d_idle,
                        const double* d_pred, cudaStream_t st) {
   World w = t->w;
@@ -2119,9 +2162,10 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
   k_tick_prologue<<<std::max(1, std::min(1024, (w.pod_cap + 255) / 256)), 256, 0, st>>>(w, now);
   RAPP_LAUNCHED();
   if (w.F > 0) {
-    k_tick_phase_a<<<(w.F + 7) / 8, 256, 0, st>>>(w, now, d_arr, d_pred);
+    RAPP_CUDA(launch_pdl(k_tick_phase_a, dim3((w.F + 7) / 8), dim3(256), 0, st, w, now, d_arr,
+                         d_pred));
     RAPP_LAUNCHED();
-    k_tick_grid<<<w.F, 256, 0, st>>>(w);
+    RAPP_CUDA(launch_pdl(k_tick_grid, dim3(w.F), dim3(256), 0, st, w));
     RAPP_LAUNCHED();
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
@@ -2144,7 +2188,8 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
                                 : size_t(2 * 32 * kRowStage) * 8 + size_t(w.G) + 16;   // ovf only
     RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
-    k_tick_commit<<<1, kCommitThreads, bytes, st>>>(w, now, smem_g, ps);
+    RAPP_CUDA(launch_pdl(k_tick_commit, dim3(1), dim3(kCommitThreads), bytes, st, w, now, smem_g,
+                         ps));
     RAPP_LAUNCHED();
   }
   return RAPP_OK;
