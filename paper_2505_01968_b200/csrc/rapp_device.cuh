@@ -12,6 +12,25 @@
 
 namespace rapp {
 
+// Programmatic dependent launch: a kernel lets its successor launch once all of its CTAs
+// are running (griddepcontrol.launch_dependents) and waits for its predecessor's completion
+// (griddepcontrol.wait) only before it reads what the predecessor wrote, so launch latency
+// and independent set-up overlap the predecessor's tail.  Kernels launched without the
+// programmatic attribute see both as no-ops.
+#ifndef RAPP_PDL
+#define RAPP_PDL 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if RAPP_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if RAPP_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // a + (b - a) * t with each operation rounded — one lerp of hs/_kernels/_grid_cy.pyx:45-51.
 __device__ __forceinline__ double lerp_rn(double a, double b, double t) {
   return __dadd_rn(a, __dmul_rn(__dsub_rn(b, a), t));

@@ -15,6 +15,27 @@
 
 namespace rapp {
 
+#ifndef RAPP_PDL
+#define RAPP_PDL 1
+#endif
+// Launch with programmatic stream serialization (the kernel calls pdl_wait before it reads
+// its predecessor's outputs; rapp_device.cuh).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = RAPP_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Thread-local error message behind rapp_last_error().
 void set_error(const char* fmt, ...);
 extern std::atomic<int64_t> g_launches;

@@ -68,6 +68,7 @@ __global__ void k_mec_prepare(const FnDesc* __restrict__ fns, const double* __re
                               int64_t fn_end, double* __restrict__ thr,
                               unsigned long long* __restrict__ minlat,
                               unsigned long long* __restrict__ keys) {
+  pdl_trigger();
   const int64_t f = fn_begin + (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (f >= fn_end) return;
@@ -87,6 +88,8 @@ __global__ void k_mec_fallback(const FnDesc* __restrict__ fns, const double* __r
                                const unsigned long long* __restrict__ minlat,
                                double* __restrict__ thr, double* __restrict__ target2,
                                int32_t* __restrict__ fallback) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t f = fn_begin + (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (f >= fn_end) return;
@@ -127,6 +130,8 @@ __global__ void __launch_bounds__(kSearchThreads)
   extern __shared__ __align__(16) double smem[];
   __shared__ uint64_t bar;
   __shared__ unsigned long long s_red[kSearchThreads / 32];
+  pdl_trigger();
+  if (GATE) pdl_wait();  // the gate reads the previous passes' keys / fallback flags
   const int64_t f = fn_begin + blockIdx.x / chunks;
   const int chunk = blockIdx.x % chunks;
   if (GATE && (MINLAT ? keys[f] != kNoKey : fallback[f] == 0)) return;
@@ -177,6 +182,8 @@ __global__ void __launch_bounds__(kSearchThreads)
     sTq[i] = t;
     sK[i] = make_int2(lo, hi);
   }
+  if (!GATE) pdl_wait();  // thresholds and key reset of k_mec_prepare (table staging and
+                         // the sm / quota brackets above overlap it)
   for (int i = threadIdx.x; i < nB; i += blockDim.x) {
     int lo, hi;
     double t;
@@ -403,6 +410,8 @@ __global__ void k_mec_decode(const TableDesc* __restrict__ tds, const double* __
                              int64_t fn_begin, int64_t fn_end,
                              const unsigned long long* __restrict__ keys,
                              int32_t* __restrict__ out_bsq, uint64_t* __restrict__ out_key) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t f = fn_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (f >= fn_end) return;
   const FnDesc fd = fns[f];
@@ -453,9 +462,10 @@ static int launch_lattice(rapp_mec_plan* pl, const double* targets, int64_t f0, 
   RAPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pl->smem_bytes));
   rapp_ctx* c = pl->ctx;
-  kern<<<(unsigned)(nf * chunks), kSearchThreads, pl->smem_bytes, st>>>(
-      c->d_desc, c->d_pool, pl->d_fn, pl->d_blist, pl->d_thr, targets, f0, chunks, pl->step,
-      pl->nQ, pl->d_key, pl->d_minlat, pl->d_fb);
+  RAPP_CUDA(launch_pdl(kern, dim3((unsigned)(nf * chunks)), dim3(kSearchThreads),
+                       pl->smem_bytes, st, c->d_desc, c->d_pool, pl->d_fn, pl->d_blist, pl->d_thr,
+                       targets, f0, chunks, pl->step, pl->nQ, pl->d_key, pl->d_minlat,
+                       pl->d_fb));
   RAPP_LAUNCHED();
   return RAPP_OK;
 }
@@ -497,18 +507,18 @@ static int run_plan(rapp_mec_plan* pl, const double* d_targets, int64_t f0, int6
   } else {
     if ((rc = launch_lattice<false, true, true>(pl, d_targets, f0, nf, chunks, st))) return rc;
   }
-  k_mec_fallback<<<hblocks, 32 * wpb, 0, st>>>(pl->d_fn, pl->d_blist, f0, f1, pl->d_key,
-                                               pl->d_minlat, pl->d_thr, pl->d_target2,
-                                               pl->d_fb);
+  RAPP_CUDA(launch_pdl(k_mec_fallback, dim3(hblocks), dim3(32 * wpb), 0, st, pl->d_fn,
+                       pl->d_blist, f0, f1, pl->d_key, pl->d_minlat, pl->d_thr, pl->d_target2,
+                       pl->d_fb));
   RAPP_LAUNCHED();
   if (pl->smem_table) {
     if ((rc = launch_lattice<true, false, true>(pl, pl->d_target2, f0, nf, chunks, st))) return rc;
   } else {
     if ((rc = launch_lattice<false, false, true>(pl, pl->d_target2, f0, nf, chunks, st))) return rc;
   }
-  k_mec_decode<<<(unsigned)((nf + 127) / 128), 128, 0, st>>>(c->d_desc, c->d_pool, pl->d_fn,
-                                                             pl->d_blist, f0, f1, pl->d_key,
-                                                             d_out_bsq, d_out_key);
+  RAPP_CUDA(launch_pdl(k_mec_decode, dim3((unsigned)((nf + 127) / 128)), dim3(128), 0, st,
+                       c->d_desc, c->d_pool, pl->d_fn, pl->d_blist, f0, f1, pl->d_key,
+                       d_out_bsq, d_out_key));
   RAPP_LAUNCHED();
   return RAPP_OK;
 }

@@ -231,23 +231,6 @@ __device__ __forceinline__ bool batch_ok(const World& w, int f, int b) {
   return !(x < ba[0] || x > ba[td.nb - 1]);  // hs/perf.py:88-91
 }
 
-// Programmatic dependent launch between the tick's kernels: each kernel lets its
-// successor launch as soon as all of its CTAs are running (griddepcontrol.launch_dependents)
-// and waits for its predecessor's completion (griddepcontrol.wait) only before it reads
-// what the predecessor wrote, so launch latency and independent set-up overlap.
-#ifndef RAPP_TICK_PDL
-#define RAPP_TICK_PDL 1
-#endif
-__device__ __forceinline__ void pdl_trigger() {
-#if RAPP_TICK_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void pdl_wait() {
-#if RAPP_TICK_PDL
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-}
 
 #ifdef RAPP_TICK_PROF
 // diagnostics build only: cycles of the commit's parts, summed over ticks (lane 0)
@@ -2135,24 +2118,6 @@ static PodId pack_id(const char* s) {
 static void unpack_id(const PodId& id, char* s) {
   for (int i = 0; i < 4; ++i)
     for (int k = 0; k < 8; ++k) s[i * 8 + k] = char((id.w[i] >> (8 * (7 - k))) & 0xFF);
-}
-
-// launch with programmatic stream serialization (the kernel calls pdl_wait before it
-// reads its predecessor's outputs)
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                              cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = RAPP_TICK_PDL;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uint8_t* d_idle,
