@@ -96,6 +96,17 @@ __host__ __device__ inline int part_alloc(uint64_t e) { return int((e >> 8) & 0x
 __host__ __device__ inline int part_npods(uint64_t e) { return int((e >> 16) & 0xFFFF); }
 __host__ __device__ inline uint32_t part_uid(uint64_t e) { return uint32_t(e >> 32); }
 
+// phase A2 tabulates only the tick-start slot sms when the quota step is at most this
+// (100 / delta >= 25 quota steps per row); coarser steps tabulate every row
+constexpr int kMaskMaxDelta = 4;
+
+// one locate() result (_grid_cy.pyx:9-33): bracket lo, hi and weight t
+struct TickBrk {
+  int32_t lo, hi;
+  double t;
+};
+constexpr int kBrkPerFn = 201;  // 100 sm values, 100 quota steps, the reference batch
+
 struct World {
   // config
   double alpha, beta, cooldown, r_min, interval_s, cold_start, kA, kQ, kH, kD, kP0;
@@ -164,6 +175,9 @@ struct World {
   double* spec_gain;             // [F][kMaxPods] gain of those steps
   FastRec* fast;                 // [F] straight-line commits (n = 0: none)
   double* tgrid;                 // [F][100][100] throughput(bref, sm, q)
+  TickBrk* brk;                  // [F][201] phase A2's brackets: sm 1..100, quota steps, bref
+  uint32_t* sm_mask;             // [4] sm values (bit sm-1) tabulated in tgrid this tick: the
+                                 // tick-start partition sms and unallocated shares
   int32_t* ndown;
   DownAct* down;                 // [F][kMaxPods]
   int32_t* stamp;                // 1: record last_down = now
@@ -301,6 +315,24 @@ __global__ void k_tick_prologue(World w, double now) {
     *w.n_actions = 0;
     *w.err = 0;
     *w.err_fn = -1;
+  }
+  // the sm values a used-GPU slot can have while no partition is released: a tick-start
+  // partition's sm (join) or a GPU's unallocated share (new partition) — phase A2 tabulates
+  // those rows; a slot on any other share (freed by a release earlier in the tick) is
+  // evaluated on demand by the commit.  The commit clears the mask after use.  With coarse
+  // quota steps the whole grid is cheap and every row is tabulated.
+  if (w.delta > kMaskMaxDelta) {
+    if (blockIdx.x == 0 && threadIdx.x < 4) w.sm_mask[threadIdx.x] = threadIdx.x < 3 ? ~0u : 0xFu;
+    return;
+  }
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < w.G; g += gridDim.x * blockDim.x) {
+    const int n = w.g_nparts[g];
+    for (int i = 0; i < n; ++i) {
+      const int sm = part_sm(w.g_parts[int64_t(g) * kPartCap + i]);
+      if (sm >= 1 && sm <= 100) atomicOr(&w.sm_mask[(sm - 1) >> 5], 1u << ((sm - 1) & 31));
+    }
+    const int fs = w.g_freesm[g];
+    if (fs >= 1 && fs <= 100) atomicOr(&w.sm_mask[(fs - 1) >> 5], 1u << ((fs - 1) & 31));
   }
 }
 
@@ -767,6 +799,19 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
   const double* qa = seg + td.oq;
   const double* v = seg + td.ov;
   const int d = w.delta, nq = 100 / d;
+  __shared__ int s_cand[100];
+  __shared__ int s_ncand;
+  if (threadIdx.x < 32) {  // the mask's sm rows, ascending
+    int nc = 0;
+    for (int base = 0; base < 100; base += 32) {
+      const int sm0 = base + int(threadIdx.x);  // row index sm - 1
+      const bool on = sm0 < 100 && ((w.sm_mask[sm0 >> 5] >> (sm0 & 31)) & 1u);
+      const unsigned m = __ballot_sync(0xffffffffu, on);
+      if (on) s_cand[nc + __popc(m & ((1u << threadIdx.x) - 1u))] = sm0;
+      nc += __popc(m);
+    }
+    if (threadIdx.x == 0) s_ncand = nc;
+  }
   for (int i = threadIdx.x; i < 100; i += blockDim.x) {
     int lo, hi;
     double t;
@@ -788,6 +833,15 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
     s_tb = t;
   }
   __syncthreads();
+  if (d <= kMaskMaxDelta) {  // the brackets, for rows the commit evaluates itself (sm
+                             // values outside the mask)
+    TickBrk* B = w.brk + int64_t(f) * kBrkPerFn;
+    for (int i = threadIdx.x; i < 100; i += blockDim.x) {
+      B[i] = TickBrk{s_j[i].x, s_j[i].y, s_ts[i]};
+      if (i < nq) B[100 + i] = TickBrk{s_k[i].x, s_k[i].y, s_tq[i]};
+    }
+    if (threadIdx.x == 0) B[200] = TickBrk{s_i0, s_i1, s_tb};
+  }
   const int64_t plane = int64_t(td.ns) * td.nq;
   const double* v0 = v + s_i0 * plane;
   const double* v1 = v + s_i1 * plane;
@@ -796,7 +850,7 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
   // kGridU entries per thread per round: every table load of the round is issued before
   // the first store (the stores could alias the loads as far as the compiler knows)
   constexpr int kGridU = 4;
-  const int total = 100 * nq;
+  const int total = s_ncand * nq;
   for (int i0 = threadIdx.x; i0 < total; i0 += kGridU * blockDim.x) {
     double lat[kGridU];
     int64_t out[kGridU];
@@ -806,7 +860,8 @@ __global__ void __launch_bounds__(256) k_tick_grid(World w) {
       out[u] = -1;
       lat[u] = 0.0;
       if (i >= total) continue;
-      const int si = i / nq, qi = i - si * nq;
+      const int ci = i / nq, qi = i - ci * nq;
+      const int si = d > kMaskMaxDelta ? ci : s_cand[ci];
       out[u] = (int64_t(f) * 100 + si) * 100 + (qi + 1) * d - 1;
       const int2 j = s_j[si], k = s_k[qi];
       const double ts = s_ts[si], tq = s_tq[qi];
@@ -897,7 +952,51 @@ __device__ __forceinline__ int fast_hash(int g, int pos) {
   return int((uint32_t(g) * 2654435761u + uint32_t(pos) * 40503u) >> 23) & (kFastHash - 1);
 }
 
-struct Commit {
+// throughput(bref, sm, q) at this lane's quota steps q = (u*32 + lane + 1)*d <= qmax, from
+// phase A2's brackets — the used-GPU branch's row when A2 did not tabulate this sm
+struct Row4 {
+  double v[4];
+};
+__device__ __forceinline__ Row4 bracket_row(const World& w, int f, int bref, int sm, int qmax,
+                                         int d, int lane) {
+  const TickBrk* B = w.brk + int64_t(f) * kBrkPerFn;
+  const TickBrk bs = B[sm - 1], bb = B[200];
+  const TableDesc td = w.tds[w.fn_table[f]];
+  const double* v = w.pool + td.off + td.ov;
+  const int64_t r00 = (int64_t(bb.lo) * td.ns + bs.lo) * td.nq;
+  const int64_t r01 = (int64_t(bb.lo) * td.ns + bs.hi) * td.nq;
+  const int64_t r10 = (int64_t(bb.hi) * td.ns + bs.lo) * td.nq;
+  const int64_t r11 = (int64_t(bb.hi) * td.ns + bs.hi) * td.nq;
+  Row4 r;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k = u * 32 + lane;  // quota step index: q = (k + 1) * d
+    r.v[u] = 0.0;
+    if ((k + 1) * d <= qmax) {
+      const TickBrk bq = B[100 + k];
+      const double c00 = lerp_rn(v[r00 + bq.lo], v[r00 + bq.hi], bq.t);
+      const double c01 = lerp_rn(v[r01 + bq.lo], v[r01 + bq.hi], bq.t);
+      const double c10 = lerp_rn(v[r10 + bq.lo], v[r10 + bq.hi], bq.t);
+      const double c11 = lerp_rn(v[r11 + bq.lo], v[r11 + bq.hi], bq.t);
+      const double lat = lerp_rn(lerp_rn(c00, c01, bs.t), lerp_rn(c10, c11, bs.t), bb.t);
+      r.v[u] = throughput(double(bref), lat);
+    }
+  }
+  return r;
+}
+
+struct CommitPre {
+  double gap0, sg0;
+  int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods, kd0;
+  int nd, dkind, dquota, didle, stamp;
+  int pos0;  // hint: position of the first pod's partition at tick start (-1: none)
+  uint32_t uid0;
+};
+
+// kMasked: phase A2 tabulated only the sm rows of w.sm_mask (fine quota steps); the
+// used-GPU branch evaluates any other row from A2's brackets.
+template <bool kMasked>
+struct CommitT {
   const World& w;
   int lane;
   // partition lists of GPUs with at most `ps` partitions live in shared memory for the
@@ -911,6 +1010,7 @@ struct Commit {
   long long* scounter;   // shared copy of *w.counter
   uint32_t* skey;        // shared argmin keys per GPU: npods > 0 ? occupancy << 18 | rank : ~0
                          // (null: scan the summaries)
+  const uint32_t* smask;  // shared copy of w.sm_mask (the sm rows phase A2 tabulated)
 
   // lane-0 code: refresh GPU g's argmin key after its pod count / occupancy changed
   __device__ void rekey0(int g) const {
@@ -1268,13 +1368,7 @@ struct Commit {
   // Function header + its first pod (scale-up: sorted[0]; scale-down: the first staged
   // action's pod), prefetched for 32 functions at once by the commit loop: nothing here can
   // change before the function's own turn in the tick.
-  struct Pre {
-    double gap0, sg0;
-    int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods, kd0;
-    int nd, dkind, dquota, didle, stamp;
-    int pos0;  // hint: position of the first pod's partition at tick start (-1: none)
-    uint32_t uid0;
-  };
+  using Pre = CommitPre;
 
   __device__ Pre prefetch(int f) const { return prefetch_of(w, f); }
 
@@ -1447,14 +1541,21 @@ struct Commit {
             __syncwarp();
             return;
           }
-          const double* T = w.tgrid + (int64_t(f) * 100 + (sm - 1)) * 100;
           // every throughput the branch may read, in one round of independent loads:
-          // lanes hold the quota steps (u*32 + lane + 1)*d <= qmax, u < 4 (d >= 1)
+          // lanes hold the quota steps (u*32 + lane + 1)*d <= qmax, u < 4 (d >= 1) —
+          // from phase A2's grid when it tabulated this sm, else evaluated here
           double tv[4];
+          if (!kMasked || ((smask[(sm - 1) >> 5] >> ((sm - 1) & 31)) & 1u)) {
+            const double* T = w.tgrid + (int64_t(f) * 100 + (sm - 1)) * 100;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int qq = (u * 32 + lane + 1) * d;
-            tv[u] = qq <= qmax ? T[qq - 1] : 0.0;
+            for (int u = 0; u < 4; ++u) {
+              const int qq = (u * 32 + lane + 1) * d;
+              tv[u] = qq <= qmax ? T[qq - 1] : 0.0;
+            }
+          } else {  // interp3 from phase A2's brackets (the same doubles as locate())
+            const Row4 r = bracket_row(w, f, bref, sm, qmax, d, lane);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) tv[u] = r.v[u];
           }
           double cmax;
           if (qmax % d == 0) {
@@ -1723,6 +1824,7 @@ constexpr int kHelpers = RAPP_TICK_HELPERS;     // helper warps filling the head
 constexpr int kPreDepth = RAPP_TICK_PREDEPTH;   // batches of function headers in the ring
 constexpr int kCommitThreads = 32 * (1 + kHelpers);
 
+template <bool kMasked>
 __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double now, int smem_g,
                                                                 int ps) {
   // dynamic shared layout: [row staging 2 x 32 x kRowStage doubles][5*G summaries]
@@ -1737,7 +1839,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   // function of the tick can change) into a shared ring while warp 0 commits, helper h
   // taking batches h-1, h-1+kHelpers, ..., so warp 0 never waits on those dependent
   // global loads.
-  __shared__ Commit::Pre s_pre[kPreDepth][32];
+  __shared__ CommitPre s_pre[kPreDepth][32];
   __shared__ int s_pcls[kPreDepth][32];
   __shared__ FastRec s_fast[kPreDepth][32];
   __shared__ uint32_t s_htab[kFastHash];
@@ -1792,7 +1894,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
       const int f = base + lane;
       const int cf = f < w.F ? w.cls[f] : kNone;
       s_pcls[slot][lane] = cf;
-      s_pre[slot][lane] = Commit::prefetch_of(w, f);
+      s_pre[slot][lane] = CommitT<kMasked>::prefetch_of(w, f);
       {
         FastRec& fr = s_fast[slot][lane];
         fr.kind = kFastNone;
@@ -1831,7 +1933,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
     s_counter = (long long)*w.counter;
   }
   __syncwarp();
-  Commit c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter, skey};
+  __shared__ uint32_t s_smask[4];
+  if (lane < 4) s_smask[lane] = w.sm_mask[lane];
+  __syncwarp();
+  CommitT<kMasked> c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter, skey, s_smask};
   bool stop = s_err != 0;
 #ifdef RAPP_TICK_PROF
   s_tprof[lane] = 0;
@@ -1926,7 +2031,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
       }
       act &= act - 1;
       const int cls = __shfl_sync(0xffffffffu, mine, i);
-      const Commit::Pre& pre = s_pre[slot][i];
+      const CommitPre& pre = s_pre[slot][i];
       if (cls == kUp) {
         if (w.policy == 0)
           c.scale_up(base + i, now, pre, s_rows + ((j & 1) * 32 + i) * kRowStage);
@@ -1956,6 +2061,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   }
   __syncwarp();
   if (lane == 0) *w.n_actions = s_nact;
+  if (lane < 4) w.sm_mask[lane] = 0u;  // rebuilt by the next tick's prologue
   for (int g = lane; g < G; g += 32)
     if (!ovf[g]) {
       const int n = v.g_nparts[g];
@@ -1990,7 +2096,8 @@ __global__ void __launch_bounds__(32) k_tick_release(World w, const int32_t* __r
   for (int g = lane; g < w.G; g += 32) rel_ovf[g] = 1;  // every list lives in global memory
   if (lane == 0) s_err = 0;
   __syncwarp();
-  Commit c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter, nullptr};
+  CommitT<false> c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter, nullptr,
+           nullptr};
   for (int i = 0; i < n; ++i) {
     const int p = list[i];
     if (w.p_state[p] == kDead) continue;
@@ -2135,11 +2242,15 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     // shared memory: GPU summaries (5 ints/GPU) + a partition cache of up to 12 entries
     // per GPU + overflow flags, within ~200 KB
     // 227 KB per CTA minus the row staging and the static shared memory
-    static size_t static_smem = 0;  // the kernel's static shared memory (header ring etc.)
+    // fine quota steps: phase A2 tabulated the mask's rows only (see k_tick_prologue)
+    const bool masked = w.delta <= kMaskMaxDelta;
+    auto commit = masked ? k_tick_commit<true> : k_tick_commit<false>;
+    static size_t static_smem = 0;  // the kernels' static shared memory (header ring etc.)
     if (static_smem == 0) {
-      cudaFuncAttributes fa{};
-      RAPP_CUDA(cudaFuncGetAttributes(&fa, k_tick_commit));
-      static_smem = fa.sharedSizeBytes + 1024;
+      cudaFuncAttributes fa{}, fb{};
+      RAPP_CUDA(cudaFuncGetAttributes(&fa, k_tick_commit<true>));
+      RAPP_CUDA(cudaFuncGetAttributes(&fb, k_tick_commit<false>));
+      static_smem = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes) + 1024;
     }
     const size_t budget = 227 * 1024 - size_t(2 * 32 * kRowStage) * 8 - static_smem;
     const size_t gbytes = size_t(5 * w.G + 1) / 2 * 2 * sizeof(int32_t);
@@ -2151,10 +2262,9 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
     const size_t bytes = smem_g ? size_t(2 * 32 * kRowStage) * 8 + gbytes + size_t(w.G) * ps * 8 +
                                       size_t((w.G + 3) & ~3) + size_t(w.G) * 4 + 16  // + keys
                                 : size_t(2 * 32 * kRowStage) * 8 + size_t(w.G) + 16;   // ovf only
-    RAPP_CUDA(cudaFuncSetAttribute(k_tick_commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RAPP_CUDA(cudaFuncSetAttribute(commit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(bytes, 48 * 1024)));
-    RAPP_CUDA(launch_pdl(k_tick_commit, dim3(1), dim3(kCommitThreads), bytes, st, w, now, smem_g,
-                         ps));
+    RAPP_CUDA(launch_pdl(commit, dim3(1), dim3(kCommitThreads), bytes, st, w, now, smem_g, ps));
     RAPP_LAUNCHED();
   }
   return RAPP_OK;
@@ -2407,6 +2517,8 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.spec_gain, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.fast, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.tgrid, FP * 100 * 100))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.sm_mask, 4))) return rc;  // zeroed
+  if ((rc = dev_alloc(t.get(), &w.brk, FP * kBrkPerFn))) return rc;
   if ((rc = dev_alloc(t.get(), &w.ndown, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.down, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.stamp, FP))) return rc;
