@@ -102,14 +102,24 @@ class TickResult:
     def actions(self) -> list[ScalingAction]:
         """Reference-shaped actions (horizontal_up carries pod_id None)."""
         if self._actions is None:
+            # device-produced records are valid by construction: each action gets its field
+            # dict directly (ScalingAction._trusted without the call and keyword overhead)
             e = self._engine
-            fids, gids, mk = e.fids, e.gids, ScalingAction._trusted
-            hup = ActionKind.HORIZONTAL_UP
+            fids, gids = e.fids, e.gids
+            r = self.raw
+            new, setattr_, cls = object.__new__, object.__setattr__, ScalingAction
             out = []
-            for a, pid in zip(self.raw.tolist(), self.pod_ids):
-                kind = KINDS[a[1]]
-                out.append(mk(fids[a[0]], kind, a[2], a[3], a[4],
-                              None if kind is hup else pid, gids[a[6]]))
+            app = out.append
+            for f, k, b, sm, q, g, pid in zip(r["fn"].tolist(), r["kind"].tolist(),
+                                               r["batch"].tolist(), r["sm"].tolist(),
+                                               r["quota"].tolist(), r["gpu"].tolist(),
+                                               self.pod_ids):
+                a = new(cls)
+                setattr_(a, "__dict__", {"function_id": fids[f], "kind": KINDS[k], "batch": b,
+                                         "sm_percent": sm, "quota_percent": q,
+                                         "pod_id": None if k == 2 else pid,
+                                         "gpu_id": gids[g]})
+                app(a)
             self._actions = out
         return self._actions
 
@@ -313,18 +323,17 @@ class TickEngine:
         counter) and maps every action to its pod id."""
         pods = raw["pod"].tolist()
         kinds = raw["kind"].tolist()
-        fns = raw["fn"].tolist()
-        pod_ids = []
-        for p, k, f in zip(pods, kinds, fns):
-            if k == 2:  # horizontal_up: a new pod at the next device index
-                assert p == len(self.pod_ids), "device pod index out of step"
-                pid = f"pod-{self.counter:06d}"
-                self.counter += 1
-                self.pod_ids.append(pid)
-                self.pod_fids.append(self.fids[f])
-            else:
-                pid = self.pod_ids[p]
-            pod_ids.append(pid)
+        ids = self.pod_ids
+        new = [i for i, k in enumerate(kinds) if k == 2]  # horizontal_up: new pods, in order
+        if new:
+            start, c0 = len(ids), self.counter
+            if [pods[i] for i in new] != list(range(start, start + len(new))):
+                raise InvariantViolation("device pod index out of step")
+            fns = raw["fn"].tolist()
+            ids.extend([f"pod-{c:06d}" for c in range(c0, c0 + len(new))])
+            self.pod_fids.extend([self.fids[fns[i]] for i in new])
+            self.counter = c0 + len(new)
+        pod_ids = [ids[p] for p in pods]
         return TickResult(self, raw, self._obs[:len(self.fids)].copy(),
                           self._pred[:len(self.fids)].copy(), pod_ids)
 
