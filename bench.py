@@ -847,7 +847,11 @@ def run_replay(args, local, name="burst-100", reps=3):
     cfg = ScalerConfig(alpha=fx(run["alpha"]), beta=fx(run["beta"]), delta_iq=run["delta"],
                        cooldown_ms=fx(run["cooldown_ms"]), r_min=fx(run["r_min"]))
     times = []
+    eng = res = None
     for rep in range(reps):
+        # the previous pass's engine (kept alive by its last TickResult) is destroyed here,
+        # not inside the first timed tick of this pass
+        eng = res = None
         eng = TickEngine(fns, tables, cluster_from(run["initial"]), cfg,
                          kalman_params={k: fx(v) for k, v in run["kalman"].items()},
                          scaler_interval_ms=fx(run["interval_ms"]),

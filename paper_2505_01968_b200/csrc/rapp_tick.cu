@@ -2534,6 +2534,11 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   }
   RAPP_CUDA(cudaMallocHost(&t->h_in, FP * 16 + (size_t)cap + 64));
   RAPP_CUDA(cudaMallocHost(&t->h_out, kOutHead + FP * 16 + 1024 * sizeof(rapp_action)));
+  // release staging sized for typical between-tick releases up front: a pinned allocation
+  // inside a tick's host call costs milliseconds (rapp_tick_release grows it if needed)
+  t->rel_cap = 1024;
+  RAPP_CUDA(cudaMalloc(&t->d_rel, (size_t)t->rel_cap * 4));
+  RAPP_CUDA(cudaMallocHost(&t->h_rel, (size_t)t->rel_cap * 4));
   t->h_npods = n_pods;
   // build the fresh-GPU search index
   for (int f0 = 0; f0 < F; f0 += 32768) {
