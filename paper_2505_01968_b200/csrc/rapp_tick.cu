@@ -176,6 +176,7 @@ struct World {
   FastRec* fast;                 // [F] straight-line commits (n = 0: none)
   double* tgrid;                 // [F][100][100] throughput(bref, sm, q)
   TickBrk* brk;                  // [F][201] phase A2's brackets: sm 1..100, quota steps, bref
+  int32_t mask_none;             // tests: tabulate no row (every used-GPU row from brackets)
   uint32_t* sm_mask;             // [4] sm values (bit sm-1) tabulated in tgrid this tick: the
                                  // tick-start partition sms and unallocated shares
   int32_t* ndown;
@@ -325,6 +326,7 @@ __global__ void k_tick_prologue(World w, double now) {
     if (blockIdx.x == 0 && threadIdx.x < 4) w.sm_mask[threadIdx.x] = threadIdx.x < 3 ? ~0u : 0xFu;
     return;
   }
+  if (w.mask_none) return;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < w.G; g += gridDim.x * blockDim.x) {
     const int n = w.g_nparts[g];
     for (int i = 0; i < n; ++i) {
@@ -2518,6 +2520,10 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.fast, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.tgrid, FP * 100 * 100))) return rc;
   if ((rc = dev_alloc(t.get(), &w.sm_mask, 4))) return rc;  // zeroed
+  {
+    const char* mn = getenv("RAPP_TICK_MASK_NONE");  // "1": test switch (see World)
+    w.mask_none = mn != nullptr && strcmp(mn, "1") == 0;
+  }
   if ((rc = dev_alloc(t.get(), &w.brk, FP * kBrkPerFn))) return rc;
   if ((rc = dev_alloc(t.get(), &w.ndown, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.down, FP * kMaxPods))) return rc;

@@ -141,9 +141,13 @@ def test_config4_ticks_vs_oracle():
 
 
 @pytest.mark.parametrize("delta,ngpu,nfn", [(1, 50, 60), (7, 30, 80), (25, 200, 150),
-                                            (10, 12, 40)])
+                                            (10, 12, 40), (2, 120, 300), (4, 60, 200),
+                                            (1, 200, 100), (3, 300, 150)])
 def test_random_worlds_vs_oracle(delta, ngpu, nfn):
-    """Quota steps 1..25, crowded and sparse clusters (fresh-GPU branch, releases)."""
+    """Quota steps 1..25, crowded and sparse clusters (fresh-GPU branch, releases).  With
+    quota steps <= 4 phase A2 tabulates only the tick-start slot sms; the shares left beside
+    fresh-GPU placements (100 - s, s on the table's 10% grid) and freed by releases are
+    evaluated by the commit from A2's brackets."""
     import bench
     from paper_2505_01968_b200.autoscaler import ScalerConfig
     fns, tables, cluster, _ = bench.make_config4_world(nfn, ngpu, seed=delta)
@@ -173,6 +177,22 @@ def test_full_grid_fresh_gpu_search_vs_oracle():
     fns, tables, cluster, _ = bench.make_config4_world(12, 40, seed=3, full_grid=True)
     cfg = ScalerConfig(alpha=0.9, beta=0.5, delta_iq=1, cooldown_ms=1000.0, r_min=1.0)
     _oracle_ticks(fns, tables, cluster, cfg, 4, seed=5, interval_ms=1000.0,
+                  cold_start_ms=1500.0)
+
+
+@pytest.mark.parametrize("delta,ngpu,nfn,full", [(1, 50, 60, False), (2, 120, 300, False),
+                                                 (4, 60, 200, False), (1, 60, 40, True)])
+def test_bracket_rows_vs_oracle(monkeypatch, delta, ngpu, nfn, full):
+    """RAPP_TICK_MASK_NONE=1 makes phase A2 tabulate no row, so every used-GPU placement reads
+    its throughput row through the commit's bracket path (the path of slot shares outside
+    the tick-start mask, rare in these worlds) — decisions must still equal the oracle."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    monkeypatch.setenv("RAPP_TICK_MASK_NONE", "1")
+    fns, tables, cluster, _ = bench.make_config4_world(nfn, ngpu, seed=delta + 40,
+                                                       full_grid=full)
+    cfg = ScalerConfig(alpha=0.85, beta=0.4, delta_iq=delta, cooldown_ms=1000.0, r_min=1.0)
+    _oracle_ticks(fns, tables, cluster, cfg, 6, seed=delta + 41, interval_ms=1000.0,
                   cold_start_ms=1500.0)
 
 
