@@ -32,7 +32,7 @@
 #include "rapp_internal.h"
 
 #ifndef RAPP_K3_UNROLL
-#define RAPP_K3_UNROLL 4
+#define RAPP_K3_UNROLL 8
 #endif
 
 namespace rapp {
