@@ -1886,13 +1886,17 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   __syncthreads();
   if (threadIdx.x >= 32) {
     const int h = (threadIdx.x >> 5) - 1;
+    bool quit = false;
     for (int b = h, base = 32 * h; base < w.F; b += kHelpers, base += 32 * kHelpers) {
       const int slot = b % kPreDepth;
       while (s_done < b - kPreDepth) {  // the slot is free once batch b - depth is done
-        if (s_stop) return;
+        if (s_stop) {
+          quit = true;
+          break;
+        }
         __nanosleep(32);
       }
-      if (s_stop) return;
+      if (quit || s_stop) break;
       const int f = base + lane;
       const int cf = f < w.F ? w.cls[f] : kNone;
       s_pcls[slot][lane] = cf;
@@ -1915,8 +1919,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
       __syncwarp();
       if (lane == 0) s_ready[slot] = b;
     }
-    return;
-  }
+  } else {  // warp 0: the commit
   World v = w;
   if (smem_g) {
     v.g_npods = sg;
@@ -2054,9 +2057,6 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   if (lane == 0) s_stop = 1;  // release the helper if the commit stopped early
   // no bulk copy may still be in flight into shared memory when the CTA exits
   for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
-#ifdef RAPP_TICK_PROF
-  const long long _epi0 = clock64();
-#endif
   if (lane == 0) {
     *w.n_pods = s_npods;
     *w.counter = s_counter;
@@ -2064,13 +2064,21 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   __syncwarp();
   if (lane == 0) *w.n_actions = s_nact;
   if (lane < 4) w.sm_mask[lane] = 0u;  // rebuilt by the next tick's prologue
-  for (int g = lane; g < G; g += 32)
+#ifdef RAPP_TICK_PROF
+  __syncwarp();
+  g_tick_prof[lane] += s_tprof[lane];
+#endif
+  }  // warp 0
+  // every warp: the shared-memory cluster state back to global memory
+  __syncthreads();
+  const int32_t* nparts = smem_g ? sg + 2 * G : w.g_nparts;
+  for (int g = threadIdx.x; g < G; g += blockDim.x)
     if (!ovf[g]) {
-      const int n = v.g_nparts[g];
+      const int n = nparts[g];
       for (int i = 0; i < n; ++i) w.g_parts[int64_t(g) * kPartCap + i] = sp[int64_t(g) * ps + i];
     }
   if (smem_g) {
-    for (int g = lane; g < G; g += 32) {
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
       w.g_npods[g] = sg[g];
       w.g_hgo[g] = sg[G + g];
       w.g_nparts[g] = sg[2 * G + g];
@@ -2078,12 +2086,6 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
       w.g_nextuid[g] = uint32_t(sg[4 * G + g]);
     }
   }
-#ifdef RAPP_TICK_PROF
-  __syncwarp();
-  if (lane == 0) s_tprof[21] = clock64() - _epi0;  // epilogue: state back to global memory
-  __syncwarp();
-  g_tick_prof[lane] += s_tprof[lane];
-#endif
 }
 
 // Releases reported by the host between ticks (a DRAINING pod whose last request finished:
@@ -2233,7 +2235,7 @@ static int launch_tick(rapp_tick* t, double now, const int64_t* d_arr, const uin
                        const double* d_pred, cudaStream_t st) {
   World w = t->w;
   w.p_idle = d_idle;
-  k_tick_prologue<<<std::max(1, std::min(1024, (w.pod_cap + 255) / 256)), 256, 0, st>>>(w, now);
+  k_tick_prologue<<<std::max(1, std::min(64, (w.pod_cap + 255) / 256)), 256, 0, st>>>(w, now);
   RAPP_LAUNCHED();
   if (w.F > 0) {
     RAPP_CUDA(launch_pdl(k_tick_phase_a, dim3((w.F + 7) / 8), dim3(256), 0, st, w, now, d_arr,
