@@ -233,6 +233,48 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------
 
 
+_ALL_CPUS = None  # the process's CPU set before numa_bind (the CPU baselines use all of it)
+
+
+class all_cpus:
+    """Context: the whole host CPU set (CPU-baseline process pools inherit it)."""
+
+    def __enter__(self):
+        self.saved = os.sched_getaffinity(0)
+        if _ALL_CPUS:
+            os.sched_setaffinity(0, _ALL_CPUS)
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.saved)
+
+
+def numa_bind(local):
+    """Best effort: run this rank's host threads on the CPUs of its GPU's NUMA node, so the
+    pinned staging buffers allocated afterwards are local to the GPU's PCIe root (the e2e
+    copies are PCIe-bound).  No-op when the topology is not exposed."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(local)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as fh:
+            node = int(fh.read().strip())
+        if node < 0:
+            return None
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as fh:
+            cpus = set()
+            for part in fh.read().strip().split(","):
+                lo, _, hi = part.partition("-")
+                cpus.update(range(int(lo), int(hi or lo) + 1))
+        if cpus:
+            global _ALL_CPUS
+            _ALL_CPUS = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, cpus)
+            return node
+    except (OSError, ValueError, AttributeError):
+        pass
+    return None
+
+
 def dist_init(gpus):
     import torch
     import torch.distributed as dist
@@ -244,6 +286,7 @@ def dist_init(gpus):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
+    numa_bind(local)
     return rank, world, local
 
 
@@ -605,9 +648,10 @@ def run_mlp(args, rank, world, local, n_per_model=None):
     import torch as _t
     sample = coords[0][:200_000].cpu().numpy()
     threads = _t.get_num_threads()
-    t0 = time.perf_counter()
-    lm.reference_forward(0, sample)
-    cdt = time.perf_counter() - t0
+    with all_cpus():
+        t0 = time.perf_counter()
+        lm.reference_forward(0, sample)
+        cdt = time.perf_counter() - t0
     cpu = {"value": len(sample) / cdt, "unit": UNIT, "cores": threads, "kind": "port",
            "sample": f"{len(sample)} queries through the fp32 torch forward on the host"}
     # the fused search over the learned predictions (feasibility + packed-key argmin in
@@ -663,6 +707,11 @@ def _lattice_worker_run(_):
         or_most_efficient_config(t._b_axis, t._s_axis, t._q_axis, t.latency_ms, target, 1,
                                  list(range(1, 33)))
     return len(_LW["work"])
+
+
+def lattice_cpu_baseline_all():
+    with all_cpus():
+        return lattice_cpu_baseline()
 
 
 def lattice_cpu_baseline(fn_per_proc=25, steps=3, procs=None):
@@ -948,7 +997,7 @@ def _worker_run(_):
 
 def host_cores():
     try:
-        return len(os.sched_getaffinity(0))
+        return len(_ALL_CPUS or os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
 
@@ -1051,10 +1100,12 @@ def main():
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline and args.workload == "stream":
-        v, info = cpu_reference(steps=3, warmup=1)
+        with all_cpus():
+            v, info = cpu_reference(steps=3, warmup=1)
         cpu = {"value": v, "unit": UNIT, **info}
     if world == 1 and not args.no_cpu_baseline and args.workload == "lattice":
-        cpu = lattice_cpu_baseline()
+        with all_cpus():
+            cpu = lattice_cpu_baseline()
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
             "higher_is_better": True, "scaling": res["scaling"], "vs_baseline": None,
@@ -1075,7 +1126,7 @@ def main():
                                     "ms_per_step": lat["ms"] / largs.steps,
                                     "roofline": lat["roofline"], "e2e": lat["e2e"],
                                     "config": lat["config"],
-                                    "cpu_baseline": lattice_cpu_baseline()}
+                                    "cpu_baseline": lattice_cpu_baseline_all()}
         margs = argparse.Namespace(**{**vars(args), "steps": 30, "queries": 25_000_000})
         mlp = run_mlp(margs, rank, world, local)
         extra["learned_mlp"] = {"value": mlp["value"], "unit": UNIT,
