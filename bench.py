@@ -109,7 +109,7 @@ def make_config4_world(nfn=1000, ngpu=400, seed=0, full_grid=False, device=None)
     b=1..32 pow2, s,q=10..100 step 10; full_grid: 32x91x100 and delta 1), one pod each at
     (b=8, s=20, q=20) placed round-robin over ngpu GPUs.  Returns (functions, tables,
     cluster, caps) with caps[f] = throughput of the initial pod."""
-    from paper_2505_01968_b200 import PerfTable, allocator
+    from paper_2505_01968_b200 import PerfTable
     from paper_2505_01968_b200.core import (ClusterState, FunctionSpec, GpuDevice, PodConfig,
                                             PodInstance, PodState)
     rng = random.Random(seed)
@@ -132,8 +132,25 @@ def make_config4_world(nfn=1000, ngpu=400, seed=0, full_grid=False, device=None)
     for i, f in enumerate(fns):
         pod = PodInstance(f"pod-{i:06d}", f.function_id, 8, 20, 20, "",
                           state=PodState.RUNNING)
-        allocator.place_pod(cluster, pod, f"gpu-{i % ngpu:03d}")
+        place_initial(cluster, pod, f"gpu-{i % ngpu:03d}")
     return fns, tables, cluster, caps
+
+
+def place_initial(cluster, pod, gpu_id):
+    """World construction: the pod joins the GPU's first same-sm partition with quota room
+    for it, else opens a new partition (the placement rule of hs/allocator.py:55-108; the
+    bench's initial worlds never exceed a GPU's SM share)."""
+    from paper_2505_01968_b200.core import SmPartition
+    parts = cluster.gpus[gpu_id].partitions
+    part = next((p for p in parts if p.sm_percent == pod.sm_percent
+                 and p.quota_allocated + pod.quota_percent <= 100), None)
+    if part is None:
+        part = SmPartition(pod.sm_percent)
+        parts.append(part)
+    part.resident_pods.append(pod.pod_id)
+    part.quota_allocated += pod.quota_percent
+    pod.gpu_id = gpu_id
+    cluster.pods[pod.pod_id] = pod
 
 
 def config4_arrivals(fns, caps, rng, interval_s, lo=0.0, hi=3.0):

@@ -88,6 +88,13 @@ int rapp_interp3_many_dev(rapp_ctx *ctx, int32_t table_id, const double *d_coord
 int rapp_interp3_many_host(rapp_ctx *ctx, int32_t table_id, const double *coords,
                            int64_t n, double *out);
 
+/* Small-batch evaluation for the scalar API (PerfTable.predict_latency / throughput,
+ * hs/perf.py:80-102): latency[i] and, if rps != NULL, throughput of coords[i,:] (host
+ * buffers, n rows of (batch, sm%, quota%)).  Persistent pinned staging: one H2D copy, one
+ * launch and one D2H copy per call, no allocation after the first. */
+int rapp_table_points(rapp_ctx *ctx, int32_t table_id, int64_t n, const double *coords,
+                      double *latency, double *rps);
+
 /* ---- perf-table ingest (load_table / validate_table_file, hs/perf.py:155-267) ----------
  * Native row reader for the strict common CSV form: the exact header line, then
  * `fid,int,int,int,float` rows with one function id, no quoting, padding, blank lines or
@@ -144,6 +151,13 @@ int rapp_mec_plan_run_dev(rapp_mec_plan *plan, const double *d_targets, int64_t 
                           int64_t fn_end, int32_t *d_out_bsq, uint64_t *d_out_key,
                           void *stream);
 
+/* Same over host buffers (the scalar most_efficient_config and PerfTableSet.search):
+ * targets[0 .. fn_end-fn_begin) for functions [fn_begin, fn_end) -> out_bsq (b,s,q) per
+ * function.  The plan keeps pinned staging and a stream: one H2D, the search launches, one
+ * D2H per call.  RAPP_E_VALUE when a target is <= 0 (hs/perf.py:114-115). */
+int rapp_mec_plan_run(rapp_mec_plan *plan, const double *targets, int64_t fn_begin,
+                      int64_t fn_end, int64_t *out_bsq);
+
 /* Measurement: when enabled (which also resets the record), every run brackets its meet
  * pass — the fused lattice kernel K3 — with CUDA events on the run's stream;
  * rapp_mec_plan_kernel_time synchronises them and returns the summed kernel time and the
@@ -169,6 +183,9 @@ typedef struct {
     double interval_s;         /* scaler_interval_ms / 1000.0, computed by the caller */
     double cold_start_ms;      /* SimConfig.cold_start_ms (new pods become RUNNING then) */
     double kal_A, kal_Q, kal_H, kal_D, kal_P0;  /* Kalman defaults (hs/kalman.py:15-19) */
+    int32_t sum_mode;          /* the caller's float sum() (hs/autoscaler.py:86-87): 0 CPython
+                                  >= 3.12 (Neumaier-compensated), 1 older (left to right) */
+    int32_t _pad;
 } rapp_scaler_config;
 
 typedef struct {

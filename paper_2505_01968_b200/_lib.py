@@ -55,6 +55,8 @@ SIGNATURES = [
                                              c_vp, c_vp]),
     ("rapp_interp3_many_host", ctypes.c_int, [c_vp, ctypes.c_int32, c_dp, ctypes.c_int64,
                                               c_dp]),
+    ("rapp_table_points", ctypes.c_int, [c_vp, ctypes.c_int32, ctypes.c_int64, c_dp, c_dp,
+                                         c_dp]),
     ("rapp_csv_parse", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, c_i64p,
                                       c_i64p, c_i64p, c_dp, c_i64p, ctypes.c_char_p,
                                       ctypes.c_int64, c_i32p]),
@@ -72,6 +74,7 @@ SIGNATURES = [
     ("rapp_mec_plan_points", ctypes.c_int, [c_vp, c_i64p]),
     ("rapp_mec_plan_run_dev", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp,
                                              c_vp, c_vp]),
+    ("rapp_mec_plan_run", ctypes.c_int, [c_vp, c_dp, ctypes.c_int64, ctypes.c_int64, c_i64p]),
     ("rapp_mec_plan_timing", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("rapp_mec_plan_kernel_time", ctypes.c_int, [c_vp, c_dp, c_i64p]),
     ("rapp_metrics_finalize", ctypes.c_int, [c_vp, ctypes.c_int64, c_dp, c_i64p, c_i64p, c_dp,

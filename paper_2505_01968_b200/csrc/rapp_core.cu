@@ -319,6 +319,24 @@ int pipe_run(rapp_ctx* ctx, const double* coords, int64_t n, double* out,
   return RAPP_OK;
 }
 
+// Grows the point staging to at least `rows` rows (rapp_table_points, rapp_locate).
+static int ensure_pts(rapp_ctx* ctx, int64_t rows) {
+  if (!ctx->pts_stream)
+    RAPP_CUDA(cudaStreamCreateWithFlags(&ctx->pts_stream, cudaStreamNonBlocking));
+  if (rows <= ctx->pts_rows) return RAPP_OK;
+  rows = rows < 1024 ? 1024 : rows;
+  RAPP_CUDA(cudaStreamSynchronize(ctx->pts_stream));
+  if (ctx->h_pts) RAPP_CUDA(cudaFreeHost(ctx->h_pts));
+  if (ctx->d_pts) RAPP_CUDA(cudaFree(ctx->d_pts));
+  ctx->h_pts = nullptr;
+  ctx->d_pts = nullptr;
+  ctx->pts_rows = 0;
+  RAPP_CUDA(cudaMallocHost(&ctx->h_pts, (size_t)rows * 5 * sizeof(double)));
+  RAPP_CUDA(cudaMalloc(&ctx->d_pts, (size_t)rows * 5 * sizeof(double)));
+  ctx->pts_rows = rows;
+  return RAPP_OK;
+}
+
 static int interp_host(rapp_ctx* ctx, int32_t table_id, const double* coords, int64_t n,
                        double* out) {
   return pipe_run(ctx, coords, n, out,
@@ -398,6 +416,9 @@ int rapp_ctx_destroy(rapp_ctx* ctx) {
   if (ctx->d_pool) cudaFree(ctx->d_pool);
   if (ctx->d_desc) cudaFree(ctx->d_desc);
   if (ctx->d_small) cudaFree(ctx->d_small);
+  if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
+  if (ctx->d_pts) cudaFree(ctx->d_pts);
+  if (ctx->pts_stream) cudaStreamDestroy(ctx->pts_stream);
   {
     std::lock_guard<std::mutex> lk(g_default_mu);
     for (auto& d : g_default)
@@ -478,22 +499,58 @@ int rapp_locate(const double* axis, int64_t n, double x, int64_t* lo, int64_t* h
   int rc = default_ctx(&ctx);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(ctx->mu);
-  double* d_axis = nullptr;
-  RAPP_CUDA(cudaMalloc(&d_axis, (size_t)n * 8));
-  RAPP_CUDA(cudaMemcpy(d_axis, axis, (size_t)n * 8, cudaMemcpyHostToDevice));
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  // the axis rides in the point staging (3 doubles per row): no allocation per call
+  if ((rc = ensure_pts(ctx, (n + 2) / 3 + 1))) return rc;
+  memcpy(ctx->h_pts, axis, (size_t)n * 8);
+  cudaStream_t st = ctx->pts_stream;
+  RAPP_CUDA(cudaMemcpyAsync(ctx->d_pts, ctx->h_pts, (size_t)n * 8, cudaMemcpyHostToDevice, st));
   int64_t* d_i = reinterpret_cast<int64_t*>(ctx->d_small);
-  k_locate1<<<1, 1>>>(d_axis, (int)n, x, d_i, ctx->d_small + 2);
+  k_locate1<<<1, 1, 0, st>>>(ctx->d_pts, (int)n, x, d_i, ctx->d_small + 2);
   g_launches.fetch_add(1);
+  RAPP_CUDA(cudaMemcpyAsync(ctx->h_pts, ctx->d_small, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                            st));
+  RAPP_CUDA(cudaStreamSynchronize(st));
   int64_t hv[2];
-  double tv;
-  cudaError_t e1 = cudaMemcpy(hv, d_i, sizeof hv, cudaMemcpyDeviceToHost);
-  cudaError_t e2 = cudaMemcpy(&tv, ctx->d_small + 2, sizeof tv, cudaMemcpyDeviceToHost);
-  cudaFree(d_axis);
-  RAPP_CUDA(e1);
-  RAPP_CUDA(e2);
+  memcpy(hv, ctx->h_pts, sizeof hv);
   *lo = hv[0];
   *hi = hv[1];
-  *t = tv;
+  *t = ctx->h_pts[2];
+  return RAPP_OK;
+}
+
+int rapp_table_points(rapp_ctx* ctx, int32_t table_id, int64_t n, const double* coords,
+                      double* latency, double* rps) {
+  if (!ctx || n < 0 || (n > 0 && (!coords || !latency))) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  if (n == 0) return RAPP_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RAPP_CUDA(cudaSetDevice(ctx->device));
+  constexpr int64_t kMaxRows = 1 << 16;
+  int rc = ensure_pts(ctx, n < kMaxRows ? n : kMaxRows);
+  if (rc) return rc;
+  cudaStream_t st = ctx->pts_stream;
+  const int64_t cap = ctx->pts_rows;
+  for (int64_t r0 = 0; r0 < n; r0 += cap) {
+    const int64_t m = n - r0 < cap ? n - r0 : cap;
+    double* h_lat = ctx->h_pts + 3 * cap;
+    double* h_rps = h_lat + cap;
+    double* d_lat = ctx->d_pts + 3 * cap;
+    double* d_rps = d_lat + cap;
+    memcpy(ctx->h_pts, coords + 3 * r0, (size_t)m * 24);
+    RAPP_CUDA(cudaMemcpyAsync(ctx->d_pts, ctx->h_pts, (size_t)m * 24, cudaMemcpyHostToDevice,
+                              st));
+    if ((rc = launch_interp(ctx, table_id, ctx->d_pts, m, d_lat, rps ? d_rps : nullptr, st)))
+      return rc;
+    RAPP_CUDA(cudaMemcpyAsync(h_lat, d_lat, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+    if (rps)
+      RAPP_CUDA(cudaMemcpyAsync(h_rps, d_rps, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+    RAPP_CUDA(cudaStreamSynchronize(st));
+    memcpy(latency + r0, h_lat, (size_t)m * 8);
+    if (rps) memcpy(rps + r0, h_rps, (size_t)m * 8);
+  }
   return RAPP_OK;
 }
 

@@ -123,6 +123,14 @@ struct rapp_ctx {
   std::vector<StatelessTable> stateless;
   uint64_t stateless_clock = 0;
   double* d_small = nullptr;  // 64 doubles of scratch for scalar calls
+  // small-batch point evaluation (rapp_table_points / rapp_locate): pinned staging
+  // [coords 3n | latency n | rps n] mirrored on the device, one stream, grown on demand,
+  // so a scalar predict_latency / throughput is one H2D, one launch, one D2H — no
+  // allocation per call
+  cudaStream_t pts_stream = nullptr;
+  double* h_pts = nullptr;
+  double* d_pts = nullptr;
+  int64_t pts_rows = 0;      // rows the staging holds
 };
 
 namespace rapp {

@@ -451,6 +451,11 @@ struct rapp_mec_plan {
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // 2 per timed launch
   size_t ev_used = 0;
+  // host-buffer runs (rapp_mec_plan_run): pinned [targets nfn | bsq 3*nfn int32] staging
+  // mirrored on the device, one stream — allocated on the first host run, reused after
+  cudaStream_t stream = nullptr;
+  uint8_t* h_stage = nullptr;
+  uint8_t* d_stage = nullptr;
 };
 
 namespace rapp {
@@ -623,6 +628,9 @@ int rapp_mec_plan_destroy(rapp_mec_plan* pl) {
   cudaFree(pl->d_target2);
   cudaFree(pl->d_fb);
   for (cudaEvent_t e : pl->ev) cudaEventDestroy(e);
+  if (pl->h_stage) cudaFreeHost(pl->h_stage);
+  if (pl->d_stage) cudaFree(pl->d_stage);
+  if (pl->stream) cudaStreamDestroy(pl->stream);
   delete pl;
   return RAPP_OK;
 }
@@ -672,6 +680,43 @@ int rapp_mec_plan_run_dev(rapp_mec_plan* pl, const double* d_targets, int64_t fn
   }
   RAPP_CUDA(cudaSetDevice(pl->ctx->device));
   return run_plan(pl, d_targets, fn_begin, fn_end, d_out_bsq, d_out_key, (cudaStream_t)stream);
+}
+
+int rapp_mec_plan_run(rapp_mec_plan* pl, const double* targets, int64_t fn_begin, int64_t fn_end,
+                      int64_t* out_bsq) {
+  if (!pl || fn_begin < 0 || fn_end > pl->nfn || fn_begin > fn_end ||
+      (fn_end > fn_begin && (!targets || !out_bsq))) {
+    set_error("bad plan run arguments");
+    return RAPP_E_ARG;
+  }
+  const int64_t nf = fn_end - fn_begin;
+  for (int64_t f = 0; f < nf; ++f)
+    if (targets[f] <= 0.0) {
+      set_error("target_rps must be positive");  // hs/perf.py:114-115
+      return RAPP_E_VALUE;
+    }
+  if (nf == 0) return RAPP_OK;
+  std::lock_guard<std::mutex> lk(pl->ctx->mu);
+  RAPP_CUDA(cudaSetDevice(pl->ctx->device));
+  const size_t tb = (size_t)pl->nfn * 8, ob = (size_t)pl->nfn * 12;
+  if (!pl->stream) {
+    RAPP_CUDA(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+    RAPP_CUDA(cudaMallocHost(&pl->h_stage, tb + ob));
+    RAPP_CUDA(cudaMalloc(&pl->d_stage, tb + ob));
+  }
+  // targets are indexed by function id inside the plan: stage them at their slots
+  memcpy(pl->h_stage + (size_t)fn_begin * 8, targets, (size_t)nf * 8);
+  RAPP_CUDA(cudaMemcpyAsync(pl->d_stage + (size_t)fn_begin * 8, pl->h_stage + (size_t)fn_begin * 8,
+                            (size_t)nf * 8, cudaMemcpyHostToDevice, pl->stream));
+  int32_t* d_o = reinterpret_cast<int32_t*>(pl->d_stage + tb);
+  int rc = run_plan(pl, reinterpret_cast<const double*>(pl->d_stage), fn_begin, fn_end, d_o,
+                    nullptr, pl->stream);
+  if (rc) return rc;
+  int32_t* h_o = reinterpret_cast<int32_t*>(pl->h_stage + tb);
+  RAPP_CUDA(cudaMemcpyAsync(h_o, d_o, (size_t)nf * 12, cudaMemcpyDeviceToHost, pl->stream));
+  RAPP_CUDA(cudaStreamSynchronize(pl->stream));
+  for (int64_t i = 0; i < nf * 3; ++i) out_bsq[i] = h_o[i];
+  return RAPP_OK;
 }
 
 int rapp_mec_batch(rapp_ctx* ctx, int64_t nfn, const int32_t* table_of_fn, const double* targets,

@@ -112,6 +112,7 @@ struct World {
   double alpha, beta, cooldown, r_min, interval_s, cold_start, kA, kQ, kH, kD, kP0;
   int delta, F, G, pod_cap;
   int policy;                    // 0 hybrid, 1 replica-count baseline
+  int sum_plain;                 // 1: CPython < 3.12 float sum (left to right, no compensation)
   const int32_t* fn_shape;       // [F][3] replica policy pod shape (b, s, q)
   int32_t* wanted;               // replica scale-up: ceil(gap / pod_cap), clamped
   // tables
@@ -188,6 +189,30 @@ struct World {
   int32_t* err;                  // first error code (RAPP_E_*)
   int32_t* err_fn;
 };
+
+// CPython's sum() over floats, started from int 0 (0 + x0 == x0 for the positive rates
+// summed here): from 3.12 on it is Neumaier-compensated, before that plain left to right.
+// The caller's interpreter decides (rapp_scaler_config.sum_mode).
+template <class Get>
+__device__ __forceinline__ double py_float_sum(const World& w, int m, Get get) {
+  double s = get(0);
+  if (w.sum_plain) {
+    for (int j = 1; j < m; ++j) s = __dadd_rn(s, get(j));
+    return s;
+  }
+  double c = 0.0;
+  for (int j = 1; j < m; ++j) {
+    const double x = get(j);
+    const double t = __dadd_rn(s, x);
+    if (fabs(s) >= fabs(x))
+      c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
+    else
+      c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+    s = t;
+  }
+  if (c != 0.0 && isfinite(c)) s = __dadd_rn(s, c);
+  return s;
+}
 
 __device__ __forceinline__ double thr_at(const World& w, int f, double b, double s, double q) {
   const TableDesc td = w.tds[w.fn_table[f]];
@@ -395,18 +420,7 @@ __device__ void replica_phase_a(const World& w, int f, int lane, double R, doubl
   const int* shape = w.fn_shape + 3 * f;
   if (!batch_ok(w, f, shape[0])) set_err(w, RAPP_E_VALUE, f);
   const double pod_cap = thr_at(w, f, double(shape[0]), double(shape[1]), double(shape[2]));
-  double s = vals[0], c = 0.0;  // sum() in dict order (CPython 3.12: Neumaier)
-  for (int j = 1; j < m; ++j) {
-    const double x = vals[j];
-    const double t = __dadd_rn(s, x);
-    if (fabs(s) >= fabs(x))
-      c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
-    else
-      c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
-    s = t;
-  }
-  if (c != 0.0 && isfinite(c)) s = __dadd_rn(s, c);
-  const double cap = s;
+  const double cap = py_float_sum(w, m, [&](int j) { return vals[j]; });  // dict order
   const double up_thr = __dmul_rn(cap, w.alpha);
   if (R > up_thr) {
     const double want = ceil(__ddiv_rn(__dsub_rn(R, up_thr), pod_cap));
@@ -537,20 +551,8 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
   int cls = kNone;
   double cap = 0.0;
   if (lane == 0) {
-    // capability = sum(...) in sorted order: CPython 3.12 float sum (Neumaier), started
-    // from the first element (int 0 + x == x)
-    double s = rows[0 * kRow + w.row_kd[f * kMaxPods + 0]], c = 0.0;
-    for (int j = 1; j < m; ++j) {
-      const double x = rows[j * kRow + w.row_kd[f * kMaxPods + j]];
-      const double t = __dadd_rn(s, x);
-      if (fabs(s) >= fabs(x))
-        c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
-      else
-        c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
-      s = t;
-    }
-    if (c != 0.0 && isfinite(c)) s = __dadd_rn(s, c);
-    cap = s;
+    // capability = sum(...) in sorted order (hs/autoscaler.py:86-87)
+    cap = py_float_sum(w, m, [&](int j) { return rows[j * kRow + w.row_kd[f * kMaxPods + j]]; });
     const double up_thr = __dmul_rn(cap, w.alpha);
     if (R > up_thr) {
       cls = kUp;
@@ -2091,13 +2093,13 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
 // Releases reported by the host between ticks (a DRAINING pod whose last request finished:
 // hs/sim.py:424-438 -> _release_pod -> allocator.release_pod, hs/allocator.py:128-139), in
 // the order given.  One warp; partition lists are read from global memory.
+// `rel_ovf` is a G-byte global array of ones: every partition list lives in global memory
+// (no shared-memory staging, so any cluster size launches).
 __global__ void __launch_bounds__(32) k_tick_release(World w, const int32_t* __restrict__ list,
-                                                     int n) {
-  extern __shared__ uint8_t rel_ovf[];
+                                                     int n, uint8_t* rel_ovf) {
   __shared__ int s_nact, s_err, s_npods;
   __shared__ long long s_counter;
   const int lane = threadIdx.x & 31;
-  for (int g = lane; g < w.G; g += 32) rel_ovf[g] = 1;  // every list lives in global memory
   if (lane == 0) s_err = 0;
   __syncwarp();
   CommitT<false> c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter, nullptr,
@@ -2194,6 +2196,8 @@ struct rapp_tick {
   int32_t* h_rel = nullptr;   // pinned staging for it
   int64_t rel_cap = 0;
   int64_t h_npods = 0;         // pods created so far (host copy of w.n_pods)
+  uint8_t* d_ovf_ones = nullptr;  // [G] ones: k_tick_release's "list in global memory" flags
+  cudaEvent_t order_ev = nullptr;  // orders rapp_tick_run_dev's stream against t->stream
 };
 
 namespace rapp {
@@ -2296,6 +2300,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   std::unique_ptr<rapp_tick> t(new rapp_tick());
   t->ctx = ctx;
   RAPP_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  RAPP_CUDA(cudaEventCreateWithFlags(&t->order_ev, cudaEventDisableTiming));
   World& w = t->w;
   w.alpha = cfg->alpha;
   w.beta = cfg->beta;
@@ -2309,6 +2314,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   w.kD = cfg->kal_D;
   w.kP0 = cfg->kal_P0;
   w.delta = cfg->delta_iq;
+  w.sum_plain = cfg->sum_mode == 1;
   if (cfg->policy != 0 && cfg->policy != 1) {
     set_error("unknown policy code %d", cfg->policy);
     return RAPP_E_VALUE;
@@ -2547,6 +2553,8 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   t->rel_cap = 1024;
   RAPP_CUDA(cudaMalloc(&t->d_rel, (size_t)t->rel_cap * 4));
   RAPP_CUDA(cudaMallocHost(&t->h_rel, (size_t)t->rel_cap * 4));
+  if ((rc = dev_alloc(t.get(), &t->d_ovf_ones, (size_t)std::max(1, w.G)))) return rc;
+  RAPP_CUDA(cudaMemsetAsync(t->d_ovf_ones, 1, (size_t)std::max(1, w.G), t->stream));
   t->h_npods = n_pods;
   // build the fresh-GPU search index
   for (int f0 = 0; f0 < F; f0 += 32768) {
@@ -2570,6 +2578,7 @@ int rapp_tick_destroy(rapp_tick* t) {
   if (t->d_rel) cudaFree(t->d_rel);
   if (t->h_rel) cudaFreeHost(t->h_rel);
   if (t->h_out) cudaFreeHost(t->h_out);
+  if (t->order_ev) cudaEventDestroy(t->order_ev);
   cudaStreamDestroy(t->stream);
   delete t;
   return RAPP_OK;
@@ -2633,7 +2642,7 @@ int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
   RAPP_CUDA(cudaMemcpyAsync(t->d_rel, t->h_rel, (size_t)n * 4, cudaMemcpyHostToDevice,
                             t->stream));
   // stream-ordered before the next tick; no host synchronisation needed here
-  k_tick_release<<<1, 32, (size_t)std::max(1, t->w.G), t->stream>>>(t->w, t->d_rel, (int)n);
+  k_tick_release<<<1, 32, 0, t->stream>>>(t->w, t->d_rel, (int)n, t->d_ovf_ones);
   RAPP_LAUNCHED();
   return RAPP_OK;
 }
@@ -2646,7 +2655,16 @@ int rapp_tick_run_dev(rapp_tick* t, double now_ms, const int64_t* d_arrivals,
   }
   RAPP_CUDA(cudaSetDevice(t->ctx->device));
   t->h_npods = -1;  // the host no longer knows the pod count without a read-back
-  return launch_tick(t, now_ms, d_arrivals, d_idle, nullptr, (cudaStream_t)stream);
+  // the world is shared with the host API's internal stream (releases, host ticks): order
+  // this tick after that stream's work and that stream's later work after this tick
+  cudaStream_t st = (cudaStream_t)stream;
+  RAPP_CUDA(cudaEventRecord(t->order_ev, t->stream));
+  RAPP_CUDA(cudaStreamWaitEvent(st, t->order_ev, 0));
+  const int rc = launch_tick(t, now_ms, d_arrivals, d_idle, nullptr, st);
+  if (rc) return rc;
+  RAPP_CUDA(cudaEventRecord(t->order_ev, st));
+  RAPP_CUDA(cudaStreamWaitEvent(t->stream, t->order_ev, 0));
+  return RAPP_OK;
 }
 
 int rapp_tick_outputs_dev(rapp_tick* t, const rapp_action** a, const int32_t** c,
@@ -2711,6 +2729,11 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
   const int64_t n = h_count[0];
   *n_actions = n;
   if (n > max_actions) {
+    // the tick is applied on the device already: keep the host's pod count in step so
+    // the caller can read the actions from the device (rapp_tick_outputs_dev) and go on
+    int32_t v = 0;
+    RAPP_CUDA(cudaMemcpy(&v, w.n_pods, 4, cudaMemcpyDeviceToHost));
+    t->h_npods = v;
     set_error("action buffer too small (%lld > %lld)", (long long)n, (long long)max_actions);
     return RAPP_E_ARG;
   }

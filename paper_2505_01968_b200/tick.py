@@ -15,19 +15,45 @@ from __future__ import annotations
 
 import ctypes
 import math
-from dataclasses import dataclass, field
+import sys
 from typing import Mapping, Optional, Sequence
 
 import numpy as np
 
-from . import _lib, allocator
-from .core import ActionKind, PodInstance, PodState, ScalingAction
+from . import _lib, core
 from .errors import ConfigError, FilterDegenerateError, InvariantViolation
 
-KINDS = (ActionKind.VERTICAL_UP, ActionKind.VERTICAL_DOWN, ActionKind.HORIZONTAL_UP,
-         ActionKind.HORIZONTAL_DOWN)
-_STATE_CODE = {PodState.COLD_STARTING: 0, PodState.RUNNING: 1, PodState.DRAINING: 2}
-_CODE_STATE = {0: PodState.COLD_STARTING, 1: PodState.RUNNING, 2: PodState.DRAINING}
+_KIND_NAMES = ("vertical_up", "vertical_down", "horizontal_up", "horizontal_down")
+_STATE_NAMES = ("cold_starting", "running", "draining")
+_STATE_CODE = {name: i for i, name in enumerate(_STATE_NAMES)}
+# hs/autoscaler.py:86-87 sums capability with the caller's float sum(): compensated from 3.12
+SUM_MODE = 0 if sys.version_info >= (3, 12) else 1
+MAX_PODS_PER_FUNCTION = 128  # kMaxPods (rapp_tick.cu); the device output block holds +4
+
+
+class CallerTypes:
+    """The record types of the caller's package, found from its ClusterState's module
+    (hybridscale.core for the reference simulator, else this package's `core`): the
+    tick emits the caller's own ActionKind / ScalingAction and creates its PodInstance /
+    PodState, and applies actions to host snapshots with the caller's own allocator when
+    the package has one (hs/allocator.py) — else by re-reading the device world."""
+
+    def __init__(self, cluster):
+        mod = sys.modules.get(type(cluster).__module__)
+        if mod is None or not all(hasattr(mod, n) for n in
+                                  ("ActionKind", "ScalingAction", "PodInstance", "PodState")):
+            mod = core
+        self.ActionKind = mod.ActionKind
+        self.ScalingAction = mod.ScalingAction
+        self.PodInstance = mod.PodInstance
+        self.PodState = mod.PodState
+        self.SmPartition = getattr(mod, "SmPartition", core.SmPartition)
+        self.kinds = tuple(self.ActionKind(k) for k in _KIND_NAMES)
+        self.states = tuple(self.PodState(k) for k in _STATE_NAMES)
+        pkg = mod.__name__.rpartition(".")[0]
+        alloc = sys.modules.get(pkg + ".allocator") if pkg else None
+        self.allocator = alloc if alloc is not None and all(
+            hasattr(alloc, n) for n in ("place_pod", "change_quota", "release_pod")) else None
 
 
 class ScalerConfigC(ctypes.Structure):
@@ -37,7 +63,8 @@ class ScalerConfigC(ctypes.Structure):
                 ("interval_s", ctypes.c_double), ("cold_start_ms", ctypes.c_double),
                 ("kal_A", ctypes.c_double), ("kal_Q", ctypes.c_double),
                 ("kal_H", ctypes.c_double), ("kal_D", ctypes.c_double),
-                ("kal_P0", ctypes.c_double)]
+                ("kal_P0", ctypes.c_double), ("sum_mode", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
 
 
 FN_DTYPE = np.dtype([("table_id", "<i4"), ("_pad", "<i4"), ("min_rps", "<f8"),
@@ -80,9 +107,7 @@ def _ptr(a):
 
 
 def _state_code(state) -> int:
-    if isinstance(state, str):
-        state = PodState(state)
-    return _STATE_CODE[PodState(state.value)]
+    return _STATE_CODE[state if isinstance(state, str) else state.value]
 
 
 class TickResult:
@@ -99,15 +124,16 @@ class TickResult:
         self._actions = None
 
     @property
-    def actions(self) -> list[ScalingAction]:
-        """Reference-shaped actions (horizontal_up carries pod_id None)."""
+    def actions(self) -> list:
+        """The caller's ScalingAction records (horizontal_up carries pod_id None)."""
         if self._actions is None:
             # device-produced records are valid by construction: each action gets its field
-            # dict directly (ScalingAction._trusted without the call and keyword overhead)
+            # dict directly (no frozen-dataclass __init__ / __post_init__ per action)
             e = self._engine
             fids, gids = e.fids, e.gids
             r = self.raw
-            new, setattr_, cls = object.__new__, object.__setattr__, ScalingAction
+            KINDS = e.types.kinds
+            new, setattr_, cls = object.__new__, object.__setattr__, e.types.ScalingAction
             out = []
             app = out.append
             for f, k, b, sm, q, g, pid in zip(r["fn"].tolist(), r["kind"].tolist(),
@@ -147,9 +173,10 @@ class TickEngine:
                  last_scale_down: Optional[Mapping[str, float]] = None,
                  promote_cold: bool = True, policy: str = "hybrid",
                  device: Optional[int] = None):
-        from .perf import PerfTable
+        from .perf import device_table_of
         self.policy = canonical_policy(policy)
         self.cluster = cluster
+        self.types = CallerTypes(cluster)
         self.config = scaler_config
         self.functions = {f.function_id: f for f in functions}
         self.fids = sorted(self.functions)
@@ -169,8 +196,7 @@ class TickEngine:
             table = tables.get(ref)
             if table is None:
                 raise ConfigError(f"missing perf table {ref!r} for {fid}")
-            if not isinstance(table, PerfTable):
-                raise ConfigError(f"table {ref!r} must be a paper_2505_01968_b200 PerfTable")
+            table = device_table_of(table, device)  # any PerfTable-shaped object
             c, tid = table.device_table()
             if ctx is None:
                 ctx = c
@@ -226,7 +252,7 @@ class TickEngine:
                             scaler_config.r_min, scaler_config.delta_iq,
                             0 if self.policy == "hybrid" else 1,
                             self.interval_ms / 1000.0, self.cold_start_ms, kal["A"], kal["Q"],
-                            kal["H"], kal["D"], kal["P0"])
+                            kal["H"], kal["D"], kal["P0"], SUM_MODE, 0)
         lat = np.asarray(lattice if lattice else [0], dtype=np.int64)
         po = np.asarray(part_off, dtype=np.int64)
         ps = np.asarray(psm if psm else [0], dtype=np.int32)
@@ -237,7 +263,9 @@ class TickEngine:
             len(self.gids), _lib.i64ptr(po), _lib.i32ptr(ps), _lib.i32ptr(pa), len(pods),
             _ptr(pods), self.counter, ctypes.byref(h)), "TickEngine")
         self._h = h
-        self._act_buf = np.zeros(max(64, len(self.fids) * 36), dtype=ACTION_DTYPE)
+        # the device's own output block: kMaxPods + 4 actions per function
+        self._act_buf = np.zeros(max(1, len(self.fids)) * (MAX_PODS_PER_FUNCTION + 4),
+                                 dtype=ACTION_DTYPE)
         self._obs = np.zeros(max(1, len(self.fids)))
         self._pred = np.zeros(max(1, len(self.fids)))
 
@@ -271,9 +299,13 @@ class TickEngine:
         _lib.check(_lib.load().rapp_tick_release(self._h, _lib.i64ptr(idx), len(idx)),
                    "release")
         if apply_to_host:
-            for pid in ids:
-                if pid in self.cluster.pods:
-                    allocator.release_pod(self.cluster, pid)
+            alloc = self.types.allocator
+            if alloc is None:
+                self.sync_host()
+            else:
+                for pid in ids:
+                    if pid in self.cluster.pods:
+                        alloc.release_pod(self.cluster, pid)
 
     # -- one tick -----------------------------------------------------------------------
 
@@ -338,25 +370,61 @@ class TickEngine:
                           self._pred[:len(self.fids)].copy(), pod_ids)
 
     def _apply_host(self, res: TickResult, now: float) -> None:
-        """Cluster effects of hs/sim.py:493-525 on the host snapshot (promotions first)."""
+        """Cluster effects of hs/sim.py:493-525 on the host snapshot (promotions first),
+        applied by the caller's own allocator (hs/allocator.py) when its package has one,
+        else re-read from the device world (`sync_host`)."""
+        T = self.types
         cl = self.cluster
-        for pod in cl.pods.values():
-            if PodState(pod.state.value) is PodState.COLD_STARTING and pod.ready_at_ms <= now:
-                pod.state = type(pod.state)("running")
         cl.clock_ms = now
+        alloc = T.allocator
+        if alloc is None:
+            self.sync_host()
+            return
+        cold, running, draining = T.states
+        for pod in cl.pods.values():
+            if pod.state.value == "cold_starting" and pod.ready_at_ms <= now:
+                pod.state = running
+        v_up, v_down, h_up, _ = T.kinds
         for act, pid, rel in zip(res.actions, res.pod_ids, res.released):
-            if act.kind in (ActionKind.VERTICAL_UP, ActionKind.VERTICAL_DOWN):
-                allocator.change_quota(cl, pid, act.quota_percent)
-            elif act.kind is ActionKind.HORIZONTAL_UP:
-                pod = PodInstance(pid, act.function_id, act.batch, act.sm_percent,
-                                  act.quota_percent, act.gpu_id, state=PodState.COLD_STARTING,
-                                  ready_at_ms=now + self.cold_start_ms)
-                allocator.place_pod(cl, pod, act.gpu_id)
+            if act.kind is v_up or act.kind is v_down:
+                alloc.change_quota(cl, pid, act.quota_percent)
+            elif act.kind is h_up:
+                pod = T.PodInstance(pid, act.function_id, act.batch, act.sm_percent,
+                                    act.quota_percent, act.gpu_id, state=cold,
+                                    ready_at_ms=now + self.cold_start_ms)
+                alloc.place_pod(cl, pod, act.gpu_id)
             else:
-                pod = cl.pods[pid]
-                pod.state = type(pod.state)("draining")
+                cl.pods[pid].state = draining
                 if rel:
-                    allocator.release_pod(cl, pid)
+                    alloc.release_pod(cl, pid)
+
+    def sync_host(self) -> None:
+        """Rewrites the host snapshot's pods and partition lists from the device world
+        (pods in creation order, partitions in list order, residents in pod order)."""
+        T = self.types
+        cl = self.cluster
+        pods = self.read_pods()
+        parts = self.read_partitions()
+        lists = {g: [T.SmPartition(sm, [], alloc) for sm, alloc, _ in parts[g]]
+                 for g in self.gids}
+        prev, fresh = cl.pods, {}
+        for i, p in enumerate(pods):
+            if p["state"] < 0:  # released
+                continue
+            pid, gid = self.pod_ids[i], self.gids[int(p["gpu"])]
+            pod = prev.get(pid)
+            if pod is None:  # created by a tick: COLD_STARTING until its ready time
+                pod = T.PodInstance(pid, self.pod_fids[i], 0, 0, 0, gid,
+                                    ready_at_ms=float(p["ready_at_ms"]))
+            pod.batch, pod.sm_percent, pod.quota_percent = (int(p["batch"]), int(p["sm"]),
+                                                            int(p["quota"]))
+            pod.gpu_id, pod.state = gid, T.states[int(p["state"])]
+            fresh[pid] = pod
+            lists[gid][int(p["part"])].resident_pods.append(pid)
+        prev.clear()
+        prev.update(fresh)
+        for g in self.gids:
+            cl.gpus[g].partitions[:] = lists[g]
 
     # -- device state readback --------------------------------------------------------------
 
@@ -395,5 +463,5 @@ class TickEngine:
                 continue
             rows.append([self.pod_ids[i], self.pod_fids[i],
                          int(p["batch"]), int(p["sm"]), int(p["quota"]), self.gids[p["gpu"]],
-                         _CODE_STATE[int(p["state"])].value])
+                         _STATE_NAMES[int(p["state"])]])
         return {"partitions": self.read_partitions(), "pods": sorted(rows, key=str)}

@@ -10,6 +10,11 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+# the reference package is the drop-in's caller: its install (baseline/_ref, git-ignored,
+# travels to the GPU box) makes the B200 path bind the caller's record and error types
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(REF_INSTALL, "hybridscale")) and REF_INSTALL not in sys.path:
+    sys.path.append(REF_INSTALL)
 
 
 def pytest_configure(config):

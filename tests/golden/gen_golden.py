@@ -23,6 +23,9 @@ import sys
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+if ROOT not in sys.path:
+    sys.path.append(ROOT)  # bench.py (world builders); after the reference's own `tests`
 REF_PKG = "/root/reference/pkg"
 SCRATCH = "/tmp/refpkg"
 
@@ -668,7 +671,7 @@ def gen_replay(hs):
                                 initial=PodConfig(4, rng.choice([20, 30, 40]), 20, 1)))
         traces.append(synth_trace("burst", {"base": rng.uniform(2, 20),
                                             "spike": rng.uniform(40, 120), "spike_prob": 0.2},
-                                  1000 + i, function_id=fid, horizon_ms=30000.0))
+                                  1000 + i, function_id=fid, horizon_ms=60000.0))
     trace = merge_traces(traces)
     cluster = build_cluster(64, functions=fns)
     cfg = ScalerConfig(alpha=0.65, beta=0.45, delta_iq=10, cooldown_ms=5000.0, r_min=1.0)
@@ -685,9 +688,132 @@ def gen_replay(hs):
     dump("replay.json", {"runs": runs})
 
 
+def _config4_world_ref(hs, nfn, ngpu, seed, full_grid):
+    """bench.make_config4_world rebuilt with the reference's own types: the same RNG draws,
+    the same gen_tables surfaces (bench.surface), one RUNNING pod (8, 20, 20) per function
+    placed round-robin by the reference's allocator."""
+    import bench
+    from hybridscale import FunctionSpec, PerfTable, PodConfig, PodInstance, PodState, allocator
+    from hybridscale.sim import build_cluster
+    rng = random.Random(seed)
+    if full_grid:
+        bs, ss, qs = list(range(1, 33)), list(range(10, 101)), list(range(1, 101))
+    else:
+        bs, ss, qs = bench.BATCHES, list(range(10, 101, 10)), list(range(10, 101, 10))
+    fns, tables, caps = [], {}, {}
+    for i in range(nfn):
+        fid = f"fn-{i:04d}"
+        fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
+        lat = bench.surface(fixed, per, floor, 1.0 - floor, bs, ss, qs)
+        tables[fid] = PerfTable(fid, bs, ss, qs, lat)
+        fns.append(FunctionSpec(function_id=fid, baseline_latency_ms=20.0, perf_table_ref=fid,
+                                allowed_batches=list(bench.BATCHES), initial=PodConfig(8, 20, 20)))
+        caps[fid] = 8 / (float(lat[bs.index(8), ss.index(20), qs.index(20)]) / 1000.0)
+    cluster = build_cluster(ngpu, functions=fns)
+    for i, f in enumerate(fns):
+        allocator.place_pod(cluster, PodInstance(f"pod-{i:06d}", f.function_id, 8, 20, 20, "",
+                                                 state=PodState.RUNNING), f"gpu-{i % ngpu:03d}")
+    return fns, tables, cluster, caps
+
+
+def gen_config4(hs):
+    """BASELINE config 4 through the reference's own SimulationEngine._handle_scaler: 1,000
+    functions on 400 GPUs, five ticks of swinging load (the bench's tick workload: interval
+    2 s, cold start 5 s, every pod idle, arrivals from bench.config4_arrivals with
+    random.Random(0)), in both grid variants (6x10x10 with delta 10; 32x91x100 with delta 1).
+    The reference takes minutes per tick here (copy.deepcopy per scale-up)."""
+    import time as _time
+    import bench
+    from hybridscale import ScalerConfig, SimConfig, WorkloadTrace
+    from hybridscale.sim import SimulationEngine, _PodRuntime
+    variants = [v for v in ("6x10x10", "32x91x100")
+                if os.environ.get("GOLDEN_C4_VARIANT", v) == v]
+    for variant in variants:
+        full = variant != "6x10x10"
+        t0 = _time.time()
+        fns, tables, cluster, caps = _config4_world_ref(hs, 1000, 400, 0, full)
+        cfg = ScalerConfig(delta_iq=1 if full else 10)
+        simcfg = SimConfig(scaler_interval_ms=2000.0, cold_start_ms=5000.0)
+        eng = SimulationEngine(WorkloadTrace(entries=[], horizon_ms=1.0), fns, tables, cluster,
+                               cfg, simcfg, "hybrid", None)
+        for pod in cluster.pods.values():  # what _bootstrap does for its own placements
+            pod.capability_rps = eng._capability(pod)
+            eng._runtimes[pod.pod_id] = _PodRuntime(pod)
+            eng._open_cost_interval(pod, 0.0)
+        eng._pod_counter = len(cluster.pods)
+        recorded = []
+        orig = eng.policy.decide
+
+        def spy(function, cl, rate, _orig=orig):
+            acts = _orig(function, cl, rate)
+            recorded.extend(acts)
+            return acts
+        eng.policy.decide = spy
+        rng = random.Random(0)
+        run = {"variant": variant, "nfn": 1000, "ngpu": 400, "seed": 0,
+               "delta": cfg.delta_iq, "interval_ms": hx(2000.0), "cold_start_ms": hx(5000.0),
+               "pod_counter0": eng._pod_counter, "ticks": []}
+        print(f"config4 {variant}: world built in {_time.time() - t0:.0f} s", flush=True)
+        for k in range(int(os.environ.get("GOLDEN_C4_TICKS", "5"))):
+            now = 2000.0 * (k + 1)
+            swing = (1.0, 1.5, 0.2, 2.0, 0.05)[k % 5]
+            arrivals = bench.config4_arrivals(fns, caps, rng, 2.0, 0.0, 3.0 * swing)
+            for fid, a in arrivals.items():
+                eng._tick_arrivals[fid] = a
+            for pid, rt in list(eng._runtimes.items()):  # ready events precede the tick
+                if rt.pod.state.value == "cold_starting" and rt.pod.ready_at_ms <= now:
+                    eng._handle_ready(now, pid)
+            recorded.clear()
+            n_before = eng._pod_counter
+            t1 = _time.time()
+            eng._handle_scaler(now)
+            tl = eng._timeline[-len(fns):]
+            run["ticks"].append({
+                "now": hx(now), "arrivals": [arrivals[f.function_id] for f in fns],
+                "actions": action_list(recorded),
+                "new_pods": [f"pod-{i:06d}" for i in range(n_before, eng._pod_counter)],
+                "observed": [hx(p.observed_rps) for p in tl],
+                "predicted": [hx(p.predicted_rps) for p in tl],
+                "capacity": [hx(p.capacity_rps) for p in tl],
+                "reference_s": round(_time.time() - t1, 3)})
+            print(f"config4 {variant}: tick {k} {len(recorded)} actions in "
+                  f"{_time.time() - t1:.0f} s", flush=True)
+        run["final"] = cluster_dict(eng.cluster)
+        dump(f"config4_{variant}.json", run)
+
+
+def _experiments_module():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "rapp_experiments", os.path.join(ROOT, "tests", "experiments.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def gen_csv(hs):
+    """sha256 of the four metric CSVs (hs/sim.py:651-685) of pure-reference runs: the demo
+    experiment (pkg/configs/demo.yaml, 3 policies) and config 3 (100 functions, 60 s burst
+    replay, hybrid and horizontal-only: 100 whole-GPU pods do not fit 64 GPUs).  The GPU tests re-run the same experiments with the B200
+    tick and compare bytes (and against a live reference run where the reference is
+    installed)."""
+    import tempfile
+    from hybridscale.sim import run
+    ex = _experiments_module()
+    out = {}
+    specs = ex.demo_runs(hs, os.path.join(REF_PKG, "configs", "demo.yaml")) + \
+        ex.config3_runs(hs, policies=("hybrid", "horizontal-only"))
+    for spec in specs:
+        with tempfile.TemporaryDirectory() as d:
+            out[spec[0]] = ex.digest(ex.run_to_csvs(run, spec, d))
+        print(spec[0], out[spec[0]]["timeline.csv"], flush=True)
+    dump("csv.json", out)
+
+
 GENERATORS = {"interp": gen_interp, "mec": gen_mec, "scale": gen_scale, "tick": gen_tick,
               "policy": gen_policy, "ingest": gen_ingest,
-              "metrics": gen_metrics, "replay": gen_replay}
+              "metrics": gen_metrics, "replay": gen_replay, "config4": gen_config4,
+              "csv": gen_csv}
 
 
 def main(argv):

@@ -1,0 +1,89 @@
+"""The drop-in boundary binds the CALLER's types (CPU only): with the reference installed
+(baseline/_ref) the records are hybridscale's own and every error derives from the
+reference class of the same name, so the reference's `except` clauses catch them; with
+RAPP_HOST_TYPES=standalone the package still imports and stands alone."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+from .conftest import REF_INSTALL, ROOT
+
+hs = pytest.importorskip("hybridscale", reason="reference install baseline/_ref missing")
+
+
+def test_records_are_the_references():
+    from paper_2505_01968_b200 import core
+    for name in ("ActionKind", "PodState", "ScalingAction", "ClusterState", "PodInstance",
+                 "GpuDevice", "SmPartition", "FunctionSpec", "PodConfig"):
+        assert getattr(core, name) is getattr(hs, name), name
+
+
+def test_errors_derive_from_the_references():
+    from hybridscale import errors as he
+
+    from paper_2505_01968_b200 import errors as e
+    assert e.BOUND
+    for name in ("SchedulerError", "UnknownFunctionError", "UnknownPodError",
+                 "UnknownGpuError", "PlacementError", "TableFormatError",
+                 "FilterDegenerateError", "UnroutableFunctionError", "TraceFormatError",
+                 "ConfigError", "InvariantViolation"):
+        ours, theirs = getattr(e, name), getattr(he, name)
+        assert issubclass(ours, theirs) and issubclass(ours, he.SchedulerError), name
+        try:
+            raise ours("x")
+        except theirs:
+            pass
+
+
+def test_tick_emits_the_callers_types():
+    from paper_2505_01968_b200 import core
+    from paper_2505_01968_b200.tick import CallerTypes
+    t = CallerTypes(hs.ClusterState())
+    assert t.ScalingAction is hs.ScalingAction and t.kinds[2] is hs.ActionKind.HORIZONTAL_UP
+    assert t.allocator is sys.modules["hybridscale.allocator"]
+    assert CallerTypes(core.ClusterState()).ScalingAction is hs.ScalingAction
+
+
+def test_standalone_mode():
+    code = ("import sys; from paper_2505_01968_b200 import core, errors; "
+            "from paper_2505_01968_b200.tick import CallerTypes; "
+            "assert not errors.BOUND and 'hybridscale' not in sys.modules; "
+            "t = CallerTypes(core.ClusterState()); assert t.allocator is None; "
+            "assert t.ScalingAction is core.ScalingAction; "
+            "assert issubclass(errors.TableFormatError, errors.SchedulerError); print('ok')")
+    env = dict(os.environ, RAPP_HOST_TYPES="standalone",
+               PYTHONPATH=os.pathsep.join([ROOT, REF_INSTALL]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd=ROOT, timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
+
+
+def test_perf_reader_matches_reference_messages(tmp_path):
+    """The csv-module reader (files outside the strict form) reports what the reference's
+    reader reports (hs/perf.py:176-206), case by case."""
+    from hybridscale import perf as hp
+
+    from paper_2505_01968_b200 import perf as pp
+    H = "function_id,batch,sm_percent,quota_percent,latency_ms\n"
+    cases = {
+        "empty": "",
+        "bad_header": "a,b\n1,2\n",
+        "only_header": H,
+        "blank_and_quoted": H + "\n\"f\",1,50,10,\"2.5\"\n",
+        "mixed": H + "f,1,50,10,2.0\ng,1,50,20,1.0\n f ,2,50,10,3.0\n",
+        "dups": H + "f,1,50,10,2.0\nf,1,50,10,2.5\nf,1,50,20,1.0\n",
+        "format": H + "f,1,50\nf,x,50,10,1.0\nf,1,50,10,nan\n,1,50,20,1.0\n",
+        "empty_fid_first": H + ",1,50,10,2.0\nf,1,50,20,1.0\n",
+    }
+    for name, text in cases.items():
+        path = tmp_path / f"{name}.csv"
+        path.write_text(text, encoding="utf-8")
+        fid, samples, issues = pp._read_samples(str(path))
+        rfid, rsamples, rissues = hp._read_samples(str(path))
+        assert fid == rfid, name
+        assert repr(list(samples.items())) == repr(list(rsamples.items())), name
+        assert [(i.kind, i.message, i.coord) for i in issues] == \
+            [(i.kind, i.message, i.coord) for i in rissues], name

@@ -131,6 +131,34 @@ def _oracle_ticks(fns, tables, cluster, cfg, nticks, seed, interval_ms=2000.0,
     return n_actions
 
 
+@pytest.mark.parametrize("variant", ["6x10x10", "32x91x100"])
+def test_config4_ticks_match_reference(variant):
+    """BASELINE config 4 pinned to the reference itself: 1,000 functions on 400 GPUs, the
+    bench's five swinging-load ticks, captured from hybridscale's own
+    SimulationEngine._handle_scaler (tests/golden/gen_golden.py gen_config4) — both grid
+    variants (6x10x10 tables with delta 10; 32x91x100 tables with delta 1, whose fresh-GPU
+    searches run on 54,600-point lattices).  Identical ordered action lists, new pod ids,
+    0-ulp observed / predicted rates and the same final cluster."""
+    import bench
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    g = load_golden(f"config4_{variant}.json")
+    fns, tables, cluster, _ = bench.make_config4_world(g["nfn"], g["ngpu"], seed=g["seed"],
+                                                       full_grid=variant != "6x10x10")
+    eng = TickEngine(fns, tables, cluster, ScalerConfig(delta_iq=g["delta"]),
+                     scaler_interval_ms=fx(g["interval_ms"]),
+                     cold_start_ms=fx(g["cold_start_ms"]), pod_counter=g["pod_counter0"])
+    fids = sorted(f.function_id for f in fns)
+    for k, t in enumerate(g["ticks"]):
+        res = eng.tick(fx(t["now"]), t["arrivals"], idle=None, apply_to_host=True)
+        assert _acts(res.actions) == [list(a) for a in t["actions"]], f"tick {k}"
+        assert [p for p, a in zip(res.pod_ids, res.actions)
+                if a.kind.value == "horizontal_up"] == t["new_pods"], f"tick {k}"
+        assert [res.observed[f] for f in fids] == [fx(x) for x in t["observed"]]
+        assert [res.predicted[f] for f in fids] == [fx(x) for x in t["predicted"]]
+    assert cluster_to(cluster) == golden_cluster_to(g["final"])
+
+
 def test_config4_ticks_vs_oracle():
     """1,000 functions on 400 GPUs (config 4), five ticks with swinging load."""
     import bench
@@ -223,7 +251,7 @@ def test_policy_hand_cases():
     from paper_2505_01968_b200.autoscaler import ScalerConfig
     from paper_2505_01968_b200.core import (ClusterState, FunctionSpec, GpuDevice, PodConfig,
                                             PodInstance, PodState)
-    from paper_2505_01968_b200 import allocator
+    from bench import place_initial
     from paper_2505_01968_b200.errors import ConfigError
     from paper_2505_01968_b200.policies import (ExclusiveGpuPolicy, HorizontalOnlyPolicy,
                                                 make_policy)
@@ -241,8 +269,8 @@ def test_policy_hand_cases():
         return ClusterState(gpus={f"gpu-{i:03d}": GpuDevice(f"gpu-{i:03d}") for i in range(n)})
 
     def put(c, pid, sm, qq, gpu):
-        allocator.place_pod(c, PodInstance(pid, "conf-fn", 8, sm, qq, gpu,
-                                           state=PodState.RUNNING), gpu)
+        place_initial(c, PodInstance(pid, "conf-fn", 8, sm, qq, gpu,
+                                     state=PodState.RUNNING), gpu)
 
     assert isinstance(make_policy("horizontal", cfg, tables), HorizontalOnlyPolicy)
     assert isinstance(make_policy("exclusive", cfg, tables), ExclusiveGpuPolicy)
