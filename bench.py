@@ -38,6 +38,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# the reference package (the drop-in's caller; baseline/install.sh) when installed: the B200
+# path then binds its record and error types, and the tick baselines time it directly
+_REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(_REF_INSTALL, "hybridscale")) and _REF_INSTALL not in sys.path:
+    sys.path.append(_REF_INSTALL)
 
 METRIC = "RaPP config predictions/sec and scaling decisions/tick latency at 1/2/4/8 B200"
 UNIT = "predictions/s"
@@ -299,6 +304,9 @@ def dist_init(gpus):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        if rank == 0:  # NCCL's init log (nRanks, transport) from rank 0 only, before its line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -423,21 +431,17 @@ def run_stream(args, rank, world, local):
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
         e2e = {"value": world * e2e_preds * e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": e2e_preds * 24, "d2h_bytes_per_step": e2e_preds * 8,
-               "steps": e2e_steps, "api": "paper_2505_01968_b200.kernels.interp3_many "
-               "(C ABI rapp_interp3_many, pinned host buffers)"}
+               "steps": e2e_steps, "api": "kernels.interp3_many, pinned host buffers"}
 
     peak, peak_kind = load_peak()
     alg_bytes = 32.0 * n  # 24 B coords read + 8 B latency written per prediction
     achieved = alg_bytes / (avg_launch_ms / 1000.0) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": load_traffic(n),
-                "kernel": "k_interp_fast (rapp_stream.cu)", "peak_source": peak_kind,
-                "alg_bytes_per_prediction": 32}
-    cfg = {"workload": "config2: 4-model sweep (resnet50, vgg19, bert-base, mobilenet), tables "
-           "6x100x100 (b=1..32 pow2, sm 1..100%, quota 1..100%), 1e8 random queries/model/GPU",
-           "queries_per_step_per_gpu": preds_per_step, "l2": "inputs 9.6 GB/GPU >> 126 MB L2 "
-           "(no flush needed)", "parallelism": f"replicas x{world} (queries sharded, no "
-           "collective on the data path)"}
+                "kernel": "k_interp_fast", "peak_source": peak_kind, "alg_B_per_pred": 32}
+    cfg = {"workload": "config2: 4 models x 1e8 random queries/GPU, tables 6x100x100",
+           "queries_per_step_per_gpu": preds_per_step, "l2": "inputs 9.6 GB/GPU >> L2",
+           "parallelism": f"replicas x{world} (no collective on the data path)"}
     return {"value": value, "ms": ms, "roofline": roofline, "e2e": e2e, "config": cfg,
             "launches": launches, "clocks": clk.summary(), "dtype": "f64",
             "scaling": "weak", "avg_launch_ms": avg_launch_ms}
@@ -940,10 +944,120 @@ def run_replay(args, local, name="burst-100", reps=3):
             "ticks": len(run["ticks"]), "actions": acts, "passes_timed": reps - 1,
             "e2e_us_median": float(np.median(times)), "e2e_us_max": float(np.max(times)),
             "decisions": "identical to the reference simulator on every tick",
-            "reference_us_per_tick": 90100.0,
-            "reference_note": "reference _handle_scaler on a 100-function replay, measured in "
-                              "the build container (SURVEY.md §8(d) config 3)",
             "api": "TickEngine.release + TickEngine.tick (host arrays, idle pod ids)"}
+
+
+def reference_package():
+    """The reference package `hybridscale` (baseline/_ref, installed by baseline/install.sh;
+    it travels to the GPU box with the snapshot), or None."""
+    try:
+        import hybridscale
+        return hybridscale
+    except ImportError:
+        return None
+
+
+def reference_config4_sample(full_grid=False, sample=40):
+    """The reference's own SimulationEngine._handle_scaler (hs/sim.py:470-491) on the
+    config-4 world (1,000 functions, 400 GPUs, the bench's first tick of load), restricted
+    to the first `sample` functions in its sorted tick order while the cluster keeps all
+    1,000 functions' pods (each decision deep-copies the whole cluster, hs/autoscaler.py:111).
+    Seconds per tick extrapolated linearly to 1,000 functions, labelled as such."""
+    hs = reference_package()
+    if hs is None:
+        return None
+    from hybridscale import (FunctionSpec, PerfTable, PodConfig, PodInstance, PodState,
+                             ScalerConfig, SimConfig, WorkloadTrace, allocator)
+    from hybridscale.sim import SimulationEngine, _PodRuntime, build_cluster
+    nfn, ngpu = 1000, 400
+    rng = random.Random(0)  # the same draws as make_config4_world
+    if full_grid:
+        bs, ss, qs = list(range(1, 33)), list(range(10, 101)), list(range(1, 101))
+    else:
+        bs, ss, qs = BATCHES, list(range(10, 101, 10)), list(range(10, 101, 10))
+    fns, tables, caps = [], {}, {}
+    for i in range(nfn):
+        fid = f"fn-{i:04d}"
+        fixed, per, floor = rng.uniform(4, 20), rng.uniform(0.5, 4), rng.uniform(0.2, 0.4)
+        lat = surface(fixed, per, floor, 1.0 - floor, bs, ss, qs)
+        tables[fid] = PerfTable(fid, bs, ss, qs, lat)
+        fns.append(FunctionSpec(function_id=fid, baseline_latency_ms=20.0, perf_table_ref=fid,
+                                allowed_batches=list(BATCHES), initial=PodConfig(8, 20, 20)))
+        caps[fid] = 8 / (float(lat[bs.index(8), ss.index(20), qs.index(20)]) / 1000.0)
+    cluster = build_cluster(ngpu, functions=fns)
+    for i, f in enumerate(fns):
+        allocator.place_pod(cluster, PodInstance(f"pod-{i:06d}", f.function_id, 8, 20, 20, "",
+                                                 state=PodState.RUNNING), f"gpu-{i % ngpu:03d}")
+    eng = SimulationEngine(WorkloadTrace(entries=[], horizon_ms=1.0), fns, tables, cluster,
+                           ScalerConfig(delta_iq=1 if full_grid else 10),
+                           SimConfig(scaler_interval_ms=2000.0, cold_start_ms=5000.0),
+                           "hybrid", None)
+    for pod in cluster.pods.values():  # what _bootstrap does for its own placements
+        pod.capability_rps = eng._capability(pod)
+        eng._runtimes[pod.pod_id] = _PodRuntime(pod)
+        eng._open_cost_interval(pod, 0.0)
+    eng._pod_counter = len(cluster.pods)
+    arrivals = config4_arrivals(fns, caps, rng, 2.0, 0.0, 3.0)  # the bench's first tick
+    for fid, a in arrivals.items():
+        eng._tick_arrivals[fid] = a
+    keep = sorted(eng.functions)[:sample]
+    eng.functions = {fid: eng.functions[fid] for fid in keep}
+    t0 = time.perf_counter()
+    eng._handle_scaler(2000.0)
+    dt = time.perf_counter() - t0
+    return {"value": dt * nfn / sample * 1e6, "unit": "us/tick", "cores": 1,
+            "kind": "reference",
+            "sample": f"hybridscale SimulationEngine._handle_scaler over the first {sample} of "
+                      f"{nfn} functions of tick 1 ({dt:.2f} s, whole 400-GPU cluster), "
+                      f"extrapolated x{nfn // sample}"}
+
+
+def reference_config3(local, policy="hybrid"):
+    """Config 3 (100 functions, 60 s burst replay, 64 GPUs, tests/experiments.py) simulated
+    twice: by the unmodified reference (`hybridscale.sim.run`) and by the drop-in
+    (`integration.hybridscale_b200.run`: the same simulator with its per-tick hook
+    `_handle_scaler` running one device tick).  Returns µs per `_handle_scaler` call of both
+    and whether the four metric CSVs (hs/sim.py:651-685) are byte-identical."""
+    hs = reference_package()
+    if hs is None:
+        return None
+    import tempfile
+    from hybridscale.sim import SimulationEngine
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import experiments as ex
+    from integration.hybridscale_b200 import B200SimulationEngine
+    from integration.hybridscale_b200 import run as b200_run
+    spec = ex.config3_runs(hs, policies=(policy,))[0]
+    times = {"reference": [], "b200": []}
+    orig_ref, orig_b200 = SimulationEngine._handle_scaler, B200SimulationEngine._handle_scaler
+
+    def timed(orig, bucket):
+        def handle(self, now):
+            t0 = time.perf_counter()
+            orig(self, now)
+            times[bucket].append((time.perf_counter() - t0) * 1e6)
+        return handle
+    digests = {}
+    try:
+        B200SimulationEngine._handle_scaler = timed(orig_b200, "b200")
+        with tempfile.TemporaryDirectory() as d:
+            digests["b200"] = ex.digest(ex.run_to_csvs(
+                lambda *a: b200_run(*a, device=local), spec, d))
+        SimulationEngine._handle_scaler = timed(orig_ref, "reference")
+        B200SimulationEngine._handle_scaler = orig_b200  # only the base class is timed now
+        with tempfile.TemporaryDirectory() as d:
+            from hybridscale.sim import run as ref_run
+            digests["reference"] = ex.digest(ex.run_to_csvs(ref_run, spec, d))
+    finally:
+        SimulationEngine._handle_scaler = orig_ref
+        B200SimulationEngine._handle_scaler = orig_b200
+    # the first B200 tick uploads the world (TickEngine construction)
+    b = times["b200"][1:]
+    r = times["reference"]
+    return {"ticks": len(r), "b200_us_median": float(np.median(b)),
+            "b200_us_max": float(np.max(b)), "ref_us_median": float(np.median(r)),
+            "ref_us_max": float(np.max(r)),
+            "csv_identical": digests["b200"] == digests["reference"]}
 
 
 def tick_cpu_baseline(args, nticks=2):
@@ -1034,12 +1148,57 @@ def cpu_reference(steps, warmup, rows_per_model=1_000_000, procs=None):
         dt = time.perf_counter() - t0
     preds = steps * procs * len(MODELS) * rows_per_model
     kind = kinds[0]
-    sample = (f"{len(MODELS)} config-2 tables x {rows_per_model} random queries per process "
-              f"per step, {procs} processes, {steps} steps ({preds} predictions, {dt:.2f} s)")
+    sample = (f"{len(MODELS)} config-2 tables x {rows_per_model} queries/process/step, "
+              f"{procs} procs, {steps} steps ({dt:.2f} s)")
     return preds / dt, {"kind": kind, "cores": procs, "sample": sample}
 
 
 # ----------------------------------------------------------------------------------------
+
+
+def split_check(rank, world, local):
+    """shard.search_split — one config-2 lattice (32 x 100 x 100 at quota step 1) split
+    over the ranks by batch slabs, meet keys combined by an NCCL all-reduce MIN (fallback:
+    all-gather) — equals the unsplit device search on every rank, for feasible, boundary and
+    unreachable targets."""
+    from paper_2505_01968_b200 import PerfTable
+    from paper_2505_01968_b200.shard import search_split
+    name, b, s, q, v = config2_arrays()[0]
+    t = PerfTable(name, BATCHES, list(range(1, 101)), list(range(1, 101)), v, device=local)
+    top = max_lattice_rps(t)
+    ok = True
+    for target in (0.5, 0.1 * top, 0.5 * top, top, 2.0 * top):
+        for step, allowed in ((1, list(range(1, 33))), (10, None)):
+            got = search_split(t, target, rank, world, quota_step=step, batches=allowed)
+            ok &= got == t.most_efficient_config(target, quota_step=step, batches=allowed)
+    return bool(ok)
+
+
+def self_launch(argv, gpus):
+    """`bench.py --gpus N` outside torchrun: relaunch as N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and pass its exit code through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd).returncode
+
+
+def _r(x, nd=1):
+    return None if x is None else round(float(x), nd)
+
+
+def tick_summary(t, ref=None):
+    """Compact driver-visible summary of one tick workload (µs per tick)."""
+    out = {"dev_med": _r(t["device_us_median"]), "dev_max": _r(t["device_us_max"]),
+           "e2e_med": _r(t["e2e_us_median"]), "e2e_max": _r(t["e2e_us_max"]),
+           "acts": _r(t["actions_per_tick_mean"]), "ticks": t["ticks"]}
+    if ref is not None:
+        out["ref_us"] = _r(ref["value"], 0)
+    return out
 
 
 def main():
@@ -1056,9 +1215,13 @@ def main():
     ap.add_argument("--functions", type=int, default=3125)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detail", default=None,
+                    help="also write the full (uncompacted) result JSON to this path")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -1067,7 +1230,7 @@ def main():
             return
         # each step is a bounded sample (~0.5 s of work per host core) of the workload
         value, info = cpu_reference(args.steps, args.warmup, rows_per_model=250_000)
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "impl": "reference",
                 "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -1076,12 +1239,14 @@ def main():
                 "cpu_baseline": {"value": value, "unit": UNIT, **info},
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
         return
 
     rank, world, local = dist_init(args.gpus)
+    detail = {}
     if args.workload == "tick":
         tick = run_tick(args, local, full_grid=args.full_grid)
+        line = None
         if rank == 0:
             line = {"metric": METRIC, "value": tick["device_us_median"], "unit": "us/tick",
                     "n_gpus": world, "steps": tick["ticks"], "warmup": 3,
@@ -1091,13 +1256,17 @@ def main():
                     "e2e": {"value": tick["e2e_us_median"], "unit": "us/tick",
                             "h2d_bytes_per_step": 1000 * 8 + 1000,
                             "d2h_bytes_per_step": "actions (32 B each) + 2 x 8 KB rates"},
-                    "tick": tick, "cpu_baseline": tick_cpu_baseline(args),
+                    "tick": tick_summary(tick),
+                    "cpu_baseline": reference_config4_sample(args.full_grid)
+                    or tick_cpu_baseline(args),
                     "gpu_launches": tick["launches_per_tick"] * tick["ticks"],
                     "clocks": tick["clocks"], "impl": "ours"}
-            print(json.dumps(line))
+            detail = {"tick": tick}
+        finish(line, detail, args, world)
         return
     if args.workload == "mlp":
         res = run_mlp(args, rank, world, local)
+        line = None
         if rank == 0:
             line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
                     "steps": res["steps"], "warmup": args.warmup,
@@ -1107,13 +1276,23 @@ def main():
                     "cpu_baseline": res["cpu_baseline"], "e2e": res["e2e"],
                     "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours",
                     "search": res["search"]}
-            print(json.dumps(line))
+        finish(line, detail, args, world)
         return
     res = (run_stream if args.workload == "stream" else run_lattice)(args, rank, world, local)
+    sharded = None
+    if world > 1 and args.workload == "stream" and not args.no_extra:
+        # the N>1 line also runs the config-5 search sharded over the ranks: per-rank
+        # function blocks + one NCCL all-gather of the decisions (and a giant-lattice split
+        # check: batch slabs, all-reduce MIN of packed keys)
+        largs = argparse.Namespace(**{**vars(args), "steps": 20, "functions": 3125,
+                                      "no_e2e": True})
+        lat = run_lattice(largs, rank, world, local)
+        sharded = {"value": lat["value"], "ms_per_step": _r(lat["ms"] / largs.steps, 4),
+                   "frac": lat["roofline"]["frac"], "split_ok": split_check(rank, world, local),
+                   "workload": "config5 3125 fn, functions sharded, NCCL all_gather",
+                   "scaling": "strong"}
     if rank != 0:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        finish(None, None, args, world)
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline and args.workload == "stream":
@@ -1129,33 +1308,68 @@ def main():
             "dtype": res["dtype"], "data": "synthetic", "config": res["config"],
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
             "gpu_launches": res["launches"], "clocks": res["clocks"], "impl": "ours"}
+    if sharded is not None:
+        line["sharded_search"] = sharded
+        line["comm"] = {"backend": "nccl", "nranks": world}
     if world == 1 and args.workload == "stream" and not args.no_extra:
-        # the second half of the metric ("scaling decisions/tick latency") and config 5
-        extra = {"tick_config4": run_tick(args, local, ticks=20),
-                 "tick_config4_full_grid": run_tick(args, local, ticks=10, full_grid=True),
-                 "tick_config3_size": run_tick(args, local, ticks=20, nfn=100, ngpu=64),
-                 "replay_config3": run_replay(args, local),
-                 "config1": run_config1(args, local)}
-        extra["tick_config4"]["cpu_baseline"] = tick_cpu_baseline(args)
+        # the second half of the metric ("scaling decisions/tick latency") and config 5;
+        # compact summaries on the line, everything else in the detail record
+        t4 = run_tick(args, local, ticks=20)
+        t4f = run_tick(args, local, ticks=20, full_grid=True)
+        t3 = run_tick(args, local, ticks=20, nfn=100, ngpu=64)
+        rep = run_replay(args, local)
+        c3 = reference_config3(local)
+        r4 = reference_config4_sample(False)
+        r4f = reference_config4_sample(True)
+        c1 = run_config1(args, local)
         largs = argparse.Namespace(**{**vars(args), "steps": 50, "functions": 3125})
         lat = run_lattice(largs, rank, world, local)
-        extra["lattice_config5"] = {"value": lat["value"], "unit": UNIT,
-                                    "ms_per_step": lat["ms"] / largs.steps,
-                                    "roofline": lat["roofline"], "e2e": lat["e2e"],
-                                    "config": lat["config"],
-                                    "cpu_baseline": lattice_cpu_baseline_all()}
+        lcpu = lattice_cpu_baseline_all()
         margs = argparse.Namespace(**{**vars(args), "steps": 30, "queries": 25_000_000})
         mlp = run_mlp(margs, rank, world, local)
-        extra["learned_mlp"] = {"value": mlp["value"], "unit": UNIT,
-                                "ms_per_step": mlp["ms"] / mlp["steps"],
-                                "roofline": mlp["roofline"], "e2e": mlp["e2e"],
-                                "cpu_baseline": mlp["cpu_baseline"], "config": mlp["config"],
-                                "search": mlp["search"]}
-        line["extra"] = extra
-    print(json.dumps(line))
+        ticks = {"config4": tick_summary(t4, r4), "config4_full_grid": tick_summary(t4f, r4f),
+                 "config3_size": tick_summary(t3),
+                 "replay_config3": {"tick_e2e_med": _r(rep["e2e_us_median"]),
+                                    "tick_e2e_max": _r(rep["e2e_us_max"])}}
+        if c3 is not None:
+            ticks["replay_config3"].update(
+                {"dropin_med": _r(c3["b200_us_median"]), "dropin_max": _r(c3["b200_us_max"]),
+                 "ref_med": _r(c3["ref_us_median"], 0), "ref_max": _r(c3["ref_us_max"], 0),
+                 "csv_identical": c3["csv_identical"]})
+        line["ticks"] = ticks
+        line["ticks_unit"] = "us/tick; dev=CUDA events, e2e=TickEngine.tick, dropin=" \
+                             "B200SimulationEngine._handle_scaler, ref=hybridscale " \
+                             "_handle_scaler (config4: 40-fn sample x25)"
+        line["lattice_config5"] = {"value": lat["value"], "ms_per_step": _r(lat["ms"] / 50, 4),
+                                   "frac": lat["roofline"]["frac"],
+                                   "e2e": _r(lat["e2e"]["value"], -6) if lat["e2e"] else None,
+                                   "cpu": _r(lcpu["value"], -3)}
+        line["learned_mlp"] = {"value": mlp["value"], "frac": mlp["roofline"]["frac"]}
+        line["config1_sweep_us"] = _r(c1["sweep_us_device"], 2)
+        detail = {"tick_config4": t4, "tick_config4_full_grid": t4f, "tick_config3_size": t3,
+                  "replay_config3": rep, "reference_config3": c3,
+                  "reference_config4": [r4, r4f], "config1": c1, "lattice_config5": lat,
+                  "lattice_cpu": lcpu, "learned_mlp": mlp,
+                  "tick_port_baseline": tick_cpu_baseline(args)}
+    finish(line, detail, args, world)
+
+
+def finish(line, detail, args, world):
+    """Rank 0 prints ONE compact JSON line last (after the process group is torn down, so
+    no later log line follows it); the full record goes to --detail and to stderr."""
     if world > 1:
         import torch.distributed as dist
+        barrier(world)
         dist.destroy_process_group()
+    if line is None:
+        return
+    if detail:
+        full = {"line": line, "detail": detail}
+        if args.detail:
+            with open(args.detail, "w") as fh:
+                json.dump(full, fh, default=str)
+        print("bench detail: " + json.dumps(detail, default=str), file=sys.stderr, flush=True)
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
