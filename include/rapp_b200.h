@@ -158,6 +158,14 @@ int rapp_mec_plan_run_dev(rapp_mec_plan *plan, const double *d_targets, int64_t 
 int rapp_mec_plan_run(rapp_mec_plan *plan, const double *targets, int64_t fn_begin,
                       int64_t fn_end, int64_t *out_bsq);
 
+/* Opt-in latency SLO (north_star: feasibility "latency <= SLO"; the reference reads
+ * FunctionSpec.slo_ms nowhere, hs/core.py:96-98, hs/perf.py:132): slo_ms[f] > 0 makes a
+ * lattice point feasible for function f only if rps >= target AND latency <= slo_ms[f];
+ * NaN means no SLO for that function; slo_ms == NULL (the default) restores the reference
+ * rule for every function.  When no point is feasible the fallback is the reference's
+ * unchanged max-throughput rule over the whole lattice.  RAPP_E_VALUE for slo <= 0. */
+int rapp_mec_plan_set_slo(rapp_mec_plan *plan, const double *slo_ms);
+
 /* Measurement: when enabled (which also resets the record), every run brackets its meet
  * pass — the fused lattice kernel K3 — with CUDA events on the run's stream;
  * rapp_mec_plan_kernel_time synchronises them and returns the summed kernel time and the
@@ -258,6 +266,11 @@ int rapp_tick_pod_count(rapp_tick *t, int64_t *n_pods);
 /* Host copy of the world (after any number of ticks): pods (alive flag via state -1 for
  * released pods), per-function Kalman / stamp state, partitions per GPU, pod counter. */
 int rapp_tick_read_pods(rapp_tick *t, rapp_pod_desc *pods, int64_t cap, int64_t *n);
+/* Opt-in latency SLO for the fresh-GPU configuration search of the tick
+ * (hs/autoscaler.py:155-165 calls most_efficient_config; see rapp_mec_plan_set_slo for the
+ * rule): slo_ms[f] > 0 per function (NaN: none); NULL restores the reference rule.  Rebuilds
+ * the tick's search index (synchronous).  RAPP_E_VALUE for slo <= 0. */
+int rapp_tick_set_slo(rapp_tick *t, const double *slo_ms);
 int rapp_tick_read_fns(rapp_tick *t, rapp_fn_desc *fns);
 int rapp_tick_read_parts(rapp_tick *t, int64_t *part_off, int32_t *part_sm,
                          int32_t *part_alloc, int32_t *part_npods, int64_t cap);

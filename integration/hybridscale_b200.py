@@ -43,8 +43,9 @@ def _policy_settings(policy, default_config):
 class B200SimulationEngine(SimulationEngine):
     """`SimulationEngine` whose scaler ticks run on the B200 (one device tick per tick)."""
 
-    def __init__(self, *args, device: Optional[int] = None, **kwargs):
+    def __init__(self, *args, device: Optional[int] = None, slo_mask: bool = False, **kwargs):
         super().__init__(*args, **kwargs)
+        self._slo_mask = slo_mask  # opt-in: fresh-GPU configs also meet FunctionSpec.slo_ms
         if getattr(self.policy, "name", None) not in POLICY_NAMES:
             raise ConfigError(f"B200SimulationEngine runs the policies {POLICY_NAMES} on the "
                               f"device; got {getattr(self.policy, 'name', self.policy)!r}")
@@ -61,7 +62,8 @@ class B200SimulationEngine(SimulationEngine):
                 kalman_params={**self._kalman_defaults, "P0": self._kalman_p0},
                 scaler_interval_ms=self.cfg.scaler_interval_ms,
                 cold_start_ms=self.cfg.cold_start_ms, pod_counter=self._pod_counter,
-                last_scale_down=stamps, policy=self.policy.name, device=self._device)
+                last_scale_down=stamps, policy=self.policy.name, device=self._device,
+                slo_mask=self._slo_mask)
             self._released_between_ticks.clear()  # the upload saw the current cluster
         return self._tick_engine
 
@@ -109,10 +111,11 @@ class B200SimulationEngine(SimulationEngine):
 
 
 def run(trace, functions, tables, cluster, scaler_config, sim_config, policy,
-        kalman_params=None, *, device: Optional[int] = None):
+        kalman_params=None, *, device: Optional[int] = None, slo_mask: bool = False):
     """`hybridscale.sim.run` (hs/sim.py:623-637) with the B200 scaler tick."""
     engine = B200SimulationEngine(trace, functions, tables, cluster, scaler_config,
-                                  sim_config, policy, kalman_params, device=device)
+                                  sim_config, policy, kalman_params, device=device,
+                                  slo_mask=slo_mask)
     metrics = engine.run()
     _assert_monotone_curves(metrics)
     return metrics

@@ -75,6 +75,7 @@ SIGNATURES = [
     ("rapp_mec_plan_run_dev", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp,
                                              c_vp, c_vp]),
     ("rapp_mec_plan_run", ctypes.c_int, [c_vp, c_dp, ctypes.c_int64, ctypes.c_int64, c_i64p]),
+    ("rapp_mec_plan_set_slo", ctypes.c_int, [c_vp, c_vp]),
     ("rapp_mec_plan_timing", ctypes.c_int, [c_vp, ctypes.c_int]),
     ("rapp_mec_plan_kernel_time", ctypes.c_int, [c_vp, c_dp, c_i64p]),
     ("rapp_metrics_finalize", ctypes.c_int, [c_vp, ctypes.c_int64, c_dp, c_i64p, c_i64p, c_dp,
@@ -106,6 +107,7 @@ SIGNATURES = [
                                              ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     ("rapp_tick_pod_count", ctypes.c_int, [c_vp, c_i64p]),
     ("rapp_tick_read_pods", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_i64p]),
+    ("rapp_tick_set_slo", ctypes.c_int, [c_vp, c_vp]),
     ("rapp_tick_read_fns", ctypes.c_int, [c_vp, c_vp]),
     ("rapp_tick_read_parts", ctypes.c_int, [c_vp, c_i64p, c_i32p, c_i32p, c_i32p,
                                             ctypes.c_int64]),

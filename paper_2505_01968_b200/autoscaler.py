@@ -50,9 +50,10 @@ def update_load_balancer_weights(cluster, function_id: str) -> dict[str, float]:
 class Autoscaler:
     """Per-function decisions on the device; holds the scale-down cooldown stamps."""
 
-    def __init__(self, config: ScalerConfig, tables: Mapping):
+    def __init__(self, config: ScalerConfig, tables: Mapping, *, slo_mask: bool = False):
         self.config = config
         self.tables = tables
+        self.slo_mask = slo_mask  # opt-in: fresh-GPU configs must also meet function.slo_ms
         self._last_scale_down: dict[str, float] = {}
 
     def _table(self, function: FunctionSpec):
@@ -69,7 +70,7 @@ class Autoscaler:
         # the snapshot's pod states are authoritative here (no ready-event promotion)
         eng = TickEngine([function], self.tables, cluster, self.config, promote_cold=False,
                          last_scale_down={fid: self._last_scale_down[fid]}
-                         if fid in self._last_scale_down else None)
+                         if fid in self._last_scale_down else None, slo_mask=self.slo_mask)
         res = eng.tick(cluster.clock_ms, {fid: 0}, idle=(), predicted={fid: predicted_rps})
         stamp = float(eng.read_functions()[0]["last_down_ms"])
         if stamp != float("-inf"):
@@ -93,8 +94,8 @@ class HybridPolicy:
 
     name = "hybrid"
 
-    def __init__(self, config: ScalerConfig, tables: Mapping):
-        self._scaler = Autoscaler(config, tables)
+    def __init__(self, config: ScalerConfig, tables: Mapping, *, slo_mask: bool = False):
+        self._scaler = Autoscaler(config, tables, slo_mask=slo_mask)
 
     def initial_config(self, function: FunctionSpec) -> PodConfig:
         return function.initial

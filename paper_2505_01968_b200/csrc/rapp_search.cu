@@ -24,6 +24,7 @@
 //    (s axis strictly ascending -> index order == value order; B_f sorted -> same), so
 //    the argmin is an order-independent min-reduction: warp shuffles -> shared memory ->
 //    one atomicMin per CTA into the per-function slot.
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <type_traits>
@@ -63,19 +64,27 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 }
 
 // One warp per function: feasibility thresholds per batch-lattice entry, key reset.
+// Opt-in latency SLO (slo != nullptr, slo[f] > 0 or NaN = none): a point is feasible iff
+// rps >= target AND lat <= slo[f].  Both are upper bounds on the latency (the first is
+// exactly lat <= threshold for positive latencies), so the mask is one threshold,
+// min(threshold, slo[f]); latency 0 (rps = inf) satisfies any positive SLO, and the
+// fallback pass (k_mec_fallback) recomputes its thresholds without the SLO.
 __global__ void k_mec_prepare(const FnDesc* __restrict__ fns, const double* __restrict__ blist,
                               const double* __restrict__ targets, int64_t fn_begin,
                               int64_t fn_end, double* __restrict__ thr,
                               unsigned long long* __restrict__ minlat,
-                              unsigned long long* __restrict__ keys) {
+                              unsigned long long* __restrict__ keys,
+                              const double* __restrict__ slo) {
   pdl_trigger();
   const int64_t f = fn_begin + (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (f >= fn_end) return;
   const FnDesc fd = fns[f];
   const double target = targets[f];
+  const double cap = slo != nullptr ? slo[f] : __longlong_as_double(0x7FF0000000000000ll);
   for (int bi = lane; bi < fd.nB; bi += 32) {
-    thr[fd.boff + bi] = feasibility_threshold(blist[fd.boff + bi], target);
+    const double th = feasibility_threshold(blist[fd.boff + bi], target);
+    thr[fd.boff + bi] = cap < th ? cap : th;  // NaN cap: no SLO
     minlat[fd.boff + bi] = 0x7FF0000000000000ull;  // +inf
   }
   if (lane == 0) keys[f] = kNoKey;
@@ -445,6 +454,7 @@ struct rapp_mec_plan {
   double* d_thr = nullptr;
   unsigned long long* d_minlat = nullptr;
   unsigned long long* d_key = nullptr;
+  double* d_slo = nullptr;  // opt-in per-function latency SLO (rapp_mec_plan_set_slo)
   double* d_target2 = nullptr;
   int32_t* d_fb = nullptr;
   // optional per-launch timing of the meet pass (bench.py's roofline): event pairs
@@ -483,7 +493,7 @@ static int run_plan(rapp_mec_plan* pl, const double* d_targets, int64_t f0, int6
   const int wpb = 8;  // warps per block for the per-function helpers
   const unsigned hblocks = (unsigned)((nf + wpb - 1) / wpb);
   k_mec_prepare<<<hblocks, 32 * wpb, 0, st>>>(pl->d_fn, pl->d_blist, d_targets, f0, f1,
-                                              pl->d_thr, pl->d_minlat, pl->d_key);
+                                              pl->d_thr, pl->d_minlat, pl->d_key, pl->d_slo);
   RAPP_LAUNCHED();
   // enough CTAs to fill the machine even for a handful of functions
   int chunks = (int)((4LL * c->sm_count + nf - 1) / nf);
@@ -627,6 +637,7 @@ int rapp_mec_plan_destroy(rapp_mec_plan* pl) {
   cudaFree(pl->d_key);
   cudaFree(pl->d_target2);
   cudaFree(pl->d_fb);
+  cudaFree(pl->d_slo);
   for (cudaEvent_t e : pl->ev) cudaEventDestroy(e);
   if (pl->h_stage) cudaFreeHost(pl->h_stage);
   if (pl->d_stage) cudaFree(pl->d_stage);
@@ -641,6 +652,31 @@ int rapp_mec_plan_points(rapp_mec_plan* pl, int64_t* points) {
     return RAPP_E_ARG;
   }
   *points = pl->points;
+  return RAPP_OK;
+}
+
+int rapp_mec_plan_set_slo(rapp_mec_plan* pl, const double* slo_ms) {
+  if (!pl) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  std::lock_guard<std::mutex> lk(pl->ctx->mu);
+  RAPP_CUDA(cudaSetDevice(pl->ctx->device));
+  RAPP_CUDA(cudaDeviceSynchronize());  // no run of this plan may still read the old values
+  if (slo_ms == nullptr) {
+    cudaFree(pl->d_slo);
+    pl->d_slo = nullptr;
+    return RAPP_OK;
+  }
+  for (int64_t f = 0; f < pl->nfn; ++f)
+    if (!(slo_ms[f] > 0.0) && !std::isnan(slo_ms[f])) {
+      set_error("slo_ms must be positive (NaN: no SLO), got %g for function %lld", slo_ms[f],
+                (long long)f);
+      return RAPP_E_VALUE;
+    }
+  if (!pl->d_slo) RAPP_CUDA(cudaMalloc(&pl->d_slo, (size_t)std::max<int64_t>(1, pl->nfn) * 8));
+  if (pl->nfn)
+    RAPP_CUDA(cudaMemcpy(pl->d_slo, slo_ms, (size_t)pl->nfn * 8, cudaMemcpyHostToDevice));
   return RAPP_OK;
 }
 

@@ -130,6 +130,8 @@ struct World {
   const int32_t* fn_npairs;
   const int32_t* pairs;          // packed s_index << 16 | q
   const double* pmax;            // prefix max of rps along the key-sorted lattice
+  const double* fn_slo;          // opt-in latency SLO per function (NaN: none), or null
+  const int64_t* fn_fb;          // with an SLO: index of the unmasked max-rps fallback
   int32_t* k_init;
   double* k_R;
   double* k_P;
@@ -1334,7 +1336,12 @@ struct CommitT {
     const double t = target <= top ? target : top;  // target > top -> max-rps fallback
     // invariant: the answer lies in [lo, hi] (pm non-decreasing, pm[hi] >= t)
     int64_t lo = 0, hi = L - 1;
-    while (true) {
+    // opt-in SLO: pm is the prefix max over SLO-compliant points only; with no compliant
+    // point meeting the target the answer is the reference's fallback over the whole
+    // lattice, precomputed (k_index_fb)
+    const int64_t fb = (w.fn_fb != nullptr && !(target <= top)) ? w.fn_fb[f] : -1;
+    if (fb >= 0) lo = fb;
+    while (fb < 0) {
       const int64_t len = hi - lo + 1;
       const int64_t step = (len + 1023) / 1024;  // probes lo + step*j, j < 1024
       bool ge[32];
@@ -2114,20 +2121,66 @@ __global__ void __launch_bounds__(32) k_tick_release(World w, const int32_t* __r
 // ---------------------------------------------------------------------------------------
 // prefix-max index for the fresh-GPU search (built once; tables are immutable)
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void index_point(const World& w, int f, int64_t i, double& lat,
+                                            double& rps) {
+  const int nb = w.fn_nb[f];
+  const TableDesc td = w.tds[w.fn_table[f]];
+  const int pair = w.pairs[w.fn_pairs_off[f] + int(i / nb)];
+  const double b = w.blist[w.fn_boff[f] + i % nb];
+  const double s = w.pool[td.off + td.os + (pair >> 16)];
+  const double q = double(pair & 0xFFFF);
+  const double* seg = w.pool + td.off;
+  lat = interp3(seg + td.ob, td.nb, seg + td.os, td.ns, seg + td.oq, td.nq, seg + td.ov, b, s,
+                q);
+  rps = throughput(b, lat);  // b / (lat / 1000.0), hs/perf.py:95-98
+}
+
+// rps of every lattice point in key order; with the opt-in SLO, points whose latency
+// exceeds it are -inf (never feasible, never raise the prefix max)
 __global__ void k_index_rps(World w, int f0) {
   const int f = f0 + blockIdx.y;
   if (f >= w.F) return;
   const int64_t L = w.fn_lat_len[f];
-  const int nb = w.fn_nb[f];
-  const TableDesc td = w.tds[w.fn_table[f]];
+  const double slo = w.fn_slo != nullptr ? w.fn_slo[f] : __longlong_as_double(-1ll);  // NaN
   double* out = const_cast<double*>(w.pmax) + w.fn_lat_off[f];
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int pair = w.pairs[w.fn_pairs_off[f] + int(i / nb)];
-    const double b = w.blist[w.fn_boff[f] + i % nb];
-    const double s = w.pool[td.off + td.os + (pair >> 16)];
-    const double q = double(pair & 0xFFFF);
-    out[i] = thr_at(w, f, b, s, q);
+    double lat, rps;
+    index_point(w, f, i, lat, rps);
+    out[i] = lat > slo ? -INFINITY : rps;
+  }
+}
+
+// order-preserving uint64 image of a double (max of images == image of the max)
+__device__ __forceinline__ unsigned long long ord_bits(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// SLO functions: the reference's fallback over the WHOLE lattice — max rps (pass 0), then
+// the first key-order point with that rps (pass 1) — argmin (-rps, s*q, s, q, b)
+__global__ void k_index_fb(World w, int f0, int pass, unsigned long long* best) {
+  const int f = f0 + blockIdx.y;
+  if (f >= w.F || !(w.fn_slo[f] == w.fn_slo[f])) return;  // NaN: no SLO, no fallback index
+  const int64_t L = w.fn_lat_len[f];
+  unsigned long long m = pass == 0 ? 0ull : ~0ull;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double lat, rps;
+    index_point(w, f, i, lat, rps);
+    if (rps != rps) continue;
+    if (pass == 0) {
+      const unsigned long long o = ord_bits(rps);
+      m = o > m ? o : m;
+    } else if (ord_bits(rps) == best[f]) {
+      m = (unsigned long long)i < m ? (unsigned long long)i : m;
+      break;  // later i of this thread are larger
+    }
+  }
+  if (pass == 0) {
+    if (m) atomicMax(&best[f], m);
+  } else if (m != ~0ull) {
+    atomicMin(reinterpret_cast<unsigned long long*>(const_cast<int64_t*>(w.fn_fb)) + f, m);
   }
 }
 
@@ -2198,6 +2251,9 @@ struct rapp_tick {
   int64_t h_npods = 0;         // pods created so far (host copy of w.n_pods)
   uint8_t* d_ovf_ones = nullptr;  // [G] ones: k_tick_release's "list in global memory" flags
   cudaEvent_t order_ev = nullptr;  // orders rapp_tick_run_dev's stream against t->stream
+  double* d_slo = nullptr;         // rapp_tick_set_slo: per-function SLO (NaN: none)
+  int64_t* d_fb = nullptr;         //   fallback index per SLO function
+  unsigned long long* d_fb_best = nullptr;  //   its max-rps image (k_index_fb pass 0)
 };
 
 namespace rapp {
@@ -2820,6 +2876,56 @@ int rapp_tick_read_pods(rapp_tick* t, rapp_pod_desc* out, int64_t cap, int64_t* 
         }
     unpack_id(id[i], o.id);
   }
+  return RAPP_OK;
+}
+
+int rapp_tick_set_slo(rapp_tick* t, const double* slo_ms) {
+  if (!t) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  World& w = t->w;
+  const int F = w.F;
+  if (slo_ms != nullptr)
+    for (int f = 0; f < F; ++f)
+      if (!(slo_ms[f] > 0.0) && !std::isnan(slo_ms[f])) {
+        set_error("slo_ms must be positive (NaN: no SLO), got %g for function %d", slo_ms[f], f);
+        return RAPP_E_VALUE;
+      }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  RAPP_CUDA(cudaSetDevice(t->ctx->device));
+  RAPP_CUDA(cudaStreamSynchronize(t->stream));
+  if (slo_ms == nullptr) {
+    w.fn_slo = nullptr;
+    w.fn_fb = nullptr;
+  } else {
+    if (t->d_slo == nullptr) {
+      int rc;
+      if ((rc = dev_alloc(t, &t->d_slo, (size_t)std::max(1, F)))) return rc;
+      if ((rc = dev_alloc(t, &t->d_fb, (size_t)std::max(1, F)))) return rc;
+      if ((rc = dev_alloc(t, &t->d_fb_best, (size_t)std::max(1, F)))) return rc;
+    }
+    if (F) RAPP_CUDA(cudaMemcpy(t->d_slo, slo_ms, (size_t)F * 8, cudaMemcpyHostToDevice));
+    RAPP_CUDA(cudaMemsetAsync(t->d_fb, 0xFF, (size_t)std::max(1, F) * 8, t->stream));  // -1
+    RAPP_CUDA(cudaMemsetAsync(t->d_fb_best, 0, (size_t)std::max(1, F) * 8, t->stream));
+    w.fn_slo = t->d_slo;
+    w.fn_fb = t->d_fb;
+  }
+  // rebuild the fresh-GPU search index (masked by the SLO when set) and the fallbacks
+  for (int f0 = 0; f0 < F; f0 += 32768) {
+    const int nf = std::min(F - f0, 32768);
+    k_index_rps<<<dim3(64, nf), 256, 0, t->stream>>>(w, f0);
+    RAPP_LAUNCHED();
+    k_index_scan<<<nf, 1024, 0, t->stream>>>(w, f0);
+    RAPP_LAUNCHED();
+    if (slo_ms != nullptr) {
+      k_index_fb<<<dim3(64, nf), 256, 0, t->stream>>>(w, f0, 0, t->d_fb_best);
+      RAPP_LAUNCHED();
+      k_index_fb<<<dim3(64, nf), 256, 0, t->stream>>>(w, f0, 1, t->d_fb_best);
+      RAPP_LAUNCHED();
+    }
+  }
+  RAPP_CUDA(cudaStreamSynchronize(t->stream));
   return RAPP_OK;
 }
 

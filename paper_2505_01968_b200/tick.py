@@ -172,7 +172,7 @@ class TickEngine:
                  kalman_states: Optional[Mapping] = None,
                  last_scale_down: Optional[Mapping[str, float]] = None,
                  promote_cold: bool = True, policy: str = "hybrid",
-                 device: Optional[int] = None):
+                 device: Optional[int] = None, slo_mask: bool = False):
         from .perf import device_table_of
         self.policy = canonical_policy(policy)
         self.cluster = cluster
@@ -263,11 +263,28 @@ class TickEngine:
             len(self.gids), _lib.i64ptr(po), _lib.i32ptr(ps), _lib.i32ptr(pa), len(pods),
             _ptr(pods), self.counter, ctypes.byref(h)), "TickEngine")
         self._h = h
+        if slo_mask:
+            self.set_slo({fid: self.functions[fid].slo_ms for fid in self.fids})
         # the device's own output block: kMaxPods + 4 actions per function
         self._act_buf = np.zeros(max(1, len(self.fids)) * (MAX_PODS_PER_FUNCTION + 4),
                                  dtype=ACTION_DTYPE)
         self._obs = np.zeros(max(1, len(self.fids)))
         self._pred = np.zeros(max(1, len(self.fids)))
+
+    def set_slo(self, slo_ms: Optional[Mapping[str, Optional[float]]]) -> None:
+        """Opt-in latency SLO for the fresh-GPU most_efficient_config of the tick
+        (hs/autoscaler.py:155-165): {fid: slo in ms or None}; a configuration is feasible
+        iff its throughput covers the gap AND its latency is <= the SLO (north_star (3);
+        the reference never reads FunctionSpec.slo_ms, hs/core.py:96-98).  With no such
+        configuration the reference's max-throughput fallback applies unchanged.  None
+        restores the reference rule.  Vertical walks and covering quotas are unaffected."""
+        if slo_ms is None:
+            _lib.check(_lib.load().rapp_tick_set_slo(self._h, None), "set_slo")
+            return
+        arr = np.array([math.nan if slo_ms.get(f) is None else float(slo_ms[f])
+                        for f in self.fids], dtype=np.float64)
+        _lib.check(_lib.load().rapp_tick_set_slo(self._h, _ptr(arr) if len(arr) else None),
+                   "set_slo")
 
     def __del__(self):
         h = getattr(self, "_h", None)
