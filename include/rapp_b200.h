@@ -67,6 +67,9 @@ typedef struct rapp_ctx rapp_ctx;
 
 int rapp_ctx_create(int device, rapp_ctx **out);
 int rapp_ctx_destroy(rapp_ctx *ctx);
+/* Destroys the internal per-device contexts of the stateless entry points
+ * (rapp_interp3_many & co.).  For a clean process shutdown only (leak checks). */
+int rapp_shutdown(void);
 /* Device the context lives on and the number of SMs. */
 int rapp_ctx_info(rapp_ctx *ctx, int *device, int *sm_count);
 

@@ -46,6 +46,7 @@ SIGNATURES = [
                                          ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, c_dp]),
     ("rapp_ctx_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("rapp_ctx_destroy", ctypes.c_int, [c_vp]),
+    ("rapp_shutdown", ctypes.c_int, []),
     ("rapp_ctx_info", ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_int),
                                      ctypes.POINTER(ctypes.c_int)]),
     ("rapp_table_create", ctypes.c_int, [c_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -193,6 +194,17 @@ class Context:
         if ctx is None:
             ctx = cls._by_device[device] = Context(device)
         return ctx
+
+
+    @classmethod
+    def close_all(cls) -> None:
+        """Destroys every context (table pools, staging).  Only for a clean shutdown once
+        no table, plan, tick world or model of the process is alive any more (leak checks)."""
+        lib = load()
+        for dev, ctx in list(cls._by_device.items()):
+            lib.rapp_ctx_destroy(ctx.handle)
+            del cls._by_device[dev]
+        lib.rapp_shutdown()
 
 
 def launch_count() -> int:

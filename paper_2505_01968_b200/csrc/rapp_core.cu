@@ -400,6 +400,18 @@ int rapp_ctx_create(int device, rapp_ctx** out) {
   return RAPP_OK;
 }
 
+int rapp_shutdown(void) {
+  rapp_ctx* victims[64];
+  int n = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_default_mu);
+    for (auto& d : g_default)
+      if (d) victims[n++] = d;
+  }
+  for (int i = 0; i < n; ++i) rapp_ctx_destroy(victims[i]);  // clears its g_default slot
+  return RAPP_OK;
+}
+
 int rapp_ctx_destroy(rapp_ctx* ctx) {
   if (!ctx) return RAPP_OK;
   cudaSetDevice(ctx->device);

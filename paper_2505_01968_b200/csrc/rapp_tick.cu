@@ -935,6 +935,25 @@ __device__ __forceinline__ void tk_bar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+__device__ __forceinline__ void mbar_init32(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)));
+}
+__device__ __forceinline__ void mbar_arrive_rel(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+      (uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
 // the first pod's quota row of a function, staged for the commit (102 doubles = 816 B,
 // the 101-entry row plus 8 bytes of the next row so the bulk size is a multiple of 16)
 constexpr int kRowStage = 102;
@@ -1125,6 +1144,7 @@ struct CommitT {
         __ballot_sync(0xffffffffu, lane < n && part_sm(e0) == s && 100 - part_alloc(e0) >= q);
     const int pos = hit ? __ffs(hit) - 1 : -1;
     const uint64_t e = __shfl_sync(0xffffffffu, e0, pos < 0 ? 0 : pos);
+    __syncwarp();  // every lane's reads of the list and the argmin keys precede the update
     if (lane == 0) {
       uint64_t* P = parts(g);
       if (pos < 0) {
@@ -1855,11 +1875,17 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   __shared__ FastRec s_fast[kPreDepth][32];
   __shared__ uint32_t s_htab[kFastHash];
   for (int i = threadIdx.x; i < kFastHash; i += blockDim.x) s_htab[i] = 0;
-  __shared__ volatile int s_ready[kPreDepth];
-  __shared__ volatile int s_done, s_stop;
-  if (threadIdx.x < kPreDepth) s_ready[threadIdx.x] = -1;
+  // ring handoff by mbarriers (acquire/release, and visible to compute-sanitizer's
+  // racecheck): full[slot] completes when all 32 helper lanes have written a batch into the
+  // slot, empty[slot] when all 32 committing lanes are done with it
+  __shared__ uint64_t s_full[kPreDepth], s_empty[kPreDepth];
+  __shared__ volatile int s_stop;
   if (threadIdx.x == 0) {
-    s_done = -1;
+    for (int k = 0; k < kPreDepth; ++k) {
+      mbar_init32(&s_full[k]);
+      mbar_init32(&s_empty[k]);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_stop = 0;
   }
 #ifdef RAPP_TICK_PROF
@@ -1897,15 +1923,19 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
     const int h = (threadIdx.x >> 5) - 1;
     bool quit = false;
     for (int b = h, base = 32 * h; base < w.F; b += kHelpers, base += 32 * kHelpers) {
-      const int slot = b % kPreDepth;
-      while (s_done < b - kPreDepth) {  // the slot is free once batch b - depth is done
-        if (s_stop) {
-          quit = true;
-          break;
+      const int slot = b % kPreDepth, use = b / kPreDepth;
+      if (use > 0) {  // the slot is free once the commit released batch b - depth
+        while (true) {
+          const bool got = mbar_try(&s_empty[slot], (use - 1) & 1);
+          if (__all_sync(0xffffffffu, got)) break;
+          if (__any_sync(0xffffffffu, s_stop != 0)) {
+            quit = true;
+            break;
+          }
+          __nanosleep(32);
         }
-        __nanosleep(32);
       }
-      if (quit || s_stop) break;
+      if (quit || __any_sync(0xffffffffu, s_stop != 0)) break;
       const int f = base + lane;
       const int cf = f < w.F ? w.cls[f] : kNone;
       s_pcls[slot][lane] = cf;
@@ -1924,9 +1954,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
           fr.kind = kind;
         }
       }
-      __threadfence_block();
-      __syncwarp();
-      if (lane == 0) s_ready[slot] = b;
+      mbar_arrive_rel(&s_full[slot]);  // release: this lane's entries are written
     }
   } else {  // warp 0: the commit
   World v = w;
@@ -1985,9 +2013,8 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   for (int base = 0; base < w.F && !stop; base += 32, ++j) {
     TPROF_ACC(6);  // (the functions of the previous batch, accounted separately)
     const int slot = j % kPreDepth;
-    while (s_ready[slot] != j) {
+    while (!__all_sync(0xffffffffu, mbar_try(&s_full[slot], (j / kPreDepth) & 1))) {
     }
-    __threadfence_block();
     const int mine = s_pcls[slot][lane];
     if (base + 32 < w.F) {
       stage(base + 32, cls_nxt, (j + 1) & 1);
@@ -2061,7 +2088,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
       }
     }
     __syncwarp();
-    if (lane == 0) s_done = j;
+    mbar_arrive_rel(&s_empty[slot]);  // the slot's entries are no longer read
   }
   if (lane == 0) s_stop = 1;  // release the helper if the commit stopped early
   // no bulk copy may still be in flight into shared memory when the CTA exits

@@ -286,10 +286,15 @@ class TickEngine:
         _lib.check(_lib.load().rapp_tick_set_slo(self._h, _ptr(arr) if len(arr) else None),
                    "set_slo")
 
-    def __del__(self):
+    def close(self) -> None:
+        """Frees the device world now (also done when the engine is garbage-collected)."""
         h = getattr(self, "_h", None)
+        self._h = None
         if h is not None and _lib._lib is not None:
             _lib._lib.rapp_tick_destroy(h)
+
+    def __del__(self):
+        self.close()
 
     # -- host events between ticks ---------------------------------------------------------
 
