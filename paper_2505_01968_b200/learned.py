@@ -234,11 +234,16 @@ class LearnedPerfModel:
     def zoo(cls, seed: int = 0, device: int | None = None) -> "LearnedPerfModel":
         return cls({k: f() for k, f in ZOO.items()}, MlpWeights.random(seed), device=device)
 
-    def __del__(self):
+    def close(self) -> None:
+        """Frees the device model now (also done when it is garbage-collected)."""
         h = getattr(self, "_h", None)
+        self._h = None
         lib = getattr(_lib, "_lib", None) if _lib is not None else None
         if h is not None and lib is not None:
             lib.rapp_mlp_destroy(h)
+
+    def __del__(self):
+        self.close()
 
     def predict_many_dev(self, model: int, coords, out, *, stream=None):
         """Device API: coords (n, 3) float64 CUDA tensor -> out (n) float64 latency ms."""

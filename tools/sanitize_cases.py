@@ -29,6 +29,7 @@ def k2():
     c = bench.gen_queries(b, s, q, n, 3, torch.device("cuda", 0))
     out = t.predict_latency_many(c).cpu().numpy()
     want = or_interp3_many(b, s, q, v, c.cpu().numpy())
+    del c
     assert np.array_equal(out.view(np.int64), want.view(np.int64))
     bl = np.array([1.0, 3.0, 7.0])  # a non-uniform axis: the LUT locate
     sl = np.array([10.0, 35.0, 100.0])
@@ -102,6 +103,7 @@ def mlp():
     ref = lm.reference_forward(0, c)
     assert np.all(np.abs(lat - ref) <= 2e-2 * ref)
     lm.search(np.array([0, 1, 2, 3]), np.array([50.0, 500.0, 5000.0, 1e9]))
+    lm.close()
 
 
 def ingest():
