@@ -409,6 +409,9 @@ int rapp_shutdown(void) {
       if (d) victims[n++] = d;
   }
   for (int i = 0; i < n; ++i) rapp_ctx_destroy(victims[i]);  // clears its g_default slot
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess)
+    for (int d = 0; d < ndev && d < 64; ++d) rapp_tick_pool_drain(d);
   return RAPP_OK;
 }
 

@@ -160,3 +160,6 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
 int launch_interp(rapp_ctx* ctx, int32_t table_id, const double* d_coords, int64_t n,
                   double* d_out, double* d_rps, cudaStream_t st);
 }  // namespace rapp
+
+// the tick worlds' allocation cache (rapp_tick.cu), emptied by rapp_shutdown
+extern "C" int rapp_tick_pool_drain(int device);

@@ -35,7 +35,9 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <algorithm>
 #include <vector>
@@ -2259,7 +2261,8 @@ constexpr size_t kOutHead = 16;  // n_actions, err, err_fn, pad (int32 each)
 struct rapp_tick {
   rapp_ctx* ctx = nullptr;
   World w{};
-  std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> allocs;  // device buffers (returned to the pool)
+  size_t h_in_bytes = 0, h_out_bytes = 0;
   cudaStream_t stream = nullptr;
   // staging for the host API
   int64_t* d_arrivals = nullptr;
@@ -2285,12 +2288,92 @@ struct rapp_tick {
 
 namespace rapp {
 
+// Allocation cache of tick worlds.  The single-function seams (Autoscaler.scale and the
+// replica policies' decide, hs/autoscaler.py:73 / hs/policies.py:25-33) build and drop a
+// world on every call, so a world's device buffers, pinned staging, stream and event go
+// back to a per-device pool when it is destroyed and the next world of similar shape takes
+// them instead of cudaMalloc / cudaMallocHost (which synchronise and cost milliseconds).
+// Bounded: beyond the caps buffers are freed; rapp_shutdown empties it.
+struct TickPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> dev, host;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> streams;
+  size_t dev_bytes = 0, host_bytes = 0;
+};
+constexpr size_t kPoolDevCap = size_t(512) << 20, kPoolHostCap = size_t(64) << 20;
+static TickPool g_tick_pool[64];
+
+static size_t pool_round(size_t b) {
+  b = std::max<size_t>(b, 256);
+  if (b <= (size_t(64) << 10)) {
+    size_t r = 256;
+    while (r < b) r <<= 1;
+    return r;
+  }
+  return (b + 65535) & ~size_t(65535);
+}
+
+static TickPool& pool_of(int dev) { return g_tick_pool[dev & 63]; }
+
+static cudaError_t pool_take(int dev, bool host, size_t bytes, void** out) {
+  const size_t r = pool_round(bytes);
+  TickPool& P = pool_of(dev);
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto& m = host ? P.host : P.dev;
+    auto it = m.find(r);
+    if (it != m.end()) {
+      *out = it->second;
+      m.erase(it);
+      (host ? P.host_bytes : P.dev_bytes) -= r;
+      return cudaSuccess;
+    }
+  }
+  return host ? cudaMallocHost(out, r) : cudaMalloc(out, r);
+}
+
+static void pool_give(int dev, bool host, void* p, size_t bytes) {
+  if (p == nullptr) return;
+  const size_t r = pool_round(bytes);
+  TickPool& P = pool_of(dev);
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    size_t& held = host ? P.host_bytes : P.dev_bytes;
+    if (held + r <= (host ? kPoolHostCap : kPoolDevCap)) {
+      (host ? P.host : P.dev).emplace(r, p);
+      held += r;
+      return;
+    }
+  }
+  if (host)
+    cudaFreeHost(p);
+  else
+    cudaFree(p);
+}
+
+static void pool_drain(int dev) {
+  TickPool& P = pool_of(dev);
+  std::lock_guard<std::mutex> lk(P.mu);
+  for (auto& kv : P.dev) cudaFree(kv.second);
+  for (auto& kv : P.host) cudaFreeHost(kv.second);
+  for (auto& se : P.streams) {
+    cudaEventDestroy(se.second);
+    cudaStreamDestroy(se.first);
+  }
+  P.dev.clear();
+  P.host.clear();
+  P.streams.clear();
+  P.dev_bytes = P.host_bytes = 0;
+}
+
+// zeroed device buffer of n T's, ordered on the world's stream
 template <typename T>
 static int dev_alloc(rapp_tick* t, T** p, size_t n) {
   void* q = nullptr;
-  RAPP_CUDA(cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T)));
-  RAPP_CUDA(cudaMemset(q, 0, std::max<size_t>(1, n) * sizeof(T)));
-  t->allocs.push_back(q);
+  const size_t bytes = std::max<size_t>(1, n) * sizeof(T);
+  RAPP_CUDA(pool_take(t->ctx->device, false, bytes, &q));
+  t->allocs.emplace_back(q, bytes);
+  RAPP_CUDA(cudaMemsetAsync(q, 0, bytes, t->stream));
   *p = static_cast<T*>(q);
   return RAPP_OK;
 }
@@ -2299,7 +2382,9 @@ template <typename T>
 static int dev_upload(rapp_tick* t, T** p, const std::vector<T>& v) {
   int rc = dev_alloc(t, p, v.size());
   if (rc) return rc;
-  if (!v.empty()) RAPP_CUDA(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  if (!v.empty())
+    RAPP_CUDA(cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice,
+                              t->stream));
   return RAPP_OK;
 }
 
@@ -2380,10 +2465,21 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   }
   std::lock_guard<std::mutex> lk(ctx->mu);
   RAPP_CUDA(cudaSetDevice(ctx->device));
-  std::unique_ptr<rapp_tick> t(new rapp_tick());
+  std::unique_ptr<rapp_tick, int (*)(rapp_tick*)> t(new rapp_tick(), rapp_tick_destroy);
   t->ctx = ctx;
-  RAPP_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
-  RAPP_CUDA(cudaEventCreateWithFlags(&t->order_ev, cudaEventDisableTiming));
+  {
+    TickPool& P = pool_of(ctx->device);
+    std::lock_guard<std::mutex> plk(P.mu);
+    if (!P.streams.empty()) {
+      t->stream = P.streams.back().first;
+      t->order_ev = P.streams.back().second;
+      P.streams.pop_back();
+    }
+  }
+  if (t->stream == nullptr) {
+    RAPP_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+    RAPP_CUDA(cudaEventCreateWithFlags(&t->order_ev, cudaEventDisableTiming));
+  }
   World& w = t->w;
   w.alpha = cfg->alpha;
   w.beta = cfg->beta;
@@ -2568,7 +2664,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   UP(w.p_ready, p_ready)
   UP(w.p_id, p_id)
   if ((rc = dev_alloc(t.get(), &w.p_ctr, (size_t)cap))) return rc;
-  RAPP_CUDA(cudaMemset(w.p_ctr, 0xFF, (size_t)cap * sizeof(int64_t)));  // -1: nothing pending
+  RAPP_CUDA(cudaMemsetAsync(w.p_ctr, 0xFF, (size_t)cap * sizeof(int64_t), t->stream));  // -1
   UP(w.fn_npods, fn_npods)
   UP(w.fn_pods, fn_pods)
 #undef UP
@@ -2629,13 +2725,17 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
     t->d_pred_in = reinterpret_cast<double*>(ib + FP * 8);
     t->d_idle = ib + FP * 16;
   }
-  RAPP_CUDA(cudaMallocHost(&t->h_in, FP * 16 + (size_t)cap + 64));
-  RAPP_CUDA(cudaMallocHost(&t->h_out, kOutHead + FP * 16 + 1024 * sizeof(rapp_action)));
+  t->h_in_bytes = FP * 16 + (size_t)cap + 64;
+  t->h_out_bytes = kOutHead + FP * 16 + 1024 * sizeof(rapp_action);
+  RAPP_CUDA(pool_take(ctx->device, true, t->h_in_bytes, reinterpret_cast<void**>(&t->h_in)));
+  RAPP_CUDA(pool_take(ctx->device, true, t->h_out_bytes, reinterpret_cast<void**>(&t->h_out)));
   // release staging sized for typical between-tick releases up front: a pinned allocation
   // inside a tick's host call costs milliseconds (rapp_tick_release grows it if needed)
   t->rel_cap = 1024;
-  RAPP_CUDA(cudaMalloc(&t->d_rel, (size_t)t->rel_cap * 4));
-  RAPP_CUDA(cudaMallocHost(&t->h_rel, (size_t)t->rel_cap * 4));
+  RAPP_CUDA(pool_take(ctx->device, false, (size_t)t->rel_cap * 4,
+                      reinterpret_cast<void**>(&t->d_rel)));
+  RAPP_CUDA(pool_take(ctx->device, true, (size_t)t->rel_cap * 4,
+                      reinterpret_cast<void**>(&t->h_rel)));
   if ((rc = dev_alloc(t.get(), &t->d_ovf_ones, (size_t)std::max(1, w.G)))) return rc;
   RAPP_CUDA(cudaMemsetAsync(t->d_ovf_ones, 1, (size_t)std::max(1, w.G), t->stream));
   t->h_npods = n_pods;
@@ -2654,16 +2754,33 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
 
 int rapp_tick_destroy(rapp_tick* t) {
   if (!t) return RAPP_OK;
-  cudaSetDevice(t->ctx->device);
-  cudaStreamSynchronize(t->stream);
-  for (void* p : t->allocs) cudaFree(p);
-  if (t->h_in) cudaFreeHost(t->h_in);
-  if (t->d_rel) cudaFree(t->d_rel);
-  if (t->h_rel) cudaFreeHost(t->h_rel);
-  if (t->h_out) cudaFreeHost(t->h_out);
-  if (t->order_ev) cudaEventDestroy(t->order_ev);
-  cudaStreamDestroy(t->stream);
+  const int dev = t->ctx->device;
+  cudaSetDevice(dev);
+  if (t->stream) cudaStreamSynchronize(t->stream);  // nothing of this world is in flight
+  for (auto& a : t->allocs) pool_give(dev, false, a.first, a.second);
+  pool_give(dev, true, t->h_in, t->h_in_bytes);
+  pool_give(dev, true, t->h_out, t->h_out_bytes);
+  pool_give(dev, false, t->d_rel, (size_t)t->rel_cap * 4);
+  pool_give(dev, true, t->h_rel, (size_t)t->rel_cap * 4);
+  bool kept = false;
+  if (t->stream) {
+    TickPool& P = pool_of(dev);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.streams.size() < 8) {
+      P.streams.emplace_back(t->stream, t->order_ev);
+      kept = true;
+    }
+  }
+  if (!kept) {
+    if (t->order_ev) cudaEventDestroy(t->order_ev);
+    if (t->stream) cudaStreamDestroy(t->stream);
+  }
   delete t;
+  return RAPP_OK;
+}
+
+int rapp_tick_pool_drain(int device) {
+  rapp::pool_drain(device);
   return RAPP_OK;
 }
 
@@ -2708,11 +2825,15 @@ int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
   }
   if (n > t->rel_cap) {  // grow the persistent release buffers
     RAPP_CUDA(cudaStreamSynchronize(t->stream));
-    if (t->d_rel) RAPP_CUDA(cudaFree(t->d_rel));
-    if (t->h_rel) RAPP_CUDA(cudaFreeHost(t->h_rel));
+    pool_give(t->ctx->device, false, t->d_rel, (size_t)t->rel_cap * 4);
+    pool_give(t->ctx->device, true, t->h_rel, (size_t)t->rel_cap * 4);
+    t->d_rel = nullptr;
+    t->h_rel = nullptr;
     t->rel_cap = std::max<int64_t>(n, 1024);
-    RAPP_CUDA(cudaMalloc(&t->d_rel, (size_t)t->rel_cap * 4));
-    RAPP_CUDA(cudaMallocHost(&t->h_rel, (size_t)t->rel_cap * 4));
+    RAPP_CUDA(pool_take(t->ctx->device, false, (size_t)t->rel_cap * 4,
+                        reinterpret_cast<void**>(&t->d_rel)));
+    RAPP_CUDA(pool_take(t->ctx->device, true, (size_t)t->rel_cap * 4,
+                        reinterpret_cast<void**>(&t->h_rel)));
   }
   for (int64_t i = 0; i < n; ++i) {
     if (pods[i] < 0 || pods[i] >= known) {
@@ -2932,7 +3053,9 @@ int rapp_tick_set_slo(rapp_tick* t, const double* slo_ms) {
       if ((rc = dev_alloc(t, &t->d_fb, (size_t)std::max(1, F)))) return rc;
       if ((rc = dev_alloc(t, &t->d_fb_best, (size_t)std::max(1, F)))) return rc;
     }
-    if (F) RAPP_CUDA(cudaMemcpy(t->d_slo, slo_ms, (size_t)F * 8, cudaMemcpyHostToDevice));
+    if (F)
+      RAPP_CUDA(cudaMemcpyAsync(t->d_slo, slo_ms, (size_t)F * 8, cudaMemcpyHostToDevice,
+                                t->stream));
     RAPP_CUDA(cudaMemsetAsync(t->d_fb, 0xFF, (size_t)std::max(1, F) * 8, t->stream));  // -1
     RAPP_CUDA(cudaMemsetAsync(t->d_fb_best, 0, (size_t)std::max(1, F) * 8, t->stream));
     w.fn_slo = t->d_slo;
