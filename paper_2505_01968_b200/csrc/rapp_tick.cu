@@ -178,6 +178,8 @@ struct World {
   int32_t* spec_avail;           // [F][kMaxPods] avail the walk assumed (-1: not walked)
   int32_t* spec_k;               // [F][kMaxPods] steps taken
   double* spec_gain;             // [F][kMaxPods] gain of those steps
+  int32_t* spec_kg;              // [F][kMaxPods] first step whose gain closes the gap the
+                                 // walk assumed (any headroom; (100 - q0) / d + 1: none)
   FastRec* fast;                 // [F] straight-line commits (n = 0: none)
   double* tgrid;                 // [F][100][100] throughput(bref, sm, q)
   TickBrk* brk;                  // [F][201] phase A2's brackets: sm 1..100, quota steps, bref
@@ -617,25 +619,33 @@ __global__ void k_tick_phase_a(World w, double now, const int64_t* __restrict__ 
         // k = first step with q0 + (k+1)d > avail or !(gap - gain_k > 0), gain_0 = 0
         // (k <= (100 - q0) / d < 128: lanes hold k = lane + 32u)
         const double cur = row[0];
-        int k = -1;
+        int k = -1, kg = -1;
         double gain = 0.0;
+        const int ku = (100 - q0) / d;
+        // k* = min(kq, kg): kq = (avail - q0) / d, the first step the quota bound stops, and
+        // kg, the first step whose gain closes the gap — kg depends on the gap alone, so the
+        // commit recomputes k* from it in O(1) when only the headroom changed
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int kk = u * 32 + lane;
-          const bool in = kk > 0 && q0 + kk * d <= avail;
-          const double gk = in ? __dsub_rn(row[kk], cur) : 0.0;
-          const bool stop = q0 + (kk + 1) * d > avail || !(__dsub_rn(gap, gk) > 0.0);
+          const bool row_in = kk > 0 && kk <= ku;
+          const double gk = row_in ? __dsub_rn(row[kk], cur) : 0.0;
+          const bool closes = row_in && !(__dsub_rn(gap, gk) > 0.0);
+          const bool stop = q0 + (kk + 1) * d > avail || closes;
           const unsigned mask = __ballot_sync(0xffffffffu, stop);
           if (mask && k < 0) {
             const int l = __ffs(mask) - 1;
             k = u * 32 + l;
             gain = __shfl_sync(0xffffffffu, gk, l);
           }
+          const unsigned cm = __ballot_sync(0xffffffffu, closes);
+          if (cm && kg < 0) kg = u * 32 + __ffs(cm) - 1;
         }
         if (lane == 0) {
           w.spec_avail[f * kMaxPods + j] = avail;
           w.spec_k[f * kMaxPods + j] = k;
           w.spec_gain[f * kMaxPods + j] = gain;
+          w.spec_kg[f * kMaxPods + j] = kg < 0 ? ku + 1 : kg;
         }
         if (k > 0) gap = __dsub_rn(gap, gain);
         // a second walked pod on the same partition would see the first one's change
@@ -1014,7 +1024,7 @@ __device__ __forceinline__ Row4 bracket_row(const World& w, int f, int bref, int
 
 struct CommitPre {
   double gap0, sg0;
-  int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods, kd0;
+  int m, p0, st0, gpu0, q0, b0, s0, sav0, sk0, bref, brefok, npods, kd0, kg0;
   int nd, dkind, dquota, didle, stamp;
   int pos0;  // hint: position of the first pod's partition at tick start (-1: none)
   uint32_t uid0;
@@ -1420,6 +1430,7 @@ struct CommitT {
       r.sk0 = w.spec_k[f * kMaxPods];
       r.sg0 = w.spec_gain[f * kMaxPods];
       r.kd0 = w.row_kd[f * kMaxPods];
+      r.kg0 = w.spec_kg[f * kMaxPods];
       r.p0 = r.m > 0 ? w.sorted[f * kMaxPods] : -1;
     } else if (cls == kDown) {
       r.nd = w.ndown[f];
@@ -1471,6 +1482,7 @@ struct CommitT {
     r.brefok = __shfl_sync(0xffffffffu, x.brefok, src);
     r.npods = __shfl_sync(0xffffffffu, x.npods, src);
     r.kd0 = __shfl_sync(0xffffffffu, x.kd0, src);
+    r.kg0 = __shfl_sync(0xffffffffu, x.kg0, src);
     r.nd = __shfl_sync(0xffffffffu, x.nd, src);
     r.dkind = __shfl_sync(0xffffffffu, x.dkind, src);
     r.dquota = __shfl_sync(0xffffffffu, x.dquota, src);
@@ -1506,8 +1518,18 @@ struct CommitT {
       if (spec_ok && sav == avail) {
         kstar = j == 0 ? pre.sk0 : w.spec_k[f * kMaxPods + j];  // phase A's walk
         gain = j == 0 ? pre.sg0 : w.spec_gain[f * kMaxPods + j];
-      } else {
+      } else if (spec_ok) {
+        // only the headroom differs from phase A's (the gap is the one it assumed): the
+        // walk stops at min(kq, kg) — kq = (avail - q0) / d from the quota bound, kg the
+        // first gap-closing step phase A recorded (autoscaler.py:124-131)
         spec_ok = false;  // later pods start from a different gap: walk them here
+        const int kd = j == 0 ? pre.kd0 : w.row_kd[f * kMaxPods + j];
+        const double* row = j == 0 ? srow0 + kd : rows + j * kRow + kd;
+        const int kg = j == 0 ? pre.kg0 : w.spec_kg[f * kMaxPods + j];
+        const int kq = (avail - q0) / d;
+        kstar = kg < kq ? kg : kq;
+        if (kstar > 0) gain = __dsub_rn(row[kstar], row[0]);
+      } else {
         const int kd = j == 0 ? pre.kd0 : w.row_kd[f * kMaxPods + j];
         // row[k] = thr at q0 + k*d
         const double* row = j == 0 ? srow0 + kd : rows + j * kRow + kd;
@@ -2704,6 +2726,7 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if ((rc = dev_alloc(t.get(), &w.spec_avail, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_k, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.spec_gain, FP * kMaxPods))) return rc;
+  if ((rc = dev_alloc(t.get(), &w.spec_kg, FP * kMaxPods))) return rc;
   if ((rc = dev_alloc(t.get(), &w.fast, FP))) return rc;
   if ((rc = dev_alloc(t.get(), &w.tgrid, FP * 100 * 100))) return rc;
   if ((rc = dev_alloc(t.get(), &w.sm_mask, 4))) return rc;  // zeroed
