@@ -1041,13 +1041,33 @@ struct CommitT {
   uint64_t* sp;
   uint8_t* ovf;
   int ps;
-  int* nact;             // shared-memory action counter
+  int* nact;             // shared-memory action counter (initial / final value)
   int* serr;             // shared: an error was raised (checked between functions)
   int* snpods;           // shared copy of *w.n_pods for the whole commit
   long long* scounter;   // shared copy of *w.counter
   uint32_t* skey;        // shared argmin keys per GPU: npods > 0 ? occupancy << 18 | rank : ~0
                          // (null: scan the summaries)
   const uint32_t* smask;  // shared copy of w.sm_mask (the sm rows phase A2 tabulated)
+  // the action / pod / id counters in registers while the warp commits (every lane holds
+  // the same value: updates are warp-uniform), loaded from and stored back to the shared
+  // copies above by load_counters / store_counters
+  mutable int nact_r = 0, npods_r = 0;
+  mutable long long counter_r = 0;
+
+  __device__ void load_counters() const {
+    nact_r = *nact;
+    npods_r = *snpods;
+    counter_r = *scounter;
+  }
+  __device__ void store_counters() const {
+    __syncwarp();
+    if (lane == 0) {
+      *nact = nact_r;
+      *snpods = npods_r;
+      *scounter = counter_r;
+    }
+    __syncwarp();
+  }
 
   // lane-0 code: refresh GPU g's argmin key after its pod count / occupancy changed
   __device__ void rekey0(int g) const {
@@ -1074,33 +1094,38 @@ struct CommitT {
     }
   }
 
-  // position of the partition with this uid on GPU g (partition_of, core.py:148-158)
-  __device__ int find_part(int g, uint32_t uid) const {
-    const uint64_t* P = parts(g);
-    const int n = w.g_nparts[g];
+  // position of the partition with this uid in list P of n entries (partition_of,
+  // core.py:148-158)
+  __device__ int find_part_in(const uint64_t* P, int n, uint32_t uid) const {
     unsigned pos = 1u << 30;
     for (int i = lane; i < n; i += 32)
       if (part_uid(P[i]) == uid) pos = min(pos, unsigned(i));
     return int(__reduce_min_sync(0xffffffffu, pos));
   }
 
-  // find_part with a position hint (checked by one load of the hinted entry)
-  __device__ int find_part_hint(int g, uint32_t uid, int hint) const {
-    if (hint >= 0 && hint < w.g_nparts[g] && part_uid(parts(g)[hint]) == uid) return hint;
-    return find_part(g, uid);
+  __device__ int find_part(int g, uint32_t uid) const {
+    return find_part_in(parts(g), w.g_nparts[g], uid);
   }
 
-  __device__ void set_entry(int g, int pos, uint64_t e) const {
+  // find_part with a position hint (checked by one load of the hinted entry); P, n: the
+  // GPU's list, fetched once by the caller
+  __device__ int find_part_hint(const uint64_t* P, int n, uint32_t uid, int hint) const {
+    if (hint >= 0 && hint < n && part_uid(P[hint]) == uid) return hint;
+    return find_part_in(P, n, uid);
+  }
+
+  __device__ void set_entry(uint64_t* P, int pos, uint64_t e) const {
     __syncwarp();
-    if (lane == 0) parts(g)[pos] = e;
+    if (lane == 0) P[pos] = e;
     __syncwarp();
   }
 
-  // change_quota (allocator.py:111-125) + occupancy bookkeeping, partition position known
-  __device__ void change_quota_at(int p, int g, int pos, int s, int old_q, int new_q) const {
-    const uint64_t e = parts(g)[pos];
+  // change_quota (allocator.py:111-125) + occupancy bookkeeping, partition position known;
+  // P: GPU g's list, e: its entry at pos (as read by the caller)
+  __device__ void change_quota_at(uint64_t* P, uint64_t e, int p, int g, int pos, int s,
+                                  int old_q, int new_q) const {
     const int delta = new_q - old_q;
-    set_entry(g, pos, part_pack(part_sm(e), part_alloc(e) + delta, part_npods(e), part_uid(e)));
+    set_entry(P, pos, part_pack(part_sm(e), part_alloc(e) + delta, part_npods(e), part_uid(e)));
     if (lane == 0) {
       const int h1 = w.g_hgo[g] + s * delta;
       w.g_hgo[g] = h1;
@@ -1147,7 +1172,8 @@ struct CommitT {
 
   // place() right after best_slot(g) (nothing changed g's list since): the lanes still hold
   // the entries of a list of <= 32 partitions, so the join search is one ballot
-  __device__ void place_known(int p, int g, int s, int q, uint64_t e0, int n) const {
+  __device__ void place_known(int p, int g, int s, int q, uint64_t e0, int n,
+                              uint64_t* P) const {
     if (n > 32) {
       place(p, g, s, q);
       return;
@@ -1158,7 +1184,6 @@ struct CommitT {
     const uint64_t e = __shfl_sync(0xffffffffu, e0, pos < 0 ? 0 : pos);
     __syncwarp();  // every lane's reads of the list and the argmin keys precede the update
     if (lane == 0) {
-      uint64_t* P = parts(g);
       if (pos < 0) {
         if (n >= kPartCap || w.g_freesm[g] < s) {
           fail0(RAPP_E_PLACEMENT, -1);
@@ -1223,25 +1248,22 @@ struct CommitT {
   }
 
   __device__ void emit(int f, int kind, int b, int s, int q, int pod, int gpu, int rel) const {
-    if (lane == 0) {
-      const int i = (*nact)++;
-      w.actions[i] = rapp_action{f, kind, b, s, q, pod, gpu, rel};
-    }
-    __syncwarp();
+    const int i = nact_r++;
+    if (lane == 0) w.actions[i] = rapp_action{f, kind, b, s, q, pod, gpu, rel};
   }
 
   // new COLD_STARTING pod pod-%06d (sim.py:337-340, 505-516); nothing in this tick reads the
   // new pod's id string, so only its counter value is recorded here.
   // npods: the function's pod count (kept by the caller across its new pods).
   __device__ int new_pod(int f, int b, int s, int q, double now, int& npods) const {
-    int p = 0;
+    int p = npods_r++;
+    const bool full = p >= w.pod_cap || npods >= kMaxPods;
+    const long long c = full ? -1 : counter_r++;
+    if (full) p = -1;
     if (lane == 0) {
-      p = (*snpods)++;
-      if (p >= w.pod_cap || npods >= kMaxPods) {
+      if (full) {
         fail0(RAPP_E_ARG, f);
-        p = -1;
       } else {
-        const long long c = (*scounter)++;
         w.p_ctr[p] = c;  // the id string is formatted later (format_pending)
         w.p_fn[p] = f;
         w.p_b[p] = b;
@@ -1253,7 +1275,7 @@ struct CommitT {
         w.fn_npods[f] = npods + 1;
       }
     }
-    p = __shfl_sync(0xffffffffu, p, 0);
+    __syncwarp();
     if (p >= 0) ++npods;
     return p;
   }
@@ -1264,17 +1286,18 @@ struct CommitT {
     // occupancy <= 100*100 per GPU, so (occupancy, rank) packs into 32 bits for up to 2^18
     // GPUs: one scan and one warp min-reduction
     if (skey != nullptr) {  // maintained keys: one shared-memory word per GPU
-      // 8 independent loads per lane in flight (a plain strided loop waits on each)
+      // 16 independent loads per lane in flight: one shared-memory round trip for up to
+      // 512 GPUs (a plain strided loop waits on each)
       unsigned best = ~0u;
-      for (int g0 = 0; g0 < w.G; g0 += 256) {
-        unsigned k[8];
+      for (int g0 = 0; g0 < w.G; g0 += 512) {
+        unsigned k[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {
           const int g = g0 + u * 32 + lane;
           k[u] = g < w.G ? skey[g] : ~0u;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) best = min(best, k[u]);
+        for (int u = 0; u < 16; ++u) best = min(best, k[u]);
       }
       best = __reduce_min_sync(0xffffffffu, best);
       return best == ~0u ? -1 : int(best & ((1u << 18) - 1));
@@ -1313,8 +1336,8 @@ struct CommitT {
   // max_avail_quota_and_sm (allocator.py:26-52): max of (sm*hr, sm, join=1) over
   // partitions with headroom (first wins ties), then (free*100, free, 0) if strictly greater
   // e0 / n: this lane's entry of the list (lane < n) and the list length, for place_known
-  __device__ void best_slot(int g, int& sm, int& q, uint64_t& e0, int& n) const {
-    const uint64_t* P = parts(g);
+  __device__ void best_slot(int g, int& sm, int& q, uint64_t& e0, int& n, uint64_t*& P) const {
+    P = parts(g);
     n = w.g_nparts[g];
     const int free_sm = w.g_freesm[g];
     e0 = lane < n ? P[lane] : 0;
@@ -1508,9 +1531,13 @@ struct CommitT {
       const int p = j == 0 ? pre.p0 : srt[j];
       if ((j == 0 ? pre.st0 : w.p_state[p]) != kRunning) continue;
       const int g = j == 0 ? pre.gpu0 : w.p_gpu[p];
-      const int pos = j == 0 ? find_part_hint(g, pre.uid0, pre.pos0) : find_part(g, w.p_puid[p]);
+      uint64_t* const P = parts(g);
+      const int np = w.g_nparts[g];
+      const int pos = j == 0 ? find_part_hint(P, np, pre.uid0, pre.pos0)
+                             : find_part_in(P, np, w.p_puid[p]);
       const int q0 = j == 0 ? pre.q0 : w.p_q[p];
-      const int avail = q0 + (100 - part_alloc(parts(g)[pos]));
+      const uint64_t ent = P[pos];
+      const int avail = q0 + (100 - part_alloc(ent));
       TPROF_ACC(5);  // headroom lookup
       int kstar = -1;
       double gain = 0.0;
@@ -1566,7 +1593,7 @@ struct CommitT {
       if (kstar > 0) {
         const int nq = q0 + kstar * d;
         const int s = j == 0 ? pre.s0 : w.p_s[p];
-        change_quota_at(p, g, pos, s, q0, nq);
+        change_quota_at(P, ent, p, g, pos, s, q0, nq);
         emit(f, kVUp, j == 0 ? pre.b0 : w.p_b[p], s, nq, p, g, 0);
         gap = __dsub_rn(gap, gain);
       }
@@ -1588,7 +1615,8 @@ struct CommitT {
       if (g >= 0) {
         int sm, qmax, nl;
         uint64_t el;
-        best_slot(g, sm, qmax, el, nl);
+        uint64_t* Pl;
+        best_slot(g, sm, qmax, el, nl, Pl);
         TPROF_ACC(9);
         if (sm > 0 && qmax > 0) {
           if (!pre.brefok) {
@@ -1643,7 +1671,7 @@ struct CommitT {
             const int p = new_pod(f, bref, sm, quota, now, npods);
             TPROF_ACC(11);  // new_pod
             if (p < 0) return;
-            place_known(p, g, sm, quota, el, nl);
+            place_known(p, g, sm, quota, el, nl, Pl);
             TPROF_ACC(12);  // place
             emit(f, kHUp, bref, sm, quota, p, g, 0);
             TPROF_ACC(13);  // emit
@@ -1796,7 +1824,7 @@ struct CommitT {
     }
     const unsigned b1 = __ballot_sync(0xffffffffu, mine && cnt >= 1);
     const unsigned b2 = __ballot_sync(0xffffffffu, mine && cnt >= 2);
-    const int at0 = *nact;
+    const int at0 = nact_r;
     __syncwarp();  // every lane's reductions are done
     if (mine) {
       int at = at0 + __popc(b1 & ((1u << lane) - 1)) + __popc(b2 & ((1u << lane) - 1));
@@ -1813,8 +1841,7 @@ struct CommitT {
         }
       if (stamp && kind == kFastDown) w.last_down[f] = now;
     }
-    __syncwarp();
-    if (lane == 0) *nact = at0 + __popc(b1) + __popc(b2);
+    nact_r = at0 + __popc(b1) + __popc(b2);
     __syncwarp();
     return run;
   }
@@ -1849,8 +1876,10 @@ struct CommitT {
         idle = w.p_idle[p];
       }
       if (kind == kVDown) {
-        change_quota_at(p, g, i == 0 ? find_part_hint(g, uid, pre.pos0) : find_part(g, uid), s, q,
-                        quota);
+        uint64_t* const P = parts(g);
+        const int np = w.g_nparts[g];
+        const int pos = i == 0 ? find_part_hint(P, np, uid, pre.pos0) : find_part_in(P, np, uid);
+        change_quota_at(P, P[pos], p, g, pos, s, q, quota);
         emit(f, kVDown, b, s, quota, p, g, 0);
       } else {
         if (lane == 0) w.p_state[p] = kDraining;
@@ -2003,6 +2032,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   if (lane < 4) s_smask[lane] = w.sm_mask[lane];
   __syncwarp();
   CommitT<kMasked> c{v, lane, sp, ovf, ps, &s_nact, &s_err, &s_npods, &s_counter, skey, s_smask};
+  c.load_counters();
   bool stop = s_err != 0;
 #ifdef RAPP_TICK_PROF
   s_tprof[lane] = 0;
@@ -2117,6 +2147,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
   if (lane == 0) s_stop = 1;  // release the helper if the commit stopped early
   // no bulk copy may still be in flight into shared memory when the CTA exits
   for (int k = j; k < staged; ++k) tk_bar_wait(&s_rbar[k & 1], (k >> 1) & 1);
+  c.store_counters();
   if (lane == 0) {
     *w.n_pods = s_npods;
     *w.counter = s_counter;
@@ -2158,10 +2189,15 @@ __global__ void __launch_bounds__(32) k_tick_release(World w, const int32_t* __r
   __shared__ int s_nact, s_err, s_npods;
   __shared__ long long s_counter;
   const int lane = threadIdx.x & 31;
-  if (lane == 0) s_err = 0;
+  if (lane == 0) {
+    s_err = 0;
+    s_nact = s_npods = 0;  // releases create no actions or pods
+    s_counter = 0;
+  }
   __syncwarp();
   CommitT<false> c{w, lane, nullptr, rel_ovf, 0, &s_nact, &s_err, &s_npods, &s_counter, nullptr,
            nullptr};
+  c.load_counters();
   for (int i = 0; i < n; ++i) {
     const int p = list[i];
     if (w.p_state[p] == kDead) continue;
