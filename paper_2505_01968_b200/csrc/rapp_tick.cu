@@ -1075,6 +1075,11 @@ struct CommitT {
       skey[g] = w.g_npods[g] > 0 ? (uint32_t(w.g_hgo[g]) << 18) | uint32_t(g) : ~0u;
   }
 
+  // x / delta for 0 <= x <= 100 (delta is 1 on the full grid: no integer division there)
+  __device__ __forceinline__ int div_d(int x) const {
+    return w.delta == 1 ? x : x / w.delta;
+  }
+
   __device__ uint64_t* parts(int g) const {
     return ovf[g] ? w.g_parts + int64_t(g) * kPartCap : sp + int64_t(g) * ps;
   }
@@ -1553,7 +1558,7 @@ struct CommitT {
         const int kd = j == 0 ? pre.kd0 : w.row_kd[f * kMaxPods + j];
         const double* row = j == 0 ? srow0 + kd : rows + j * kRow + kd;
         const int kg = j == 0 ? pre.kg0 : w.spec_kg[f * kMaxPods + j];
-        const int kq = (avail - q0) / d;
+        const int kq = div_d(avail - q0);
         kstar = kg < kq ? kg : kq;
         if (kstar > 0) gain = __dsub_rn(row[kstar], row[0]);
       } else {
@@ -1613,6 +1618,26 @@ struct CommitT {
       const int g = argmin_used();
       TPROF_ACC(8);
       if (g >= 0) {
+        // The slot is usually a new partition on g's unallocated share (its sm * 100 beats
+        // every join): that throughput row is requested now, while best_slot runs, and
+        // used when best_slot agrees.  Every step's value is loaded (steps past qmax are
+        // never read).
+        double tv[4];
+        int tv_sm = 0;
+#ifdef RAPP_TICK_TSPEC  // measured: +-2% (tools/ab_tickprof.sh), off
+        if (pre.brefok) {
+          const int fs = w.g_freesm[g];
+          if (fs > 0 && (!kMasked || ((smask[(fs - 1) >> 5] >> ((fs - 1) & 31)) & 1u))) {
+            const double* T = w.tgrid + (int64_t(f) * 100 + (fs - 1)) * 100;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int qq = (u * 32 + lane + 1) * d;
+              tv[u] = qq <= 100 ? T[qq - 1] : 0.0;
+            }
+            tv_sm = fs;
+          }
+        }
+#endif
         int sm, qmax, nl;
         uint64_t el;
         uint64_t* Pl;
@@ -1627,8 +1652,9 @@ struct CommitT {
           // every throughput the branch may read, in one round of independent loads:
           // lanes hold the quota steps (u*32 + lane + 1)*d <= qmax, u < 4 (d >= 1) —
           // from phase A2's grid when it tabulated this sm, else evaluated here
-          double tv[4];
-          if (!kMasked || ((smask[(sm - 1) >> 5] >> ((sm - 1) & 31)) & 1u)) {
+          if (sm == tv_sm) {
+            // prefetched above
+          } else if (!kMasked || ((smask[(sm - 1) >> 5] >> ((sm - 1) & 31)) & 1u)) {
             const double* T = w.tgrid + (int64_t(f) * 100 + (sm - 1)) * 100;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1641,8 +1667,9 @@ struct CommitT {
             for (int u = 0; u < 4; ++u) tv[u] = r.v[u];
           }
           double cmax;
-          if (qmax % d == 0) {
-            const int kq = qmax / d - 1;  // the step index of qmax
+          const int qd = div_d(qmax);
+          if (qd * d == qmax) {
+            const int kq = qd - 1;  // the step index of qmax
             cmax = __shfl_sync(0xffffffffu, tv[0], kq & 31);
             if (kq >= 32) cmax = __shfl_sync(0xffffffffu, tv[1], kq & 31);
             if (kq >= 64) cmax = __shfl_sync(0xffffffffu, tv[2], kq & 31);
