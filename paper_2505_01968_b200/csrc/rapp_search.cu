@@ -323,6 +323,30 @@ __global__ void __launch_bounds__(kSearchThreads)
     // first in lattice order); each run needs one new row value.  kK3Pairs (s, q) pairs per
     // thread share the run bookkeeping and every (tb, threshold) load.
     const int last = nb - 1;
+    // pair index -> (sm index, quota index) without an integer division: the float quotient
+    // is off by at most one for pairs < 2^24, and the remainder test corrects it
+    const float inv_nq = 1.0f / float(nQ);
+    auto split = [&](int pu, int& s, int& q) {
+      int a = int((float(pu) + 0.5f) * inv_nq);
+      int r = pu - a * nQ;
+      if (r < 0) { --a; r += nQ; } else if (r >= nQ) { ++a; r -= nQ; }
+      s = a;
+      q = r;
+    };
+    // table rows: shared-memory tables are read with 32-bit shared addresses (one LDS per
+    // corner, the row offset added once per run), global ones through pointers
+    using RowRef = typename std::conditional<SMEM, uint32_t, const double*>::type;
+    const uint32_t v_sh = SMEM ? (uint32_t)__cvta_generic_to_shared(v) : 0u;
+    const uint32_t row_bytes = uint32_t(row_stride) * 8u;
+    auto corner = [&](RowRef r, int64_t row) -> double {
+      if constexpr (SMEM) {
+        double x;
+        asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(r + uint32_t(row) * row_bytes));
+        return x;
+      } else {
+        return r[row * row_stride];
+      }
+    };
     // pairs pa, pa + bd, ..., pa + (NP - 1) * bd (all < p1)
     auto fast = [&](int pa, auto np_tag) {
       constexpr int NP = decltype(np_tag)::value;
@@ -330,9 +354,7 @@ __global__ void __launch_bounds__(kSearchThreads)
       bool node = true;
 #pragma unroll
       for (int u = 0; u < NP; ++u) {
-        const int pu = pa + u * bd;
-        si[u] = pu / nQ;
-        qi[u] = pu - si[u] * nQ;
+        split(pa + u * bd, si[u], qi[u]);
         const int2 j = sJ[si[u]];
         node = node && j.x == j.y;
       }
@@ -341,16 +363,20 @@ __global__ void __launch_bounds__(kSearchThreads)
         for (int u = 0; u < NP; ++u) record(si[u], qi[u], generic_pair(si[u], qi[u]));
         return;
       }
-      const double* __restrict__ r0[NP];
-      const double* __restrict__ r1[NP];
+      RowRef r0[NP], r1[NP];
       double tq[NP], cu[NP], c0[NP], d[NP];
       int fnd[NP];
 #pragma unroll
       for (int u = 0; u < NP; ++u) {
         const int js = sJ[si[u]].x;
         const int2 k = sK[qi[u]];
-        r0[u] = v + (js * nq + k.x);
-        r1[u] = v + (js * nq + k.y);
+        if constexpr (SMEM) {
+          r0[u] = v_sh + uint32_t(js * nq + k.x) * 8u;
+          r1[u] = v_sh + uint32_t(js * nq + k.y) * 8u;
+        } else {
+          r0[u] = v + (js * nq + k.x);
+          r1[u] = v + (js * nq + k.y);
+        }
         tq[u] = sTq[qi[u]];
         cu[u] = 0.0;
         fnd[u] = 1 << 30;
@@ -358,15 +384,14 @@ __global__ void __launch_bounds__(kSearchThreads)
       int up = -2;
       for (int sg = nlo - 1; sg >= 0; --sg) {
         const int4 S = sLo[sg];
-        const int64_t o = int64_t(S.x) * row_stride;
         const bool top = S.x == last, reuse = S.x + 1 == up;
 #pragma unroll
         for (int u = 0; u < NP; ++u) {
-          c0[u] = lerp_rn(r0[u][o], r1[u][o], tq[u]);
+          c0[u] = lerp_rn(corner(r0[u], S.x), corner(r1[u], S.x), tq[u]);
           d[u] = 0.0;
           if (!top) {
-            const double c1 = reuse ? cu[u] : lerp_rn(r0[u][o + row_stride],
-                                                      r1[u][o + row_stride], tq[u]);
+            const double c1 = reuse ? cu[u] : lerp_rn(corner(r0[u], S.x + 1),
+                                                      corner(r1[u], S.x + 1), tq[u]);
             d[u] = __dsub_rn(c1, c0[u]);
           }
           cu[u] = c0[u];

@@ -1,6 +1,2 @@
-timeout 900 python -m pytest tests/test_tick_gpu.py -q -x 2>&1 | tail -2
-RAPP_LIB=build_variants/prof.so timeout 300 python tools/tick_commit_breakdown.py --full-grid 2>&1 | tail -12 | head -4
-for i in 1 2; do
-echo "== new full"; TICKS=40 timeout 300 python tools/tick_profile.py --full-grid 2>&1 | python tools/tick_summary.py
-echo "== prev full"; RAPP_LIB=build_variants/prev.so TICKS=40 timeout 300 python tools/tick_profile.py --full-grid 2>&1 | python tools/tick_summary.py
-done
+timeout 600 python -m pytest tests/test_interp_gpu.py tests/test_config1.py -x -q 2>&1 | tail -2 > gpurun_out/r2s3_ab_k2.txt
+bash tools/ab_stream.sh k2_r1 k2_r2 k2_r2_sus k2_r1_sus k2_r2_s3 >> gpurun_out/r2s3_ab_k2.txt 2>&1
