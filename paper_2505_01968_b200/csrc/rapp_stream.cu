@@ -294,11 +294,25 @@ __device__ __forceinline__ void load_row(const double* p, bool smem, double& v0,
 #ifndef RAPP_STREAM_CONSUMERS
 #define RAPP_STREAM_CONSUMERS 16
 #endif
+#ifndef RAPP_STREAM_ROWS
+#define RAPP_STREAM_ROWS 1  // 2 rows per lane (3 stages): same speed, measured
+#endif
+#ifndef RAPP_STREAM_STAGES
+#define RAPP_STREAM_STAGES 4
+#endif
+#ifndef RAPP_STREAM_SUSPEND_NS
+#define RAPP_STREAM_SUSPEND_NS 0
+#endif
 constexpr int kConsumers = RAPP_STREAM_CONSUMERS;  // consumer warps per CTA
 constexpr int kProducer = kConsumers;              // warp index of the TMA producer
 constexpr int kFastThreads = (kConsumers + 1) * 32;
-constexpr int kTile = kConsumers * 32;  // rows per TMA stage: one per consumer lane
-constexpr int kStages = 4;
+// rows per consumer lane per stage: each full/empty barrier round trip (and its
+// shared-memory polls) is paid once per kRows rows.  Measured on config 2: 2 rows x 3
+// stages runs at the speed of 1 row x 4 stages (0.394 ms per 5e7 queries), 2 x 4 stages is
+// 14% slower (one CTA per SM), a try_wait suspend-time hint changes nothing.
+constexpr int kRows = RAPP_STREAM_ROWS;
+constexpr int kTile = kConsumers * 32 * kRows;  // rows per TMA stage
+constexpr int kStages = RAPP_STREAM_STAGES;
 
 // One row per lane (row index i, coordinates x0..x2); see the header comment, item 4.
 template <int MB, int MS, int MQ, bool CELLS_SMEM>
@@ -352,12 +366,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
   uint32_t done = 0;
   while (!done) {
+#if RAPP_STREAM_SUSPEND_NS > 0
+    // suspend-time hint: the warp sleeps in the barrier until the phase completes (or the
+    // hint expires) instead of re-polling it through the shared-memory pipe
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(sbar), "r"(parity), "n"(RAPP_STREAM_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(sbar), "r"(parity)
         : "memory");
+#endif
   }
 }
 
@@ -419,15 +444,26 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
   for (int j = 0; t < n_tiles; ++j, t += gridDim.x) {
     const int s = j % kStages;
     mbar_wait(&full[s], (j / kStages) & 1);
-    const double* row = buf0 + s * 3 * kTile + 3 * (warp * 32 + lane);
-    const double xb = row[0], xs = row[1], xq = row[2];
+    // this warp's kRows x 32 rows of the stage, row r of lane l at (r * kConsumers + warp)
+    // * 32 + l: each LDS.64 and each output store stays a contiguous 32-row slice
+    double x[kRows][3];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const double* row = buf0 + s * 3 * kTile + 3 * ((r * kConsumers + warp) * 32 + lane);
+      x[r][0] = row[0];
+      x[r][1] = row[1];
+      x[r][2] = row[2];
+    }
     // The next TMA write into this stage is an async-proxy access; order our generic-proxy
     // reads before it (WAR across proxies), then release the stage.
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are in registers
-    interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq,
-                                       t * kTile + warp * 32 + lane, n, out, rps);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+      interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x[r][0], x[r][1], x[r][2],
+                                         t * kTile + (r * kConsumers + warp) * 32 + lane, n,
+                                         out, rps);
   }
   // remainder rows: direct loads, warp-uniform grid-stride (every lane shuffles)
   const int64_t warps_total = int64_t(gridDim.x) * kConsumers;
