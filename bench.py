@@ -356,6 +356,27 @@ def gen_queries(b, s, q, n, seed, device):
     return c
 
 
+def transfer_ceiling(h_in, h_out, dev, reps=3):
+    """Queries/s the PCIe link sustains for the e2e stream's copies alone: h_in (n, 3)
+    float64 host->device and h_out (n,) float64 device->host, pinned, on two streams."""
+    import torch
+    d_in = torch.empty(h_in.shape, dtype=h_in.dtype, device=dev)
+    d_out = torch.empty(h_out.shape, dtype=h_out.dtype, device=dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = float("inf")
+    for _ in range(reps + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            h_out.copy_(d_out, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        best = min(best, time.perf_counter() - t0)
+    del d_in, d_out
+    return h_in.shape[0] / best
+
+
 def run_stream(args, rank, world, local):
     import torch
     from paper_2505_01968_b200 import PerfTable, _lib, kernels
@@ -432,6 +453,13 @@ def run_stream(args, rank, world, local):
         e2e = {"value": world * e2e_preds * e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": e2e_preds * 24, "d2h_bytes_per_step": e2e_preds * 8,
                "steps": e2e_steps, "api": "kernels.interp3_many, pinned host buffers"}
+        # the link's own ceiling for this traffic: the same bytes moved by bare copies
+        # (24 B/query in and 8 B/query out on two streams, both directions at once)
+        link = transfer_ceiling(hc[0], ho[0], dev)
+        e2e["link"] = {"preds_per_s": round(world * link, 1), "unit": UNIT,
+                       "frac": round(e2e["value"] / (world * link), 4),
+                       "what": "cudaMemcpyAsync H2D 24 B + D2H 8 B per query, pinned, "
+                               "concurrent on two streams (no kernel)"}
 
     peak, peak_kind = load_peak()
     alg_bytes = 32.0 * n  # 24 B coords read + 8 B latency written per prediction

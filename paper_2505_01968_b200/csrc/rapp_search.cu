@@ -521,7 +521,10 @@ static int run_plan(rapp_mec_plan* pl, const double* d_targets, int64_t f0, int6
                                               pl->d_thr, pl->d_minlat, pl->d_key, pl->d_slo);
   RAPP_LAUNCHED();
   // enough CTAs to fill the machine even for a handful of functions
-  int chunks = (int)((4LL * c->sm_count + nf - 1) / nf);
+#ifndef RAPP_K3_CTAS_PER_SM
+#define RAPP_K3_CTAS_PER_SM 4
+#endif
+  int chunks = (int)((int64_t(RAPP_K3_CTAS_PER_SM) * c->sm_count + nf - 1) / nf);
   const int max_chunks = (pl->max_pairs + kSearchThreads - 1) / kSearchThreads;
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
