@@ -48,6 +48,8 @@
 namespace rapp {
 
 constexpr int kMaxPods = 128;  // pods per managed function (RAPP_E_ARG beyond)
+constexpr int kMaxGpus = 1 << 18;  // GPUs per world (rank field of the argmin keys)
+constexpr int kMaxFns = 1 << 20;   // managed functions per world
 constexpr int kPartCap = 100;  // partitions per GPU (each >= 1 SM%, sum <= 100)
 constexpr int kRow = 101;      // quota steps per pod row
 constexpr int kCold = 0, kRunning = 1, kDraining = 2, kDead = -1;
@@ -1678,6 +1680,16 @@ struct CommitT {
             cmax = lane == 0 ? thr_at(w, f, double(bref), double(sm), double(qmax)) : 0.0;
             cmax = __shfl_sync(0xffffffffu, cmax, 0);
           }
+#ifdef RAPP_TICK_PROF
+          // diagnostics: the row read's own latency (cmax depends on it), how often the slot
+          // is a new partition on the GPU's unallocated share, and the step count
+          if (lane == 0) {
+            s_tprof[22] += (unsigned long long)((long long)clock64() - _tp0) *
+                           (unsigned long long)(cmax == cmax);
+            s_tprof[23] += sm == w.g_freesm[g] && qmax == 100;
+            s_tprof[24] += 1;
+          }
+#endif
           if (cmax > gap) {
             // _covering_quota (autoscaler.py:168-175): first multiple of d <= qmax with
             // throughput >= gap, else qmax
@@ -2547,6 +2559,14 @@ int rapp_tick_create(rapp_ctx* ctx, const rapp_scaler_config* cfg, int64_t n_fns
   if (cfg->delta_iq < 1 || cfg->delta_iq > 100) {
     set_error("delta_iq %d outside [1, 100]", cfg->delta_iq);
     return RAPP_E_VALUE;
+  }
+  // world sizes the device layout supports: GPU ranks in 18-bit argmin keys, functions and
+  // pods in int32 indices ([F][kMaxPods] tables)
+  if (n_gpus > kMaxGpus || n_fns > kMaxFns || n_pods > int64_t(kMaxFns) * kMaxPods) {
+    set_error("world of %lld functions / %lld GPUs / %lld pods exceeds the tick's limits "
+              "(%d functions, %d GPUs, %d pods per function)", (long long)n_fns,
+              (long long)n_gpus, (long long)n_pods, kMaxFns, kMaxGpus, kMaxPods);
+    return RAPP_E_ARG;
   }
   std::lock_guard<std::mutex> lk(ctx->mu);
   RAPP_CUDA(cudaSetDevice(ctx->device));

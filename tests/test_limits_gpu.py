@@ -96,3 +96,22 @@ def test_lattice_search_key_limits():
     huge = _table(sms=[50, 1 << 24], quotas=[50, 100])  # s*q would overflow the cost field
     with pytest.raises(DeviceError, match="2\\^24"):
         PerfTableSet([(huge, [8])], quota_step=50)
+
+
+def test_tick_world_size_limits_at_the_c_abi():
+    """rapp_tick_create refuses worlds beyond its index widths (2^18 GPUs: the rank field of
+    the packed argmin keys; 2^20 functions) before touching any input array."""
+    import ctypes
+    from paper_2505_01968_b200 import _lib
+    from paper_2505_01968_b200.errors import DeviceError
+    from paper_2505_01968_b200.tick import ScalerConfigC
+    lib = _lib.load()
+    ctx = _lib.Context.get(0)
+    cfg = ScalerConfigC(0.9, 0.5, 1000.0, 1.0, 10, 0, 2.0, 5000.0, 1.0, 4.0, 1.0, 16.0, 1.0,
+                        0, 0)
+    h = _lib.c_vp()
+    for n_fns, n_gpus in (((1 << 20) + 1, 1), (1, (1 << 18) + 1)):
+        rc = lib.rapp_tick_create(ctx.handle, ctypes.byref(cfg), n_fns, None, None, n_gpus,
+                                  None, None, None, 0, None, 0, ctypes.byref(h))
+        with pytest.raises(DeviceError, match="exceeds the tick's limits"):
+            _lib.check(rc, "TickEngine")

@@ -1,1 +1,1 @@
-bash tools/ab_lattice.sh k3_c4 k3_c32 k3_c64 > gpurun_out/r2s3_ab_k3c.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2s3_gputest3.log 2>&1; echo "pytest exit $?" >> gpurun_out/r2s3_gputest3.log
