@@ -1607,6 +1607,12 @@ struct CommitT {
       TPROF_ACC(7);  // change_quota + emit
     }
     TPROF_ACC(1);
+#ifdef RAPP_TICK_PROF
+    if (lane == 0) {
+      s_tprof[25] += 1;          // generic scale-up commits
+      s_tprof[26] += gap > 0.0;  // ... that go on to the horizontal branch
+    }
+#endif
     scale_up_h(f, now, pre, gap, npods);
   }
 
@@ -2153,6 +2159,9 @@ __global__ void __launch_bounds__(kCommitThreads) k_tick_commit(World w, double 
           const unsigned tl = done & tailm;  // the run's last lane, walk applied
           if (tl) {
             const int k = __ffs(tl) - 1;
+#ifdef RAPP_TICK_PROF
+            if (lane == 0) s_tprof[27] += 1;  // straight-line walks ending in the horizontal branch
+#endif
             c.scale_up_h(base + k, now, s_pre[slot][k], s_fast[slot][k].gap, s_pre[slot][k].npods);
             __syncwarp();
             if (s_err) {

@@ -20,8 +20,9 @@ NAMES = ["batch wait", "vertical spec/walk", "used-GPU rest", "fresh-GPU branch"
          "scale-down", "vertical headroom", "functions (wall)", "vertical change+emit",
          "hu argmin", "hu best_slot", "hu T+covering", "hu new_pod", "hu place", "hu emit",
          "fast lanes", "fast candidates", "fast_run", "fast_run calls", "-", "runs committed",
-         "prologue", "epilogue", "hu T row read", "hu new-partition slots", "hu steps"]
-COUNTS = (14, 15, 17, 19, 23, 24)
+         "prologue", "epilogue", "hu T row read", "hu new-partition slots", "hu steps", "generic ups",
+         "generic ups to horizontal", "tail horizontals"]
+COUNTS = (14, 15, 17, 19, 23, 24, 25, 26, 27)
 
 
 def main(full_grid, nticks=6):
