@@ -351,45 +351,6 @@ __device__ __forceinline__ void interp_row(const FastAxis& ab, const FastAxis& a
   }
 }
 
-#ifndef RAPP_STREAM_DUAL
-#define RAPP_STREAM_DUAL 0
-#endif
-// Dual variant: both lanes of a pair read BOTH rows' coordinates (three 16-byte shared loads
-// of the pair's 48 bytes; the two lanes hit the same addresses, so it costs the same
-// wavefronts as one row each) and locate both queries, so nothing but the finished batch
-// rows crosses the pair: 2 shuffles per query instead of 7.  Row q of the pair is owned by
-// lane 2p + q; lane h keeps batch row h of both cells.
-template <int MB, int MS, int MQ, bool CELLS_SMEM>
-__device__ __forceinline__ void interp_pair(const FastAxis& ab, const FastAxis& as,
-                                            const FastAxis& aq, const double* cells, int CS,
-                                            int CQ, const double (&x)[6], int64_t i, int64_t n,
-                                            double* __restrict__ out,
-                                            double* __restrict__ rps) {
-  const int half = threadIdx.x & 1;
-  int ib0, js0, kq0, ib1, js1, kq1;
-  double tb0, ts0, tq0, tb1, ts1, tq1;
-  locate_fast<MB>(ab, x[0], ib0, tb0);
-  locate_fast<MS>(as, x[1], js0, ts0);
-  locate_fast<MQ>(aq, x[2], kq0, tq0);
-  locate_fast<MB>(ab, x[3], ib1, tb1);
-  locate_fast<MS>(as, x[4], js1, ts1);
-  locate_fast<MQ>(aq, x[5], kq1, tq1);
-  const int c0 = (ib0 * CS + js0) * CQ + kq0, c1 = (ib1 * CS + js1) * CQ + kq1;
-  double v[2][4];
-  load_row(cells + int64_t(c0) * 8 + half * 4, CELLS_SMEM, v[0][0], v[0][1], v[0][2], v[0][3]);
-  load_row(cells + int64_t(c1) * 8 + half * 4, CELLS_SMEM, v[1][0], v[1][1], v[1][2], v[1][3]);
-  const double r0 = lerp_rn(lerp_rn(v[0][0], v[0][1], tq0), lerp_rn(v[0][2], v[0][3], tq0), ts0);
-  const double r1 = lerp_rn(lerp_rn(v[1][0], v[1][1], tq1), lerp_rn(v[1][2], v[1][3], tq1), ts1);
-  const double mine = half ? r1 : r0;    // row h of my query
-  const double theirs = half ? r0 : r1;  // row h of my partner's query
-  const double other = __shfl_xor_sync(0xffffffffu, theirs, 1);  // row 1-h of my query
-  const double lat = half ? lerp_rn(other, mine, tb1) : lerp_rn(mine, other, tb0);
-  if (i < n) {
-    __stcs(out + i, lat);
-    if (rps != nullptr) __stcs(rps + i, throughput(half ? x[3] : x[0], lat));
-  }
-}
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
       (uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
@@ -485,17 +446,6 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     mbar_wait(&full[s], (j / kStages) & 1);
     // this warp's kRows x 32 rows of the stage, row r of lane l at (r * kConsumers + warp)
     // * 32 + l: each LDS.64 and each output store stays a contiguous 32-row slice
-#if RAPP_STREAM_DUAL
-    double x[kRows][6];
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const double2* pr = reinterpret_cast<const double2*>(
-          buf0 + s * 3 * kTile + 3 * ((r * kConsumers + warp) * 32 + (lane & ~1)));
-      const double2 a = pr[0], b = pr[1], c = pr[2];
-      x[r][0] = a.x; x[r][1] = a.y; x[r][2] = b.x;
-      x[r][3] = b.y; x[r][4] = c.x; x[r][5] = c.y;
-    }
-#else
     double x[kRows][3];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
@@ -504,7 +454,6 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
       x[r][1] = row[1];
       x[r][2] = row[2];
     }
-#endif
     // The next TMA write into this stage is an async-proxy access; order our generic-proxy
     // reads before it (WAR across proxies), then release the stage.
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -512,15 +461,9 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp's rows are in registers
 #pragma unroll
     for (int r = 0; r < kRows; ++r)
-#if RAPP_STREAM_DUAL
-      interp_pair<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x[r],
-                                          t * kTile + (r * kConsumers + warp) * 32 + lane, n,
-                                          out, rps);
-#else
       interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x[r][0], x[r][1], x[r][2],
                                          t * kTile + (r * kConsumers + warp) * 32 + lane, n,
                                          out, rps);
-#endif
   }
   // remainder rows: direct loads, warp-uniform grid-stride (every lane shuffles)
   const int64_t warps_total = int64_t(gridDim.x) * kConsumers;
