@@ -495,6 +495,7 @@ int rapp_interp3_many_dev(rapp_ctx* ctx, int32_t table_id, const double* d_coord
 
 int rapp_interp3_many_host(rapp_ctx* ctx, int32_t table_id, const double* coords, int64_t n,
                            double* out) {
+  RAPP_RANGE("rapp_interp3_many_host");
   if (!ctx) {
     set_error("null context");
     return RAPP_E_ARG;
@@ -658,6 +659,7 @@ int rapp_interp3(const double* b_axis, int64_t nb, const double* s_axis, int64_t
 int rapp_interp3_many(const double* b_axis, int64_t nb, const double* s_axis, int64_t ns,
                       const double* q_axis, int64_t nq, const double* values,
                       const double* coords, int64_t n, double* out) {
+  RAPP_RANGE("rapp_interp3_many");
   rapp_ctx* ctx = nullptr;
   int rc = default_ctx(&ctx);
   if (rc) return rc;

@@ -316,6 +316,7 @@ int rapp_csv_parse(const char* buf, int64_t len, int64_t cap, int64_t* batch, in
 
 int rapp_ingest_create(rapp_ctx* ctx, int64_t n, const int64_t* batch, const int64_t* sm,
                        const int64_t* quota, const double* lat, rapp_ingest** out) {
+  RAPP_RANGE("rapp_ingest_create");
   if (!ctx || !out || n < 1 || !batch || !sm || !quota || !lat) {
     set_error("null argument or empty sample set");
     return RAPP_E_ARG;

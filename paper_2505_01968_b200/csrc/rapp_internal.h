@@ -13,6 +13,33 @@
 
 #include "../../include/rapp_b200.h"
 
+// NVTX ranges around the host entry points and the phases of a host tick (header-only
+// NVTX3: a push/pop is a couple of branches when no profiler is attached; nsys / ncu
+// --nvtx show them).  RAPP_NVTX=0 compiles them out.
+#ifndef RAPP_NVTX
+#define RAPP_NVTX 1
+#endif
+#if RAPP_NVTX
+#include <nvtx3/nvToolsExt.h>
+namespace rapp {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace rapp
+#define RAPP_NVTX_CAT2(a, b) a##b
+#define RAPP_NVTX_CAT(a, b) RAPP_NVTX_CAT2(a, b)
+#define RAPP_RANGE(name) ::rapp::NvtxRange RAPP_NVTX_CAT(rapp_nvtx_, __LINE__)(name)
+#define RAPP_MARK_PUSH(name) nvtxRangePushA(name)
+#define RAPP_MARK_POP() nvtxRangePop()
+#else
+#define RAPP_RANGE(name) (void)0
+#define RAPP_MARK_PUSH(name) (void)0
+#define RAPP_MARK_POP() (void)0
+#endif
+
 namespace rapp {
 
 #ifndef RAPP_PDL

@@ -637,6 +637,7 @@ int rapp_mlp_predict_dev(rapp_mlp* m, int32_t model, const double* d_coords, int
 
 int rapp_mlp_predict_host(rapp_mlp* m, int32_t model, const double* coords, int64_t n,
                           double* out) {
+  RAPP_RANGE("rapp_mlp_predict_host");
   if (!m || model < 0 || model >= m->n_models || n < 0 || (n > 0 && (!coords || !out))) {
     set_error("bad mlp handle, model id or buffers");
     return RAPP_E_ARG;

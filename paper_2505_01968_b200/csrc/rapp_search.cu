@@ -738,6 +738,7 @@ int rapp_mec_plan_kernel_time(rapp_mec_plan* pl, double* total_ms, int64_t* laun
 int rapp_mec_plan_run_dev(rapp_mec_plan* pl, const double* d_targets, int64_t fn_begin,
                           int64_t fn_end, int32_t* d_out_bsq, uint64_t* d_out_key,
                           void* stream) {
+  RAPP_RANGE("rapp_mec_plan_run_dev");
   if (!pl || fn_begin < 0 || fn_end > pl->nfn || fn_begin > fn_end) {
     set_error("bad plan or function range");
     return RAPP_E_ARG;
@@ -748,6 +749,7 @@ int rapp_mec_plan_run_dev(rapp_mec_plan* pl, const double* d_targets, int64_t fn
 
 int rapp_mec_plan_run(rapp_mec_plan* pl, const double* targets, int64_t fn_begin, int64_t fn_end,
                       int64_t* out_bsq) {
+  RAPP_RANGE("rapp_mec_plan_run");
   if (!pl || fn_begin < 0 || fn_end > pl->nfn || fn_begin > fn_end ||
       (fn_end > fn_begin && (!targets || !out_bsq))) {
     set_error("bad plan run arguments");

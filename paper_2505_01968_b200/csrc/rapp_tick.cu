@@ -2925,6 +2925,7 @@ static int tick_error(rapp_tick* t) {
 }
 
 int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
+  RAPP_RANGE("rapp_tick_release");
   if (!t || n < 0 || (n > 0 && !pods)) {
     set_error("null argument");
     return RAPP_E_ARG;
@@ -2968,6 +2969,7 @@ int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
 
 int rapp_tick_run_dev(rapp_tick* t, double now_ms, const int64_t* d_arrivals,
                       const uint8_t* d_idle, void* stream) {
+  RAPP_RANGE("rapp_tick_run_dev");
   if (!t) {
     set_error("null tick");
     return RAPP_E_ARG;
@@ -3002,6 +3004,7 @@ int rapp_tick_outputs_dev(rapp_tick* t, const rapp_action** a, const int32_t** c
 int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const uint8_t* idle,
                   const double* predicted_in, rapp_action* actions, int64_t max_actions,
                   int64_t* n_actions, double* observed_out, double* predicted_out) {
+  RAPP_RANGE("rapp_tick_run");
   if (!t || !arrivals || !n_actions) {
     set_error("null argument");
     return RAPP_E_ARG;
@@ -3023,14 +3026,19 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
   int64_t* s_arr = reinterpret_cast<int64_t*>(t->h_in);
   double* s_pred = reinterpret_cast<double*>(t->h_in + FP * 8);
   uint8_t* s_idle = t->h_in + FP * 16;
+  RAPP_MARK_PUSH("tick.h2d");
   if (F) memcpy(s_arr, arrivals, F * 8);
   if (predicted_in && F) memcpy(s_pred, predicted_in, F * 8);
   if (idle && np) memcpy(s_idle, idle, (size_t)np);
   RAPP_CUDA(cudaMemcpyAsync(t->d_in, t->h_in, FP * 16 + (idle ? (size_t)np : 0),
                             cudaMemcpyHostToDevice, st));
   if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
+  RAPP_MARK_POP();
+  RAPP_MARK_PUSH("tick.launch (prologue, phase A, A2, commit)");
   int rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr, st);
+  RAPP_MARK_POP();
   if (rc) return rc;
+  RAPP_RANGE("tick.d2h + sync");
   // one D2H copy and one synchronisation for the usual case: count, status, rates and the
   // first actions (the output block's prefix)
   const int64_t spec = actions ? std::min<int64_t>(max_actions, 1024) : 0;
