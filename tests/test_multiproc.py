@@ -187,3 +187,27 @@ def test_split_single_rank_matches():
     for t, st, bl in SPLIT_CASES:
         assert search_split(big, t, 0, 1, quota_step=st, batches=bl) == \
             tuple(big.most_efficient_config(t, quota_step=st, batches=bl))
+
+
+def test_bench_self_launches_n_ranks_on_cpu():
+    """`bench.py --gpus 2` outside torchrun relaunches itself as 2 ranks through
+    torch.distributed.run (127.0.0.1); the reference arm needs no GPU, so the whole path —
+    launch, rank 0 alone printing one JSON line with n_gpus = 2, rank 1 exiting 0 — runs on
+    CPU.  Needs the reference kernel built by build() (oracle/_ref)."""
+    import glob
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not glob.glob(os.path.join(root, "oracle", "_ref", "_grid_cy*.so")):
+        pytest.skip("oracle/_ref not built (run build())")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference" and line["value"] > 0
