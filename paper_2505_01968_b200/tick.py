@@ -110,6 +110,23 @@ def _state_code(state) -> int:
     return _STATE_CODE[state if isinstance(state, str) else state.value]
 
 
+_LOW3 = [f"{i:03d}" for i in range(1000)]
+
+
+def _pod_names(c0: int, n: int) -> list[str]:
+    """["pod-%06d" % c for c in range(c0, c0 + n)] (hs/sim.py:337-340), built from a table of
+    the three low digits: one string concatenation per name."""
+    out: list[str] = []
+    c, end = c0, c0 + n
+    while c < end:
+        hi, lo = divmod(c, 1000)
+        k = min(end - c, 1000 - lo)
+        head = "pod-" + (_LOW3[hi] if hi < 1000 else str(hi))
+        out.extend([head + t for t in _LOW3[lo:lo + k]])
+        c += k
+    return out
+
+
 class TickResult:
     """One tick's output.  `raw` holds the packed action records (rapp_action) in
     emission order and `observed_rps`/`predicted_rps` the per-function rates in sorted
@@ -375,19 +392,18 @@ class TickEngine:
     def _bookkeep(self, raw: np.ndarray) -> TickResult:
         """Names the pods the device created (pod-%06d in apply order, like the sim's
         counter) and maps every action to its pod id."""
-        pods = raw["pod"].tolist()
-        kinds = raw["kind"].tolist()
+        pods = raw["pod"]
         ids = self.pod_ids
-        new = [i for i, k in enumerate(kinds) if k == 2]  # horizontal_up: new pods, in order
-        if new:
+        new = np.flatnonzero(raw["kind"] == 2)  # horizontal_up: new pods, in order
+        if len(new):
             start, c0 = len(ids), self.counter
-            if [pods[i] for i in new] != list(range(start, start + len(new))):
+            if not np.array_equal(pods[new], np.arange(start, start + len(new))):
                 raise InvariantViolation("device pod index out of step")
-            fns = raw["fn"].tolist()
-            ids.extend([f"pod-{c:06d}" for c in range(c0, c0 + len(new))])
-            self.pod_fids.extend([self.fids[fns[i]] for i in new])
+            ids.extend(_pod_names(c0, len(new)))
+            fids = self.fids
+            self.pod_fids.extend([fids[f] for f in raw["fn"][new].tolist()])
             self.counter = c0 + len(new)
-        pod_ids = [ids[p] for p in pods]
+        pod_ids = [ids[p] for p in pods.tolist()]
         return TickResult(self, raw, self._obs[:len(self.fids)].copy(),
                           self._pred[:len(self.fids)].copy(), pod_ids)
 

@@ -87,3 +87,12 @@ def test_perf_reader_matches_reference_messages(tmp_path):
         assert repr(list(samples.items())) == repr(list(rsamples.items())), name
         assert [(i.kind, i.message, i.coord) for i in issues] == \
             [(i.kind, i.message, i.coord) for i in rissues], name
+
+
+def test_new_pod_names_match_the_simulator_counter():
+    """New pods are named pod-%06d from the simulator's counter (hs/sim.py:337-340); the
+    tick names them from a table of three-digit suffixes, across the 999/1000 and
+    999,999/1,000,000 boundaries too."""
+    from paper_2505_01968_b200.tick import _pod_names
+    for c0, n in [(0, 0), (0, 5), (995, 10), (123_456, 300), (999_995, 10), (1_234_560, 2_500)]:
+        assert _pod_names(c0, n) == ["pod-%06d" % c for c in range(c0, c0 + n)]
