@@ -384,17 +384,30 @@ __global__ void __launch_bounds__(kSearchThreads)
       int up = -2;
       for (int sg = nlo - 1; sg >= 0; --sg) {
         const int4 S = sLo[sg];
-        const bool top = S.x == last, reuse = S.x + 1 == up;
+        // one branch per run (not per pair): the upper row is the previous run's lower row
+        // (runs of consecutive rows, the usual case), the top row (no upper), or fresh
+        if (S.x + 1 == up) {
 #pragma unroll
-        for (int u = 0; u < NP; ++u) {
-          c0[u] = lerp_rn(corner(r0[u], S.x), corner(r1[u], S.x), tq[u]);
-          d[u] = 0.0;
-          if (!top) {
-            const double c1 = reuse ? cu[u] : lerp_rn(corner(r0[u], S.x + 1),
-                                                      corner(r1[u], S.x + 1), tq[u]);
-            d[u] = __dsub_rn(c1, c0[u]);
+          for (int u = 0; u < NP; ++u) {
+            c0[u] = lerp_rn(corner(r0[u], S.x), corner(r1[u], S.x), tq[u]);
+            d[u] = __dsub_rn(cu[u], c0[u]);
+            cu[u] = c0[u];
           }
-          cu[u] = c0[u];
+        } else if (S.x == last) {
+#pragma unroll
+          for (int u = 0; u < NP; ++u) {
+            c0[u] = lerp_rn(corner(r0[u], S.x), corner(r1[u], S.x), tq[u]);
+            d[u] = 0.0;
+            cu[u] = c0[u];
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < NP; ++u) {
+            c0[u] = lerp_rn(corner(r0[u], S.x), corner(r1[u], S.x), tq[u]);
+            const double c1 = lerp_rn(corner(r0[u], S.x + 1), corner(r1[u], S.x + 1), tq[u]);
+            d[u] = __dsub_rn(c1, c0[u]);
+            cu[u] = c0[u];
+          }
         }
         up = S.x;
 #pragma unroll (kK3Unroll)
