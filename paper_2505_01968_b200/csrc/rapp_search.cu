@@ -43,6 +43,10 @@ constexpr int kK3Unroll = RAPP_K3_UNROLL;  // unroll of the per-batch-entry loop
 #define RAPP_K3_PAIRS 3
 #endif
 constexpr int kK3Pairs = RAPP_K3_PAIRS;  // (s, q) pairs per thread in the meet pass
+#ifndef RAPP_K3_RUN_UNROLL
+#define RAPP_K3_RUN_UNROLL 1
+#endif
+constexpr int kK3RunUnroll = RAPP_K3_RUN_UNROLL;  // unroll of the per-run loop
 
 struct FnDesc {
   int32_t table;
@@ -174,6 +178,7 @@ __global__ void __launch_bounds__(kSearchThreads)
   double2* sTT = (double2*)p;      p += 2 * nB;  // (tb, threshold) per batch entry
   int4* sSeg = (int4*)p;           p += 2 * nB;  // runs of entries sharing a row bracket
   int4* sLo = (int4*)p;            p += 2 * nB;  // runs of entries sharing a lower row
+  uint32_t* sSv = (uint32_t*)p;    p += (ns + 1) / 2;  // sm values as integers (< 2^24)
   __shared__ int s_nseg, s_nlo;
 
   // per-axis brackets, once per CTA (locate semantics, _grid_cy.pyx:9-33)
@@ -183,6 +188,7 @@ __global__ void __launch_bounds__(kSearchThreads)
     locate(sa, ns, sa[i], lo, hi, t);  // the lattice's sm values are the table's own sms
     sTs[i] = t;
     sJ[i] = make_int2(lo, hi);
+    sSv[i] = uint32_t(sa[i]);  // integral and < 2^24 (sm_keyable, checked at plan creation)
   }
   for (int i = threadIdx.x; i < nQ; i += blockDim.x) {
     int lo, hi;
@@ -248,10 +254,10 @@ __global__ void __launch_bounds__(kSearchThreads)
 
   auto record = [&](int si, int qi, int found) {
     if (found < (1 << 30)) {
-      const uint64_t s = uint64_t(sa[si]);
-      const uint64_t q = uint64_t((qi + 1) * step);
-      const unsigned long long k =
-          ((s * q) << 32) | (uint64_t(si) << 20) | (q << 12) | uint64_t(found);
+      const uint32_t q = uint32_t((qi + 1) * step);
+      const uint32_t cost = sSv[si] * q;  // < 2^24 * 100: exact in 32 bits
+      const unsigned long long k = (uint64_t(cost) << 32) |
+                                   ((uint32_t(si) << 20) | (q << 12) | uint32_t(found));
       best = k < best ? k : best;
     }
   };
@@ -382,6 +388,7 @@ __global__ void __launch_bounds__(kSearchThreads)
         fnd[u] = 1 << 30;
       }
       int up = -2;
+#pragma unroll (kK3RunUnroll)
       for (int sg = nlo - 1; sg >= 0; --sg) {
         const int4 S = sLo[sg];
         // one branch per run (not per pair): the upper row is the previous run's lower row
@@ -642,7 +649,7 @@ int rapp_mec_plan_create(rapp_ctx* ctx, int64_t nfn, const int32_t* table_of_fn,
     }
   pl->total_b = (int64_t)blist.size();
   pl->smem_table = max_seg * 8 <= kSearchSmemTable;
-  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 12 * max_nB + 2;
+  const int64_t brk = 2 * max_ns + 2 * pl->nQ + 12 * max_nB + 2 + (max_ns + 1) / 2;
   pl->smem_bytes = (size_t)((pl->smem_table ? max_seg : 0) + brk) * 8;
   if (pl->smem_bytes > 200 * 1024) {
     set_error("lattice search shared-memory footprint %zu bytes too large", pl->smem_bytes);
