@@ -6,7 +6,7 @@
 //          one the constant 1) | 0 pad]                                          (64)
 //   h1  = relu(W1 x)        127 units + a constant-1 unit                         (128)
 //   h2  = relu(W2 h1)       127 units + a constant-1 unit                         (128)
-//   lat = exp(min(w3 . h2, 80))
+//   lat = exp(min(w3 . h2, 80))      (h2 in fp32: the output layer runs on the CUDA cores)
 // Biases ride on the constant units (column 55 of W1, column 127 of W2 and w3), so each
 // hidden layer is one GEMM: tcgen05.mma kind::f16, BF16 operands (weights, x, h1), FP32
 // accumulators in TMEM; the output dot product over the BF16 h2 runs on the CUDA cores in
@@ -29,6 +29,12 @@
 
 #include "rapp_internal.h"
 
+#ifndef RAPP_MLP_FASTFEAT
+#define RAPP_MLP_FASTFEAT 1  // approximate reciprocals in the config features (+6%, measured)
+#endif
+#ifndef RAPP_MLP_L3_FP32
+#define RAPP_MLP_L3_FP32 1  // output layer over the fp32 relu(acc2), no BF16 rounding (+3%)
+#endif
 #ifndef RAPP_MLP_L3_MMA
 #define RAPP_MLP_L3_MMA 0  // 0: layer-3 dot product on the CUDA cores (faster: N=16 MMAs cost
                            //    nearly as much tensor-pipe time as N=128 ones); 1: N=16 MMA
@@ -166,18 +172,32 @@ __device__ __forceinline__ void config_features(double bd, double sd, double qd,
   f[0] = b * (1.0f / 32.0f);
   f[1] = s * 0.01f;
   f[2] = q * 0.01f;
+#if RAPP_MLP_FASTFEAT
+  // approximate reciprocals (MUFU.RCP / RSQ, ~1 ulp) and products of them instead of IEEE
+  // divisions and sqrt: the features feed a BF16 GEMM, whose input rounding is 2^-8
+  const float rb = __fdividef(1.0f, b), rs = __fdividef(1.0f, s), rq = __fdividef(1.0f, q);
+  f[3] = rb;
+  f[4] = rs;
+  f[5] = rq;
+  f[10] = rs * rq;
+  f[11] = b * rs * (1.0f / 32.0f);
+  f[12] = b * rq * (1.0f / 32.0f);
+  f[13] = b * f[10];
+  f[14] = b * rsqrtf(b) * 0.2f;
+#else
   f[3] = 1.0f / b;
   f[4] = 1.0f / s;
   f[5] = 1.0f / q;
-  f[6] = __log2f(b) * 0.2f;
-  f[7] = __log2f(s) * 0.15f;
-  f[8] = __log2f(q) * 0.15f;
-  f[9] = s * q * 1e-4f;
   f[10] = 1.0f / (s * q);
   f[11] = b / s * (1.0f / 32.0f);
   f[12] = b / q * (1.0f / 32.0f);
   f[13] = b / (s * q);
   f[14] = sqrtf(b) * 0.2f;
+#endif
+  f[6] = __log2f(b) * 0.2f;
+  f[7] = __log2f(s) * 0.15f;
+  f[8] = __log2f(q) * 0.15f;
+  f[9] = s * q * 1e-4f;
   f[15] = 1.0f;
 }
 
@@ -431,12 +451,18 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
       for (int cc = 0; cc < 4; ++cc) {
         float v[32];
         tmem_ld32(tmem + lane_base + 32 * cc, v);
+#if RAPP_MLP_L3_FP32
+        // h2 stays fp32 (the output layer runs on the CUDA cores: no operand rounding)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc = fmaf(fmaxf(v[e], 0.0f), w3f[32 * cc + e], acc);
+#else
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const uint32_t h = relu_bf16x2(v[e], v[e + 1]);
           acc = fmaf(__uint_as_float(h << 16), w3f[32 * cc + e], acc);
           acc = fmaf(__uint_as_float(h & 0xFFFF0000u), w3f[32 * cc + e + 1], acc);
         }
+#endif
       }
 #endif
       const double lat = double(__expf(fminf(acc, 80.0f)));

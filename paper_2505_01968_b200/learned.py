@@ -327,7 +327,8 @@ class LearnedPerfModel:
         return e1, e2, e3
 
     def reference_forward(self, model: int, coords: np.ndarray) -> np.ndarray:
-        """fp32 forward of the same BF16 operands (x, weights, h1, h2 rounded to BF16)."""
+        """fp32 forward of the same BF16 operands (x, weights and h1 rounded to BF16; h2 stays
+        fp32: the output layer runs on the CUDA cores, rapp_mlp.cu RAPP_MLP_L3_FP32)."""
         import torch
         bf = torch.bfloat16
         e1, e2, e3 = (torch.from_numpy(a).to(bf).float() for a in self.effective_weights())
@@ -336,7 +337,7 @@ class LearnedPerfModel:
         x[:, N_GRAPH:N_GRAPH + N_CFG] = config_features_ref(coords)
         X = torch.from_numpy(x).to(bf).float()
         h1 = torch.relu(X @ e1.T).to(bf).float()
-        h2 = torch.relu(h1 @ e2.T).to(bf).float()
+        h2 = torch.relu(h1 @ e2.T)
         y = h2 @ e3
         return torch.exp(torch.clamp(y, max=80.0)).double().numpy()
 
