@@ -32,6 +32,9 @@
 #ifndef RAPP_MLP_FASTFEAT
 #define RAPP_MLP_FASTFEAT 1  // approximate reciprocals in the config features (+6%, measured)
 #endif
+#ifndef RAPP_MLP_L3_FFMA2
+#define RAPP_MLP_L3_FFMA2 1  // output layer as packed fma.rn.f32x2 pairs (+1%, measured)
+#endif
 #ifndef RAPP_MLP_L3_FP32
 #define RAPP_MLP_L3_FP32 1  // output layer over the fp32 relu(acc2), no BF16 rounding (+3%)
 #endif
@@ -443,15 +446,29 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
     {
       const float acc = tmem_ld1(tmem + lane_base);
 #else
-    // ---- epilogue 2 + layer 3 on the CUDA cores: h2 = bf16(relu(acc)), acc3 = w3 . h2 ----
+    // ---- epilogue 2 + layer 3 on the CUDA cores: h2 = relu(acc) (fp32), acc3 = w3 . h2 ----
     {
       float acc = 0.0f;
+#if RAPP_MLP_L3_FP32 && RAPP_MLP_L3_FFMA2
+      unsigned long long acc2 = 0ull;  // two fp32 partial sums (+0.0f, +0.0f)
+#endif
       const float* w3f = reinterpret_cast<const float*>(sgraph + kMlpMaxModels * kGraphChunks);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         float v[32];
         tmem_ld32(tmem + lane_base + 32 * cc, v);
-#if RAPP_MLP_L3_FP32
+#if RAPP_MLP_L3_FP32 && RAPP_MLP_L3_FFMA2
+        // h2 stays fp32; pairs of values through the packed FP32 FMA (fma.rn.f32x2) into two
+        // running sums, added at the end
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 w = *reinterpret_cast<const float2*>(w3f + 32 * cc + e);
+          const float h0 = fmaxf(v[e], 0.0f), h1 = fmaxf(v[e + 1], 0.0f);
+          asm("{\n .reg .b64 a, b;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
+              " fma.rn.f32x2 %0, a, b, %1;\n}\n"
+              : "=l"(acc2) : "l"(acc2), "f"(h0), "f"(h1), "f"(w.x), "f"(w.y));
+        }
+#elif RAPP_MLP_L3_FP32
         // h2 stays fp32 (the output layer runs on the CUDA cores: no operand rounding)
 #pragma unroll
         for (int e = 0; e < 32; ++e) acc = fmaf(fmaxf(v[e], 0.0f), w3f[32 * cc + e], acc);
@@ -464,6 +481,9 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp(MlpParams P, MlpWork W) 
         }
 #endif
       }
+#endif
+#if !RAPP_MLP_L3_MMA && RAPP_MLP_L3_FP32 && RAPP_MLP_L3_FFMA2
+      acc = __uint_as_float(uint32_t(acc2)) + __uint_as_float(uint32_t(acc2 >> 32));
 #endif
       const double lat = double(__expf(fminf(acc, 80.0f)));
       if (MODE == kStream) {

@@ -1,1 +1,1 @@
-bash tools/ab_mlp.sh mlp_ff mlp_ff_l3 > gpurun_out/r2s3_ab_mlp2.txt 2>&1
+bash tools/ab_mlp.sh mlp_l3 mlp_ffma2 mlp_ffma2_db2 > gpurun_out/r2s3_ab_mlp5.txt 2>&1
