@@ -1678,10 +1678,10 @@ struct CommitT {
           const int qd = div_d(qmax);
           if (qd * d == qmax) {
             const int kq = qd - 1;  // the step index of qmax
-            cmax = __shfl_sync(0xffffffffu, tv[0], kq & 31);
-            if (kq >= 32) cmax = __shfl_sync(0xffffffffu, tv[1], kq & 31);
-            if (kq >= 64) cmax = __shfl_sync(0xffffffffu, tv[2], kq & 31);
-            if (kq >= 96) cmax = __shfl_sync(0xffffffffu, tv[3], kq & 31);
+            // every lane picks the register that holds step kq, then one shuffle
+            const int u = kq >> 5;
+            const double src = u == 0 ? tv[0] : u == 1 ? tv[1] : u == 2 ? tv[2] : tv[3];
+            cmax = __shfl_sync(0xffffffffu, src, kq & 31);
           } else {  // max_quota_capability at an off-step quota (autoscaler.py:144)
             cmax = lane == 0 ? thr_at(w, f, double(bref), double(sm), double(qmax)) : 0.0;
             cmax = __shfl_sync(0xffffffffu, cmax, 0);
@@ -1701,16 +1701,20 @@ struct CommitT {
             // throughput >= gap, else qmax
             int quota = qmax;
             double tq = cmax;
+            // the four steps' ballots are independent: all issued, then the first hit
+            unsigned mk[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int qq = (u * 32 + lane + 1) * d;
-              const unsigned mask = __ballot_sync(0xffffffffu, qq <= qmax && tv[u] >= gap);
-              if (mask) {
-                const int l = __ffs(mask) - 1;
-                quota = (u * 32 + l + 1) * d;
-                tq = __shfl_sync(0xffffffffu, tv[u], l);
-                break;
-              }
+              mk[u] = __ballot_sync(0xffffffffu, qq <= qmax && tv[u] >= gap);
+            }
+            const int uh = mk[0] ? 0 : mk[1] ? 1 : mk[2] ? 2 : mk[3] ? 3 : -1;
+            if (uh >= 0) {
+              const unsigned mask = mk[uh];
+              const int l = __ffs(mask) - 1;
+              quota = (uh * 32 + l + 1) * d;
+              const double src = uh == 0 ? tv[0] : uh == 1 ? tv[1] : uh == 2 ? tv[2] : tv[3];
+              tq = __shfl_sync(0xffffffffu, src, l);
             }
             TPROF_ACC(10);  // T loads + covering quota
             const int p = new_pod(f, bref, sm, quota, now, npods);
