@@ -32,12 +32,8 @@ struct NvtxRange {
 #define RAPP_NVTX_CAT2(a, b) a##b
 #define RAPP_NVTX_CAT(a, b) RAPP_NVTX_CAT2(a, b)
 #define RAPP_RANGE(name) ::rapp::NvtxRange RAPP_NVTX_CAT(rapp_nvtx_, __LINE__)(name)
-#define RAPP_MARK_PUSH(name) nvtxRangePushA(name)
-#define RAPP_MARK_POP() nvtxRangePop()
 #else
 #define RAPP_RANGE(name) (void)0
-#define RAPP_MARK_PUSH(name) (void)0
-#define RAPP_MARK_POP() (void)0
 #endif
 
 namespace rapp {

@@ -3030,17 +3030,21 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
   int64_t* s_arr = reinterpret_cast<int64_t*>(t->h_in);
   double* s_pred = reinterpret_cast<double*>(t->h_in + FP * 8);
   uint8_t* s_idle = t->h_in + FP * 16;
-  RAPP_MARK_PUSH("tick.h2d");
-  if (F) memcpy(s_arr, arrivals, F * 8);
-  if (predicted_in && F) memcpy(s_pred, predicted_in, F * 8);
-  if (idle && np) memcpy(s_idle, idle, (size_t)np);
-  RAPP_CUDA(cudaMemcpyAsync(t->d_in, t->h_in, FP * 16 + (idle ? (size_t)np : 0),
-                            cudaMemcpyHostToDevice, st));
-  if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
-  RAPP_MARK_POP();
-  RAPP_MARK_PUSH("tick.launch (prologue, phase A, A2, commit)");
-  int rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr, st);
-  RAPP_MARK_POP();
+  {
+    RAPP_RANGE("tick.h2d");
+    if (F) memcpy(s_arr, arrivals, F * 8);
+    if (predicted_in && F) memcpy(s_pred, predicted_in, F * 8);
+    if (idle && np) memcpy(s_idle, idle, (size_t)np);
+    RAPP_CUDA(cudaMemcpyAsync(t->d_in, t->h_in, FP * 16 + (idle ? (size_t)np : 0),
+                              cudaMemcpyHostToDevice, st));
+    if (!idle && np) RAPP_CUDA(cudaMemsetAsync(t->d_idle, 0, (size_t)np, st));
+  }
+  int rc;
+  {
+    RAPP_RANGE("tick.launch (prologue, phase A, A2, commit)");
+    rc = launch_tick(t, now_ms, t->d_arrivals, t->d_idle, predicted_in ? t->d_pred_in : nullptr,
+                     st);
+  }
   if (rc) return rc;
   RAPP_RANGE("tick.d2h + sync");
   // one D2H copy and one synchronisation for the usual case: count, status, rates and the
