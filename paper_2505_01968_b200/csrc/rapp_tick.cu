@@ -1116,9 +1116,16 @@ struct CommitT {
 
   // find_part with a position hint (checked by one load of the hinted entry); P, n: the
   // GPU's list, fetched once by the caller
-  __device__ int find_part_hint(const uint64_t* P, int n, uint32_t uid, int hint) const {
-    if (hint >= 0 && hint < n && part_uid(P[hint]) == uid) return hint;
-    return find_part_in(P, n, uid);
+  // (the entry is returned too: the hint's load is the entry, no second read)
+  __device__ int find_part_hint(const uint64_t* P, int n, uint32_t uid, int hint,
+                                uint64_t& e) const {
+    if (hint >= 0 && hint < n) {
+      e = P[hint];
+      if (part_uid(e) == uid) return hint;
+    }
+    const int pos = find_part_in(P, n, uid);
+    e = P[pos];
+    return pos;
   }
 
   __device__ void set_entry(uint64_t* P, int pos, uint64_t e) const {
@@ -1540,10 +1547,15 @@ struct CommitT {
       const int g = j == 0 ? pre.gpu0 : w.p_gpu[p];
       uint64_t* const P = parts(g);
       const int np = w.g_nparts[g];
-      const int pos = j == 0 ? find_part_hint(P, np, pre.uid0, pre.pos0)
-                             : find_part_in(P, np, w.p_puid[p]);
+      int pos;
+      uint64_t ent;
+      if (j == 0) {
+        pos = find_part_hint(P, np, pre.uid0, pre.pos0, ent);
+      } else {
+        pos = find_part_in(P, np, w.p_puid[p]);
+        ent = P[pos];
+      }
       const int q0 = j == 0 ? pre.q0 : w.p_q[p];
-      const uint64_t ent = P[pos];
       const int avail = q0 + (100 - part_alloc(ent));
       TPROF_ACC(5);  // headroom lookup
       int kstar = -1;
@@ -1927,8 +1939,15 @@ struct CommitT {
       if (kind == kVDown) {
         uint64_t* const P = parts(g);
         const int np = w.g_nparts[g];
-        const int pos = i == 0 ? find_part_hint(P, np, uid, pre.pos0) : find_part_in(P, np, uid);
-        change_quota_at(P, P[pos], p, g, pos, s, q, quota);
+        int pos;
+        uint64_t ent;
+        if (i == 0) {
+          pos = find_part_hint(P, np, uid, pre.pos0, ent);
+        } else {
+          pos = find_part_in(P, np, uid);
+          ent = P[pos];
+        }
+        change_quota_at(P, ent, p, g, pos, s, q, quota);
         emit(f, kVDown, b, s, quota, p, g, 0);
       } else {
         if (lane == 0) w.p_state[p] = kDraining;

@@ -1,1 +1,2 @@
-CASES="mlp" bash tools/sanitize.sh > /dev/null 2>&1; cp gpurun_out/sanitize_summary.txt gpurun_out/r2s3_sanitize_mlp.txt
+timeout 900 python -m pytest tests/test_tick_gpu.py tests/test_integration_gpu.py tests/test_limits_gpu.py -x -q 2>&1 | tail -1 > gpurun_out/r2s3_fph.txt
+bash tools/ab_tickprof.sh build_variants/tick_base.so >> gpurun_out/r2s3_fph.txt 2>&1
