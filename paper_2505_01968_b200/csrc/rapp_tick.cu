@@ -1310,8 +1310,12 @@ struct CommitT {
           const int g = g0 + u * 32 + lane;
           k[u] = g < w.G ? skey[g] : ~0u;
         }
+        // pairwise tree (4 levels) rather than a 16-long dependent chain
 #pragma unroll
-        for (int u = 0; u < 16; ++u) best = min(best, k[u]);
+        for (int h = 8; h > 0; h >>= 1)
+#pragma unroll
+          for (int u = 0; u < h; ++u) k[u] = min(k[u], k[u + h]);
+        best = min(best, k[0]);
       }
       best = __reduce_min_sync(0xffffffffu, best);
       return best == ~0u ? -1 : int(best & ((1u << 18) - 1));
@@ -1419,10 +1423,16 @@ struct CommitT {
         const int64_t pos = lo + step * (int64_t(lane) * 32 + u);
         ge[u] = pos > hi || pm[pos] >= t;
       }
-      int first = 32;  // first probe of this lane that is >= t
+      // first probe of this lane that is >= t (32: none): lowest set bit of the probe mask,
+      // the mask ORed as a tree
+      unsigned bits[32];
 #pragma unroll
-      for (int u = 31; u >= 0; --u)
-        if (ge[u]) first = u;
+      for (int u = 0; u < 32; ++u) bits[u] = ge[u] ? 1u << u : 0u;
+#pragma unroll
+      for (int h = 16; h > 0; h >>= 1)
+#pragma unroll
+        for (int u = 0; u < h; ++u) bits[u] |= bits[u + h];
+      const int first = bits[0] ? __ffs(bits[0]) - 1 : 32;
       const unsigned mask = __ballot_sync(0xffffffffu, first < 32);
       const int l0 = __ffs(mask) - 1;  // lane of the first >= probe (pm[hi] >= t: exists)
       const int u0 = __shfl_sync(0xffffffffu, first, l0);
