@@ -287,6 +287,11 @@ class TickEngine:
                                  dtype=ACTION_DTYPE)
         self._obs = np.zeros(max(1, len(self.fids)))
         self._pred = np.zeros(max(1, len(self.fids)))
+        # the host call's persistent buffers as plain addresses (no ctypes object per tick)
+        self._act_addr = self._act_buf.ctypes.data
+        self._obs_addr, self._pred_addr = self._obs.ctypes.data, self._pred.ctypes.data
+        self._nact = ctypes.c_int64()
+        self._fids_np = np.array(self.fids, dtype=object)
 
     def set_slo(self, slo_ms: Optional[Mapping[str, Optional[float]]]) -> None:
         """Opt-in latency SLO for the fresh-GPU most_efficient_config of the tick
@@ -375,11 +380,12 @@ class TickEngine:
         pred_in = None
         if predicted is not None:
             pred_in = np.array([float(predicted[f]) for f in self.fids], dtype=np.float64)
-        nact = ctypes.c_int64()
-        rc = lib.rapp_tick_run(self._h, float(now_ms), _lib.i64ptr(arr) if F else None,
-                               _ptr(idle_arr), _ptr(pred_in) if pred_in is not None else None,
-                               _ptr(self._act_buf), len(self._act_buf), ctypes.byref(nact),
-                               _ptr(self._obs), _ptr(self._pred))
+        nact = self._nact
+        rc = lib.rapp_tick_run(self._h, float(now_ms), arr.ctypes.data if F else None,
+                               idle_arr.ctypes.data if idle_arr.size else None,
+                               pred_in.ctypes.data if pred_in is not None else None,
+                               self._act_addr, len(self._act_buf), ctypes.byref(nact),
+                               self._obs_addr, self._pred_addr)
         if rc == _lib.RAPP_E_DEGENERATE:
             raise FilterDegenerateError("H*P'*H + D == 0")
         _lib.check(rc, "tick")
@@ -394,16 +400,28 @@ class TickEngine:
         counter) and maps every action to its pod id."""
         pods = raw["pod"]
         ids = self.pod_ids
+        # an object-array mirror of the id list (capacity doubling), for indexing by pod
+        if getattr(self, "_ids_np", None) is None or self._ids_n != len(ids):
+            self._ids_np = np.empty(max(1024, 2 * len(ids)), dtype=object)
+            self._ids_np[:len(ids)] = ids
+            self._ids_n = len(ids)
         new = np.flatnonzero(raw["kind"] == 2)  # horizontal_up: new pods, in order
         if len(new):
             start, c0 = len(ids), self.counter
             if not np.array_equal(pods[new], np.arange(start, start + len(new))):
                 raise InvariantViolation("device pod index out of step")
-            ids.extend(_pod_names(c0, len(new)))
-            fids = self.fids
-            self.pod_fids.extend([fids[f] for f in raw["fn"][new].tolist()])
+            names = _pod_names(c0, len(new))
+            ids.extend(names)
+            end = start + len(names)
+            if end > len(self._ids_np):
+                grown = np.empty(2 * end, dtype=object)
+                grown[:start] = self._ids_np[:start]
+                self._ids_np = grown
+            self._ids_np[start:end] = names
+            self._ids_n = end
+            self.pod_fids.extend(self._fids_np[raw["fn"][new]].tolist())
             self.counter = c0 + len(new)
-        pod_ids = [ids[p] for p in pods.tolist()]
+        pod_ids = self._ids_np[pods].tolist() if len(pods) else []
         return TickResult(self, raw, self._obs[:len(self.fids)].copy(),
                           self._pred[:len(self.fids)].copy(), pod_ids)
 

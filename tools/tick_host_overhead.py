@@ -29,13 +29,14 @@ kw = dict(scaler_interval_ms=2000.0, cold_start_ms=5000.0, pod_counter=len(clust
           device=0)
 eng = TickEngine(fns, tables, cluster, cfg, **kw)
 eng2 = TickEngine(fns, tables, cluster2, cfg, **kw)
+eng3 = TickEngine(fns, tables, copy.deepcopy(cluster2), cfg, **kw)
 eng._all_idle = np.ones(1 << 20, dtype=np.uint8)  # every pod idle, as d_idle below
 lib = _lib.load()
 rng = random.Random(0)
 order = sorted(fns, key=lambda f: f.function_id)
 d_idle = torch.ones(1 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream()
-host, dev, call = [], [], []
+host, dev, call, full = [], [], [], []
 for k in range(25):
     swing = (1.0, 1.5, 0.2, 2.0, 0.05)[k % 5]
     a = bench.config4_arrivals(fns, caps, rng, 2.0, 0.0, 3.0 * swing)
@@ -56,8 +57,16 @@ for k in range(25):
     t3 = time.perf_counter()
     _lib.check(rc)
     eng.counter += int((eng._act_buf[:nact.value]["kind"] == 2).sum())
+    t4 = time.perf_counter()
+    eng3.tick(2000.0 * (k + 1), arr, idle=None)
+    t5 = time.perf_counter()
     if k >= 5:
         dev.append((t1 - t0) * 1e6)
         call.append((t3 - t2) * 1e6)
+        full.append((t5 - t4) * 1e6)
 print(f"run_dev+sync median {np.median(dev):7.1f} us   rapp_tick_run (C ABI) median "
       f"{np.median(call):7.1f} us   difference {np.median(np.array(call) - np.array(dev)):6.1f} us")
+for name, xs in (("run_dev+sync", dev), ("C ABI call", call), ("TickEngine.tick", full)):
+    print(f"{name:16s} median {np.median(xs):7.1f}  max {np.max(xs):7.1f} us")
+i = int(np.argmax(dev))
+print(f"heaviest tick: run_dev+sync {dev[i]:.1f}, C ABI {call[i]:.1f}, TickEngine.tick {full[i]:.1f} us")
