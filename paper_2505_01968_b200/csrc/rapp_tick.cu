@@ -1692,6 +1692,9 @@ struct CommitT {
               tv[u] = qq <= qmax ? T[qq - 1] : 0.0;
             }
           } else {  // interp3 from phase A2's brackets (the same doubles as locate())
+#ifdef RAPP_TICK_PROF
+            if (lane == 0) s_tprof[28] += 1;  // rows evaluated here (sm outside the mask)
+#endif
             const Row4 r = bracket_row(w, f, bref, sm, qmax, d, lane);
 #pragma unroll
             for (int u = 0; u < 4; ++u) tv[u] = r.v[u];

@@ -21,8 +21,8 @@ NAMES = ["batch wait", "vertical spec/walk", "used-GPU rest", "fresh-GPU branch"
          "hu argmin", "hu best_slot", "hu T+covering", "hu new_pod", "hu place", "hu emit",
          "fast lanes", "fast candidates", "fast_run", "fast_run calls", "-", "runs committed",
          "prologue", "epilogue", "hu T row read", "hu new-partition slots", "hu steps", "generic ups",
-         "generic ups to horizontal", "tail horizontals"]
-COUNTS = (14, 15, 17, 19, 23, 24, 25, 26, 27)
+         "generic ups to horizontal", "tail horizontals", "hu rows outside the mask"]
+COUNTS = (14, 15, 17, 19, 23, 24, 25, 26, 27, 28)
 
 
 def main(full_grid, nticks=6):
