@@ -1,1 +1,5 @@
-RAPP_LIB=build_variants/prof.so timeout 300 python tools/tick_commit_breakdown.py --full-grid > gpurun_out/r2s3_commit_breakdown4.txt 2>&1
+mkdir -p gpurun_out
+timeout 900 python bench.py --detail gpurun_out/r2j_default_detail.json > gpurun_out/r2j_default.log 2>&1
+timeout 600 python bench.py --workload tick --full-grid > gpurun_out/r2j_tick_full.log 2>&1
+timeout 600 python bench.py --workload tick > gpurun_out/r2j_tick_c4.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2j_gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r2j_gputest.log
