@@ -1,5 +1,3 @@
-mkdir -p gpurun_out
-timeout 900 python bench.py --detail gpurun_out/r2j_default_detail.json > gpurun_out/r2j_default.log 2>&1
-timeout 600 python bench.py --workload tick --full-grid > gpurun_out/r2j_tick_full.log 2>&1
-timeout 600 python bench.py --workload tick > gpurun_out/r2j_tick_c4.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2j_gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r2j_gputest.log
+timeout 900 python -m pytest tests/test_tick_gpu.py tests/test_integration_gpu.py tests/test_slo.py tests/test_limits_gpu.py -x -q 2>&1 | tail -1 > gpurun_out/r2s3_lazy.txt
+RAPP_TICK_MASK_NONE=1 timeout 900 python -m pytest tests/test_tick_gpu.py -x -q -k "bracket or config4 or random" 2>&1 | tail -1 >> gpurun_out/r2s3_lazy.txt
+bash tools/ab_tickprof.sh build_variants/tick_base.so >> gpurun_out/r2s3_lazy.txt 2>&1
