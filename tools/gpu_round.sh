@@ -1,3 +1,6 @@
-timeout 900 python -m pytest tests/test_tick_gpu.py tests/test_integration_gpu.py tests/test_slo.py tests/test_limits_gpu.py -x -q 2>&1 | tail -1 > gpurun_out/r2s3_lazy.txt
-RAPP_TICK_MASK_NONE=1 timeout 900 python -m pytest tests/test_tick_gpu.py -x -q -k "bracket or config4 or random" 2>&1 | tail -1 >> gpurun_out/r2s3_lazy.txt
-bash tools/ab_tickprof.sh build_variants/tick_base.so >> gpurun_out/r2s3_lazy.txt 2>&1
+mkdir -p gpurun_out
+for tool in racecheck synccheck memcheck; do
+  extra=""; [ "$tool" = memcheck ] && extra="--leak-check full"
+  timeout 1500 compute-sanitizer --tool $tool $extra --error-exitcode 9 --print-limit 20 python tools/sanitize_cases.py tick_full > gpurun_out/sanitize_${tool}_tick_full.log 2>&1
+  echo "$tool tick_full rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|LEAK SUMMARY' gpurun_out/sanitize_${tool}_tick_full.log | tr '\n' ' ')"
+done > gpurun_out/r2s3_sanitize_tickfull.txt

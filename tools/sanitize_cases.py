@@ -143,7 +143,29 @@ def _report_refs(obj):
         print(f"  {type(obj).__name__}: {n} references ({kinds})", flush=True)
 
 
-CASES = {"k2": k2, "k3": k3, "tick": tick, "mlp": mlp, "ingest": ingest, "metrics": metrics}
+def tick_full():
+    """The benchmark-sized tick: config 4's full grid (1,000 functions, 400 GPUs, 32x91x100
+    tables, quota step 1) over three swinging-load ticks, incl. the heavy scale-up tick —
+    the commit's header ring, straight-line runs and staged rows at full size (hazard
+    checks only: the oracle at this size is the tick GPU tests' job)."""
+    from paper_2505_01968_b200.autoscaler import ScalerConfig
+    from paper_2505_01968_b200.tick import TickEngine
+    fns, tables, cluster, caps = bench.make_config4_world(1000, 400, seed=0, full_grid=True,
+                                                          device=0)
+    eng = TickEngine(fns, tables, cluster, ScalerConfig(delta_iq=1), scaler_interval_ms=2000.0,
+                     cold_start_ms=5000.0, pod_counter=len(cluster.pods))
+    rng = random.Random(0)
+    n = 0
+    for k in range(3):
+        arr = bench.config4_arrivals(fns, caps, rng, 2.0, 0.0, 3.0 * (1.0, 1.5, 0.2)[k])
+        n += len(eng.tick(2000.0 * (k + 1), arr).raw)
+    assert n > 500, n
+    eng.read_pods()
+    eng.close()
+
+
+CASES = {"k2": k2, "k3": k3, "tick": tick, "mlp": mlp, "ingest": ingest, "metrics": metrics,
+         "tick_full": tick_full}
 
 if __name__ == "__main__":
     import gc
