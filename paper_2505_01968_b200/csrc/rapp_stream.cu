@@ -189,11 +189,17 @@ int build_fast_extras(int64_t nb, int64_t ns, int64_t nq, const double* b, const
   return RAPP_OK;
 }
 
+#ifndef RAPP_LOCATE_MAGIC
+#define RAPP_LOCATE_MAGIC 0  // 1: uniform locate without F2I/I2F (measured 4% slower)
+#endif
+
 struct FastAxis {
   const uint32_t* lut;
   const double2* iv;
   int last;
+  int e0;  // geom2: binary exponent of a0 (params[4]), converted once per CTA
   double a0, al, scale, h, invh;
+  double topd;  // last - 1 as a double (the uniform locate's clamp)
 };
 
 __device__ __forceinline__ FastAxis load_axis(const double* ext, int a, const uint32_t* lut,
@@ -208,6 +214,8 @@ __device__ __forceinline__ FastAxis load_axis(const double* ext, int a, const ui
   ax.h = p[4];
   ax.invh = p[5];
   ax.last = int(p[6]) - 1;
+  ax.e0 = int(p[4]);
+  ax.topd = double(ax.last - 1);
   return ax;
 }
 
@@ -233,7 +241,7 @@ __device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c
     // x is normal and a0*2^i <= x < a0*2^(i+1)  <=>  exponent(x) == exponent(a0) + i.
     // lo = 2^ex exactly; width a[i+1] - a[i] = 2^ex, so t = RN((x - lo) * 2^-ex) exactly.
     const int ex = ((__double2hiint(x) >> 20) & 0x7FF) - 1023;
-    c = ex - int(ax.h);
+    c = ex - ax.e0;
     const double lo = __hiloint2double((ex + 1023) << 20, 0);
     const double inv = __hiloint2double((1023 - ex) << 20, 0);
     t = __dmul_rn(__dsub_rn(x, lo), inv);
@@ -244,14 +252,25 @@ __device__ __forceinline__ void locate_fast(const FastAxis& ax, double x, int& c
     // i*h < RN(x - a0) < (i+1)*h, and since every a0 + k*h is exact and RN monotone,
     // a[i] < x < a[i+1].  If u is integral, x is within rounding of a node: compare.
     const double u = __dmul_rn(__dsub_rn(x, ax.a0), ax.invh);
+#if RAPP_LOCATE_MAGIC
+    // trunc(u) without the (reduced-rate) F2I/I2F conversions: 0 <= u < 2^52, so
+    // RZ(u + 2^52) = 2^52 + trunc(u) exactly; its low word is trunc(u) and subtracting
+    // 2^52 back is exact.  Same (i, fi) as min(int(u), top), double(i).
+    const double big = __dadd_rz(u, 0x1p52);
+    int i = min(__double2loint(big), top);
+    double fi = fmin(__dsub_rn(big, 0x1p52), ax.topd);
+#else
     int i = min(int(u), top);
-    double lo = fma(double(i), ax.h, ax.a0);  // exact: == a[i]
-    if (double(i) == u) {
+    double fi = double(i);
+#endif
+    double lo = fma(fi, ax.h, ax.a0);  // exact: == a[i]
+    if (fi == u) {
       if (lo > x) {
         --i;
-        lo = fma(double(i), ax.h, ax.a0);
+        fi = __dsub_rn(fi, 1.0);
+        lo = fma(fi, ax.h, ax.a0);
       } else if (i < top) {
-        const double nx = fma(double(i + 1), ax.h, ax.a0);
+        const double nx = fma(__dadd_rn(fi, 1.0), ax.h, ax.a0);
         if (nx <= x) {
           ++i;
           lo = nx;
@@ -288,6 +307,13 @@ __device__ __forceinline__ void load_row(const double* p, bool smem, double& v0,
   }
 }
 
+#ifndef RAPP_STREAM_DIRECT
+// 1: every row by direct loads with a one-slice prefetch (no TMA ring): 0.386-0.387 ms vs
+// 0.394-0.395 ms per 5e7 config-2 queries for the ring (same box, tools/ab_stream.sh); the
+// ring's cp.async.bulk reads and its smem reads/mbarrier polls cost more L1 wavefronts
+// than the three strided 8-byte loads per lane
+#define RAPP_STREAM_DIRECT 1
+#endif
 #ifndef RAPP_STREAM_MINB
 #define RAPP_STREAM_MINB 2
 #endif
@@ -465,16 +491,28 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
                                          t * kTile + (r * kConsumers + warp) * 32 + lane, n,
                                          out, rps);
   }
-  // remainder rows: direct loads, warp-uniform grid-stride (every lane shuffles)
+  // remainder rows (all rows when RAPP_STREAM_DIRECT): direct loads, warp-uniform
+  // grid-stride (every lane shuffles); the next slice's coordinates are loaded before this
+  // slice is interpolated
   const int64_t warps_total = int64_t(gridDim.x) * kConsumers;
-  for (int64_t wb = n_tiles * kTile + (int64_t(blockIdx.x) * kConsumers + warp) * 32; wb < n;
-       wb += warps_total * 32) {
+  const int64_t wstride = warps_total * 32;
+  int64_t wb = n_tiles * kTile + (int64_t(blockIdx.x) * kConsumers + warp) * 32;
+  double nb = ab.a0, ns = as.a0, nq = aq.a0;  // harmless in-range filler past the end
+  if (wb + lane < n) {
+    nb = __ldcs(coords + 3 * (wb + lane));
+    ns = __ldcs(coords + 3 * (wb + lane) + 1);
+    nq = __ldcs(coords + 3 * (wb + lane) + 2);
+  }
+  for (; wb < n; wb += wstride) {
     const int64_t i = wb + lane;
-    double xb = ab.a0, xs = as.a0, xq = aq.a0;  // harmless in-range filler past the end
-    if (i < n) {
-      xb = __ldcs(coords + 3 * i);
-      xs = __ldcs(coords + 3 * i + 1);
-      xq = __ldcs(coords + 3 * i + 2);
+    const double xb = nb, xs = ns, xq = nq;
+    const int64_t j = i + wstride;
+    if (j < n) {
+      nb = __ldcs(coords + 3 * j);
+      ns = __ldcs(coords + 3 * j + 1);
+      nq = __ldcs(coords + 3 * j + 2);
+    } else {
+      nb = ab.a0; ns = as.a0; nq = aq.a0;
     }
     interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq, i, n, out, rps);
   }
@@ -503,13 +541,14 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   const int64_t small_bytes = int64_t(td.x_small) * 8;
   const bool cells_smem = cell_bytes + small_bytes <= kFastCellsSmem;
   const int64_t ext_bytes = cells_smem ? small_bytes + cell_bytes : small_bytes;
-  const size_t smem = (size_t)(((ext_bytes + 127) & ~int64_t(127)) + kStages * 3 * kTile * 8);
+  const size_t smem = (size_t)(((ext_bytes + 127) & ~int64_t(127)) +
+                               (RAPP_STREAM_DIRECT ? 0 : kStages * 3 * kTile * 8));
   if (smem > 220 * 1024) {
     set_error("fast-path shared-memory footprint %zu too large", smem);
     return RAPP_E_ARG;
   }
   const bool aligned = (reinterpret_cast<uintptr_t>(d_coords) & 15) == 0;
-  const int64_t n_tiles = aligned ? n / kTile : 0;
+  const int64_t n_tiles = aligned && !RAPP_STREAM_DIRECT ? n / kTile : 0;
   int64_t blocks = n_tiles > 0 ? n_tiles : (n + kTile - 1) / kTile;
   const int64_t per_sm = std::max<int64_t>(
       1, std::min<int64_t>(RAPP_STREAM_MINB, (220 * 1024) / (int64_t)(smem + 1024)));
