@@ -314,6 +314,9 @@ __device__ __forceinline__ void load_row(const double* p, bool smem, double& v0,
 // than the three strided 8-byte loads per lane
 #define RAPP_STREAM_DIRECT 1
 #endif
+#ifndef RAPP_STREAM_TEX
+#define RAPP_STREAM_TEX 0  // 1: the partner query's cell through the texture pipe, 2: both
+#endif
 #ifndef RAPP_STREAM_MINB
 #define RAPP_STREAM_MINB 2
 #endif
@@ -346,7 +349,8 @@ __device__ __forceinline__ void interp_row(const FastAxis& ab, const FastAxis& a
                                            const FastAxis& aq, const double* cells, int CS,
                                            int CQ, double xb, double xs, double xq, int64_t i,
                                            int64_t n, double* __restrict__ out,
-                                           double* __restrict__ rps) {
+                                           double* __restrict__ rps,
+                                           cudaTextureObject_t tex, int tcell0) {
   const int half = threadIdx.x & 1;
   int ib, js, kq;
   double tb, ts, tq;
@@ -360,8 +364,24 @@ __device__ __forceinline__ void interp_row(const FastAxis& ab, const FastAxis& a
   // query r of the pair is owned by lane 2p + r
   const int c0 = half ? cell_p : cell, c1 = half ? cell : cell_p;
   double v[2][4];
-  load_row(cells + int64_t(c0) * 8 + half * 4, CELLS_SMEM, v[0][0], v[0][1], v[0][2], v[0][3]);
-  load_row(cells + int64_t(c1) * 8 + half * 4, CELLS_SMEM, v[1][0], v[1][1], v[1][2], v[1][3]);
+#if RAPP_STREAM_TEX
+  if (!CELLS_SMEM) {
+    // texels are 16 bytes: cell c = texels 4c..4c+3, row `half` = texels 4c + 2 half + {0,1}
+    auto tex_row = [&](int c, double& a0, double& a1, double& a2, double& a3) {
+      const int t = tcell0 + 4 * c + 2 * half;
+      const int4 p = tex1Dfetch<int4>(tex, t), q = tex1Dfetch<int4>(tex, t + 1);
+      a0 = __hiloint2double(p.y, p.x); a1 = __hiloint2double(p.w, p.z);
+      a2 = __hiloint2double(q.y, q.x); a3 = __hiloint2double(q.w, q.z);
+    };
+    if (RAPP_STREAM_TEX >= 2) tex_row(c0, v[0][0], v[0][1], v[0][2], v[0][3]);
+    else load_row(cells + int64_t(c0) * 8 + half * 4, false, v[0][0], v[0][1], v[0][2], v[0][3]);
+    tex_row(c1, v[1][0], v[1][1], v[1][2], v[1][3]);
+  } else
+#endif
+  {
+    load_row(cells + int64_t(c0) * 8 + half * 4, CELLS_SMEM, v[0][0], v[0][1], v[0][2], v[0][3]);
+    load_row(cells + int64_t(c1) * 8 + half * 4, CELLS_SMEM, v[1][0], v[1][1], v[1][2], v[1][3]);
+  }
   // row h of each query: lerp(lerp(v[j0,k0], v[j0,k1], tq), lerp(v[j1,k0], v[j1,k1], tq), ts)
   const double tq0 = half ? tq_p : tq, tq1 = half ? tq : tq_p;
   const double ts0 = half ? ts_p : ts, ts1 = half ? ts : ts_p;
@@ -433,7 +453,8 @@ template <int MB, int MS, int MQ, bool CELLS_SMEM>
 __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     k_interp_fast(const TableDesc td, const double* __restrict__ pool,
                   const double* __restrict__ coords, int64_t n, int64_t n_tiles,
-                  double* __restrict__ out, double* __restrict__ rps) {
+                  double* __restrict__ out, double* __restrict__ rps,
+                  cudaTextureObject_t tex, int tcell0) {
   extern __shared__ __align__(128) double sm[];
   __shared__ uint64_t bar_ext;
   __shared__ uint64_t full[kStages], empty[kStages];
@@ -489,7 +510,7 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     for (int r = 0; r < kRows; ++r)
       interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, x[r][0], x[r][1], x[r][2],
                                          t * kTile + (r * kConsumers + warp) * 32 + lane, n,
-                                         out, rps);
+                                         out, rps, tex, tcell0);
   }
   // remainder rows (all rows when RAPP_STREAM_DIRECT): direct loads, warp-uniform
   // grid-stride (every lane shuffles); the next slice's coordinates are loaded before this
@@ -514,7 +535,8 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
     } else {
       nb = ab.a0; ns = as.a0; nq = aq.a0;
     }
-    interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq, i, n, out, rps);
+    interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq, i, n, out, rps,
+                                       tex, tcell0);
   }
 }
 
@@ -523,17 +545,51 @@ constexpr int64_t kFastCellsSmem = 96 * 1024;
 template <int MB, int MS, int MQ>
 static void launch_modes(bool cells_smem, unsigned blocks, size_t smem, cudaStream_t st,
                          const TableDesc& td, const double* pool, const double* coords,
-                         int64_t n, int64_t n_tiles, double* out, double* rps) {
+                         int64_t n, int64_t n_tiles, double* out, double* rps,
+                         cudaTextureObject_t tex, int tcell0) {
   if (cells_smem) {
     auto k = k_interp_fast<MB, MS, MQ, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    k<<<blocks, kFastThreads, smem, st>>>(td, pool, coords, n, n_tiles, out, rps);
+    k<<<blocks, kFastThreads, smem, st>>>(td, pool, coords, n, n_tiles, out, rps, tex,
+                                          tcell0);
   } else {
     auto k = k_interp_fast<MB, MS, MQ, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    k<<<blocks, kFastThreads, smem, st>>>(td, pool, coords, n, n_tiles, out, rps);
+    k<<<blocks, kFastThreads, smem, st>>>(td, pool, coords, n, n_tiles, out, rps, tex,
+                                          tcell0);
   }
 }
+
+#if RAPP_STREAM_TEX
+// One int4 texture object over the whole table pool, rebuilt when the pool moves or grows.
+static int pool_texture(rapp_ctx* ctx, cudaTextureObject_t* out) {
+  static std::mutex mu;
+  static const double* ptr = nullptr;
+  static int64_t cap = -1;
+  static cudaTextureObject_t obj = 0;
+  std::lock_guard<std::mutex> g(mu);
+  if (ptr != ctx->d_pool || cap != ctx->pool_cap) {
+    if (obj) cudaDestroyTextureObject(obj);
+    obj = 0;
+    if (ctx->pool_cap / 2 >= (int64_t(1) << 27)) {
+      set_error("table pool too large for the texture path");
+      return RAPP_E_ARG;
+    }
+    cudaResourceDesc rd = {};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = const_cast<double*>(ctx->d_pool);
+    rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+    rd.res.linear.sizeInBytes = size_t(ctx->pool_cap) * 8;
+    cudaTextureDesc tdsc = {};
+    tdsc.readMode = cudaReadModeElementType;
+    RAPP_CUDA(cudaCreateTextureObject(&obj, &rd, &tdsc, nullptr));
+    ptr = ctx->d_pool;
+    cap = ctx->pool_cap;
+  }
+  *out = obj;
+  return RAPP_OK;
+}
+#endif
 
 int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coords, int64_t n,
                        double* d_out, double* d_rps, cudaStream_t st) {
@@ -557,8 +613,18 @@ int launch_interp_fast(rapp_ctx* ctx, const TableDesc& td, const double* d_coord
   if (blocks < 1) blocks = 1;
   const unsigned nb = (unsigned)blocks;
   const double* pool = ctx->d_pool;
+  cudaTextureObject_t tex = 0;
+  int tcell0 = 0;
+#if RAPP_STREAM_TEX
+  if (!cells_smem) {
+    int rc = pool_texture(ctx, &tex);
+    if (rc != RAPP_OK) return rc;
+    tcell0 = int((td.xoff + td.x_small) / 2);  // 64-byte aligned cells: an even double index
+  }
+#endif
 #define RAPP_LM(B, S, Q) \
-  launch_modes<B, S, Q>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps)
+  launch_modes<B, S, Q>(cells_smem, nb, smem, st, td, pool, d_coords, n, n_tiles, d_out, d_rps, \
+                        tex, tcell0)
   // bit 0: batch axis uniform, bit 1: sm uniform, bit 2: quota uniform, bit 3: batch geom2
   switch (td.modes & 15) {
     case 0: RAPP_LM(0, 0, 0); break;
