@@ -254,6 +254,16 @@ int rapp_tick_run(rapp_tick *t, double now_ms, const int64_t *arrivals, const ui
                   const double *predicted_in, rapp_action *actions, int64_t max_actions,
                   int64_t *n_actions, double *observed_out, double *predicted_out);
 
+/* rapp_tick_run in two halves, so the caller can work while the tick runs on the device:
+ * submit copies the inputs and enqueues the tick and its output copy (no synchronisation);
+ * collect waits for it and returns what rapp_tick_run returns (same arguments, same
+ * errors).  Exactly one collect follows each successful submit, with no other call on the
+ * handle in between (RAPP_E_ARG otherwise). */
+int rapp_tick_submit(rapp_tick *t, double now_ms, const int64_t *arrivals, const uint8_t *idle,
+                     const double *predicted_in, int64_t max_actions);
+int rapp_tick_collect(rapp_tick *t, rapp_action *actions, int64_t max_actions,
+                      int64_t *n_actions, double *observed_out, double *predicted_out);
+
 /* Host events between ticks: pods the simulator released (a DRAINING pod whose last
  * request completed, hs/sim.py:424-438), applied in order before the next tick. */
 int rapp_tick_release(rapp_tick *t, const int64_t *pods, int64_t n);

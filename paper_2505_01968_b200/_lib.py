@@ -102,6 +102,9 @@ SIGNATURES = [
     ("rapp_tick_destroy", ctypes.c_int, [c_vp]),
     ("rapp_tick_run", ctypes.c_int, [c_vp, ctypes.c_double, c_vp, c_vp, c_vp, c_vp,
                                      ctypes.c_int64, c_i64p, c_vp, c_vp]),
+    ("rapp_tick_submit", ctypes.c_int, [c_vp, ctypes.c_double, c_vp, c_vp, c_vp,
+                                        ctypes.c_int64]),
+    ("rapp_tick_collect", ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_i64p, c_vp, c_vp]),
     ("rapp_tick_release", ctypes.c_int, [c_vp, c_i64p, ctypes.c_int64]),
     ("rapp_tick_run_dev", ctypes.c_int, [c_vp, ctypes.c_double, c_vp, c_vp, c_vp]),
     ("rapp_tick_outputs_dev", ctypes.c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),

@@ -2402,6 +2402,7 @@ constexpr size_t kOutHead = 16;  // n_actions, err, err_fn, pad (int32 each)
 
 struct rapp_tick {
   rapp_ctx* ctx = nullptr;
+  int64_t pend_spec = -1;  // submitted host tick awaiting rapp_tick_collect (-1: none)
   World w{};
   std::vector<std::pair<void*, size_t>> allocs;  // device buffers (returned to the pool)
   size_t h_in_bytes = 0, h_out_bytes = 0;
@@ -2968,6 +2969,10 @@ int rapp_tick_release(rapp_tick* t, const int64_t* pods, int64_t n) {
   }
   if (n == 0) return RAPP_OK;
   std::lock_guard<std::mutex> lk(t->ctx->mu);
+  if (t->pend_spec >= 0) {
+    set_error("a submitted tick has not been collected");
+    return RAPP_E_ARG;
+  }
   RAPP_CUDA(cudaSetDevice(t->ctx->device));
   int64_t known = t->h_npods;
   if (known < 0) {
@@ -3010,6 +3015,10 @@ int rapp_tick_run_dev(rapp_tick* t, double now_ms, const int64_t* d_arrivals,
     set_error("null tick");
     return RAPP_E_ARG;
   }
+  if (t->pend_spec >= 0) {
+    set_error("a submitted tick has not been collected");
+    return RAPP_E_ARG;
+  }
   RAPP_CUDA(cudaSetDevice(t->ctx->device));
   t->h_npods = -1;  // the host no longer knows the pod count without a read-back
   // the world is shared with the host API's internal stream (releases, host ticks): order
@@ -3037,15 +3046,18 @@ int rapp_tick_outputs_dev(rapp_tick* t, const rapp_action** a, const int32_t** c
   return RAPP_OK;
 }
 
-int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const uint8_t* idle,
-                  const double* predicted_in, rapp_action* actions, int64_t max_actions,
-                  int64_t* n_actions, double* observed_out, double* predicted_out) {
-  RAPP_RANGE("rapp_tick_run");
-  if (!t || !arrivals || !n_actions) {
+int rapp_tick_submit(rapp_tick* t, double now_ms, const int64_t* arrivals, const uint8_t* idle,
+                     const double* predicted_in, int64_t max_actions) {
+  RAPP_RANGE("rapp_tick_submit");
+  if (!t || !arrivals) {
     set_error("null argument");
     return RAPP_E_ARG;
   }
   std::lock_guard<std::mutex> lk(t->ctx->mu);
+  if (t->pend_spec >= 0) {
+    set_error("a submitted tick has not been collected");
+    return RAPP_E_ARG;
+  }
   RAPP_CUDA(cudaSetDevice(t->ctx->device));
   World& w = t->w;
   cudaStream_t st = t->stream;
@@ -3078,13 +3090,37 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
                      st);
   }
   if (rc) return rc;
-  RAPP_RANGE("tick.d2h + sync");
-  // one D2H copy and one synchronisation for the usual case: count, status, rates and the
-  // first actions (the output block's prefix)
-  const int64_t spec = actions ? std::min<int64_t>(max_actions, 1024) : 0;
+  // one D2H copy for the usual case: count, status, rates and the first actions (the
+  // output block's prefix)
+  const int64_t spec = std::min<int64_t>(std::max<int64_t>(max_actions, 0), 1024);
   RAPP_CUDA(cudaMemcpyAsync(t->h_out, t->d_out,
                             kOutHead + FP * 16 + (size_t)spec * sizeof(rapp_action),
                             cudaMemcpyDeviceToHost, st));
+  t->pend_spec = spec;
+  return RAPP_OK;
+}
+
+int rapp_tick_collect(rapp_tick* t, rapp_action* actions, int64_t max_actions,
+                      int64_t* n_actions, double* observed_out, double* predicted_out) {
+  RAPP_RANGE("rapp_tick_collect");
+  if (!t || !n_actions) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  std::lock_guard<std::mutex> lk(t->ctx->mu);
+  if (t->pend_spec < 0) {
+    set_error("no submitted tick");
+    return RAPP_E_ARG;
+  }
+  const int64_t spec = actions ? std::min(t->pend_spec, max_actions) : 0;
+  t->pend_spec = -1;
+  RAPP_CUDA(cudaSetDevice(t->ctx->device));
+  World& w = t->w;
+  cudaStream_t st = t->stream;
+  const size_t F = (size_t)w.F;
+  const size_t FP = std::max<size_t>(F, 1);
+  int rc;
+  RAPP_RANGE("tick.d2h + sync");
   const int32_t* h_count = reinterpret_cast<const int32_t*>(t->h_out);
   const double* s_obs = reinterpret_cast<const double*>(t->h_out + kOutHead);
   const double* s_prd = s_obs + FP;
@@ -3121,6 +3157,20 @@ int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const ui
     t->h_npods = v;
   }
   return RAPP_OK;
+}
+
+int rapp_tick_run(rapp_tick* t, double now_ms, const int64_t* arrivals, const uint8_t* idle,
+                  const double* predicted_in, rapp_action* actions, int64_t max_actions,
+                  int64_t* n_actions, double* observed_out, double* predicted_out) {
+  RAPP_RANGE("rapp_tick_run");
+  if (!t || !arrivals || !n_actions) {
+    set_error("null argument");
+    return RAPP_E_ARG;
+  }
+  const int rc = rapp_tick_submit(t, now_ms, arrivals, idle, predicted_in,
+                                  actions ? max_actions : 0);
+  if (rc) return rc;
+  return rapp_tick_collect(t, actions, max_actions, n_actions, observed_out, predicted_out);
 }
 
 int rapp_tick_read_pods(rapp_tick* t, rapp_pod_desc* out, int64_t cap, int64_t* n) {

@@ -381,11 +381,13 @@ class TickEngine:
         if predicted is not None:
             pred_in = np.array([float(predicted[f]) for f in self.fids], dtype=np.float64)
         nact = self._nact
-        rc = lib.rapp_tick_run(self._h, float(now_ms), arr.ctypes.data if F else None,
-                               idle_arr.ctypes.data if idle_arr.size else None,
-                               pred_in.ctypes.data if pred_in is not None else None,
-                               self._act_addr, len(self._act_buf), ctypes.byref(nact),
-                               self._obs_addr, self._pred_addr)
+        _lib.check(lib.rapp_tick_submit(self._h, float(now_ms), arr.ctypes.data if F else None,
+                                        idle_arr.ctypes.data if idle_arr.size else None,
+                                        pred_in.ctypes.data if pred_in is not None else None,
+                                        len(self._act_buf)), "tick")
+        self._top_up_names()  # while the tick runs on the device
+        rc = lib.rapp_tick_collect(self._h, self._act_addr, len(self._act_buf),
+                                   ctypes.byref(nact), self._obs_addr, self._pred_addr)
         if rc == _lib.RAPP_E_DEGENERATE:
             raise FilterDegenerateError("H*P'*H + D == 0")
         _lib.check(rc, "tick")
@@ -394,6 +396,43 @@ class TickEngine:
         if apply_to_host:
             self._apply_host(res, float(now_ms))
         return res
+
+    # new pod ids come from a cache of pod-%06d names for the next counter values, topped up
+    # between rapp_tick_submit and rapp_tick_collect (hidden under the device tick); a tick
+    # that outruns the cache names the rest itself
+    _NAMES_TOPUP_MAX = 1024
+
+    def _top_up_names(self) -> None:
+        c0 = getattr(self, "_names_c0", None)
+        if c0 is None:
+            self._names, self._names_c0, self._names_reserve = [], self.counter, 256
+            c0 = self.counter
+        names = self._names
+        used = self.counter - c0
+        if used < 0 or used > len(names):  # counter moved outside the cache: restart it
+            names.clear()
+            self._names_c0 = c0 = self.counter
+            used = 0
+        elif used > 4096:
+            del names[:used]
+            self._names_c0 = c0 = self.counter
+            used = 0
+        short = self._names_reserve - (len(names) - used)
+        if short > 0:
+            names.extend(_pod_names(c0 + len(names), min(short, self._NAMES_TOPUP_MAX)))
+
+    def _new_names(self, c0: int, k: int) -> list[str]:
+        base = getattr(self, "_names_c0", None)
+        if base is None:
+            return _pod_names(c0, k)
+        self._names_reserve = max(self._names_reserve, 2 * k)
+        lo = c0 - base
+        if lo < 0:
+            return _pod_names(c0, k)
+        have = self._names[lo:lo + k]
+        if len(have) < k:
+            have.extend(_pod_names(c0 + len(have), k - len(have)))
+        return have
 
     def _bookkeep(self, raw: np.ndarray) -> TickResult:
         """Names the pods the device created (pod-%06d in apply order, like the sim's
@@ -410,7 +449,7 @@ class TickEngine:
             start, c0 = len(ids), self.counter
             if not np.array_equal(pods[new], np.arange(start, start + len(new))):
                 raise InvariantViolation("device pod index out of step")
-            names = _pod_names(c0, len(new))
+            names = self._new_names(c0, len(new))
             ids.extend(names)
             end = start + len(names)
             if end > len(self._ids_np):

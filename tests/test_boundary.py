@@ -96,3 +96,29 @@ def test_new_pod_names_match_the_simulator_counter():
     from paper_2505_01968_b200.tick import _pod_names
     for c0, n in [(0, 0), (0, 5), (995, 10), (123_456, 300), (999_995, 10), (1_234_560, 2_500)]:
         assert _pod_names(c0, n) == ["pod-%06d" % c for c in range(c0, c0 + n)]
+
+
+def test_new_pod_name_cache_follows_the_counter():
+    """TickEngine's name cache (topped up between rapp_tick_submit and rapp_tick_collect)
+    hands out exactly the pod-%06d names of the counter values a tick consumes, including
+    ticks that outrun the cache and counters that jump outside it."""
+    from paper_2505_01968_b200.tick import TickEngine
+
+    class Stub:
+        counter = 0
+        _NAMES_TOPUP_MAX = 1024
+        _top_up_names = TickEngine._top_up_names
+        _new_names = TickEngine._new_names
+
+    e = Stub()
+    import numpy as np
+    rng = np.random.default_rng(3)
+    for step in range(200):
+        e._top_up_names()
+        k = int(rng.choice([0, 1, 5, 300, 700, 2500]))
+        if step == 120:
+            e.counter += 10_000  # e.g. a rebuilt engine: the cache restarts
+            e._top_up_names()
+        got = e._new_names(e.counter, k)
+        assert got == ["pod-%06d" % c for c in range(e.counter, e.counter + k)]
+        e.counter += k

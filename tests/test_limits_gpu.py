@@ -115,3 +115,33 @@ def test_tick_world_size_limits_at_the_c_abi():
                                   None, None, None, 0, None, 0, ctypes.byref(h))
         with pytest.raises(DeviceError, match="exceeds the tick's limits"):
             _lib.check(rc, "TickEngine")
+
+
+def test_tick_submit_collect_pairing():
+    """rapp_tick_submit / rapp_tick_collect (the two halves of rapp_tick_run) refuse an
+    unpaired collect, a second submit and any other world call in between, and a paired
+    call returns what rapp_tick_run returns."""
+    import ctypes
+    from paper_2505_01968_b200 import _lib
+    tables = {"conf-fn": _table(sms=(10, 50, 100))}
+    fn, c = _world(4, 4)
+    eng = _engine(fn, c, tables)
+    lib = _lib.load()
+    n = ctypes.c_int64()
+    arr = np.array([50], dtype=np.int64)
+    assert lib.rapp_tick_collect(eng._h, eng._act_addr, len(eng._act_buf), ctypes.byref(n),
+                                 None, None) == _lib.RAPP_E_ARG
+    assert "no submitted tick" in _lib.last_error()
+    assert lib.rapp_tick_submit(eng._h, 1000.0, arr.ctypes.data, None, None,
+                                len(eng._act_buf)) == 0
+    assert lib.rapp_tick_submit(eng._h, 1000.0, arr.ctypes.data, None, None,
+                                len(eng._act_buf)) == _lib.RAPP_E_ARG
+    pods = np.array([0], dtype=np.int64)
+    assert lib.rapp_tick_release(eng._h, pods.ctypes.data, 1) == _lib.RAPP_E_ARG
+    assert lib.rapp_tick_collect(eng._h, eng._act_addr, len(eng._act_buf), ctypes.byref(n),
+                                 None, None) == 0
+    eng._bookkeep(eng._act_buf[:n.value].copy())  # keep the host's pod list in step
+    # the engine goes on normally afterwards (its own tick is submit + collect)
+    res = eng.tick(2000.0, {"conf-fn": 50})
+    assert res.observed["conf-fn"] >= 0.0
+    eng.close()
