@@ -137,7 +137,8 @@ def test_tick_submit_collect_pairing():
     assert lib.rapp_tick_submit(eng._h, 1000.0, arr.ctypes.data, None, None,
                                 len(eng._act_buf)) == _lib.RAPP_E_ARG
     pods = np.array([0], dtype=np.int64)
-    assert lib.rapp_tick_release(eng._h, pods.ctypes.data, 1) == _lib.RAPP_E_ARG
+    assert lib.rapp_tick_release(eng._h, pods.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                 1) == _lib.RAPP_E_ARG
     assert lib.rapp_tick_collect(eng._h, eng._act_addr, len(eng._act_buf), ctypes.byref(n),
                                  None, None) == 0
     eng._bookkeep(eng._act_buf[:n.value].copy())  # keep the host's pod list in step
