@@ -317,9 +317,6 @@ __device__ __forceinline__ void load_row(const double* p, bool smem, double& v0,
 #ifndef RAPP_STREAM_TEX
 #define RAPP_STREAM_TEX 0  // 1: the partner query's cell through the texture pipe, 2: both
 #endif
-#ifndef RAPP_STREAM_COORD128
-#define RAPP_STREAM_COORD128 0  // 1: a lane pair's coordinates by two 16-byte loads per lane
-#endif
 #ifndef RAPP_STREAM_MINB
 #define RAPP_STREAM_MINB 2
 #endif
@@ -521,35 +518,23 @@ __global__ void __launch_bounds__(kFastThreads, RAPP_STREAM_MINB)
   const int64_t warps_total = int64_t(gridDim.x) * kConsumers;
   const int64_t wstride = warps_total * 32;
   int64_t wb = n_tiles * kTile + (int64_t(blockIdx.x) * kConsumers + warp) * 32;
-  // one slice's coordinates into (b, s, q) of this lane's row; rows past the end get a
-  // harmless in-range filler
-  const bool vec = RAPP_STREAM_COORD128 && (reinterpret_cast<uintptr_t>(coords) & 15) == 0;
-  auto load_slice = [&](int64_t base, double& b, double& s, double& q) {
-    if (vec && base + 32 <= n) {
-      // a lane pair's two rows are 48 contiguous bytes: the even lane reads [0,16) and the
-      // odd lane [32,48), then both read [16,32) (the same 16 bytes: one request)
-      const double2* p = reinterpret_cast<const double2*>(coords + 3 * (base + (lane & ~1)));
-      const double2 x = __ldcs(p + ((lane & 1) << 1));
-      const double2 y = __ldcs(p + 1);
-      if (lane & 1) { b = y.y; s = x.x; q = x.y; }
-      else { b = x.x; s = x.y; q = y.x; }
-      return;
-    }
-    const int64_t r = base + lane;
-    if (r < n) {
-      b = __ldcs(coords + 3 * r);
-      s = __ldcs(coords + 3 * r + 1);
-      q = __ldcs(coords + 3 * r + 2);
-    } else {
-      b = ab.a0; s = as.a0; q = aq.a0;
-    }
-  };
-  double nb, ns, nq;
-  load_slice(wb, nb, ns, nq);
+  double nb = ab.a0, ns = as.a0, nq = aq.a0;  // harmless in-range filler past the end
+  if (wb + lane < n) {
+    nb = __ldcs(coords + 3 * (wb + lane));
+    ns = __ldcs(coords + 3 * (wb + lane) + 1);
+    nq = __ldcs(coords + 3 * (wb + lane) + 2);
+  }
   for (; wb < n; wb += wstride) {
     const int64_t i = wb + lane;
     const double xb = nb, xs = ns, xq = nq;
-    load_slice(wb + wstride, nb, ns, nq);
+    const int64_t j = i + wstride;
+    if (j < n) {
+      nb = __ldcs(coords + 3 * j);
+      ns = __ldcs(coords + 3 * j + 1);
+      nq = __ldcs(coords + 3 * j + 2);
+    } else {
+      nb = ab.a0; ns = as.a0; nq = aq.a0;
+    }
     interp_row<MB, MS, MQ, CELLS_SMEM>(ab, as, aq, cells, CS, CQ, xb, xs, xq, i, n, out, rps,
                                        tex, tcell0);
   }
