@@ -132,13 +132,23 @@ class TickResult:
     emission order and `observed_rps`/`predicted_rps` the per-function rates in sorted
     function order; the reference-shaped views below are built on first access."""
 
-    def __init__(self, engine, raw, obs, pred, pod_ids):
+    def __init__(self, engine, raw, obs, pred):
         self.raw = raw
         self.observed_rps = obs
         self.predicted_rps = pred
-        self.pod_ids = pod_ids          # pod each action refers to (new pods: new id)
         self._engine = engine
         self._actions = None
+        self._pod_ids = None
+
+    @property
+    def pod_ids(self) -> list[str]:
+        """The pod each action refers to (new pods: their new id), in action order."""
+        if self._pod_ids is None:
+            pods = self.raw["pod"]
+            # device pod indices are stable and the id list only grows, so the mirror read
+            # at any later time gives the ids of this tick
+            self._pod_ids = self._engine._ids_mirror()[pods].tolist() if len(pods) else []
+        return self._pod_ids
 
     @property
     def actions(self) -> list:
@@ -249,7 +259,8 @@ class TickEngine:
             part_off.append(len(psm))
         # pods
         self.pod_ids: list[str] = []
-        self.pod_fids: list[str] = []
+        self._pod_fids: list[str] = []
+        self._pod_fn_pending: list[np.ndarray] = []  # function indices of new pods, unnamed
         pods = np.zeros(len(cluster.pods), dtype=POD_DTYPE)
         for i, pod in enumerate(cluster.pods.values()):
             raw = pod.pod_id.encode("utf-8")
@@ -263,7 +274,7 @@ class TickEngine:
                        float(getattr(pod, "ready_at_ms", 0.0)) if promote_cold else math.inf,
                        raw)
             self.pod_ids.append(pod.pod_id)
-            self.pod_fids.append(pod.function_id)
+            self._pod_fids.append(pod.function_id)
         self.counter = int(pod_counter)
         cfg = ScalerConfigC(scaler_config.alpha, scaler_config.beta, scaler_config.cooldown_ms,
                             scaler_config.r_min, scaler_config.delta_iq,
@@ -434,35 +445,46 @@ class TickEngine:
             have.extend(_pod_names(c0 + len(have), k - len(have)))
         return have
 
+    @property
+    def pod_fids(self) -> list[str]:
+        """Function id of every device pod index (new pods' entries are named on demand)."""
+        if self._pod_fn_pending:
+            for fn in self._pod_fn_pending:
+                self._pod_fids.extend(self._fids_np[fn].tolist())
+            self._pod_fn_pending.clear()
+        return self._pod_fids
+
+    def _ids_mirror(self) -> np.ndarray:
+        """An object-array copy of the pod id list (capacity doubling), brought up to date on
+        demand, for gathering ids by device pod index."""
+        ids = self.pod_ids
+        mirror, n = getattr(self, "_ids_np", None), getattr(self, "_ids_n", 0)
+        if mirror is None or len(mirror) < len(ids):
+            grown = np.empty(max(1024, 2 * len(ids)), dtype=object)
+            if mirror is not None:
+                grown[:n] = mirror[:n]
+            mirror = self._ids_np = grown
+        if n < len(ids):
+            mirror[n:len(ids)] = ids[n:]
+            self._ids_n = len(ids)
+        return mirror
+
     def _bookkeep(self, raw: np.ndarray) -> TickResult:
         """Names the pods the device created (pod-%06d in apply order, like the sim's
-        counter) and maps every action to its pod id."""
+        counter); the per-action pod ids and the new pods' function ids are views built on
+        first access (TickResult.pod_ids, TickEngine.pod_fids)."""
         pods = raw["pod"]
         ids = self.pod_ids
-        # an object-array mirror of the id list (capacity doubling), for indexing by pod
-        if getattr(self, "_ids_np", None) is None or self._ids_n != len(ids):
-            self._ids_np = np.empty(max(1024, 2 * len(ids)), dtype=object)
-            self._ids_np[:len(ids)] = ids
-            self._ids_n = len(ids)
         new = np.flatnonzero(raw["kind"] == 2)  # horizontal_up: new pods, in order
         if len(new):
             start, c0 = len(ids), self.counter
             if not np.array_equal(pods[new], np.arange(start, start + len(new))):
                 raise InvariantViolation("device pod index out of step")
-            names = self._new_names(c0, len(new))
-            ids.extend(names)
-            end = start + len(names)
-            if end > len(self._ids_np):
-                grown = np.empty(2 * end, dtype=object)
-                grown[:start] = self._ids_np[:start]
-                self._ids_np = grown
-            self._ids_np[start:end] = names
-            self._ids_n = end
-            self.pod_fids.extend(self._fids_np[raw["fn"][new]].tolist())
+            ids.extend(self._new_names(c0, len(new)))
+            self._pod_fn_pending.append(raw["fn"][new])
             self.counter = c0 + len(new)
-        pod_ids = self._ids_np[pods].tolist() if len(pods) else []
-        return TickResult(self, raw, self._obs[:len(self.fids)].copy(),
-                          self._pred[:len(self.fids)].copy(), pod_ids)
+        F = len(self.fids)
+        return TickResult(self, raw, self._obs[:F].copy(), self._pred[:F].copy())
 
     def _apply_host(self, res: TickResult, now: float) -> None:
         """Cluster effects of hs/sim.py:493-525 on the host snapshot (promotions first),
