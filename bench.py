@@ -845,22 +845,29 @@ def run_tick(args, local, ticks=None, warmup=None, full_grid=False, nfn=1000, ng
                       cold_start_ms=5000.0, pod_counter=len(cluster0.pods), device=local)
     rng = random.Random(0)
     host_arr = [arrivals_for(k) for k in range(total)]
-    e2e_us, acts = [], []
+    e2e_us, obj_us, acts = [], [], []
     for k in range(total):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         res = eng2.tick(interval_ms * (k + 1), host_arr[k], idle=None)
-        e2e_us.append((time.perf_counter() - t1) * 1e6)
-        acts.append(len(res.actions))
-    e2e_us = e2e_us[warmup:]
+        t2 = time.perf_counter()
+        acts.append(len(res.actions))  # the caller's ScalingAction objects (built on access)
+        t3 = time.perf_counter()
+        e2e_us.append((t2 - t1) * 1e6)
+        obj_us.append((t3 - t1) * 1e6)
+    e2e_us, obj_us = e2e_us[warmup:], obj_us[warmup:]
     acts = acts[warmup:]
     return {"functions": nfn, "gpus_simulated": ngpu, "grid": "32x91x100, delta 1" if full_grid
             else "6x10x10, delta 10", "ticks": ticks,
             "device_us_median": float(np.median(dev_us)), "device_us_max": float(np.max(dev_us)),
             "e2e_us_median": float(np.median(e2e_us)), "e2e_us_max": float(np.max(e2e_us)),
+            "e2e_objects_us_median": float(np.median(obj_us)),
+            "e2e_objects_us_max": float(np.max(obj_us)),
             "actions_per_tick_mean": float(np.mean(acts)), "launches_per_tick": int(launches),
             "world_build_s": round(build_s, 3), "clocks": clk.summary(),
-            "e2e_api": "TickEngine.tick (rapp_tick_run: H2D arrivals+idle, D2H actions+rates)"}
+            "e2e_api": "TickEngine.tick -> TickResult (rapp_tick_submit/collect: H2D arrivals+idle, "
+                       "D2H packed actions+rates, new pod ids named); e2e_objects adds building "
+                       "the caller's ScalingAction objects with their pod ids"}
 
 
 def run_config1(args, local, reps=20):
@@ -1224,6 +1231,9 @@ def tick_summary(t, ref=None):
     out = {"dev_med": _r(t["device_us_median"]), "dev_max": _r(t["device_us_max"]),
            "e2e_med": _r(t["e2e_us_median"]), "e2e_max": _r(t["e2e_us_max"]),
            "acts": _r(t["actions_per_tick_mean"]), "ticks": t["ticks"]}
+    if "e2e_objects_us_median" in t:
+        out["obj_med"] = _r(t["e2e_objects_us_median"])
+        out["obj_max"] = _r(t["e2e_objects_us_max"])
     if ref is not None:
         out["ref_us"] = _r(ref["value"], 0)
     return out
@@ -1365,7 +1375,8 @@ def main():
                  "ref_med": _r(c3["ref_us_median"], 0), "ref_max": _r(c3["ref_us_max"], 0),
                  "csv_identical": c3["csv_identical"]})
         line["ticks"] = ticks
-        line["ticks_unit"] = "us/tick; dev=CUDA events, e2e=TickEngine.tick, dropin=" \
+        line["ticks_unit"] = "us/tick; dev=CUDA events, e2e=TickEngine.tick, obj=e2e + the " \
+                             "ScalingAction objects, dropin=" \
                              "B200SimulationEngine._handle_scaler, ref=hybridscale " \
                              "_handle_scaler (config4: 40-fn sample x25)"
         line["lattice_config5"] = {"value": lat["value"], "ms_per_step": _r(lat["ms"] / 50, 4),
