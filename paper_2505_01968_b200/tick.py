@@ -396,9 +396,11 @@ class TickEngine:
                                         idle_arr.ctypes.data if idle_arr.size else None,
                                         pred_in.ctypes.data if pred_in is not None else None,
                                         len(self._act_buf)), "tick")
-        self._top_up_names()  # while the tick runs on the device
-        rc = lib.rapp_tick_collect(self._h, self._act_addr, len(self._act_buf),
-                                   ctypes.byref(nact), self._obs_addr, self._pred_addr)
+        try:
+            self._top_up_names()  # while the tick runs on the device
+        finally:  # a submitted tick is always collected (the handle accepts nothing else)
+            rc = lib.rapp_tick_collect(self._h, self._act_addr, len(self._act_buf),
+                                       ctypes.byref(nact), self._obs_addr, self._pred_addr)
         if rc == _lib.RAPP_E_DEGENERATE:
             raise FilterDegenerateError("H*P'*H + D == 0")
         _lib.check(rc, "tick")
