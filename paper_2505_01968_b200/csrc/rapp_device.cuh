@@ -95,15 +95,43 @@ __device__ __forceinline__ double throughput(double batch, double latency_ms) {
 //   throughput(b, lat) >= target  <=>  lat <= threshold(b, target)     for lat > 0,
 // which lets the lattice search replace two divisions per point with one compare and
 // still reproduce the reference's `rps >= target_rps` test (hs/perf.py:132) bit for bit.
-// Binary search over the ordered bit patterns of (0, +inf].
+// Search over the ordered bit patterns of (0, +inf]: the boundary is bracketed by galloping
+// (steps 1, 2, 4, ... ulps) from the estimate RN(RN(b / target) * 1000), which lies within a
+// few ulps of it for finite positive operands, then bisected; the predicate is monotone, so
+// the result is the one a bisection of the whole range finds (2-8 evaluations instead of 63).
+#ifndef RAPP_THRESHOLD_GALLOP
+#define RAPP_THRESHOLD_GALLOP 1
+#endif
 __device__ __forceinline__ double feasibility_threshold(double b, double target) {
   auto ok = [&](uint64_t bits) {
     return throughput(b, __longlong_as_double((long long)bits)) >= target;
   };
-  uint64_t lo = 1ull;                   // smallest positive denormal
-  uint64_t hi = 0x7FF0000000000000ull;  // +inf
+  constexpr uint64_t kLo = 1ull;                   // smallest positive denormal
+  constexpr uint64_t kHi = 0x7FF0000000000000ull;  // +inf
+  uint64_t lo = kLo, hi = kHi;
   if (!ok(lo)) return 0.0;
   if (ok(hi)) return __longlong_as_double((long long)hi);
+#if RAPP_THRESHOLD_GALLOP
+  const double g = __dmul_rn(__ddiv_rn(b, target), 1000.0);
+  if (g > 0.0 && g < __longlong_as_double((long long)kHi)) {  // NaN fails both
+    const uint64_t gb = (uint64_t)__double_as_longlong(g);
+    if (ok(gb)) {
+      lo = gb;
+      for (uint64_t step = 1;; step <<= 1) {  // terminates: !ok(kHi)
+        const uint64_t c = kHi - lo > step ? lo + step : kHi;
+        if (!ok(c)) { hi = c; break; }
+        lo = c;
+      }
+    } else {
+      hi = gb;
+      for (uint64_t step = 1;; step <<= 1) {  // terminates: ok(kLo)
+        const uint64_t c = hi - kLo > step ? hi - step : kLo;
+        if (ok(c)) { lo = c; break; }
+        hi = c;
+      }
+    }
+  }
+#endif
   while (hi - lo > 1) {                 // invariant: ok(lo) && !ok(hi)
     const uint64_t mid = lo + ((hi - lo) >> 1);
     if (ok(mid)) lo = mid; else hi = mid;
