@@ -27,8 +27,11 @@
 //     load) — both lanes hit the same 64-byte cell in one instruction, so a warp-wide load
 //     touches 16 lines.  Each lane does the quota and sm lerps of its row for both
 //     queries, and one exchange gives each lane the other row of its own query.
-//  5. Coordinates stream through a 4-stage TMA (cp.async.bulk) ring in shared memory fed
-//     by a producer warp (full/empty mbarriers); outputs are streaming stores.
+//  5. Coordinates: each warp walks 32-row slices grid-stride and loads the next slice
+//     (three strided 8-byte streaming loads per lane) before it interpolates the current
+//     one (RAPP_STREAM_DIRECT, the default: measured faster than the alternative kept
+//     behind RAPP_STREAM_DIRECT=0, a 4-stage TMA (cp.async.bulk) ring in shared memory fed
+//     by a producer warp with full/empty mbarriers); outputs are streaming stores.
 #include <cmath>
 #include <cstring>
 #include <vector>
