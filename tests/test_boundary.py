@@ -122,3 +122,33 @@ def test_new_pod_name_cache_follows_the_counter():
         got = e._new_names(e.counter, k)
         assert got == ["pod-%06d" % c for c in range(e.counter, e.counter + k)]
         e.counter += k
+
+
+def test_pod_id_mirror_and_lazy_views():
+    """TickEngine's object-array mirror of the pod id list (for gathering a tick's pod ids
+    by device pod index) follows the list as ticks append to it, across capacity growth,
+    and the lazily named function ids of new pods come out in pod order."""
+    import numpy as np
+    from paper_2505_01968_b200.tick import TickEngine
+
+    class Stub:
+        _ids_mirror = TickEngine._ids_mirror
+        pod_fids = TickEngine.pod_fids
+
+    e = Stub()
+    e.pod_ids = [f"init-{i}" for i in range(5)]
+    e.fids = ["fa", "fb", "fc"]
+    e._fids_np = np.array(e.fids, dtype=object)
+    e._pod_fids = ["fa"] * 5
+    e._pod_fn_pending = []
+    rng = np.random.default_rng(7)
+    want_f = list(e._pod_fids)
+    for _ in range(40):
+        k = int(rng.integers(0, 900))
+        e.pod_ids.extend(f"pod-{len(e.pod_ids) + j:06d}" for j in range(k))
+        fn = rng.integers(0, 3, k).astype(np.int32)
+        e._pod_fn_pending.append(fn)
+        want_f.extend(e.fids[i] for i in fn)
+        idx = rng.integers(0, len(e.pod_ids), 50)
+        assert e._ids_mirror()[idx].tolist() == [e.pod_ids[i] for i in idx]
+    assert e.pod_fids == want_f
