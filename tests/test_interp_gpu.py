@@ -291,3 +291,27 @@ def test_stateless_table_cache_alternating_tables(kern):
         out = np.empty(len(c))
         kern.interp3_many(b, s, q, v, c, out)
         assert same_bits(out, or_interp3_many(b, s, q, v, c)), k
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 511, 513, 9_473, 1_000_003])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_stream_tails_and_unaligned_coords(n, offset):
+    """K2's direct-load walk (32-row slices, grid-stride, next slice prefetched): ragged
+    tails, odd lane pairs, 8-byte-misaligned coordinate rows and a guarded output — 0 ulp
+    vs the oracle and not one byte written outside the n outputs."""
+    import torch
+    import bench
+    from paper_2505_01968_b200 import PerfTable
+    dev = torch.device("cuda", 0)
+    name, b, s, q, v = bench.config2_arrays()[1]
+    t = PerfTable(name, bench.BATCHES, list(range(1, 101)), list(range(1, 101)), v)
+    c = bench.gen_queries(b, s, q, n + 1, 900 + n, dev)
+    flat = c.view(-1)[offset:offset + 3 * n]
+    coords = flat.view(n, 3)
+    guard = torch.full((n + 64,), -7.25, dtype=torch.float64, device=dev)
+    out = guard[32:32 + n]
+    t.predict_latency_many(coords, out)
+    torch.cuda.synchronize()
+    g = guard.cpu().numpy()
+    assert (g[:32] == -7.25).all() and (g[32 + n:] == -7.25).all()
+    assert same_bits(g[32:32 + n], or_interp3_many(b, s, q, v, coords.cpu().numpy()))
