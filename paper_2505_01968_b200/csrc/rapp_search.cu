@@ -494,6 +494,7 @@ struct rapp_mec_plan {
   int max_pairs = 0;
   bool smem_table = true;
   size_t smem_bytes = 0;
+  size_t smem_brk_bytes = 0;  // the bracket arrays alone (table read from global memory)
   FnDesc* d_fn = nullptr;
   double* d_blist = nullptr;
   double* d_thr = nullptr;
@@ -513,17 +514,22 @@ struct rapp_mec_plan {
   uint8_t* d_stage = nullptr;
 };
 
+#ifndef RAPP_K3_GATED_GLOBAL
+#define RAPP_K3_GATED_GLOBAL 1
+#endif
+
 namespace rapp {
 
 template <bool SMEM, bool MINLAT, bool GATE>
 static int launch_lattice(rapp_mec_plan* pl, const double* targets, int64_t f0, int64_t nf,
                           int chunks, cudaStream_t st) {
   auto kern = k_mec_lattice<SMEM, MINLAT, GATE>;
+  const size_t smem = SMEM ? pl->smem_bytes : pl->smem_brk_bytes;
   RAPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pl->smem_bytes));
+                                 (int)std::max<size_t>(smem, 1)));
   rapp_ctx* c = pl->ctx;
   RAPP_CUDA(launch_pdl(kern, dim3((unsigned)(nf * chunks)), dim3(kSearchThreads),
-                       pl->smem_bytes, st, c->d_desc, c->d_pool, pl->d_fn, pl->d_blist, pl->d_thr,
+                       smem, st, c->d_desc, c->d_pool, pl->d_fn, pl->d_blist, pl->d_thr,
                        targets, f0, chunks, pl->step, pl->nQ, pl->d_key, pl->d_minlat,
                        pl->d_fb));
   RAPP_LAUNCHED();
@@ -565,7 +571,10 @@ static int run_plan(rapp_mec_plan* pl, const double* d_targets, int64_t f0, int6
     if ((rc = launch_lattice<false, false, false>(pl, d_targets, f0, nf, chunks, st))) return rc;
   }
   if (t1) RAPP_CUDA(cudaEventRecord(t1, st));
-  if (pl->smem_table) {
+  // the gated passes (functions without a feasible point; usually none) read the table from
+  // global memory: their small shared-memory footprint lets 8 CTAs per SM retire the
+  // early-exiting ones in a third of the waves
+  if (pl->smem_table && !RAPP_K3_GATED_GLOBAL) {
     if ((rc = launch_lattice<true, true, true>(pl, d_targets, f0, nf, chunks, st))) return rc;
   } else {
     if ((rc = launch_lattice<false, true, true>(pl, d_targets, f0, nf, chunks, st))) return rc;
@@ -574,7 +583,7 @@ static int run_plan(rapp_mec_plan* pl, const double* d_targets, int64_t f0, int6
                        pl->d_blist, f0, f1, pl->d_key, pl->d_minlat, pl->d_thr, pl->d_target2,
                        pl->d_fb));
   RAPP_LAUNCHED();
-  if (pl->smem_table) {
+  if (pl->smem_table && !RAPP_K3_GATED_GLOBAL) {
     if ((rc = launch_lattice<true, false, true>(pl, pl->d_target2, f0, nf, chunks, st))) return rc;
   } else {
     if ((rc = launch_lattice<false, false, true>(pl, pl->d_target2, f0, nf, chunks, st))) return rc;
@@ -651,6 +660,7 @@ int rapp_mec_plan_create(rapp_ctx* ctx, int64_t nfn, const int32_t* table_of_fn,
   pl->smem_table = max_seg * 8 <= kSearchSmemTable;
   const int64_t brk = 2 * max_ns + 2 * pl->nQ + 12 * max_nB + 2 + (max_ns + 1) / 2;
   pl->smem_bytes = (size_t)((pl->smem_table ? max_seg : 0) + brk) * 8;
+  pl->smem_brk_bytes = (size_t)brk * 8;
   if (pl->smem_bytes > 200 * 1024) {
     set_error("lattice search shared-memory footprint %zu bytes too large", pl->smem_bytes);
     return RAPP_E_ARG;
