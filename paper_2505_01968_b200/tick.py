@@ -371,7 +371,10 @@ class TickEngine:
         the Kalman step (Autoscaler.scale semantics)."""
         lib = _lib.load()
         F = len(self.fids)
-        if isinstance(arrivals, Mapping):
+        if (type(arrivals) is np.ndarray and arrivals.dtype == np.int64
+                and arrivals.flags.c_contiguous):
+            arr = arrivals  # the usual host-array call: no conversion
+        elif isinstance(arrivals, Mapping):
             arr = np.array([int(arrivals.get(f, 0)) for f in self.fids], dtype=np.int64)
         else:
             arr = np.ascontiguousarray(arrivals, dtype=np.int64)
@@ -383,6 +386,7 @@ class TickEngine:
         if idle is None:
             if getattr(self, "_all_idle", None) is None or len(self._all_idle) < max(1, n):
                 self._all_idle = np.ones(max(1024, 2 * n), dtype=np.uint8)
+                self._all_idle_addr = self._all_idle.ctypes.data
             idle_arr = self._all_idle
         else:
             idle_set = set(idle)
@@ -392,8 +396,10 @@ class TickEngine:
         if predicted is not None:
             pred_in = np.array([float(predicted[f]) for f in self.fids], dtype=np.float64)
         nact = self._nact
+        idle_addr = (self._all_idle_addr if idle_arr is getattr(self, "_all_idle", None)
+                     else idle_arr.ctypes.data)
         _lib.check(lib.rapp_tick_submit(self._h, float(now_ms), arr.ctypes.data if F else None,
-                                        idle_arr.ctypes.data if idle_arr.size else None,
+                                        idle_addr if idle_arr.size else None,
                                         pred_in.ctypes.data if pred_in is not None else None,
                                         len(self._act_buf)), "tick")
         try:
